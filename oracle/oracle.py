@@ -1,0 +1,407 @@
+"""fp64 oracle for the DiffVC-RT decode hot path (TEST INFRASTRUCTURE ONLY).
+
+Plain, slow, obviously correct.  Heavy loops (conv, group norm, unshuffle,
+rounding) live in ``dvc_oracle.c`` as direct loops; this module composes them
+in exactly the order the paper / readings define.  Citations:
+``P:<line>`` -> /root/reference/PAPER.md, ``S:<line>`` -> /root/reference/SPEC.md,
+``R<n>`` -> readings in DESIGN.md section 3.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline /
+``--impl reference`` legs may use this module.  It never imports the product.
+
+Parity status: every function below is pinned by a
+``-m "not gpu"`` test in tests/test_oracle_pins.py except agreement with the
+paper's trained model, which is unpinnable (no weights are published):
+the readings R2-R4, R8, R11, R13 are "parity unpinned" against the paper's
+numbers and pinned only structurally.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dvc_oracle.c")
+_SO = os.path.join(_HERE, "liboracle.so")
+_LIB = None
+
+_D = ctypes.POINTER(ctypes.c_double)
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle (plain gcc, fp64, OpenMP).  Returns the .so path."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O3", "-fopenmp", "-fPIC", "-shared", "-std=c11",
+               "-o", _SO + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_SO + ".tmp", _SO)
+    return _SO
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        _LIB = ctypes.CDLL(build())
+        i, d, sz = ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+        _LIB.orc_unshuffle.argtypes = [_D, i, i, i, i, i, _D]
+        _LIB.orc_shuffle.argtypes = [_D, i, i, i, i, i, _D]
+        _LIB.orc_conv2d.argtypes = [_D, i, i, i, i, _D, _D, i, i, i, i, _D]
+        _LIB.orc_groupnorm.argtypes = [_D, i, i, i, i, _D, _D, d, _D]
+        _LIB.orc_silu.argtypes = [_D, sz, _D]
+        _LIB.orc_nearest_to.argtypes = [_D, i, i, i, i, i, i, _D]
+        _LIB.orc_round.argtypes = [_D, sz, i]
+        _LIB.orc_round1.argtypes = [d, i]
+        _LIB.orc_round1.restype = d
+        _LIB.orc_num_threads.restype = i
+    return _LIB
+
+
+def _p(a):
+    return a.ctypes.data_as(_D)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def num_threads() -> int:
+    return lib().orc_num_threads()
+
+
+# --------------------------------------------------------------------------
+# precision emulation (R15)
+# --------------------------------------------------------------------------
+_MODES = {None: 0, "f32": 0, "fp16": 1, "bf16": 2}
+
+
+def rnd(x, mode):
+    """Round-to-nearest-even, directly from fp64, to binary16 ('fp16') or
+    bfloat16 ('bf16'); identity for None / 'f32'.  Returns a new array."""
+    x = _f64(x).copy()
+    m = _MODES[mode]
+    if m:
+        lib().orc_round(_p(x), x.size, m)
+    return x
+
+
+def rnd1(v: float, mode) -> float:
+    return lib().orc_round1(float(v), _MODES[mode])
+
+
+# --------------------------------------------------------------------------
+# a1. PixelUnshuffle (R12) and its inverse
+# --------------------------------------------------------------------------
+def unshuffle(F, s: int = 8):
+    """F [T,C,H,W] -> L [T,H/s,W/s,C*s*s] with L[t,y,x,c*s*s+i*s+j] = F[t,c,s*y+i,s*x+j]."""
+    F = _f64(F)
+    T, C, H, W = F.shape
+    if H % s or W % s:
+        raise ValueError("divisibility error: H and W must be multiples of s (S:56)")
+    L = np.empty((T, H // s, W // s, C * s * s))
+    assert lib().orc_unshuffle(_p(F), T, C, H, W, s, _p(L)) == 0
+    return L
+
+
+def shuffle(L, C: int, s: int = 8):
+    """Inverse of unshuffle: L [T,h,w,C*s*s] -> F [T,C,h*s,w*s]."""
+    L = _f64(L)
+    T, h, w, CL = L.shape
+    if CL != C * s * s:
+        raise ValueError("divisibility error: channels must be C*s*s")
+    F = np.empty((T, C, h * s, w * s))
+    assert lib().orc_shuffle(_p(L), T, C, h, w, s, _p(F)) == 0
+    return F
+
+
+# --------------------------------------------------------------------------
+# conv / norm / activation / resize primitives (R2-R4, R11)
+# --------------------------------------------------------------------------
+def conv2d(X, Wt, b=None, stride: int = 1, pad: int | None = None):
+    """X [T,H,W,Cin], Wt OHWI [Cout,k,k,Cin], b [Cout] -> [T,Ho,Wo,Cout]; zero padding."""
+    X, Wt = _f64(X), _f64(Wt)
+    T, H, W, Cin = X.shape
+    Cout, k, k2, Cin2 = Wt.shape
+    if k != k2 or Cin != Cin2:
+        raise ValueError("shape mismatch (S:47)")
+    if pad is None:
+        pad = k // 2
+    Ho, Wo = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+    Y = np.empty((T, Ho, Wo, Cout))
+    bp = None
+    if b is not None:
+        b = _f64(b)
+        bp = _p(b)
+    lib().orc_conv2d(_p(X), T, H, W, Cin, _p(Wt), bp, Cout, k, stride, pad, _p(Y))
+    return Y
+
+
+def conv1x1(X, Wt, b=None):
+    """1x1 conv with Wt [Cout,Cin]."""
+    Wt = _f64(Wt)
+    return conv2d(X, Wt.reshape(Wt.shape[0], 1, 1, Wt.shape[1]), b, 1, 0)
+
+
+def groupnorm(X, G: int, gamma, beta, eps: float = 1e-5):
+    """Per-(frame, group) GroupNorm, biased two-pass variance (R3, R4)."""
+    X = _f64(X)
+    T = X.shape[0]
+    C = X.shape[-1]
+    HW = int(np.prod(X.shape[1:-1]))
+    if C % G:
+        raise ValueError("divisibility error: G must divide C")
+    Y = np.empty_like(X)
+    g, bt = _f64(gamma), _f64(beta)
+    assert lib().orc_groupnorm(_p(X), T, HW, C, G, _p(g), _p(bt), float(eps), _p(Y)) == 0
+    return Y
+
+
+def silu(X):
+    X = _f64(X)
+    Y = np.empty_like(X)
+    lib().orc_silu(_p(X), X.size, _p(Y))
+    return Y
+
+
+def nearest_to(V, Ho: int, Wo: int):
+    """U[t,y,x] = V[t, floor(y*H/Ho), floor(x*W/Wo)] (R11)."""
+    V = _f64(V)
+    T, H, W, C = V.shape
+    U = np.empty((T, Ho, Wo, C))
+    lib().orc_nearest_to(_p(V), T, H, W, C, Ho, Wo, _p(U))
+    return U
+
+
+# --------------------------------------------------------------------------
+# a2. Latent Channel Expansion, encoder side (reading R13)
+# --------------------------------------------------------------------------
+def expand(L, Wexp, bexp, mode=None):
+    """E[t,y,x,k] = b_k + sum_m W[k,m] L[t,y,x,m]; stored 16-bit in 16-bit modes."""
+    return rnd(conv1x1(L, Wexp, bexp), mode)
+
+
+def encode(F, Wexp, bexp, s: int = 8, mode=None):
+    """a1 + a2: frames [T,3,H,W] -> expanded latent [T,H/s,W/s,c_lat]."""
+    return expand(unshuffle(F, s), Wexp, bexp, mode)
+
+
+# --------------------------------------------------------------------------
+# a3. Temporal shift: batch form and online form
+# --------------------------------------------------------------------------
+def _check_p(C, P):
+    if P < 1 or C % P:
+        raise ValueError("divisibility error: P must divide C (S:228)")
+    return C // P
+
+
+def shift_batch(X, carry, P: int):
+    """Batch-dimension OTSM: for c < C/P, frame t receives frame t-1's
+    channel c (intra-batch); frame 0 receives ``carry`` (inter-batch); the
+    rest is unchanged.  carry=None means zeros (chain start, R8).
+    Returns (X_shifted, carry_out = X[T-1][..., :C/P])."""
+    X = _f64(X)
+    c = _check_p(X.shape[-1], P)
+    Y = X.copy()
+    Y[1:, ..., :c] = X[:-1, ..., :c]
+    Y[0, ..., :c] = 0.0 if carry is None else _f64(carry)
+    return Y, X[-1, ..., :c].copy()
+
+
+def shift_online(x_t, state, P: int):
+    """Online TSM with a per-layer buffer ("the first segment is cached
+    ... the remaining segment is concatenated with the buffered feature slice";
+    S:215-218).  x_t [h,w,C]; state [h,w,C/P] or None (zeros at sequence start).
+    Returns (y_t, state')."""
+    x_t = _f64(x_t)
+    C = x_t.shape[-1]
+    c = _check_p(C, P)
+    cached = np.zeros(x_t.shape[:-1] + (c,)) if state is None else _f64(state)
+    y = np.concatenate([cached, x_t[..., c:]], axis=-1)   # buffered slice ++ remaining segment
+    return y, x_t[..., :c].copy()                          # first segment cached for frame t+1
+
+
+# --------------------------------------------------------------------------
+# a3-a8. One OTSM ResBlock over T consecutive frames (R2, R5-R8, R15)
+# --------------------------------------------------------------------------
+def resblock(X, carry, w: dict, G: int, P: int, eps: float = 1e-5, mode=None,
+             shift: str = "batch"):
+    """Out = S(X) + conv2(silu(gn2(conv1(silu(gn1(shift(X, carry))))))).
+
+    X [T,h,w,Cin]; carry [h,w,Cin/P] or None.  w holds gn1_w, gn1_b, conv1_w,
+    conv1_b, gn2_w, gn2_b, conv2_w, conv2_b and, iff Cin != Cout, sc_w [Cout,Cin],
+    sc_b.  The shift sits at the entry of the residual branch (R5); the shortcut
+    sees the unshifted X.  mode rounds at the storage points H1, Y1, H2, Out
+    (R15).  shift='online' runs the shift frame by frame with a buffer instead of
+    the batch formula (the two must agree exactly).
+    Returns (Out, carry_out)."""
+    X = _f64(X)
+    if shift == "batch":
+        Xs, k_out = shift_batch(X, carry, P)
+    else:
+        frames, st = [], carry
+        for t in range(X.shape[0]):
+            y, st = shift_online(X[t], st, P)
+            frames.append(y)
+        Xs, k_out = np.stack(frames), st
+    H1 = rnd(silu(groupnorm(Xs, G, w["gn1_w"], w["gn1_b"], eps)), mode)
+    Y1 = rnd(conv2d(H1, w["conv1_w"], w["conv1_b"]), mode)
+    H2 = rnd(silu(groupnorm(Y1, G, w["gn2_w"], w["gn2_b"], eps)), mode)
+    Y2 = conv2d(H2, w["conv2_w"], w["conv2_b"])
+    S = X if w.get("sc_w") is None else conv1x1(X, w["sc_w"], w["sc_b"])
+    return rnd(S + Y2, mode), k_out
+
+
+# --------------------------------------------------------------------------
+# a9-a10. The pruned U-Net ResBlock skeleton (R1, R9-R11)
+# --------------------------------------------------------------------------
+def unet_blocks(width=(240, 480, 960, 960)):
+    """The oracle's own statement of reading R1 (SD-2.1-base U-Net, widths x0.75,
+    layers_per_block 2, 22 ResBlocks).  Returns [(name, level, cin, cout)] in
+    execution order; up-block cin counts the concatenated skip."""
+    blocks = []
+    skips = [width[0]]                           # conv_in output
+    cur = width[0]
+    for l in range(4):
+        for r in range(2):
+            blocks.append((f"down{l}.r{r}", l, cur, width[l]))
+            cur = width[l]
+            skips.append(cur)
+        if l < 3:
+            skips.append(cur)                    # stride-2 downsampler output
+    for r in range(2):
+        blocks.append((f"mid.r{r}", 3, cur, cur))
+    for u in range(4):
+        l = 3 - u
+        for r in range(3):
+            sk = skips.pop()
+            blocks.append((f"up{u}.r{r}", l, cur + sk, width[l]))
+            cur = width[l]
+    return blocks
+
+
+def param_count(width=(240, 480, 960, 960), c_in=512, c_out=256, attention=True):
+    """Closed-form parameter count of reading R1, used to pin it to Table 8's
+    444.78 M.  Transformer2D blocks (cross-attention removed) count
+    18C^2 + 18C each: GN 2C, proj_in/out 2(C^2+C), LN1 2C, qkv 3C^2, out C^2+C,
+    LN 2C, GEGLU C->8C (8C^2+8C), FF out 4C->C (4C^2+C)."""
+    n = 9 * c_in * width[0] + width[0]
+    for _, _, ci, co in unet_blocks(width):
+        n += 9 * ci * co + co + 9 * co * co + co + 2 * ci + 2 * co
+        if ci != co:
+            n += ci * co + co
+    for C in (width[0], width[1], width[2]):           # 3 downsamplers
+        n += 9 * C * C + C
+    for C in (width[3], width[2], width[1]):           # 3 upsamplers
+        n += 9 * C * C + C
+    n += 2 * width[0] + 9 * width[0] * c_out + c_out   # norm_out + conv_out
+    if attention:
+        tb = lambda C: 18 * C * C + 18 * C  # noqa: E731
+        n += 2 * (tb(width[0]) + tb(width[1]) + tb(width[2]))   # down 0..2
+        n += tb(width[3])                                      # mid
+        n += 3 * (tb(width[2]) + tb(width[1]) + tb(width[0]))   # up 1..3
+    return n
+
+
+def _take(it, shape, name):
+    nm, a = next(it)
+    a = _f64(a)
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"weight {nm} has shape {a.shape}, oracle expected {name} {shape}")
+    return a
+
+
+def _rb_weights(it, cin, cout):
+    w = {
+        "gn1_w": _take(it, (cin,), "gn1_w"), "gn1_b": _take(it, (cin,), "gn1_b"),
+        "conv1_w": _take(it, (cout, 3, 3, cin), "conv1_w"), "conv1_b": _take(it, (cout,), "conv1_b"),
+        "gn2_w": _take(it, (cout,), "gn2_w"), "gn2_b": _take(it, (cout,), "gn2_b"),
+        "conv2_w": _take(it, (cout, 3, 3, cout), "conv2_w"), "conv2_b": _take(it, (cout,), "conv2_b"),
+        "sc_w": None, "sc_b": None,
+    }
+    if cin != cout:
+        w["sc_w"] = _take(it, (cout, cin), "sc_w")
+        w["sc_b"] = _take(it, (cout,), "sc_b")
+    return w
+
+
+def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int = 8,
+             eps: float = 1e-5, carries=None, mode=None, record=None, shift="batch"):
+    """The pruned U-Net's ResBlock skeleton over T frames of one chain (R1, R11):
+        x0 = conv_in(concat(Lbar, Cm));  push x0
+        for level l = 0..3: two ResBlocks (push each); if l < 3: conv3x3 stride 2 (push)
+        mid: two ResBlocks
+        for u = 0..3 (level 3-u): three ResBlocks on concat(h, pop());
+                                  if u < 3: nearest to the next skip's size, conv3x3
+        out = conv_out(silu(gn_out(h)))
+    The 16 self-attention Transformer2D blocks are elided (identity; NEXT-1).
+    weights: iterable of (name, array) in the blob order of include/dvc.h.
+    carries: list of 22 slices [h_l, w_l, Cin_k/P] (None = chain start, zeros).
+    record: optional list that receives every ResBlock output.
+    Returns (out [T,h,w,c_out], carries_out)."""
+    it = iter(weights)
+    lat, ctx = _f64(lat), _f64(ctx)
+    c_cat = lat.shape[-1] + ctx.shape[-1]
+    blocks = unet_blocks(width)
+    if carries is None:
+        carries = [None] * len(blocks)
+    k_out = []
+    bi = 0
+
+    def run_block(h):
+        nonlocal bi
+        name, _, cin, cout = blocks[bi]
+        if h.shape[-1] != cin:
+            raise ValueError(f"{name}: input has {h.shape[-1]} channels, expected {cin}")
+        w = _rb_weights(it, cin, cout)
+        out, k = resblock(h, carries[bi], w, G, P, eps, mode, shift)
+        k_out.append(k)
+        if record is not None:
+            record.append(out)
+        bi += 1
+        return out
+
+    w_in = _take(it, (width[0], 3, 3, c_cat), "conv_in_w")
+    b_in = _take(it, (width[0],), "conv_in_b")
+    h = rnd(conv2d(np.concatenate([lat, ctx], axis=-1), w_in, b_in), mode)
+    skips = [h]
+    for l in range(4):
+        for _ in range(2):
+            h = run_block(h)
+            skips.append(h)
+        if l < 3:
+            C = h.shape[-1]
+            wd = _take(it, (C, 3, 3, C), "down_w")
+            bd = _take(it, (C,), "down_b")
+            h = rnd(conv2d(h, wd, bd, stride=2, pad=1), mode)
+            skips.append(h)
+    for _ in range(2):
+        h = run_block(h)
+    for u in range(4):
+        for _ in range(3):
+            h = run_block(np.concatenate([h, skips.pop()], axis=-1))
+        if u < 3:
+            C = h.shape[-1]
+            Ho, Wo = skips[-1].shape[1], skips[-1].shape[2]
+            wu = _take(it, (C, 3, 3, C), "up_w")
+            bu = _take(it, (C,), "up_b")
+            h = rnd(conv2d(nearest_to(h, Ho, Wo), wu, bu), mode)
+    C = h.shape[-1]
+    g_o = _take(it, (C,), "gn_out_w")
+    b_o = _take(it, (C,), "gn_out_b")
+    c_out = lat.shape[-1]
+    w_o = _take(it, (c_out, 3, 3, C), "conv_out_w")
+    bo = _take(it, (c_out,), "conv_out_b")
+    hn = rnd(silu(groupnorm(h, G, g_o, b_o, eps)), mode)
+    out = rnd(conv2d(hn, w_o, bo), mode)
+    rest = list(it)
+    if rest:
+        raise ValueError(f"{len(rest)} unused weight tensors")
+    return out, k_out
+
+
+def rel_l2(a, ref) -> float:
+    """||a - ref||_2 / ||ref||_2 (R16)."""
+    a, ref = _f64(a), _f64(ref)
+    return float(np.linalg.norm((a - ref).ravel()) / max(np.linalg.norm(ref.ravel()), 1e-300))

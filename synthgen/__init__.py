@@ -1,0 +1,126 @@
+"""Seeded synthetic input generators shared by the tests, the bench and smoke().
+
+This module holds none of the method's arithmetic: it only draws random
+numbers with the shapes and distributions of the paper's workloads (recipe in
+DESIGN.md section 5).  Both the oracle and the CUDA path consume what it
+produces; neither is imported here.
+
+Recipe (reading R19):
+  * frames: k/255 with k ~ U{0..255} (8-bit video), NCHW [T,3,H,W]      seed 2
+  * latents / contexts: N(0,1), NHWC [T,h,w,256]                         seed 1
+  * conv W, b ~ U(+-1/sqrt(fan_in)) (PyTorch default conv init)          seed 0
+  * GroupNorm gamma ~ U(0.5, 1.5), beta ~ U(-0.5, 0.5)  (beta != 0 so the
+    chain-start slice SiLU(beta) of reading R8 is observable)
+Arrays are float32; callers cast to the device dtype and hand the oracle the
+exact (cast) values.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SEED_WEIGHTS, SEED_INPUTS, SEED_FRAMES = 0, 1, 2
+
+
+def rng(seed: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def frames_u8(T: int, H: int, W: int, seed: int = SEED_FRAMES) -> np.ndarray:
+    """Synthetic 8-bit RGB frames, NCHW [T,3,H,W] uint8."""
+    return rng(seed).integers(0, 256, size=(T, 3, H, W), dtype=np.uint8)
+
+
+def frames(T: int, H: int, W: int, seed: int = SEED_FRAMES) -> np.ndarray:
+    """Frames in [0,1] as k/255 (float32), NCHW [T,3,H,W]."""
+    return (frames_u8(T, H, W, seed).astype(np.float64) / 255.0).astype(np.float32)
+
+
+def normal(shape, seed: int = SEED_INPUTS, scale: float = 1.0) -> np.ndarray:
+    return (rng(seed).standard_normal(size=shape) * scale).astype(np.float32)
+
+
+def _conv(g, cout, k, cin):
+    bound = 1.0 / np.sqrt(cin * k * k)
+    w = g.uniform(-bound, bound, size=(cout, k, k, cin)).astype(np.float32)   # OHWI
+    b = g.uniform(-bound, bound, size=(cout,)).astype(np.float32)
+    return w, b
+
+
+def _gn(g, c):
+    return (g.uniform(0.5, 1.5, size=(c,)).astype(np.float32),
+            g.uniform(-0.5, 0.5, size=(c,)).astype(np.float32))
+
+
+def resblock_weights(cin: int, cout: int, seed: int = SEED_WEIGHTS, g=None) -> dict:
+    """One ResBlock's parameters in the order of include/dvc.h's dvc_resblock."""
+    g = rng(seed) if g is None else g
+    d = {}
+    d["gn1_w"], d["gn1_b"] = _gn(g, cin)
+    d["conv1_w"], d["conv1_b"] = _conv(g, cout, 3, cin)
+    d["gn2_w"], d["gn2_b"] = _gn(g, cout)
+    d["conv2_w"], d["conv2_b"] = _conv(g, cout, 3, cout)
+    if cin != cout:
+        w, b = _conv(g, cout, 1, cin)
+        d["sc_w"], d["sc_b"] = w.reshape(cout, cin), b
+    else:
+        d["sc_w"] = d["sc_b"] = None
+    return d
+
+
+RB_ORDER = ("gn1_w", "gn1_b", "conv1_w", "conv1_b", "gn2_w", "gn2_b",
+            "conv2_w", "conv2_b", "sc_w", "sc_b")
+
+
+def expansion_weights(c_lat: int = 256, c_in: int = 192, seed: int = SEED_WEIGHTS):
+    """Encoder-side Latent Channel Expansion 1x1 conv (reading R13): W [c_lat, c_in], b."""
+    w, b = _conv(rng(seed), c_lat, 1, c_in)
+    return w.reshape(c_lat, c_in), b
+
+
+def unet_weights(width=(240, 480, 960, 960), c_lat: int = 256, c_ctx: int = 256,
+                 seed: int = SEED_WEIGHTS):
+    """All skeleton tensors as [(name, float32 array)] in the blob order that
+    include/dvc.h documents for dvc_unet_create:
+      conv_in{w,b}; the 22 ResBlocks in U-Net order, each
+      {gn1_w,gn1_b,conv1_w,conv1_b,gn2_w,gn2_b,conv2_w,conv2_b[,sc_w,sc_b]}, with the
+      stride-2 conv{w,b} after down_l.r1 (l<3) and the post-upsample conv{w,b}
+      after up_u.r2 (u<3); then gn_out{w,b}; conv_out{w,b}."""
+    g = rng(seed)
+    out = []
+
+    def conv(name, cout, cin, k=3):
+        w, b = _conv(g, cout, k, cin)
+        out.append((name + ".w", w))
+        out.append((name + ".b", b))
+
+    def block(name, cin, cout):
+        d = resblock_weights(cin, cout, g=g)
+        for k in RB_ORDER:
+            if d[k] is not None:
+                out.append((f"{name}.{k}", d[k]))
+
+    conv("conv_in", width[0], c_lat + c_ctx)
+    skip_ch = [width[0]]
+    cur = width[0]
+    for l in range(4):
+        for r in range(2):
+            block(f"down{l}.r{r}", cur, width[l])
+            cur = width[l]
+            skip_ch.append(cur)
+        if l < 3:
+            conv(f"down{l}.ds", cur, cur)
+            skip_ch.append(cur)
+    for r in range(2):
+        block(f"mid.r{r}", cur, cur)
+    for u in range(4):
+        lvl = 3 - u
+        for r in range(3):
+            block(f"up{u}.r{r}", cur + skip_ch.pop(), width[lvl])
+            cur = width[lvl]
+        if u < 3:
+            conv(f"up{u}.us", cur, cur)
+    gw, gb = _gn(g, cur)
+    out.append(("gn_out.w", gw))
+    out.append(("gn_out.b", gb))
+    conv("conv_out", c_lat, cur)
+    return out
