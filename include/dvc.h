@@ -1,0 +1,199 @@
+/*
+ * dvc.h -- C-ABI of libdvc.so, the B200-native (sm_100a) decode hot path of
+ * DiffVC-RT (arXiv 2601.20564).
+ *
+ * Citations: P:<line> = the paper's text (/root/reference/PAPER.md at build
+ * time), S:<line> = its CPU-program specification, R<n> = the
+ * readings listed in DESIGN.md section 3 (the paper is silent there).
+ *
+ * Conventions (all entry points):
+ *   - Every tensor pointer is a DEVICE pointer unless stated; the caller owns
+ *     every buffer.  The library owns only the opaque handles it creates.
+ *   - Activations are NHWC ("[T,h,w,C]", frames of one chain packed on the
+ *     batch dimension), contiguous, 16-byte aligned.  Frames are NCHW.
+ *     Conv weights are OHWI [C_out][k][k][C_in]; 1x1 weights [C_out][C_in].
+ *   - dtype: DVC_BF16 (the paper's U-Net precision), DVC_F16, or DVC_F32
+ *     (validation mode: fp32 storage, fp32 SIMT arithmetic, no tensor cores).
+ *     In 16-bit modes all weights, biases and GN affine parameters are in the
+ *     same 16-bit dtype; the tensor-core convolutions accumulate in fp32 (TMEM).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).  No
+ *     entry point synchronises the host or allocates device memory on the
+ *     forward path; calls are stream-ordered and asynchronous.
+ *   - Argument, shape, divisibility and architecture errors are detected and
+ *     returned BEFORE any launch: no partial writes.  Asynchronous CUDA faults
+ *     surface as DVC_ERR_CUDA from a later call.  There is no CPU fallback:
+ *     a device that is not sm_100 returns DVC_ERR_UNSUPPORTED.
+ *   - dvc_last_error() returns a thread-local human-readable detail string.
+ */
+#ifndef DVC_H_
+#define DVC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DVC_API __attribute__((visibility("default")))
+#else
+#define DVC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DVC_ABI_VERSION 1
+
+typedef enum {
+    DVC_OK = 0,
+    DVC_ERR_ARG = 1,          /* null pointer / bad enum / negative size            */
+    DVC_ERR_DIVISIBILITY = 2, /* H%s, W%s, C%P, C%G                   */
+    DVC_ERR_SHAPE = 3,        /* shape mismatch between arguments           */
+    DVC_ERR_UNSUPPORTED = 4,  /* not sm_100, or a shape the kernels do not cover    */
+    DVC_ERR_WORKSPACE = 5,    /* workspace too small                                */
+    DVC_ERR_CUDA = 6,         /* a CUDA runtime error (including earlier async ones) */
+    DVC_ERR_NCCL = 7          /* an NCCL error (multi-GPU halo)                     */
+} dvc_status;
+
+typedef enum { DVC_BF16 = 0, DVC_F16 = 1, DVC_F32 = 2 } dvc_dtype;
+
+DVC_API const char *dvc_status_string(dvc_status s);
+DVC_API const char *dvc_last_error(void);
+DVC_API int dvc_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * a1 + a2.  Encoder front end: PixelUnshuffle ("PixelUnshuffle
+ * operation for space-to-depth") fused with the Latent Channel Expansion
+ * ("expanding the latent dimension ... to 256"; 1x1 conv + bias, R13).
+ *
+ *   frames  [T,3,H,W] NCHW in `dt` (values in [0,1])
+ *   w_exp   [c_lat][3*s*s], b_exp [c_lat]  (dt), or both NULL
+ *   latent  [T,H/s,W/s,c_lat] NHWC in `dt`
+ *
+ * w_exp == NULL: unshuffle only, c_lat must be 3*s*s; the result is a pure
+ * permutation, bit-exact: latent[t,y,x,c*s*s+i*s+j] = frames[t,c,s*y+i,s*x+j]
+ * (torch channel order, R12).  Otherwise E = b + W.L with fp32 accumulation,
+ * computed on tcgen05 tensor cores (16-bit) with the 3*s*s-channel latent
+ * never written to memory; 16-bit expansion requires s == 8.
+ * Errors: DIVISIBILITY if H%s or W%s; ARG on nulls / T<1.
+ * ------------------------------------------------------------------------ */
+DVC_API dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype dt, int T, int H, int W, int s,
+                                     const void *w_exp, const void *b_exp, int c_lat,
+                                     void *latent, void *stream);
+
+/* ------------------------------------------------------------------------
+ * a3-a8.  One OTSM ResBlock over T consecutive frames of one chain (P:320,
+ * App. A; P:151 Batch-dimension OTSM).  Input X = concat(x_a[c_a], x_b[c_b])
+ * along channels (c_b = 0 except on the U-Net's up path).  Reading R2/R5:
+ *
+ *   Xs   = shift(X, carry_in)        frame t gets frame t-1's channels [0,C_in/P)
+ *                                     (intra-batch); frame 0 gets carry_in
+ *                                     (inter-batch)
+ *   H1   = SiLU(GN1(Xs))             GN per (frame, group), biased var, eps (R3, R4)
+ *   Y1   = conv3x3(H1) + b1          tensor cores (16-bit) / SIMT (F32)
+ *   H2   = SiLU(GN2(Y1))
+ *   Out  = S(X) + conv3x3(H2) + b2   S = identity if C_in == C_out, else a 1x1
+ *                                     conv + bias on the UNSHIFTED X
+ *   carry_out = X[T-1][..., 0:C_in/P]  (raw block input, for the next batch)
+ *
+ * Requirements: C_in = c_a + c_b; C_in % P == 0; C_in/P <= c_a; G | C_in and
+ * G | C_out; c_a, c_b, C_out multiples of 16 on the tensor-core path (16-bit)
+ * and of 8 in F32; T >= 1.
+ * carry_in: [H,W,C_in/P] or NULL (= zeros: chain start, R8).
+ * carry_out: [H,W,C_in/P] or NULL.  y: [T,H,W,C_out]; must not alias inputs.
+ * workspace: device scratch of at least dvc_resblock_workspace_size() bytes,
+ * 256-byte aligned.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    int c_a, c_b, c_out, groups, shift_p;
+    float eps;
+    dvc_dtype dt;
+    const void *gn1_w, *gn1_b, *conv1_w, *conv1_b; /* conv1_w [c_out][3][3][c_in] */
+    const void *gn2_w, *gn2_b, *conv2_w, *conv2_b; /* conv2_w [c_out][3][3][c_out] */
+    const void *sc_w, *sc_b;                       /* [c_out][c_in]; NULL iff c_in == c_out */
+} dvc_resblock;
+
+DVC_API dvc_status dvc_resblock_workspace_size(const dvc_resblock *b, int T, int H, int W, size_t *bytes);
+DVC_API dvc_status dvc_resblock_tsm_forward(const dvc_resblock *b, const void *x_a, const void *x_b,
+                                    int T, int H, int W, const void *carry_in, void *carry_out,
+                                    void *y, void *workspace, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Test-only: materialise Xs = shift(X, carry) (a3) with the same addressing
+ * function the GN/SiLU operand producer uses.  xs [T,H,W,C_in] in dt.
+ * ------------------------------------------------------------------------ */
+DVC_API dvc_status dvc_debug_shift_gather(const void *x_a, const void *x_b, int c_a, int c_b, int shift_p,
+                                  dvc_dtype dt, int T, int H, int W, const void *carry_in,
+                                  void *xs, void *stream);
+
+/* ------------------------------------------------------------------------
+ * a9 + a10 + e.  The pruned U-Net's ResBlock skeleton over a group of frames
+ * (reading R1):
+ *   x0 = conv_in(concat(Lbar_t, Cm_t))                 (P:110, 512 -> width[0])
+ *   levels 0..3: 2 OTSM ResBlocks each, a stride-2 3x3 conv after levels 0..2
+ *   mid: 2 OTSM ResBlocks
+ *   up levels 3..0: 3 OTSM ResBlocks on concat(h, skip) each, nearest resize to
+ *   the next skip's size + 3x3 conv after the first three (R11)
+ *   out = conv_out(SiLU(GN_out(h)))                    (width[0] -> c_lat)
+ * The 16 self-attention Transformer2D blocks are not part of this path (they
+ * are the next row, NEXT-1) and are treated as identity.
+ *
+ * Weight blob (host memory, dt elements, concatenated in this order):
+ *   conv_in{w [W0][3][3][c_lat+c_ctx], b}
+ *   the 22 ResBlocks in U-Net order (down0.r0, down0.r1, ..., mid.r1, up0.r0 .. up3.r2),
+ *     each {gn1_w, gn1_b, conv1_w, conv1_b, gn2_w, gn2_b, conv2_w, conv2_b[, sc_w, sc_b]},
+ *     with the stride-2 conv {w, b} after down_l.r1 (l = 0..2) and the
+ *     post-resize conv {w, b} after up_u.r2 (u = 0..2)
+ *   gn_out{w, b}; conv_out{w [c_lat][3][3][W0], b}
+ * Packed carries: the 22 slices [h_l][w_l][C_in_k/P] of block k's input,
+ * concatenated in block order (dvc_unet_carry_size gives the element count).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    int width[4];      /* 240, 480, 960, 960 (SD-2.1 widths x 0.75, R1) */
+    int c_lat, c_ctx;  /* 256, 256 -> conv_in input 512 */
+    int groups, shift_p;
+    float eps;
+    dvc_dtype dt;
+    int h, w;          /* latent size, e.g. 90x160 (720p), 135x240 (1080p) */
+    int max_T;         /* largest T_local per call; sizes the workspace */
+} dvc_unet_config;
+
+typedef struct dvc_unet dvc_unet;
+typedef struct dvc_comm dvc_comm;
+
+DVC_API dvc_status dvc_unet_create(const dvc_unet_config *cfg, const void *host_weights, size_t bytes,
+                           dvc_unet **out);
+DVC_API dvc_status dvc_unet_destroy(dvc_unet *n);
+/* Number of blob elements the config expects. */
+DVC_API dvc_status dvc_unet_weight_count(const dvc_unet_config *cfg, size_t *elems);
+/* Element count of the packed 22-slice carry. */
+DVC_API dvc_status dvc_unet_carry_size(const dvc_unet *n, size_t *elems);
+DVC_API dvc_status dvc_unet_workspace_size(const dvc_unet *n, int T_local, size_t *bytes);
+
+/* One call decodes T_local consecutive frames [t0, t0+T_local) of one chain.
+ *   lat, ctx  [T_local,h,w,c_lat] / [T_local,h,w,c_ctx]: Lbar_t and C^m_t
+ *   out       [T_local,h,w,c_lat]: Lhat_t
+ *   carry_in  packed carry of frame t0-1, or NULL = chain start (zeros, R8).
+ *             With comm and rank > 0 the carry comes from rank-1 instead.
+ *   carry_out packed carry of the last frame, or NULL.  With comm, only the
+ *             last rank writes it.
+ *   comm      NULL = single GPU; else the halo of every ResBlock moves over
+ *             NCCL from rank r to rank r+1 (contiguous frame chunks). */
+DVC_API dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, const void *ctx,
+                               int T_local, const void *carry_in, void *carry_out, void *out,
+                               void *workspace, size_t ws_bytes, void *stream);
+
+/* Multi-GPU halo communicator (NCCL, loaded at run time from the process's
+ * libnccl.so.2).  id128: 128-byte ncclUniqueId, created on rank 0 and
+ * broadcast by the caller (e.g. torch.distributed). */
+DVC_API dvc_status dvc_comm_unique_id(void *id128);
+DVC_API dvc_status dvc_comm_create(int rank, int world, const void *id128, dvc_comm **out);
+DVC_API dvc_status dvc_comm_destroy(dvc_comm *c);
+
+/* Device / build introspection (no compute). */
+DVC_API dvc_status dvc_device_check(int device);   /* DVC_OK iff the device is sm_100 */
+DVC_API int dvc_kernel_launch_count(void);         /* kernels launched by this process so far */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DVC_H_ */

@@ -1,0 +1,9 @@
+"""B200-native (sm_100a) decode hot path of DiffVC-RT (arXiv 2601.20564).
+
+The compute lives in libdvc.so (hand-written CUDA for sm_100a behind the
+C-ABI of include/dvc.h); this package is its thin Python binding.
+"""
+from .dvc import (  # noqa: F401
+    Comm, DvcError, ResBlockParams, UNet, device_check, dvc_debug_shift_gather, dvc_encode_pixelunshuffle,
+    dvc_resblock_tsm_forward, dvc_unet_decode_gop, launch_count, pack_weights, unet_config, unet_weight_count,
+)

@@ -1,0 +1,262 @@
+// dvc_api.cu -- C-ABI entry points (include/dvc.h): argument validation,
+// workspace carving and launch order.  No host sync and no allocation on the
+// forward path; every check happens before the first launch.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include "dvc_conv.cuh"
+#include "dvc_norm.cuh"
+#include "dvc_resblock.cuh"
+
+namespace dvc {
+
+int g_launches = 0;
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+dvc_status check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return DVC_ERR_CUDA;
+    }
+    return DVC_OK;
+}
+
+dvc_status check_device() {
+    int dev = 0;
+    DVC_CUDA(cudaGetDevice(&dev));
+    static int cached[64];   // 0 unknown, 1 ok, 2 bad
+    if (dev >= 0 && dev < 64 && cached[dev] == 1) return DVC_OK;
+    cudaDeviceProp prop;
+    DVC_CUDA(cudaGetDeviceProperties(&prop, dev));
+    bool ok = prop.major == 10 && prop.minor == 0;
+    if (dev >= 0 && dev < 64) cached[dev] = ok ? 1 : 2;
+    DVC_CHECK_ARG(ok, DVC_ERR_UNSUPPORTED, "device %d is sm_%d%d; libdvc is built for sm_100a only (no fallback)",
+                  dev, prop.major, prop.minor);
+    // surface earlier asynchronous faults
+    cudaError_t e = cudaPeekAtLastError();
+    DVC_CHECK_ARG(e == cudaSuccess, DVC_ERR_CUDA, "pending CUDA error: %s", cudaGetErrorString(e));
+    return DVC_OK;
+}
+
+// ----------------------------------------------------------------- ResBlock (a3-a8)
+size_t resblock_ws_bytes(int ca, int cb, int cout, int G, int T, int HW, dvc_dtype dt) {
+    const size_t es = dt_size(dt);
+    const int cin = ca + cb;
+    return align256(gn_workspace_bytes(T, HW, G)) + align256((size_t)T * HW * cin * es) +
+           2 * align256((size_t)T * HW * cout * es);
+}
+
+dvc_status resblock_validate(const RB &b, int T, int H, int W) {
+    const int cin = b.ca + b.cb;
+    DVC_CHECK_ARG(dt_valid(b.dt), DVC_ERR_ARG, "bad dtype");
+    DVC_CHECK_ARG(T >= 1 && H >= 1 && W >= 1, DVC_ERR_ARG, "T, H, W must be >= 1");
+    DVC_CHECK_ARG(b.ca > 0 && b.cb >= 0 && b.cout > 0, DVC_ERR_ARG, "bad channel counts");
+    DVC_CHECK_ARG(b.P >= 1 && cin % b.P == 0, DVC_ERR_DIVISIBILITY, "shift_p=%d must divide C_in=%d", b.P, cin);
+    DVC_CHECK_ARG(b.G >= 1 && cin % b.G == 0 && b.cout % b.G == 0, DVC_ERR_DIVISIBILITY,
+                  "groups=%d must divide C_in=%d and C_out=%d", b.G, cin, b.cout);
+    DVC_CHECK_ARG(cin / b.P <= b.ca, DVC_ERR_UNSUPPORTED, "shift slice C_in/P must lie in x_a");
+    DVC_CHECK_ARG(b.gn1_w && b.gn1_b && b.conv1_w && b.conv1_b && b.gn2_w && b.gn2_b && b.conv2_w && b.conv2_b,
+                  DVC_ERR_ARG, "null ResBlock parameter");
+    DVC_CHECK_ARG((b.sc_w == nullptr) == (cin == b.cout), DVC_ERR_SHAPE,
+                  "sc_w must be given iff C_in != C_out (C_in=%d, C_out=%d)", cin, b.cout);
+    DVC_CHECK_ARG(b.sc_w == nullptr || b.sc_b != nullptr, DVC_ERR_ARG, "sc_b missing");
+    DVC_CHECK_ARG(b.sc_w != nullptr || b.cb == 0, DVC_ERR_UNSUPPORTED, "identity shortcut needs one source");
+    const int q = b.dt == DVC_F32 ? 8 : 16;
+    DVC_CHECK_ARG(b.ca % q == 0 && b.cb % q == 0 && b.cout % q == 0, DVC_ERR_UNSUPPORTED,
+                  "channel counts must be multiples of %d", q);
+    DVC_CHECK_ARG(cin <= 2048 && b.cout <= 2048, DVC_ERR_UNSUPPORTED, "at most 2048 channels");
+    DVC_CHECK_ARG(T < 256 && H < 4096 && W < 4096, DVC_ERR_UNSUPPORTED, "T < 256, H, W < 4096");
+    return DVC_OK;
+}
+
+// The block as a launch sequence.  ws holds GN scratch, H1 [T][HW][C_in], Y1 and H2 [T][HW][C_out].
+dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, int H, int W, const void *carry_in,
+                           void *carry_out, void *y, void *ws, cudaStream_t stream) {
+    const int HW = H * W, cin = b.ca + b.cb, cs = cin / b.P;
+    const size_t es = dt_size(b.dt);
+    uint8_t *p = reinterpret_cast<uint8_t *>(ws);
+    void *gnws = p;
+    p += align256(gn_workspace_bytes(T, HW, b.G));
+    void *h1 = p;
+    p += align256((size_t)T * HW * cin * es);
+    void *y1 = p;
+    p += align256((size_t)T * HW * b.cout * es);
+    void *h2 = p;
+    dvc_status st;
+    // carry_out = X[T-1][..., 0:C_in/P] (raw input, before this block overwrites nothing; y never aliases x)
+    if (carry_out) {
+        DVC_CUDA(cudaMemcpy2DAsync(carry_out, cs * es, reinterpret_cast<const uint8_t *>(xa) +
+                                                           (size_t)(T - 1) * HW * b.ca * es,
+                                   b.ca * es, cs * es, HW, cudaMemcpyDeviceToDevice, stream));
+    }
+    // a3 + a4: H1 = SiLU(GN1(shift(X, carry)))
+    NormArgs n1{xa, xb, carry_in, b.ca, b.cb, cs, T, HW, b.G, b.eps, b.gn1_w, b.gn1_b, h1, gnws};
+    if ((st = gn_silu_run(n1, b.dt, stream)) != DVC_OK) return st;
+    // a5: Y1 = conv3x3(H1) + b1
+    ConvDesc c1{};
+    c1.seg[0] = ConvSeg{h1, cin, SEG_SAME, H, W, 9, b.conv1_w, 9 * cin, 0, cin};
+    c1.nseg = 1;
+    c1.T = T;
+    c1.ho = H;
+    c1.wo = W;
+    c1.cout = b.cout;
+    c1.bias0 = b.conv1_b;
+    c1.out = y1;
+    c1.dt = b.dt;
+    if ((st = conv_run(c1, stream)) != DVC_OK) return st;
+    // a6: H2 = SiLU(GN2(Y1))
+    NormArgs n2{y1, nullptr, nullptr, b.cout, 0, 0, T, HW, b.G, b.eps, b.gn2_w, b.gn2_b, h2, gnws};
+    if ((st = gn_silu_run(n2, b.dt, stream)) != DVC_OK) return st;
+    // a7 + a8: Out = S(X) + conv3x3(H2) + b2; the 1x1 shortcut on the UNSHIFTED X is
+    // extra K segments of the same GEMM (same fp32 accumulator), identity = epilogue add.
+    ConvDesc c2{};
+    c2.seg[0] = ConvSeg{h2, b.cout, SEG_SAME, H, W, 9, b.conv2_w, 9 * b.cout, 0, b.cout};
+    c2.nseg = 1;
+    if (b.sc_w) {
+        c2.seg[c2.nseg++] = ConvSeg{xa, b.ca, SEG_SAME, H, W, 1, b.sc_w, cin, 0, 0};
+        if (b.cb > 0) c2.seg[c2.nseg++] = ConvSeg{xb, b.cb, SEG_SAME, H, W, 1, b.sc_w, cin, b.ca, 0};
+        c2.bias1 = b.sc_b;
+    } else {
+        c2.residual = xa;
+    }
+    c2.T = T;
+    c2.ho = H;
+    c2.wo = W;
+    c2.cout = b.cout;
+    c2.bias0 = b.conv2_b;
+    c2.out = y;
+    c2.dt = b.dt;
+    return conv_run(c2, stream);
+}
+
+static RB rb_from_abi(const dvc_resblock *b) {
+    RB r;
+    r.ca = b->c_a;
+    r.cb = b->c_b;
+    r.cout = b->c_out;
+    r.G = b->groups;
+    r.P = b->shift_p;
+    r.eps = b->eps;
+    r.dt = b->dt;
+    r.gn1_w = b->gn1_w;
+    r.gn1_b = b->gn1_b;
+    r.conv1_w = b->conv1_w;
+    r.conv1_b = b->conv1_b;
+    r.gn2_w = b->gn2_w;
+    r.gn2_b = b->gn2_b;
+    r.conv2_w = b->conv2_w;
+    r.conv2_b = b->conv2_b;
+    r.sc_w = b->sc_w;
+    r.sc_b = b->sc_b;
+    return r;
+}
+
+}  // namespace dvc
+
+using namespace dvc;
+
+extern "C" {
+
+const char *dvc_status_string(dvc_status s) {
+    switch (s) {
+        case DVC_OK: return "DVC_OK";
+        case DVC_ERR_ARG: return "DVC_ERR_ARG";
+        case DVC_ERR_DIVISIBILITY: return "DVC_ERR_DIVISIBILITY";
+        case DVC_ERR_SHAPE: return "DVC_ERR_SHAPE";
+        case DVC_ERR_UNSUPPORTED: return "DVC_ERR_UNSUPPORTED";
+        case DVC_ERR_WORKSPACE: return "DVC_ERR_WORKSPACE";
+        case DVC_ERR_CUDA: return "DVC_ERR_CUDA";
+        case DVC_ERR_NCCL: return "DVC_ERR_NCCL";
+    }
+    return "DVC_ERR_UNKNOWN";
+}
+
+const char *dvc_last_error(void) { return g_err; }
+int dvc_abi_version(void) { return DVC_ABI_VERSION; }
+int dvc_kernel_launch_count(void) { return g_launches; }
+
+dvc_status dvc_device_check(int device) {
+    int cur = 0;
+    DVC_CUDA(cudaGetDevice(&cur));
+    if (device != cur) DVC_CUDA(cudaSetDevice(device));
+    dvc_status st = check_device();
+    if (device != cur) cudaSetDevice(cur);
+    return st;
+}
+
+dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype dt, int T, int H, int W, int s, const void *w_exp,
+                                     const void *b_exp, int c_lat, void *latent, void *stream) {
+    DVC_CHECK_ARG(frames && latent, DVC_ERR_ARG, "null frames/latent");
+    DVC_CHECK_ARG(dt_valid(dt), DVC_ERR_ARG, "bad dtype");
+    DVC_CHECK_ARG(T >= 1 && H >= 1 && W >= 1 && s >= 1, DVC_ERR_ARG, "T, H, W, s must be >= 1");
+    DVC_CHECK_ARG(H % s == 0 && W % s == 0, DVC_ERR_DIVISIBILITY, "H=%d and W=%d must be multiples of s=%d", H, W,
+                  s);
+    DVC_CHECK_ARG((w_exp == nullptr) == (b_exp == nullptr), DVC_ERR_ARG, "w_exp and b_exp go together");
+    dvc_status st = check_device();
+    if (st != DVC_OK) return st;
+    cudaStream_t strm = reinterpret_cast<cudaStream_t>(stream);
+    if (w_exp == nullptr) {
+        DVC_CHECK_ARG(c_lat == 3 * s * s, DVC_ERR_SHAPE, "unshuffle only: c_lat must be 3*s*s=%d", 3 * s * s);
+        return unshuffle_run(frames, dt, T, H, W, s, latent, strm);
+    }
+    DVC_CHECK_ARG(s == 8, DVC_ERR_UNSUPPORTED, "fused expansion needs s == 8");
+    DVC_CHECK_ARG(c_lat >= 16 && c_lat % 16 == 0, DVC_ERR_UNSUPPORTED, "c_lat must be a multiple of 16");
+    ConvDesc d{};
+    d.seg[0] = ConvSeg{frames, 192, SEG_UNSHUFFLE8, H, W, 1, w_exp, 192, 0, 0};
+    d.nseg = 1;
+    d.T = T;
+    d.ho = H / 8;
+    d.wo = W / 8;
+    d.cout = c_lat;
+    d.bias0 = b_exp;
+    d.out = latent;
+    d.dt = dt;
+    return conv_run(d, strm);
+}
+
+dvc_status dvc_resblock_workspace_size(const dvc_resblock *b, int T, int H, int W, size_t *bytes) {
+    DVC_CHECK_ARG(b && bytes, DVC_ERR_ARG, "null argument");
+    RB r = rb_from_abi(b);
+    DVC_CHECK_ARG(r.G >= 1 && r.ca >= 0 && r.cb >= 0 && r.cout >= 0 && T >= 1 && H >= 1 && W >= 1, DVC_ERR_ARG,
+                  "bad sizes");
+    *bytes = resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, H * W, r.dt);
+    return DVC_OK;
+}
+
+dvc_status dvc_resblock_tsm_forward(const dvc_resblock *b, const void *x_a, const void *x_b, int T, int H, int W,
+                                    const void *carry_in, void *carry_out, void *y, void *workspace,
+                                    size_t ws_bytes, void *stream) {
+    DVC_CHECK_ARG(b && x_a && y && workspace, DVC_ERR_ARG, "null argument");
+    RB r = rb_from_abi(b);
+    dvc_status st = resblock_validate(r, T, H, W);
+    if (st != DVC_OK) return st;
+    DVC_CHECK_ARG(r.cb == 0 || x_b != nullptr, DVC_ERR_ARG, "x_b is null but c_b > 0");
+    DVC_CHECK_ARG(ws_bytes >= resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, H * W, r.dt), DVC_ERR_WORKSPACE,
+                  "workspace too small");
+    DVC_CHECK_ARG(((uintptr_t)workspace & 255) == 0, DVC_ERR_ARG, "workspace must be 256-byte aligned");
+    if ((st = check_device()) != DVC_OK) return st;
+    return resblock_launch(r, x_a, r.cb ? x_b : nullptr, T, H, W, carry_in, carry_out, y, workspace,
+                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+dvc_status dvc_debug_shift_gather(const void *x_a, const void *x_b, int c_a, int c_b, int shift_p, dvc_dtype dt,
+                                  int T, int H, int W, const void *carry_in, void *xs, void *stream) {
+    DVC_CHECK_ARG(x_a && xs && (c_b == 0 || x_b), DVC_ERR_ARG, "null argument");
+    DVC_CHECK_ARG(dt_valid(dt) && T >= 1 && H >= 1 && W >= 1 && c_a > 0 && c_b >= 0, DVC_ERR_ARG, "bad sizes");
+    DVC_CHECK_ARG(shift_p >= 1 && (c_a + c_b) % shift_p == 0, DVC_ERR_DIVISIBILITY, "P must divide C");
+    dvc_status st = check_device();
+    if (st != DVC_OK) return st;
+    NormArgs a{x_a, c_b ? x_b : nullptr, carry_in, c_a, c_b, (c_a + c_b) / shift_p, T, H * W, 1, 0.f,
+               nullptr, nullptr, xs, nullptr};
+    return shift_gather_run(a, dt, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

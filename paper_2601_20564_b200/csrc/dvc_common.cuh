@@ -1,0 +1,139 @@
+// dvc_common.cuh -- shared device/host helpers of libdvc (product path only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstddef>
+#include "../../include/dvc.h"
+
+namespace dvc {
+
+// ----------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+extern int g_launches;   // kernels launched through launch helpers (bookkeeping for bench)
+
+#define DVC_CHECK_ARG(cond, code, ...)        \
+    do {                                      \
+        if (!(cond)) {                        \
+            ::dvc::set_error(__VA_ARGS__);    \
+            return code;                      \
+        }                                     \
+    } while (0)
+
+#define DVC_CUDA(call)                                                              \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess) {                                                    \
+            ::dvc::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,             \
+                             cudaGetErrorString(e_));                               \
+            return DVC_ERR_CUDA;                                                    \
+        }                                                                           \
+    } while (0)
+
+// Returns DVC_ERR_CUDA if a previous asynchronous launch failed (sticky or not).
+dvc_status check_launch(const char *what);
+dvc_status check_device();   // cached: current device must be sm_100
+
+inline size_t dt_size(dvc_dtype dt) { return dt == DVC_F32 ? 4 : 2; }
+inline bool dt_valid(dvc_dtype dt) { return dt == DVC_BF16 || dt == DVC_F16 || dt == DVC_F32; }
+
+// ----------------------------------------------------------------- element conversion
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+    static __device__ __forceinline__ float to_f(float v) { return v; }
+    static __device__ __forceinline__ float from_f(float v) { return v; }
+};
+template <> struct Elem<__half> {
+    static __device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
+    static __device__ __forceinline__ __half from_f(float v) { return __float2half_rn(v); }
+};
+template <> struct Elem<__nv_bfloat16> {
+    static __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+    static __device__ __forceinline__ __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+};
+
+// 8 consecutive elements as one vector unit (16 B for 16-bit types, 32 B for fp32).
+template <typename T>
+struct alignas(16) Vec8 {
+    T v[8];
+};
+
+template <typename T>
+__device__ __forceinline__ void load8(const T *p, float (&f)[8]) {
+    Vec8<T> u;
+    if constexpr (sizeof(T) == 2) {
+        *reinterpret_cast<uint4 *>(&u) = __ldg(reinterpret_cast<const uint4 *>(p));
+    } else {
+        reinterpret_cast<float4 *>(&u)[0] = __ldg(reinterpret_cast<const float4 *>(p));
+        reinterpret_cast<float4 *>(&u)[1] = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = Elem<T>::to_f(u.v[i]);
+}
+
+template <typename T>
+__device__ __forceinline__ void store8(T *p, const float (&f)[8]) {
+    Vec8<T> u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u.v[i] = Elem<T>::from_f(f[i]);
+    if constexpr (sizeof(T) == 2) {
+        *reinterpret_cast<uint4 *>(p) = *reinterpret_cast<uint4 *>(&u);
+    } else {
+        reinterpret_cast<float4 *>(p)[0] = reinterpret_cast<float4 *>(&u)[0];
+        reinterpret_cast<float4 *>(p)[1] = reinterpret_cast<float4 *>(&u)[1];
+    }
+}
+
+__device__ __forceinline__ float silu_f(float z) { return z / (1.0f + __expf(-z)); }
+
+inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
+
+// ----------------------------------------------------------------- shifted-operand addressing (a3)
+// One ResBlock input X = concat(xa[ca], xb[cb]) over frames [T][HW].  The
+// Batch-dimension temporal shift is pure addressing:
+//   Xs[t][p][c] = c < cs ? (t > 0 ? X[t-1][p][c] : carry[p][c] (0 if null)) : X[t][p][c]
+// used identically by the GN statistics, the GN/SiLU operand producer and the
+// test-only gather.
+template <typename T>
+struct ShiftSrc {
+    const T *xa, *xb, *carry;
+    int ca, cb, cs;   // cs = C_in / P (0 = no shift)
+    int HW;
+
+    __device__ __forceinline__ int C() const { return ca + cb; }
+
+    // raw (unshifted) 8-vector X[t][p][c..c+7]; c % 8 == 0 and ca % 8 == 0
+    __device__ __forceinline__ void raw8(int t, int p, int c, float (&f)[8]) const {
+        if (c < ca) load8(xa + ((size_t)t * HW + p) * ca + c, f);
+        else load8(xb + ((size_t)t * HW + p) * cb + (c - ca), f);
+    }
+    // shifted-slice source for the same channels: frame t-1 or the carry
+    __device__ __forceinline__ void prev8(int t, int p, int c, float (&f)[8]) const {
+        if (t > 0) { raw8(t - 1, p, c, f); return; }
+        if (carry == nullptr) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = 0.f;
+            return;
+        }
+        // carry is [HW][cs]; cs may not be a multiple of 8: per element
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            int cc = c + i;
+            f[i] = cc < cs ? Elem<T>::to_f(carry[(size_t)p * cs + cc]) : 0.f;
+        }
+    }
+    __device__ __forceinline__ void shifted8(int t, int p, int c, float (&f)[8]) const {
+        if (c + 8 <= cs) { prev8(t, p, c, f); return; }
+        raw8(t, p, c, f);
+        if (c < cs) {   // vector straddles the slice boundary
+            float g[8];
+            prev8(t, p, c, g);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (c + i < cs) f[i] = g[i];
+        }
+    }
+};
+
+}  // namespace dvc

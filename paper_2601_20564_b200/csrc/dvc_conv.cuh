@@ -1,0 +1,71 @@
+// dvc_conv.cuh -- one description of "a convolution of the hot path", executed
+// either by the tcgen05 implicit-GEMM engine (16-bit) or the fp32 SIMT engine
+// (DVC_F32 validation mode).
+//
+// A convolution is a sum of K segments.  Segment s contributes
+//   sum_{tap} sum_{c < c_src} W_s[n][col0 + tap*tapstride + c] * A_s(m, tap, c)
+// where A_s is an activation gathered from `src` by an addressing mode:
+//   SEG_SAME      3x3 pad 1 (taps=9) or 1x1 (taps=1) at the output resolution
+//   SEG_STRIDE2   3x3 stride 2 pad 1 (down-sampler glue, R11)
+//   SEG_UPNEAREST 3x3 pad 1 over nearest_to(src, ho, wo) (up-sampler glue, R11)
+//   SEG_UNSHUFFLE8 1x1 over PixelUnshuffle(frames, 8) (a1 fused into a2, R12)
+// Output row m = (t*ho + y)*wo + x; out[m][n] = bias0[n] (+bias1[n]) + sum + residual[m][n].
+#pragma once
+#include "dvc_common.cuh"
+
+namespace dvc {
+
+enum SegMode { SEG_SAME = 0, SEG_STRIDE2 = 1, SEG_UPNEAREST = 2, SEG_UNSHUFFLE8 = 3 };
+
+struct ConvSeg {
+    const void *src;   // activations [T][hi][wi][c_src] (or frames [T][3][8ho][8wo])
+    int c_src;         // channels per src pixel (row stride in elements)
+    int mode;          // SegMode
+    int hi, wi;        // src spatial dims
+    int taps;          // 9 or 1
+    const void *w;     // weights as a 2D [cout][w_ld] matrix
+    int w_ld;          // row length of w (elements)
+    int w_col0;        // first column of this segment
+    int w_tapstride;   // columns between taps
+};
+
+struct ConvDesc {
+    ConvSeg seg[4];
+    int nseg;
+    int T, ho, wo, cout;
+    const void *bias0, *bias1;   // [cout] or null
+    const void *residual;        // [M][cout] or null
+    void *out;                   // [M][cout]
+    dvc_dtype dt;
+    long M() const { return (long)T * ho * wo; }
+};
+
+// Validates the descriptor for the given engine; returns DVC_OK or an error.
+dvc_status conv_check(const ConvDesc &d, bool tensor_core);
+// Launches (no host sync).  16-bit: tcgen05 engine; F32: SIMT engine.
+dvc_status conv_run(const ConvDesc &d, cudaStream_t stream);
+dvc_status conv_tc_run(const ConvDesc &d, cudaStream_t stream);
+dvc_status conv_simt_run(const ConvDesc &d, cudaStream_t stream);
+
+// Row-address helper shared by both engines: source pixel index of output
+// pixel (t, y, x) for tap (dy, dx), or -1 when the tap falls in the zero padding.
+__device__ __forceinline__ long seg_src_pixel(const ConvSeg &s, int ho, int wo, int t, int y, int x,
+                                              int dy, int dx) {
+    int iy, ix;
+    if (s.mode == SEG_STRIDE2) {
+        iy = 2 * y + dy;
+        ix = 2 * x + dx;
+    } else if (s.mode == SEG_UPNEAREST) {
+        int uy = y + dy, ux = x + dx;
+        if (uy < 0 || uy >= ho || ux < 0 || ux >= wo) return -1;
+        iy = (int)(((long)uy * s.hi) / ho);
+        ix = (int)(((long)ux * s.wi) / wo);
+    } else {
+        iy = y + dy;
+        ix = x + dx;
+    }
+    if (iy < 0 || iy >= s.hi || ix < 0 || ix >= s.wi) return -1;
+    return ((long)t * s.hi + iy) * s.wi + ix;
+}
+
+}  // namespace dvc

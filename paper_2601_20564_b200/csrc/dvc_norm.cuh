@@ -1,0 +1,27 @@
+#pragma once
+#include "dvc_common.cuh"
+
+namespace dvc {
+
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// One GroupNorm(+SiLU) application over the (optionally shifted) operand
+// X = concat(xa[ca], xb[cb]) of T frames x HW pixels.
+struct NormArgs {
+    const void *xa, *xb, *carry;
+    int ca, cb, cs;          // cs = shifted slice width (0 = no shift)
+    int T, HW, G;
+    float eps;
+    const void *gamma, *beta;
+    void *out;               // [T][HW][ca+cb]
+    void *ws;                // gn_workspace_bytes(T, HW, G)
+};
+
+size_t gn_workspace_bytes(int T, int HW, int G);
+dvc_status gn_silu_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream);
+dvc_status shift_gather_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream);
+
+dvc_status unshuffle_run(const void *frames, dvc_dtype dt, int T, int H, int W, int s, void *latent,
+                         cudaStream_t stream);
+
+}  // namespace dvc

@@ -1,0 +1,491 @@
+// dvc_unet.cu -- a9/a10/e: the pruned U-Net ResBlock skeleton over a group of
+// frames (reading R1, R11) and the multi-GPU halo.
+//
+// Topology (the product's own statement of reading R1; SD-2.1-base U-Net with
+// widths x0.75, 2 ResBlocks per down level, 3 per up level, 2 mid):
+//   conv_in(concat(Lbar, Cm)) -> x0 (push)
+//   level l = 0..3: 2 ResBlocks (push each); l < 3: 3x3 stride-2 conv (push)
+//   mid: 2 ResBlocks
+//   up u = 0..3 (level 3-u): 3 ResBlocks on concat(h, pop()); u < 3: nearest
+//   resize to the next skip's size + 3x3 conv
+//   out = conv_out(SiLU(GN_out(h)))
+// Multi-GPU: a chain's frames are split into contiguous chunks, one
+// per rank; before ResBlock k, rank r sends the C_in/P-channel slice of its
+// last frame's block input to rank r+1 and receives rank r-1's (NCCL P2P on
+// the compute stream).  Weights are replicated.
+#include <dlfcn.h>
+#include <nccl.h>
+#include <cstring>
+#include <vector>
+#include "dvc_conv.cuh"
+#include "dvc_norm.cuh"
+#include "dvc_resblock.cuh"
+
+using namespace dvc;
+
+// ----------------------------------------------------------------- NCCL (dlopen'd)
+namespace {
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        // prefer the copy already loaded in the process (torch's), then the system one
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+            api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+            api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
+                     api.GroupStart && api.GroupEnd;
+        }
+    }
+    return api;
+}
+
+#define DVC_NCCL(call)                                                                                   \
+    do {                                                                                                 \
+        ncclResult_t r_ = (call);                                                                        \
+        if (r_ != ncclSuccess) {                                                                         \
+            set_error("%s: NCCL error %d (%s)", #call, (int)r_,                                         \
+                      nccl().GetErrorString ? nccl().GetErrorString(r_) : "?");                          \
+            return DVC_ERR_NCCL;                                                                         \
+        }                                                                                                \
+    } while (0)
+}  // namespace
+
+struct dvc_comm {
+    ncclComm_t comm;
+    int rank, world;
+};
+
+// ----------------------------------------------------------------- the network
+struct ConvW {
+    const void *w, *b;
+};
+
+struct dvc_unet {
+    dvc_unet_config cfg;
+    void *dweights = nullptr;
+    size_t welems = 0;
+    ConvW conv_in, ds[3], us[3], conv_out;
+    const void *gno_w = nullptr, *gno_b = nullptr;
+    RB blk[22];
+    int blevel[22];
+    int lh[4], lw[4];
+    size_t carry_off[22];
+    size_t carry_total = 0;
+};
+
+namespace {
+
+// Walks the topology; for every tensor calls take(elements) which returns its
+// device pointer.  Also fills the block table.
+template <typename Take>
+void walk(dvc_unet &n, Take take) {
+    const dvc_unet_config &c = n.cfg;
+    const int *W = c.width;
+    auto conv = [&](int cout, int cin, int k) {
+        ConvW cw;
+        cw.w = take((size_t)cout * k * k * cin);
+        cw.b = take((size_t)cout);
+        return cw;
+    };
+    int bi = 0;
+    auto block = [&](int cin, int cout, int level, int cb) {
+        RB &r = n.blk[bi];
+        r.ca = cin - cb;
+        r.cb = cb;
+        r.cout = cout;
+        r.G = c.groups;
+        r.P = c.shift_p;
+        r.eps = c.eps;
+        r.dt = c.dt;
+        r.gn1_w = take(cin);
+        r.gn1_b = take(cin);
+        r.conv1_w = take((size_t)cout * 9 * cin);
+        r.conv1_b = take(cout);
+        r.gn2_w = take(cout);
+        r.gn2_b = take(cout);
+        r.conv2_w = take((size_t)cout * 9 * cout);
+        r.conv2_b = take(cout);
+        if (cin != cout) {
+            r.sc_w = take((size_t)cout * cin);
+            r.sc_b = take(cout);
+        } else {
+            r.sc_w = r.sc_b = nullptr;
+        }
+        n.blevel[bi] = level;
+        ++bi;
+    };
+    n.conv_in = conv(W[0], c.c_lat + c.c_ctx, 3);
+    std::vector<int> skips{W[0]};
+    int cur = W[0];
+    for (int l = 0; l < 4; ++l) {
+        for (int r = 0; r < 2; ++r) {
+            block(cur, W[l], l, 0);
+            cur = W[l];
+            skips.push_back(cur);
+        }
+        if (l < 3) {
+            n.ds[l] = conv(cur, cur, 3);
+            skips.push_back(cur);
+        }
+    }
+    for (int r = 0; r < 2; ++r) block(cur, cur, 3, 0);
+    for (int u = 0; u < 4; ++u) {
+        const int l = 3 - u;
+        for (int r = 0; r < 3; ++r) {
+            const int sk = skips.back();
+            skips.pop_back();
+            block(cur + sk, W[l], l, sk);
+            cur = W[l];
+        }
+        if (u < 3) n.us[u] = conv(cur, cur, 3);
+    }
+    n.gno_w = take(cur);
+    n.gno_b = take(cur);
+    n.conv_out = conv(c.c_lat, cur, 3);
+}
+
+dvc_status validate_cfg(const dvc_unet_config *c) {
+    DVC_CHECK_ARG(c, DVC_ERR_ARG, "null config");
+    DVC_CHECK_ARG(dt_valid(c->dt), DVC_ERR_ARG, "bad dtype");
+    DVC_CHECK_ARG(c->h >= 8 && c->w >= 8 && c->max_T >= 1 && c->max_T < 256, DVC_ERR_ARG,
+                  "latent size >= 8x8 and 1 <= max_T < 256 required");
+    DVC_CHECK_ARG(c->groups >= 1 && c->shift_p >= 1 && c->c_lat > 0 && c->c_ctx > 0, DVC_ERR_ARG, "bad config");
+    for (int i = 0; i < 4; ++i) DVC_CHECK_ARG(c->width[i] > 0, DVC_ERR_ARG, "bad width");
+    return DVC_OK;
+}
+
+size_t plan_workspace(const dvc_unet &n, int T, size_t *offs /* 16 regions */) {
+    // regions: 0..11 skips, 12,13 ping-pong h, 14 ResBlock scratch (also GN_out operand), 15 halo send/recv
+    const dvc_unet_config &c = n.cfg;
+    const size_t es = dt_size(c.dt);
+    const int *W = c.width;
+    size_t sz[16] = {};
+    auto hw = [&](int l) { return (size_t)n.lh[l] * n.lw[l]; };
+    int k = 0;
+    sz[k++] = T * hw(0) * W[0];
+    for (int l = 0; l < 4; ++l) {
+        sz[k++] = T * hw(l) * W[l];
+        sz[k++] = T * hw(l) * W[l];
+        if (l < 3) sz[k++] = T * hw(l + 1) * W[l];
+    }
+    size_t hmax = 0;
+    for (int l = 0; l < 4; ++l) hmax = std::max(hmax, T * hw(l) * (size_t)W[l]);
+    for (int l = 1; l < 4; ++l) hmax = std::max(hmax, T * hw(l - 1) * (size_t)W[l]);
+    hmax = std::max(hmax, T * hw(0) * (size_t)c.c_lat);
+    sz[12] = sz[13] = hmax;
+    size_t rbws = 0;
+    for (int b = 0; b < 22; ++b) {
+        const RB &r = n.blk[b];
+        const int l = n.blevel[b];
+        rbws = std::max(rbws, resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, (int)hw(l), c.dt));
+    }
+    rbws = std::max(rbws, align256(gn_workspace_bytes(T, (int)hw(0), c.groups)) + T * hw(0) * W[0] * es);
+    size_t total = 0;
+    for (int i = 0; i < 16; ++i) {
+        size_t bytes = i == 14 ? rbws : i == 15 ? (n.carry_total * 2 + 2 * hw(0) * 2048) * es : sz[i] * es;
+        offs[i] = total;
+        total += align256(bytes);
+    }
+    return total;
+}
+
+}  // namespace
+
+extern "C" {
+
+dvc_status dvc_comm_unique_id(void *id128) {
+    DVC_CHECK_ARG(id128, DVC_ERR_ARG, "null id");
+    DVC_CHECK_ARG(nccl().ok, DVC_ERR_NCCL, "libnccl.so.2 not found");
+    ncclUniqueId id;
+    DVC_NCCL(nccl().GetUniqueId(&id));
+    memcpy(id128, &id, sizeof(id));
+    return DVC_OK;
+}
+
+dvc_status dvc_comm_create(int rank, int world, const void *id128, dvc_comm **out) {
+    DVC_CHECK_ARG(out && id128 && world >= 1 && rank >= 0 && rank < world, DVC_ERR_ARG, "bad comm arguments");
+    DVC_CHECK_ARG(nccl().ok, DVC_ERR_NCCL, "libnccl.so.2 not found");
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    dvc_comm *c = new dvc_comm{nullptr, rank, world};
+    ncclResult_t r = nccl().CommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        set_error("ncclCommInitRank failed: %d", (int)r);
+        return DVC_ERR_NCCL;
+    }
+    *out = c;
+    return DVC_OK;
+}
+
+dvc_status dvc_comm_destroy(dvc_comm *c) {
+    if (!c) return DVC_OK;
+    if (c->comm) nccl().CommDestroy(c->comm);
+    delete c;
+    return DVC_OK;
+}
+
+dvc_status dvc_unet_weight_count(const dvc_unet_config *cfg, size_t *elems) {
+    dvc_status st = validate_cfg(cfg);
+    if (st != DVC_OK) return st;
+    DVC_CHECK_ARG(elems, DVC_ERR_ARG, "null elems");
+    dvc_unet tmp;
+    tmp.cfg = *cfg;
+    size_t n = 0;
+    walk(tmp, [&](size_t e) -> const void * {
+        n += e;
+        return nullptr;
+    });
+    *elems = n;
+    return DVC_OK;
+}
+
+dvc_status dvc_unet_create(const dvc_unet_config *cfg, const void *host_weights, size_t bytes, dvc_unet **out) {
+    dvc_status st = validate_cfg(cfg);
+    if (st != DVC_OK) return st;
+    DVC_CHECK_ARG(host_weights && out, DVC_ERR_ARG, "null argument");
+    if ((st = check_device()) != DVC_OK) return st;
+    size_t elems = 0;
+    dvc_unet_weight_count(cfg, &elems);
+    const size_t es = dt_size(cfg->dt);
+    DVC_CHECK_ARG(bytes == elems * es, DVC_ERR_SHAPE, "weight blob has %zu bytes, config expects %zu", bytes,
+                  elems * es);
+    dvc_unet *n = new dvc_unet();
+    n->cfg = *cfg;
+    n->lh[0] = cfg->h;
+    n->lw[0] = cfg->w;
+    for (int l = 1; l < 4; ++l) {   // 3x3 stride 2 pad 1: ceil halving (R11)
+        n->lh[l] = (n->lh[l - 1] - 1) / 2 + 1;
+        n->lw[l] = (n->lw[l - 1] - 1) / 2 + 1;
+    }
+    // each tensor gets a 16-byte aligned slot in one device allocation
+    size_t dev_bytes = 0;
+    walk(*n, [&](size_t e) -> const void * {
+        dev_bytes += (e * es + 255) & ~size_t(255);
+        return nullptr;
+    });
+    if (cudaMalloc(&n->dweights, dev_bytes) != cudaSuccess) {
+        delete n;
+        set_error("cudaMalloc of %zu weight bytes failed", dev_bytes);
+        return DVC_ERR_CUDA;
+    }
+    size_t src_off = 0, dst_off = 0;
+    cudaError_t err = cudaSuccess;
+    walk(*n, [&](size_t e) -> const void * {
+        uint8_t *dst = reinterpret_cast<uint8_t *>(n->dweights) + dst_off;
+        if (err == cudaSuccess)
+            err = cudaMemcpy(dst, reinterpret_cast<const uint8_t *>(host_weights) + src_off, e * es,
+                             cudaMemcpyHostToDevice);
+        src_off += e * es;
+        dst_off += (e * es + 255) & ~size_t(255);
+        return dst;
+    });
+    if (err != cudaSuccess) {
+        cudaFree(n->dweights);
+        delete n;
+        set_error("weight upload failed: %s", cudaGetErrorString(err));
+        return DVC_ERR_CUDA;
+    }
+    for (int b = 0; b < 22; ++b) {
+        const RB &r = n->blk[b];
+        const int l = n->blevel[b];
+        st = resblock_validate(r, 1, n->lh[l], n->lw[l]);
+        if (st != DVC_OK) {
+            cudaFree(n->dweights);
+            delete n;
+            return st;
+        }
+        n->carry_off[b] = n->carry_total;
+        n->carry_total += (size_t)n->lh[l] * n->lw[l] * ((r.ca + r.cb) / r.P);
+    }
+    n->welems = elems;
+    *out = n;
+    return DVC_OK;
+}
+
+dvc_status dvc_unet_destroy(dvc_unet *n) {
+    if (!n) return DVC_OK;
+    cudaFree(n->dweights);
+    delete n;
+    return DVC_OK;
+}
+
+dvc_status dvc_unet_carry_size(const dvc_unet *n, size_t *elems) {
+    DVC_CHECK_ARG(n && elems, DVC_ERR_ARG, "null argument");
+    *elems = n->carry_total;
+    return DVC_OK;
+}
+
+dvc_status dvc_unet_workspace_size(const dvc_unet *n, int T, size_t *bytes) {
+    DVC_CHECK_ARG(n && bytes && T >= 1 && T <= n->cfg.max_T, DVC_ERR_ARG, "bad arguments (1 <= T <= max_T)");
+    size_t offs[16];
+    *bytes = plan_workspace(*n, T, offs);
+    return DVC_OK;
+}
+
+dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, const void *ctx, int T,
+                               const void *carry_in, void *carry_out, void *out, void *workspace, size_t ws_bytes,
+                               void *stream) {
+    DVC_CHECK_ARG(n && lat && ctx && out && workspace, DVC_ERR_ARG, "null argument");
+    DVC_CHECK_ARG(T >= 1 && T <= n->cfg.max_T, DVC_ERR_ARG, "T_local=%d outside [1, max_T=%d]", T, n->cfg.max_T);
+    DVC_CHECK_ARG(((uintptr_t)workspace & 255) == 0, DVC_ERR_ARG, "workspace must be 256-byte aligned");
+    size_t offs[16];
+    const size_t need = plan_workspace(*n, T, offs);
+    DVC_CHECK_ARG(ws_bytes >= need, DVC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
+    const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
+    if (world > 1) DVC_CHECK_ARG(nccl().ok, DVC_ERR_NCCL, "NCCL unavailable");
+    dvc_status st = check_device();
+    if (st != DVC_OK) return st;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const dvc_unet_config &c = n->cfg;
+    const dvc_dtype dt = c.dt;
+    const size_t es = dt_size(dt);
+    const int *W = c.width;
+    uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
+    void *skip[12];
+    for (int i = 0; i < 12; ++i) skip[i] = ws + offs[i];
+    void *hb[2] = {ws + offs[12], ws + offs[13]};
+    void *rbws = ws + offs[14];
+    uint8_t *halo = ws + offs[15];
+    uint8_t *recv = halo;                                    // packed received carries
+    uint8_t *sendb = halo + align256(n->carry_total * es);   // one slice staging buffer
+    auto hw = [&](int l) { return n->lh[l] * n->lw[l]; };
+
+    int bi = 0;
+    // one ResBlock with its halo exchange
+    auto run_block = [&](const void *xa, const void *xb, void *y) -> dvc_status {
+        const RB &r = n->blk[bi];
+        const int l = n->blevel[bi];
+        const int H = n->lh[l], Wd = n->lw[l];
+        const int cs = (r.ca + r.cb) / r.P;
+        const size_t off = n->carry_off[bi] * es;
+        const void *cin_ptr = carry_in ? reinterpret_cast<const uint8_t *>(carry_in) + off : nullptr;
+        if (world > 1) {
+            NcclApi &api = nccl();
+            if (rank < world - 1)
+                DVC_CUDA(cudaMemcpy2DAsync(sendb, cs * es,
+                                           reinterpret_cast<const uint8_t *>(xa) + (size_t)(T - 1) * H * Wd * r.ca * es,
+                                           r.ca * es, cs * es, (size_t)H * Wd, cudaMemcpyDeviceToDevice, s));
+            DVC_NCCL(api.GroupStart());
+            const ncclDataType_t ty = dt == DVC_F32 ? ncclFloat32 : dt == DVC_F16 ? ncclFloat16 : ncclBfloat16;
+            if (rank < world - 1) DVC_NCCL(api.Send(sendb, (size_t)H * Wd * cs, ty, rank + 1, comm->comm, s));
+            if (rank > 0) DVC_NCCL(api.Recv(recv + off, (size_t)H * Wd * cs, ty, rank - 1, comm->comm, s));
+            DVC_NCCL(api.GroupEnd());
+            if (rank > 0) cin_ptr = recv + off;
+        }
+        void *cout_ptr = nullptr;
+        if (carry_out && (world == 1 || rank == world - 1)) cout_ptr = reinterpret_cast<uint8_t *>(carry_out) + off;
+        dvc_status e = resblock_launch(r, xa, xb, T, H, Wd, cin_ptr, cout_ptr, y, rbws, s);
+        ++bi;
+        return e;
+    };
+    auto conv3 = [&](const void *src, int cin, int mode, int hi, int wi, const ConvW &cw, int cout, int ho, int wo,
+                     void *dst) {
+        ConvDesc d{};
+        d.seg[0] = ConvSeg{src, cin, mode, hi, wi, 9, cw.w, 9 * cin, 0, cin};
+        d.nseg = 1;
+        d.T = T;
+        d.ho = ho;
+        d.wo = wo;
+        d.cout = cout;
+        d.bias0 = cw.b;
+        d.out = dst;
+        d.dt = dt;
+        return conv_run(d, s);
+    };
+
+    // conv_in on concat(Lbar, Cm): two K segments, no materialised concat
+    {
+        ConvDesc d{};
+        const int cc = c.c_lat + c.c_ctx;
+        d.seg[0] = ConvSeg{lat, c.c_lat, SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_in.w, 9 * cc, 0, cc};
+        d.seg[1] = ConvSeg{ctx, c.c_ctx, SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_in.w, 9 * cc, c.c_lat, cc};
+        d.nseg = 2;
+        d.T = T;
+        d.ho = n->lh[0];
+        d.wo = n->lw[0];
+        d.cout = W[0];
+        d.bias0 = n->conv_in.b;
+        d.out = skip[0];
+        d.dt = dt;
+        if ((st = conv_run(d, s)) != DVC_OK) return st;
+    }
+    int k = 1;
+    const void *h = skip[0];
+    for (int l = 0; l < 4; ++l) {
+        for (int r = 0; r < 2; ++r) {
+            if ((st = run_block(h, nullptr, skip[k])) != DVC_OK) return st;
+            h = skip[k++];
+        }
+        if (l < 3) {
+            if ((st = conv3(h, W[l], SEG_STRIDE2, n->lh[l], n->lw[l], n->ds[l], W[l], n->lh[l + 1], n->lw[l + 1],
+                            skip[k])) != DVC_OK)
+                return st;
+            h = skip[k++];
+        }
+    }
+    int pp = 0;
+    for (int r = 0; r < 2; ++r) {
+        if ((st = run_block(h, nullptr, hb[pp])) != DVC_OK) return st;
+        h = hb[pp];
+        pp ^= 1;
+    }
+    for (int u = 0; u < 4; ++u) {
+        const int l = 3 - u;
+        for (int r = 0; r < 3; ++r) {
+            if ((st = run_block(h, skip[--k], hb[pp])) != DVC_OK) return st;
+            h = hb[pp];
+            pp ^= 1;
+        }
+        if (u < 3) {
+            if ((st = conv3(h, W[l], SEG_UPNEAREST, n->lh[l], n->lw[l], n->us[u], W[l], n->lh[l - 1], n->lw[l - 1],
+                            hb[pp])) != DVC_OK)
+                return st;
+            h = hb[pp];
+            pp ^= 1;
+        }
+    }
+    // out = conv_out(SiLU(GN_out(h)))
+    {
+        uint8_t *gnws = reinterpret_cast<uint8_t *>(rbws);
+        void *op = gnws + align256(gn_workspace_bytes(T, hw(0), c.groups));
+        NormArgs na{h, nullptr, nullptr, W[0], 0, 0, T, hw(0), c.groups, c.eps, n->gno_w, n->gno_b, op, gnws};
+        if ((st = gn_silu_run(na, dt, s)) != DVC_OK) return st;
+        if ((st = conv3(op, W[0], SEG_SAME, n->lh[0], n->lw[0], n->conv_out, c.c_lat, n->lh[0], n->lw[0], out)) !=
+            DVC_OK)
+            return st;
+    }
+    if (world > 1 && nccl().CommGetAsyncError) {
+        ncclResult_t ar = ncclSuccess;
+        nccl().CommGetAsyncError(comm->comm, &ar);
+        DVC_CHECK_ARG(ar == ncclSuccess || ar == ncclInProgress, DVC_ERR_NCCL, "NCCL async error %d", (int)ar);
+    }
+    return DVC_OK;
+}
+
+}  // extern "C"

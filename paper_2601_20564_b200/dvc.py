@@ -1,0 +1,204 @@
+"""Python binding of the C-ABI with the same names (include/dvc.h).
+
+Only argument marshalling: torch tensors are used for device memory and the
+current CUDA stream; every step of the hot path runs in libdvc.so's kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import DVC_BF16, DVC_F16, DVC_F32, DvcError, check, lib  # noqa: F401
+
+_DT = {torch.bfloat16: DVC_BF16, torch.float16: DVC_F16, torch.float32: DVC_F32}
+
+lib()   # load libdvc.so now: a missing native library is an ImportError, never a silent fallback
+
+
+def dtype_code(t: torch.dtype) -> int:
+    if t not in _DT:
+        raise TypeError(f"unsupported dtype {t}")
+    return _DT[t]
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libdvc takes device tensors")
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def device_check(device: int = 0) -> None:
+    check(lib().dvc_device_check(device))
+
+
+def launch_count() -> int:
+    return lib().dvc_kernel_launch_count()
+
+
+# ------------------------------------------------------------------ a1 + a2
+def dvc_encode_pixelunshuffle(frames: torch.Tensor, w_exp=None, b_exp=None, s: int = 8, out=None, stream=None):
+    """frames [T,3,H,W] -> latent [T,H/s,W/s,c_lat] (c_lat = 3 s^2 without expansion)."""
+    T, C, H, W = frames.shape
+    if C != 3:
+        raise ValueError("frames must be [T,3,H,W]")
+    c_lat = 3 * s * s if w_exp is None else w_exp.shape[0]
+    if out is None:
+        out = torch.empty((T, H // s, W // s, c_lat), dtype=frames.dtype, device=frames.device)
+    check(lib().dvc_encode_pixelunshuffle(_ptr(frames), dtype_code(frames.dtype), T, H, W, s, _ptr(w_exp),
+                                          _ptr(b_exp), c_lat, _ptr(out), _stream(stream)))
+    return out
+
+
+# ------------------------------------------------------------------ a3-a8
+class ResBlockParams:
+    """Device-side parameters of one OTSM ResBlock (keeps the tensors alive)."""
+
+    KEYS = ("gn1_w", "gn1_b", "conv1_w", "conv1_b", "gn2_w", "gn2_b", "conv2_w", "conv2_b", "sc_w", "sc_b")
+
+    def __init__(self, tensors: dict, c_a: int, c_b: int, groups: int, shift_p: int, eps: float = 1e-5):
+        self.t = {k: (None if tensors.get(k) is None else tensors[k].contiguous()) for k in self.KEYS}
+        w1 = self.t["conv1_w"]
+        dt = w1.dtype
+        self.c_out = w1.shape[0]
+        self.struct = _lib.dvc_resblock(c_a, c_b, self.c_out, groups, shift_p, eps, dtype_code(dt),
+                                        *[None if self.t[k] is None else self.t[k].data_ptr() for k in self.KEYS])
+        self.c_a, self.c_b = c_a, c_b
+
+    def workspace_size(self, T, H, W) -> int:
+        n = ctypes.c_size_t()
+        check(lib().dvc_resblock_workspace_size(ctypes.byref(self.struct), T, H, W, ctypes.byref(n)))
+        return n.value
+
+
+def dvc_resblock_tsm_forward(params: ResBlockParams, x_a, x_b=None, carry_in=None, carry_out=None, out=None,
+                             workspace=None, stream=None):
+    T, H, W, _ = x_a.shape
+    if out is None:
+        out = torch.empty((T, H, W, params.c_out), dtype=x_a.dtype, device=x_a.device)
+    ws = params.workspace_size(T, H, W)
+    if workspace is None:
+        workspace = _ws(ws, x_a.device)
+    check(lib().dvc_resblock_tsm_forward(ctypes.byref(params.struct), _ptr(x_a), _ptr(x_b), T, H, W,
+                                         _ptr(carry_in), _ptr(carry_out), _ptr(out), _ptr(workspace),
+                                         workspace.numel() * workspace.element_size(), _stream(stream)))
+    return out
+
+
+def dvc_debug_shift_gather(x_a, x_b=None, shift_p: int = 8, carry_in=None, out=None, stream=None):
+    T, H, W, ca = x_a.shape
+    cb = 0 if x_b is None else x_b.shape[-1]
+    if out is None:
+        out = torch.empty((T, H, W, ca + cb), dtype=x_a.dtype, device=x_a.device)
+    check(lib().dvc_debug_shift_gather(_ptr(x_a), _ptr(x_b), ca, cb, shift_p, dtype_code(x_a.dtype), T, H, W,
+                                       _ptr(carry_in), _ptr(out), _stream(stream)))
+    return out
+
+
+# ------------------------------------------------------------------ a9 + a10 + e
+def unet_config(width=(240, 480, 960, 960), c_lat=256, c_ctx=256, groups=24, shift_p=8, eps=1e-5,
+                dtype=torch.bfloat16, h=90, w=160, max_T=32):
+    return _lib.dvc_unet_config((ctypes.c_int * 4)(*width), c_lat, c_ctx, groups, shift_p, eps,
+                                dtype_code(dtype), h, w, max_T)
+
+
+def unet_weight_count(cfg) -> int:
+    n = ctypes.c_size_t()
+    check(lib().dvc_unet_weight_count(ctypes.byref(cfg), ctypes.byref(n)))
+    return n.value
+
+
+class Comm:
+    """NCCL halo communicator; the 128-byte unique id travels over torch.distributed."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        idt = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf = (ctypes.c_uint8 * 128)()
+            check(lib().dvc_comm_unique_id(buf))
+            idt = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if dist.is_initialized() and world > 1:
+            dev = idt.cuda() if dist.get_backend(group) == "nccl" else idt
+            dist.broadcast(dev, 0, group=group)
+            idt = dev.cpu()
+        raw = (ctypes.c_uint8 * 128)(*idt.tolist())
+        self.handle = ctypes.c_void_p()
+        check(lib().dvc_comm_create(rank, world, raw, ctypes.byref(self.handle)))
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.handle:
+            lib().dvc_comm_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class UNet:
+    """Handle of the device-resident skeleton (dvc_unet_create)."""
+
+    def __init__(self, cfg, host_blob: torch.Tensor):
+        if host_blob.is_cuda:
+            raise ValueError("the weight blob is host memory")
+        self.cfg = cfg
+        blob = host_blob.contiguous()
+        self.handle = ctypes.c_void_p()
+        check(lib().dvc_unet_create(ctypes.byref(cfg), ctypes.c_void_p(blob.data_ptr()),
+                                    blob.numel() * blob.element_size(), ctypes.byref(self.handle)))
+        n = ctypes.c_size_t()
+        check(lib().dvc_unet_carry_size(self.handle, ctypes.byref(n)))
+        self.carry_elems = n.value
+
+    def workspace_size(self, T: int) -> int:
+        n = ctypes.c_size_t()
+        check(lib().dvc_unet_workspace_size(self.handle, T, ctypes.byref(n)))
+        return n.value
+
+    def close(self):
+        if self.handle:
+            lib().dvc_unet_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dvc_unet_decode_gop(net: UNet, lat, ctx, comm: Comm | None = None, carry_in=None, carry_out=None, out=None,
+                        workspace=None, stream=None):
+    T = lat.shape[0]
+    if out is None:
+        out = torch.empty((T, lat.shape[1], lat.shape[2], net.cfg.c_lat), dtype=lat.dtype, device=lat.device)
+    if workspace is None:
+        workspace = _ws(net.workspace_size(T), lat.device)
+    check(lib().dvc_unet_decode_gop(net.handle, None if comm is None else comm.handle, _ptr(lat), _ptr(ctx), T,
+                                    _ptr(carry_in), _ptr(carry_out), _ptr(out), _ptr(workspace),
+                                    workspace.numel() * workspace.element_size(), _stream(stream)))
+    return out
+
+
+def pack_weights(named, dtype=torch.bfloat16) -> torch.Tensor:
+    """Concatenate [(name, array)] (blob order of include/dvc.h) into one host tensor of `dtype`."""
+    parts = [torch.as_tensor(a).reshape(-1).to(dtype) for _, a in named]
+    return torch.cat(parts)
