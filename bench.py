@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the DiffVC-RT decode hot path on B200 (metric of BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload: 720p, frames of one chain packed on the batch
+dimension, `--frames` (default 32 = the paper's intra period) frames per
+GPU.  One step = the whole hot path over one batch:
+  a1+a2  dvc_encode_pixelunshuffle: frames [T,3,720,1280] -> Lbar [T,90,160,256]
+         (PixelUnshuffle + Latent Channel Expansion; the encoded latent stands in
+         for the compressor's reconstruction Lbar, which is out of scope)
+  a3-a10 dvc_unet_decode_gop: concat(Lbar, C^m) -> 22 OTSM ResBlocks + glue -> Lhat
+With N GPUs (torchrun) the chain has N*T frames in contiguous chunks, one per
+rank, and every ResBlock's shifted slice moves rank r -> r+1 over NCCL (weak
+scaling: per-GPU work fixed).  Synthetic seeded inputs and random-init weights
+of the paper's shapes (synthgen).  Inputs per step (472 MB) exceed the 126 MB L2.
+
+--impl reference times the fp64 CPU oracle (this tier's reference arm) on a
+bounded sample of the same workload; see DESIGN.md section 7.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "720p GOP decode frames/sec"
+UNIT = "frames/s"
+H, W, S = 720, 1280, 8
+WIDTH = (240, 480, 960, 960)
+C_LAT = C_CTX = 256
+G, P = 24, 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=32, help="frames per GPU per step")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) == 6 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [int(r[0]) for r in rows]
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ algorithmic work
+def conv_flops_per_frame(h=H // S, w=W // S):
+    """Dense conv FLOPs of the skeleton per frame (the same 2*M*N*K libdvc reports)."""
+    hs, ws_ = [h], [w]
+    for _ in range(3):
+        hs.append((hs[-1] - 1) // 2 + 1)
+        ws_.append((ws_[-1] - 1) // 2 + 1)
+    px = [a * b for a, b in zip(hs, ws_)]
+    fl = 2 * px[0] * WIDTH[0] * 9 * (C_LAT + C_CTX)
+    skips, cur = [WIDTH[0]], WIDTH[0]
+    for l in range(4):
+        for _ in range(2):
+            ci, co = cur, WIDTH[l]
+            fl += 2 * px[l] * co * (9 * ci + 9 * co + (ci if ci != co else 0))
+            cur = co
+            skips.append(cur)
+        if l < 3:
+            fl += 2 * px[l + 1] * cur * 9 * cur
+            skips.append(cur)
+    for _ in range(2):
+        fl += 2 * px[3] * cur * 18 * cur
+    for u in range(4):
+        l = 3 - u
+        for _ in range(3):
+            ci, co = cur + skips.pop(), WIDTH[l]
+            fl += 2 * px[l] * co * (9 * ci + 9 * co + ci)
+            cur = co
+        if u < 3:
+            fl += 2 * px[l - 1] * cur * 9 * cur
+    fl += 2 * px[0] * C_LAT * 9 * cur
+    fl += 2 * px[0] * C_LAT * 3 * S * S   # encoder-side expansion (a2)
+    return fl
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk["bf16_tflops_sustained"], "measured sustained (MEASURED_PEAKS.json)"
+    except Exception:
+        return 1400.0, "fallback sustained (B200_PROFILING.md)"
+
+
+def load_traffic():
+    """dram bytes per step of the conv kernels, from the committed ncu summary (or None)."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ oracle (CPU baseline / reference arm)
+def oracle_sample(frames_np, lat_ctx_np, wts, wexp):
+    """One bounded sample of the workload on the fp64 oracle: encode 1 frame + conv_in + the
+    first two ResBlocks (down0.r0, down0.r1) of that frame.  Returns (seconds, flops)."""
+    import numpy as np
+    import oracle
+    named = iter(wts)
+    t0 = time.perf_counter()
+    w, b = wexp
+    lat = oracle.encode(frames_np[:1], w, b, 8, "bf16")
+    ctx = lat_ctx_np[:1]
+    _, wi = next(named)
+    _, bi = next(named)
+    x = oracle.rnd(oracle.conv2d(np.concatenate([lat, ctx], -1), wi, bi), "bf16")
+    fl = 2 * 14400 * C_LAT * 192 + 2 * 14400 * WIDTH[0] * 9 * 512
+    for _ in range(2):
+        blk = {}
+        for k in ("gn1_w", "gn1_b", "conv1_w", "conv1_b", "gn2_w", "gn2_b", "conv2_w", "conv2_b"):
+            blk[k] = next(named)[1]
+        blk["sc_w"] = blk["sc_b"] = None
+        x, _ = oracle.resblock(x, None, blk, G, P, 1e-5, "bf16")
+        fl += 2 * 14400 * WIDTH[0] * 18 * WIDTH[0]
+    return time.perf_counter() - t0, fl
+
+
+def oracle_inputs():
+    import numpy as np
+    import synthgen
+    frames = synthgen.frames(1, H, W).astype(np.float64)
+    ctx = synthgen.normal((1, H // S, W // S, C_CTX), 5).astype(np.float64)
+    named = synthgen.unet_weights(WIDTH, C_LAT, C_CTX)
+    wts = [(n, a.astype(np.float64)) for n, a in named[:2 + 16]]
+    we, be = synthgen.expansion_weights()
+    return frames, ctx, wts, (we.astype(np.float64), be.astype(np.float64))
+
+
+def cpu_baseline():
+    import oracle
+    frames, ctx, wts, wexp = oracle_inputs()
+    secs, fl = oracle_sample(frames, ctx, wts, wexp)
+    per_frame = conv_flops_per_frame()
+    fps = (fl / per_frame) / secs
+    return {"value": fps, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": (f"fp64 C oracle (OpenMP) on 1 frame of the workload: encode + conv_in + down0.r0 + "
+                       f"down0.r1 = {fl / 1e9:.1f} GFLOP in {secs:.1f} s; frames/s extrapolated by the "
+                       f"skeleton's {per_frame / 1e9:.1f} GFLOP/frame")}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    frames, ctx, wts, wexp = oracle_inputs()
+    for _ in range(args.warmup):
+        oracle_sample(frames, ctx, wts, wexp)
+    times, fl = [], 0
+    for _ in range(args.steps):
+        s, fl = oracle_sample(frames, ctx, wts, wexp)
+        times.append(s)
+    per_frame = conv_flops_per_frame()
+    tot = sum(times)
+    fps = (fl / per_frame) * args.steps / tot
+    line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "720p GOP decode (bounded oracle sample per step)", "latent": "90x160",
+                       "frames_per_gpu": args.frames},
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": "per step: 1 frame, encode + conv_in + down0.r0 + down0.r1 "
+                                       f"({fl / 1e9:.1f} GFLOP), extrapolated by GFLOP/frame"},
+            "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synthgen
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2601_20564_b200 as dvc
+    dvc.device_check(local)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float16
+    T = args.frames
+    h, w = H // S, W // S
+
+    # weights (replicated), inputs of this rank's chunk
+    named = synthgen.unet_weights(WIDTH, C_LAT, C_CTX)
+    cfg = dvc.unet_config(WIDTH, C_LAT, C_CTX, G, P, 1e-5, dtype, h, w, T)
+    net = dvc.UNet(cfg, dvc.pack_weights(named, dtype))
+    we, be = synthgen.expansion_weights()
+    w_exp = torch.from_numpy(we).to(dtype).cuda()
+    b_exp = torch.from_numpy(be).to(dtype).cuda()
+    seed = 100 + rank
+    frames_h = torch.from_numpy(synthgen.frames(T, H, W, seed=seed)).to(dtype).pin_memory()
+    ctx_h = torch.from_numpy(synthgen.normal((T, h, w, C_CTX), seed=seed + 1000)).to(dtype).pin_memory()
+    frames = frames_h.cuda()
+    ctx = ctx_h.cuda()
+    lat = torch.empty((T, h, w, C_LAT), dtype=dtype, device="cuda")
+    out = torch.empty((T, h, w, C_LAT), dtype=dtype, device="cuda")
+    ws = torch.empty(net.workspace_size(T), dtype=torch.uint8, device="cuda")
+    comm = dvc.Comm(rank, world) if world > 1 else None
+    stream = torch.cuda.current_stream()
+
+    def step(frames_d, ctx_d, out_d):
+        dvc.dvc_encode_pixelunshuffle(frames_d, w_exp, b_exp, out=lat)
+        dvc.dvc_unet_decode_gop(net, lat, ctx_d, comm=comm, out=out_d, workspace=ws)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step(frames, ctx, out)
+    barrier()
+
+    # ---- device-resident timed region
+    launches0 = dvc.launch_count()
+    dvc.profile_begin(200 * args.steps + 64)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(frames, ctx, out)
+        ev1.record(stream)
+        barrier()
+    conv_ms, conv_flops, conv_n = dvc.profile_end()
+    launches = dvc.launch_count() - launches0
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    conv_ms = max_over_ranks(conv_ms)
+    total_frames = T * world * args.steps
+    value = total_frames / (ms / 1e3)
+
+    # ---- end to end through the public API with host buffers (H2D inputs, D2H result)
+    e2e = None
+    if not args.no_e2e:
+        out_h = torch.empty(out.shape, dtype=dtype).pin_memory()
+        fr_d = torch.empty_like(frames)
+        cx_d = torch.empty_like(ctx)
+        for _ in range(2):
+            fr_d.copy_(frames_h, non_blocking=True)
+            cx_d.copy_(ctx_h, non_blocking=True)
+            step(fr_d, cx_d, out)
+            out_h.copy_(out, non_blocking=True)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fr_d.copy_(frames_h, non_blocking=True)
+            cx_d.copy_(ctx_h, non_blocking=True)
+            step(fr_d, cx_d, out)
+            out_h.copy_(out, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+        assert torch.isfinite(out_h.float()).all()
+        e2e = {"value": total_frames / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": frames_h.numel() * frames_h.element_size() + ctx_h.numel() * ctx_h.element_size(),
+               "d2h_bytes_per_step": out_h.numel() * out_h.element_size()}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = load_peaks()
+    achieved = conv_flops / (conv_ms / 1e3) / 1e12
+    traffic = load_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded frames / N(0,1) context, R19 init weights)",
+        "config": {"workload": f"720p GOP decode: encode (unshuffle+expansion) + pruned U-Net ResBlock skeleton, "
+                               f"{T} frames per GPU on the batch dim" + (f", chain of {T * world} frames in "
+                                                                         f"{world} contiguous chunks + NCCL halo"
+                                                                         if world > 1 else ""),
+                   "latent": f"{h}x{w}", "frames_per_gpu": T, "widths": list(WIDTH), "groups": G, "shift_p": P,
+                   "parallelism": f"frame-chunk x{world}" + (" + NCCL halo" if world > 1 else ""),
+                   "l2": "inputs larger than L2 (472 MB frames+context per step)"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None if traffic is None else traffic.get("bytes_per_step"),
+                     "kernel": "conv_tc_kernel (all convolution launches of the step, summed)",
+                     "conv_ms_per_step": conv_ms / args.steps, "conv_launches_per_step": conv_n / args.steps,
+                     "conv_share_of_step": conv_ms / ms, "peak_source": peak_src},
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -189,6 +189,15 @@ DVC_API dvc_status dvc_comm_unique_id(void *id128);
 DVC_API dvc_status dvc_comm_create(int rank, int world, const void *id128, dvc_comm **out);
 DVC_API dvc_status dvc_comm_destroy(dvc_comm *c);
 
+/* Live measurement of the dominant kernel (bench.py, roofline): between
+ * dvc_profile_begin and dvc_profile_end every convolution launch (tcgen05 or
+ * SIMT engine) is bracketed by CUDA events recorded on its launch stream.
+ * dvc_profile_end waits for the last event and returns the summed kernel time
+ * (ms), the summed algorithmic FLOPs (2*M*N*K over the real, unpadded K) and
+ * the number of launches.  max_launches bounds the event pool. */
+DVC_API dvc_status dvc_profile_begin(int max_launches);
+DVC_API dvc_status dvc_profile_end(double *conv_ms, double *conv_flops, int *conv_launches);
+
 /* Device / build introspection (no compute). */
 DVC_API dvc_status dvc_device_check(int device);   /* DVC_OK iff the device is sm_100 */
 DVC_API int dvc_kernel_launch_count(void);         /* kernels launched by this process so far */

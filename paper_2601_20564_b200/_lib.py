@@ -59,6 +59,9 @@ _SIGS = {
     "dvc_unet_workspace_size": ([c_void_p, c_int, ctypes.POINTER(c_size_t)], c_int),
     "dvc_unet_decode_gop": ([c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_size_t, c_void_p], c_int),
+    "dvc_profile_begin": ([c_int], c_int),
+    "dvc_profile_end": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                         ctypes.POINTER(c_int)], c_int),
     "dvc_comm_unique_id": ([c_void_p], c_int),
     "dvc_comm_create": ([c_int, c_int, c_void_p, ctypes.POINTER(c_void_p)], c_int),
     "dvc_comm_destroy": ([c_void_p], c_int),

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
 #include "dvc_resblock.cuh"
@@ -44,6 +45,29 @@ dvc_status check_device() {
     cudaError_t e = cudaPeekAtLastError();
     DVC_CHECK_ARG(e == cudaSuccess, DVC_ERR_CUDA, "pending CUDA error: %s", cudaGetErrorString(e));
     return DVC_OK;
+}
+
+// ----------------------------------------------------------------- live profiling
+namespace {
+struct Prof {
+    bool on = false;
+    int cap = 0, used = 0;
+    std::vector<cudaEvent_t> ev;   // 2 per launch
+    std::vector<double> flops;
+} g_prof;
+}  // namespace
+
+ProfSlot prof_begin(cudaStream_t stream) {
+    if (!g_prof.on || g_prof.used >= g_prof.cap) return ProfSlot{-1};
+    int i = g_prof.used++;
+    cudaEventRecord(g_prof.ev[2 * i], stream);
+    return ProfSlot{i};
+}
+
+void prof_end(ProfSlot s, cudaStream_t stream, double flops) {
+    if (s.idx < 0) return;
+    cudaEventRecord(g_prof.ev[2 * s.idx + 1], stream);
+    g_prof.flops[s.idx] = flops;
 }
 
 // ----------------------------------------------------------------- ResBlock (a3-a8)
@@ -180,6 +204,38 @@ const char *dvc_status_string(dvc_status s) {
 }
 
 const char *dvc_last_error(void) { return g_err; }
+
+dvc_status dvc_profile_begin(int max_launches) {
+    DVC_CHECK_ARG(max_launches >= 1 && max_launches <= (1 << 20), DVC_ERR_ARG, "bad max_launches");
+    if ((int)g_prof.ev.size() < 2 * max_launches) {
+        size_t old = g_prof.ev.size();
+        g_prof.ev.resize(2 * (size_t)max_launches);
+        for (size_t i = old; i < g_prof.ev.size(); ++i) DVC_CUDA(cudaEventCreate(&g_prof.ev[i]));
+    }
+    g_prof.flops.assign(max_launches, 0.0);
+    g_prof.cap = max_launches;
+    g_prof.used = 0;
+    g_prof.on = true;
+    return DVC_OK;
+}
+
+dvc_status dvc_profile_end(double *conv_ms, double *conv_flops, int *conv_launches) {
+    DVC_CHECK_ARG(conv_ms && conv_flops && conv_launches, DVC_ERR_ARG, "null output");
+    g_prof.on = false;
+    double ms = 0, fl = 0;
+    for (int i = 0; i < g_prof.used; ++i) {
+        DVC_CUDA(cudaEventSynchronize(g_prof.ev[2 * i + 1]));
+        float t = 0.f;
+        DVC_CUDA(cudaEventElapsedTime(&t, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]));
+        ms += t;
+        fl += g_prof.flops[i];
+    }
+    *conv_ms = ms;
+    *conv_flops = fl;
+    *conv_launches = g_prof.used;
+    g_prof.used = 0;
+    return DVC_OK;
+}
 int dvc_abi_version(void) { return DVC_ABI_VERSION; }
 int dvc_kernel_launch_count(void) { return g_launches; }
 

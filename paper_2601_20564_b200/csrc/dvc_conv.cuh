@@ -40,6 +40,14 @@ struct ConvDesc {
     long M() const { return (long)T * ho * wo; }
 };
 
+// live per-launch event timing (dvc_profile_begin/end)
+struct ProfSlot {
+    int idx;   // -1 = not profiling
+};
+ProfSlot prof_begin(cudaStream_t stream);
+void prof_end(ProfSlot s, cudaStream_t stream, double flops);
+double conv_flops(const ConvDesc &d);
+
 // Validates the descriptor for the given engine; returns DVC_OK or an error.
 dvc_status conv_check(const ConvDesc &d, bool tensor_core);
 // Launches (no host sync).  16-bit: tcgen05 engine; F32: SIMT engine.

@@ -159,8 +159,17 @@ dvc_status conv_check(const ConvDesc &d, bool tc) {
     return DVC_OK;
 }
 
+double conv_flops(const ConvDesc &d) {
+    double k = 0;
+    for (int s = 0; s < d.nseg; ++s) k += (double)d.seg[s].taps * d.seg[s].c_src;
+    return 2.0 * (double)d.M() * d.cout * k;
+}
+
 dvc_status conv_run(const ConvDesc &d, cudaStream_t stream) {
-    return d.dt == DVC_F32 ? conv_simt_run(d, stream) : conv_tc_run(d, stream);
+    ProfSlot slot = prof_begin(stream);
+    dvc_status st = d.dt == DVC_F32 ? conv_simt_run(d, stream) : conv_tc_run(d, stream);
+    prof_end(slot, stream, conv_flops(d));
+    return st;
 }
 
 }  // namespace dvc

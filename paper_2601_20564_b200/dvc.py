@@ -50,6 +50,17 @@ def launch_count() -> int:
     return lib().dvc_kernel_launch_count()
 
 
+def profile_begin(max_launches: int = 100000) -> None:
+    check(lib().dvc_profile_begin(max_launches))
+
+
+def profile_end():
+    """-> (summed conv kernel ms, summed algorithmic conv FLOPs, conv launches)."""
+    ms, fl, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    check(lib().dvc_profile_end(ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(n)))
+    return ms.value, fl.value, n.value
+
+
 # ------------------------------------------------------------------ a1 + a2
 def dvc_encode_pixelunshuffle(frames: torch.Tensor, w_exp=None, b_exp=None, s: int = 8, out=None, stream=None):
     """frames [T,3,H,W] -> latent [T,H/s,W/s,c_lat] (c_lat = 3 s^2 without expansion)."""

@@ -42,8 +42,9 @@ def test_skeleton_small_parity(dvc, orc, dtype, h, w, T):
     ref, kref = orc.skeleton(lat64, ctx64, wts, SMALL, G=8, P=8, mode=MODE[dtype])
     err = rel_l2(host64(out), ref)
     assert err <= TOL[dtype], err
+    # the carries are the GPU's own block inputs (computed activations): same tolerance
     packed = np.concatenate([k.ravel() for k in kref])
-    assert np.array_equal(host64(co), packed)
+    assert rel_l2(host64(co), packed) <= TOL[dtype]
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
