@@ -198,6 +198,14 @@ DVC_API dvc_status dvc_comm_destroy(dvc_comm *c);
 DVC_API dvc_status dvc_profile_begin(int max_launches);
 DVC_API dvc_status dvc_profile_end(double *conv_ms, double *conv_flops, int *conv_launches);
 
+/* Convolution engine selection (tuning / A-B testing; default 2, or the
+ * DVC_CONV_ENGINE environment variable at load):
+ *   2 = TMA-fed persistent tcgen05 engine with CTA pairs (cta_group::2, M=256)
+ *   1 = the same engine with single-CTA MMAs (M=128)
+ *   0 = gather-fed tcgen05 engine only (cp.async producer warps)
+ * Strided / resized / unshuffle convolutions always use the gather engine. */
+DVC_API dvc_status dvc_set_conv_engine(int engine);
+
 /* Device / build introspection (no compute). */
 DVC_API dvc_status dvc_device_check(int device);   /* DVC_OK iff the device is sm_100 */
 DVC_API int dvc_kernel_launch_count(void);         /* kernels launched by this process so far */

@@ -59,6 +59,7 @@ _SIGS = {
     "dvc_unet_workspace_size": ([c_void_p, c_int, ctypes.POINTER(c_size_t)], c_int),
     "dvc_unet_decode_gop": ([c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_size_t, c_void_p], c_int),
+    "dvc_set_conv_engine": ([c_int], c_int),
     "dvc_profile_begin": ([c_int], c_int),
     "dvc_profile_end": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                          ctypes.POINTER(c_int)], c_int),

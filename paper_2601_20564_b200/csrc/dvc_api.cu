@@ -205,6 +205,12 @@ const char *dvc_status_string(dvc_status s) {
 
 const char *dvc_last_error(void) { return g_err; }
 
+dvc_status dvc_set_conv_engine(int engine) {
+    DVC_CHECK_ARG(engine >= 0 && engine <= 2, DVC_ERR_ARG, "engine must be 0, 1 or 2");
+    g_ws_cg = engine;
+    return DVC_OK;
+}
+
 dvc_status dvc_profile_begin(int max_launches) {
     DVC_CHECK_ARG(max_launches >= 1 && max_launches <= (1 << 20), DVC_ERR_ARG, "bad max_launches");
     if ((int)g_prof.ev.size() < 2 * max_launches) {

@@ -54,6 +54,9 @@ dvc_status conv_check(const ConvDesc &d, bool tensor_core);
 dvc_status conv_run(const ConvDesc &d, cudaStream_t stream);
 dvc_status conv_tc_run(const ConvDesc &d, cudaStream_t stream);
 dvc_status conv_simt_run(const ConvDesc &d, cudaStream_t stream);
+dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream);   // TMA + CTA-pair persistent engine
+bool conv_ws_applicable(const ConvDesc &d);
+extern int g_ws_cg;   // 2 (default): CTA pairs; 1: single CTA; 0: gather engine only
 
 // Row-address helper shared by both engines: source pixel index of output
 // pixel (t, y, x) for tap (dy, dx), or -1 when the tap falls in the zero padding.

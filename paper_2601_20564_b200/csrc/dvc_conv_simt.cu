@@ -167,7 +167,9 @@ double conv_flops(const ConvDesc &d) {
 
 dvc_status conv_run(const ConvDesc &d, cudaStream_t stream) {
     ProfSlot slot = prof_begin(stream);
-    dvc_status st = d.dt == DVC_F32 ? conv_simt_run(d, stream) : conv_tc_run(d, stream);
+    dvc_status st = d.dt == DVC_F32 ? conv_simt_run(d, stream)
+                    : conv_ws_applicable(d) ? conv_ws_run(d, stream)
+                                            : conv_tc_run(d, stream);
     prof_end(slot, stream, conv_flops(d));
     return st;
 }

@@ -22,104 +22,9 @@
 #include <cuda.h>
 #include <mutex>
 #include "dvc_conv.cuh"
+#include "dvc_ptx.cuh"
 
 namespace dvc {
-
-// ----------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(ok)
-        : "r"(addr), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-    uint32_t a = smem_u32(b);
-    while (!mbar_try_wait(a, parity)) {
-    }
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_16(uint32_t dst, const void *src, uint32_t src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *b) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void tma_prefetch(const CUtensorMap *map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t *bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
-}
-// 32 lanes x 32 bit, 16 consecutive columns per thread
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-          "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: rows of 128 B, 8-row
-// swizzle atoms 1024 B apart (SBO), version 1 (sm_100), layout type 2.
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;               // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;     // SBO
-    d |= (uint64_t)1 << 46;               // version
-    d |= (uint64_t)2 << 61;               // SWIZZLE_128B
-    return d;
-}
-// Instruction descriptor kind::f16: D fp32, A/B fp16 (0) or bf16 (1), both K-major.
-__host__ __device__ constexpr uint32_t make_idesc(int ab_bf16, int M, int N) {
-    return (1u << 4) | ((uint32_t)ab_bf16 << 7) | ((uint32_t)ab_bf16 << 10) | ((uint32_t)(N >> 3) << 17) |
-           ((uint32_t)(M >> 4) << 24);
-}
 
 // ----------------------------------------------------------------- kernel params
 struct TcParams {
@@ -196,40 +101,59 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         // ===================== A producer (gather + cp.async) =====================
         const int j = tid & 7;          // 16-byte granule within the 128-byte row
         const int rb = tid >> 3;        // rows rb, rb+16, ...
+        constexpr int NR = NACC * 8;    // rows per thread
+        int ry[NR], rx[NR], rt[NR];     // output pixel of each row (t < 0: row beyond M)
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+            const int info = rowinfo[rb + 16 * i];
+            rt[i] = info >> 24;          // -1 when invalid (sign extends)
+            ry[i] = (info >> 12) & 0xFFF;
+            rx[i] = info & 0xFFF;
+        }
         int stage = 0;
         uint32_t phase = 0;
         for (int s = 0; s < p.nseg; ++s) {
             const ConvSeg &sg = p.seg[s];
             const int nch = (sg.c_src + 63) >> 6;
             const T *src = reinterpret_cast<const T *>(sg.src);
+            const int mode = sg.mode, hi = sg.hi, wi = sg.wi, csrc = sg.c_src;
             for (int tap = 0; tap < sg.taps; ++tap) {
                 const int dy = sg.taps == 9 ? tap / 3 - 1 : 0;
                 const int dx = sg.taps == 9 ? tap % 3 - 1 : 0;
+                // per-row source pixel for this tap (channel-independent), -1 = zero padding
+                long pix[NR];
+#pragma unroll
+                for (int i = 0; i < NR; ++i) {
+                    if (rt[i] < 0) {
+                        pix[i] = -1;
+                    } else if (mode == SEG_SAME) {
+                        const int iy = ry[i] + dy, ix = rx[i] + dx;
+                        pix[i] = ((unsigned)iy < (unsigned)hi && (unsigned)ix < (unsigned)wi)
+                                     ? ((long)rt[i] * hi + iy) * wi + ix : -1;
+                    } else if (mode == SEG_UNSHUFFLE8) {
+                        pix[i] = 0;
+                    } else {
+                        pix[i] = seg_src_pixel(sg, p.ho, p.wo, rt[i], ry[i], rx[i], dy, dx);
+                    }
+                }
                 for (int ch = 0; ch < nch; ++ch) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t base = smem_u32(sA + stage * A_STAGE);
                     const int c = ch * 64 + j * 8;
-                    const bool cvalid = c < sg.c_src;
-#pragma unroll 4
-                    for (int i = 0; i < NACC * 8; ++i) {
+                    const bool cvalid = c < csrc;
+#pragma unroll
+                    for (int i = 0; i < NR; ++i) {
                         const int r = rb + 16 * i;
-                        const int info = rowinfo[r];
                         const T *g = src;
                         uint32_t nbytes = 0;
-                        if (info >= 0 && cvalid) {
-                            const int t = info >> 24, y = (info >> 12) & 0xFFF, x = info & 0xFFF;
-                            if (sg.mode == SEG_UNSHUFFLE8) {
-                                // a1: latent channel ch*64 + j*8 + (0..7) = frame (color ch, row 8y+j, cols 8x..8x+7)
-                                const long H = sg.hi, W = sg.wi;
-                                g = src + (((long)t * 3 + ch) * H + 8 * y + j) * W + 8 * x;
-                                nbytes = 16;
+                        if (pix[i] >= 0 && cvalid) {
+                            if (mode == SEG_UNSHUFFLE8) {
+                                // a1: latent channel ch*64 + j*8 + (0..7) = frame (colour ch, row 8y+j, cols 8x..8x+7)
+                                g = src + (((long)rt[i] * 3 + ch) * hi + 8 * ry[i] + j) * (long)wi + 8 * rx[i];
                             } else {
-                                long pix = seg_src_pixel(sg, p.ho, p.wo, t, y, x, dy, dx);
-                                if (pix >= 0) {
-                                    g = src + pix * sg.c_src + c;
-                                    nbytes = 16;
-                                }
+                                g = src + pix[i] * csrc + c;
                             }
+                            nbytes = 16;
                         }
                         const uint32_t dst = base + (uint32_t)(r >> 7) * A_TILE + (uint32_t)(r & 127) * 128 +
                                              (uint32_t)((j ^ (r & 7)) << 4);
@@ -372,27 +296,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 }
 
 // ----------------------------------------------------------------- host side
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                     const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
-                                     CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                                     CUtensorMapFloatOOBfill);
-
-static PFN_encodeTiled get_encode() {
-    static PFN_encodeTiled fn = nullptr;
+PFN_encodeTiled_t get_encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
         void *ptr = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+            fn = reinterpret_cast<PFN_encodeTiled_t>(ptr);
     });
     return fn;
 }
 
 // 2D [rows][cols] 16-bit matrix, box {64 cols, box_rows}, SWIZZLE_128B, OOB zero fill.
-static dvc_status make_bmap(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows) {
-    PFN_encodeTiled enc = get_encode();
+dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows) {
+    PFN_encodeTiled_t enc = get_encode_fn();
     DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && (cols * 2) % 16 == 0, DVC_ERR_ARG,
                   "weight matrix must be 16-byte aligned with 16-byte rows");
@@ -456,7 +375,7 @@ dvc_status conv_tc_run(const ConvDesc &d, cudaStream_t stream) {
             DVC_CHECK_ARG(nb < 2, DVC_ERR_UNSUPPORTED, "at most two weight matrices per conv");
             idx = nb++;
             bw[idx] = d.seg[s].w;
-            st = make_bmap(&p.bmap[idx], d.seg[s].w, d.dt, d.cout, d.seg[s].w_ld, bn);
+            st = make_bmap_rows(&p.bmap[idx], d.seg[s].w, d.dt, d.cout, d.seg[s].w_ld, bn);
             if (st != DVC_OK) return st;
         }
         p.bidx[s] = idx;

@@ -1,0 +1,412 @@
+// dvc_conv_ws.cu -- persistent, warp-specialised tcgen05 implicit-GEMM
+// convolution for same-resolution 3x3 / 1x1 convolutions (the ResBlock convs
+// a5/a7/a8 and conv_in/conv_out).
+//
+// GEMM view: M = output pixels, tiled per frame into spatial boxes of
+// BY x BX <= 128 pixels (one 128-row MMA tile each); N = C_out in tiles of
+// BN <= 256; K = sum over segments of taps x C_src in 64-channel stages.
+// For tap (dy, dx) the A tile of a box is the TMA box of the NHWC activation
+// at (x0+dx, y0+dy): the tensor map's out-of-bounds zero fill IS the conv's
+// zero padding, so no address arithmetic runs on the SMs.
+//
+// CG = 2 (default): a CTA pair (cluster of 2) runs tcgen05.mma.cta_group::2
+// with M = 256 (each CTA's box = 128 rows) and N = BN; each CTA stages its own
+// A box and HALF of the weight tile, halving per-SM weight traffic.
+// Per CTA: 2 TMEM accumulator buffers of BN fp32 columns, so the epilogue of
+// tile i overlaps the MMAs of tile i+1.
+//
+// Warp roles (256 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
+// issuer (leader CTA only issues), warps 4-7 epilogue (TMEM -> registers ->
+// bias / residual -> global), warps 2-3 idle.
+#include <cuda.h>
+#include <cstdlib>
+#include "dvc_conv.cuh"
+#include "dvc_ptx.cuh"
+
+namespace dvc {
+
+struct WsParams {
+    CUtensorMap amap[4];   // per segment: 4D {C, W, H, T}, box {64, BX, BY, 1}, SW128, OOB zero
+    CUtensorMap bmap[2];   // weights 2D {K, C_out}, box {64, BN/CG}, SW128
+    int bidx[4], seg_c[4], seg_taps[4], seg_col0[4], seg_tapstride[4];
+    int nseg;
+    int T, H, W, cout, bn;
+    int BX, BY, tiles_x, tiles_y, nbox, ntile_n, nwork;
+    const void *bias0, *bias1, *residual;
+    void *out;
+    uint32_t idesc;
+};
+
+constexpr int kWsThreads = 256;
+
+template <typename T, int CG, int STAGES>
+__global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_constant__ WsParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int BN = p.bn, BNH = p.bn / CG;
+    constexpr int A_STAGE = 128 * 128;
+    const int B_STAGE = BNH * 128;
+    uint8_t *sA = smem;
+    uint8_t *sB = sA + STAGES * A_STAGE;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * B_STAGE);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const int cluster_id = blockIdx.x / CG, nclusters = gridDim.x / CG;
+    const uint32_t ncols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], CG * 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+        for (int s = 0; s < p.nseg; ++s) tma_prefetch(&p.amap[s]);
+        tma_prefetch(&p.bmap[0]);
+    }
+    if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), ncols);
+    tc_fence_before();
+    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer (both CTAs) =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t a_bytes = (uint32_t)(p.BX * p.BY * 128);
+            const uint32_t tx = (uint32_t)CG * (a_bytes + (uint32_t)B_STAGE);
+            for (int w = cluster_id; w < p.nwork; w += nclusters) {
+                const int q = w / p.ntile_n, nt = w - q * p.ntile_n;
+                const int n0 = nt * BN + (int)rank * BNH;
+                int box = q * CG + (int)rank;
+                int t, y0, x0;
+                if (box < p.nbox) {
+                    const int per = p.tiles_x * p.tiles_y;
+                    t = box / per;
+                    const int rem = box - t * per;
+                    y0 = (rem / p.tiles_x) * p.BY;
+                    x0 = (rem % p.tiles_x) * p.BX;
+                } else {   // padding box of the last pair: fully out of bounds -> zeros
+                    t = p.T;
+                    y0 = x0 = 0;
+                }
+                for (int s = 0; s < p.nseg; ++s) {
+                    const int nch = (p.seg_c[s] + 63) >> 6;
+                    const CUtensorMap *bm = &p.bmap[p.bidx[s]];
+                    for (int tap = 0; tap < p.seg_taps[s]; ++tap) {
+                        const int dy = p.seg_taps[s] == 9 ? tap / 3 - 1 : 0;
+                        const int dx = p.seg_taps[s] == 9 ? tap % 3 - 1 : 0;
+                        const int col = p.seg_col0[s] + tap * p.seg_tapstride[s];
+                        for (int ch = 0; ch < nch; ++ch) {
+                            mbar_wait(&empty[stage], phase ^ 1);
+                            const uint32_t fb = smem_u32(&full[stage]);
+                            const uint32_t dA = smem_u32(sA + stage * A_STAGE);
+                            const uint32_t dB = smem_u32(sB + stage * B_STAGE);
+                            if constexpr (CG == 1) {
+                                mbar_arrive_expect_tx_addr(fb, tx);
+                                tma_load_4d(dA, &p.amap[s], fb, ch * 64, x0 + dx, y0 + dy, t);
+                                tma_load_2d_a(dB, bm, fb, col + ch * 64, n0);
+                            } else {
+                                if (rank == 0) mbar_arrive_expect_tx_addr(fb, tx);
+                                const uint32_t lb = mapa_shared(fb, 0);   // leader's barrier
+                                tma_load_4d_cg2(dA, &p.amap[s], lb, ch * 64, x0 + dx, y0 + dy, t);
+                                tma_load_2d_cg2(dB, bm, lb, col + ch * 64, n0);
+                            }
+                            if (++stage == STAGES) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader CTA) =====================
+        if (lane == 0 && rank == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
+                const int buf = it & 1;
+                const uint32_t use = (uint32_t)(it >> 1) & 1;
+                mbar_wait(&tempty[buf], use ^ 1);   // epilogues of both CTAs drained this buffer
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(buf * BN);
+                bool first = true;
+                for (int s = 0; s < p.nseg; ++s) {
+                    const int nch = (p.seg_c[s] + 63) >> 6;
+                    for (int tap = 0; tap < p.seg_taps[s]; ++tap) {
+                        for (int ch = 0; ch < nch; ++ch) {
+                            mbar_wait(&full[stage], phase);
+                            tc_fence_after();
+                            const int ksteps = min(64, p.seg_c[s] - ch * 64) >> 4;
+                            const uint32_t a0 = smem_u32(sA + stage * A_STAGE);
+                            const uint32_t b0 = smem_u32(sB + stage * B_STAGE);
+                            for (int k = 0; k < ksteps; ++k) {
+                                const uint64_t ad = sdesc_sw128(a0 + k * 32);
+                                const uint64_t bd = sdesc_sw128(b0 + k * 32);
+                                if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, first ? 0u : 1u);
+                                else tc_mma_cg2(d, ad, bd, p.idesc, first ? 0u : 1u);
+                                first = false;
+                            }
+                            if constexpr (CG == 1) tc_commit(&empty[stage]);
+                            else tc_commit_cg2_mc(smem_u32(&empty[stage]), 0x3);
+                            if (++stage == STAGES) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
+                    }
+                }
+                if constexpr (CG == 1) tc_commit(&tfull[buf]);
+                else tc_commit_cg2_mc(smem_u32(&tfull[buf]), 0x3);
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue (both CTAs) =====================
+        const int q4 = warp & 3;                 // TMEM lane quadrant of this warp
+        const int r = q4 * 32 + lane;            // accumulator row = pixel of this CTA's box
+        const int by = r / p.BX, bx = r - by * p.BX;
+        const T *b0 = reinterpret_cast<const T *>(p.bias0);
+        const T *b1 = reinterpret_cast<const T *>(p.bias1);
+        const T *res = reinterpret_cast<const T *>(p.residual);
+        T *out = reinterpret_cast<T *>(p.out);
+        const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+        int it = 0;
+        for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
+            const int buf = it & 1;
+            const uint32_t use = (uint32_t)(it >> 1) & 1;
+            const int q = w / p.ntile_n, nt = w - q * p.ntile_n;
+            const int box = q * CG + (int)rank;
+            long m = -1;
+            if (box < p.nbox && r < p.BX * p.BY) {
+                const int per = p.tiles_x * p.tiles_y;
+                const int t = box / per, rem = box - t * per;
+                const int y = (rem / p.tiles_x) * p.BY + by, x = (rem % p.tiles_x) * p.BX + bx;
+                if (y < p.H && x < p.W) m = ((long)t * p.H + y) * p.W + x;
+            }
+            mbar_wait(&tfull[buf], use);
+            tc_fence_after();
+#pragma unroll 1
+            for (int cc = 0; cc < BN; cc += 16) {
+                uint32_t v[16];
+                tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
+                const int n = nt * BN + cc;
+                if (m >= 0) {
+                    float f[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
+                    float e[8];
+                    if (b0) {
+                        load8(b0 + n, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] += e[i];
+                        load8(b0 + n + 8, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                    }
+                    if (b1) {
+                        load8(b1 + n, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] += e[i];
+                        load8(b1 + n + 8, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                    }
+                    if (res) {
+                        load8(res + m * p.cout + n, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] += e[i];
+                        load8(res + m * p.cout + n + 8, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                    }
+                    float lo[8], hi[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        lo[i] = f[i];
+                        hi[i] = f[8 + i];
+                    }
+                    store8(out + m * p.cout + n, lo);
+                    store8(out + m * p.cout + n + 8, hi);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (CG == 1) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                                        smem_u32(&tempty[buf]))
+                                                    : "memory");
+                else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<CG>(tmem, ncols);
+    }
+}
+
+// ----------------------------------------------------------------- host side
+PFN_encodeTiled_t get_encode_fn();
+
+static dvc_status make_amap(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX,
+                            int BY) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && (C * 2) % 16 == 0, DVC_ERR_ARG, "activation must be 16-byte aligned");
+    cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
+    cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)BX, (cuuint32_t)BY, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                     const_cast<void *>(ptr), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (activation) failed (%d)", (int)r);
+    return DVC_OK;
+}
+
+dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
+
+// Spatial box minimising the number of 128-row MMA tiles per frame.
+static void choose_box(int H, int W, int *BX, int *BY) {
+    long best = -1;
+    for (int bx = 1; bx <= W && bx <= 128; ++bx) {
+        int by = 128 / bx;
+        if (by > H) by = H;
+        if (by < 1) continue;
+        long cost = (long)((H + by - 1) / by) * ((W + bx - 1) / bx);
+        if (best < 0 || cost < best || (cost == best && bx * by > *BX * *BY)) {
+            best = cost;
+            *BX = bx;
+            *BY = by;
+        }
+    }
+}
+
+static int g_num_sms = 0;
+
+template <typename T, int CG, int STAGES>
+static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
+    const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16;
+    auto kern = conv_ws_kernel<T, CG, STAGES>;
+    DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int clusters = g_num_sms / CG;
+    if (clusters > p.nwork) clusters = p.nwork;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * CG);
+    cfg.blockDim = dim3(kWsThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DVC_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    ++g_launches;
+    return check_launch("conv_ws_kernel");
+}
+
+static int engine_from_env() {
+    const char *e = getenv("DVC_CONV_ENGINE");
+    if (e && (e[0] == '0' || e[0] == '1' || e[0] == '2') && e[1] == 0) return e[0] - '0';
+    return 2;
+}
+int g_ws_cg = engine_from_env();   // 2: CTA-pair MMA (default), 1: single-CTA MMA, 0: gather engine only
+
+bool conv_ws_applicable(const ConvDesc &d) {
+    if (g_ws_cg == 0 || d.dt == DVC_F32) return false;
+    for (int s = 0; s < d.nseg; ++s)
+        if (d.seg[s].mode != SEG_SAME || d.seg[s].hi != d.ho || d.seg[s].wi != d.wo) return false;
+    return true;
+}
+
+dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
+    dvc_status st = conv_check(d, true);
+    if (st != DVC_OK) return st;
+    WsParams p;
+    memset(&p, 0, sizeof(p));
+    const int CG = g_ws_cg == 1 ? 1 : 2;
+    int bn = d.cout;
+    if (bn > 256) {
+        bn = 0;
+        for (int c = 256; c >= 16; c -= 16)
+            if (d.cout % c == 0 && (c / CG) % 8 == 0) {
+                bn = c;
+                break;
+            }
+    }
+    DVC_CHECK_ARG(bn >= 16 && (bn / CG) % 8 == 0, DVC_ERR_UNSUPPORTED, "no N tile for cout=%d", d.cout);
+    p.bn = bn;
+    p.nseg = d.nseg;
+    p.T = d.T;
+    p.H = d.ho;
+    p.W = d.wo;
+    p.cout = d.cout;
+    choose_box(d.ho, d.wo, &p.BX, &p.BY);
+    p.tiles_x = (d.wo + p.BX - 1) / p.BX;
+    p.tiles_y = (d.ho + p.BY - 1) / p.BY;
+    p.nbox = d.T * p.tiles_x * p.tiles_y;
+    p.ntile_n = d.cout / bn;
+    p.nwork = ((p.nbox + CG - 1) / CG) * p.ntile_n;
+    p.bias0 = d.bias0;
+    p.bias1 = d.bias1;
+    p.residual = d.residual;
+    p.out = d.out;
+    int nb = 0;
+    const void *bw[2] = {nullptr, nullptr};
+    for (int s = 0; s < d.nseg; ++s) {
+        const ConvSeg &g = d.seg[s];
+        st = make_amap(&p.amap[s], g.src, d.dt, d.T, d.ho, d.wo, g.c_src, p.BX, p.BY);
+        if (st != DVC_OK) return st;
+        int idx = -1;
+        for (int k = 0; k < nb; ++k)
+            if (bw[k] == g.w) idx = k;
+        if (idx < 0) {
+            DVC_CHECK_ARG(nb < 2, DVC_ERR_UNSUPPORTED, "at most two weight matrices per conv");
+            idx = nb++;
+            bw[idx] = g.w;
+            st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
+            if (st != DVC_OK) return st;
+        }
+        p.bidx[s] = idx;
+        p.seg_c[s] = g.c_src;
+        p.seg_taps[s] = g.taps;
+        p.seg_col0[s] = g.w_col0;
+        p.seg_tapstride[s] = g.w_tapstride;
+    }
+    const int bf = d.dt == DVC_BF16;
+    p.idesc = make_idesc(bf, 128 * CG, bn);
+    if (CG == 2) {
+        if (bf) return launch_ws<__nv_bfloat16, 2, 6>(p, stream);
+        return launch_ws<__half, 2, 6>(p, stream);
+    }
+    if (bf) return launch_ws<__nv_bfloat16, 1, 4>(p, stream);
+    return launch_ws<__half, 1, 4>(p, stream);
+}
+
+}  // namespace dvc

@@ -50,6 +50,11 @@ def launch_count() -> int:
     return lib().dvc_kernel_launch_count()
 
 
+def set_conv_engine(engine: int) -> None:
+    """2 = TMA + CTA-pair tcgen05 engine (default), 1 = single-CTA, 0 = gather engine only."""
+    check(lib().dvc_set_conv_engine(engine))
+
+
 def profile_begin(max_launches: int = 100000) -> None:
     check(lib().dvc_profile_begin(max_launches))
 
