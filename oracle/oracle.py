@@ -327,7 +327,7 @@ def _rb_weights(it, cin, cout):
 
 
 def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int = 8,
-             eps: float = 1e-5, carries=None, mode=None, record=None, shift="batch"):
+             eps: float = 1e-5, carries=None, mode=None, record=None, shift="batch", halo=None):
     """The pruned U-Net's ResBlock skeleton over T frames of one chain (R1, R11):
         x0 = conv_in(concat(Lbar, Cm));  push x0
         for level l = 0..3: two ResBlocks (push each); if l < 3: conv3x3 stride 2 (push)
@@ -339,6 +339,9 @@ def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int 
     weights: iterable of (name, array) in the blob order of include/dvc.h.
     carries: list of 22 slices [h_l, w_l, Cin_k/P] (None = chain start, zeros).
     record: optional list that receives every ResBlock output.
+    halo: optional callable (k, X) -> carry for block k, called right before block k
+    with its input X (multi-GPU lockstep: send X's last-frame slice onward, receive the
+    predecessor's); overrides carries[k].
     Returns (out [T,h,w,c_out], carries_out)."""
     it = iter(weights)
     lat, ctx = _f64(lat), _f64(ctx)
@@ -355,7 +358,8 @@ def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int 
         if h.shape[-1] != cin:
             raise ValueError(f"{name}: input has {h.shape[-1]} channels, expected {cin}")
         w = _rb_weights(it, cin, cout)
-        out, k = resblock(h, carries[bi], w, G, P, eps, mode, shift)
+        carry = halo(bi, h) if halo is not None else carries[bi]
+        out, k = resblock(h, carry, w, G, P, eps, mode, shift)
         k_out.append(k)
         if record is not None:
             record.append(out)

@@ -74,7 +74,7 @@ void prof_end(ProfSlot s, cudaStream_t stream, double flops) {
 size_t resblock_ws_bytes(int ca, int cb, int cout, int G, int T, int HW, dvc_dtype dt) {
     const size_t es = dt_size(dt);
     const int cin = ca + cb;
-    return align256(gn_workspace_bytes(T, HW, G)) + align256((size_t)T * HW * cin * es) +
+    return align256(gn_workspace_bytes(T, HW, G, cin > cout ? cin : cout)) + align256((size_t)T * HW * cin * es) +
            2 * align256((size_t)T * HW * cout * es);
 }
 
@@ -108,7 +108,7 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
     const size_t es = dt_size(b.dt);
     uint8_t *p = reinterpret_cast<uint8_t *>(ws);
     void *gnws = p;
-    p += align256(gn_workspace_bytes(T, HW, b.G));
+    p += align256(gn_workspace_bytes(T, HW, b.G, cin > b.cout ? cin : b.cout));
     void *h1 = p;
     p += align256((size_t)T * HW * cin * es);
     void *y1 = p;

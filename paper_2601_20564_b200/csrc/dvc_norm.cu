@@ -2,16 +2,114 @@
 // producer (reading R2-R4), with the Batch-dimension temporal
 // shift folded into the element addressing (a3).
 //
+// HBM-bound.  Every thread owns one 8-channel vector of the pixel row and
+// walks pixels with a fixed stride, so (a) the shift / concat / carry source
+// of its vector is resolved once, outside the pixel loop, (b) a warp reads
+// 32 consecutive 16-byte vectors (coalesced), (c) the per-channel GN
+// coefficients live in registers.
+//
 // Statistics are deterministic and independent of batching (H4): frame t's
 // (mean, rstd) per group come only from frame t's shifted input, reduced in a
 // fixed order (per-thread fp64 sums over a fixed pixel stride, fixed-order
-// merge over 128-pixel chunks).  HBM-bound: one read of the operand.
+// smem merge per 256-pixel chunk, fixed-order merge over chunks).
 #include "dvc_norm.cuh"
 
 namespace dvc {
 
-constexpr int kStatPix = 128;   // pixels per partial-statistics chunk
+constexpr int kPixPerThread = 16;   // pixels per thread per statistics / apply block
 
+// pixels per block: every thread owns one 8-channel vector and kPixPerThread pixels
+__host__ __device__ __forceinline__ int chunk_pix(int C) { return (256 / (C >> 3)) * kPixPerThread; }
+
+// Source of one thread's 8-channel vector of the (shifted, concatenated) operand
+// for frame t.  mode: 0 = zeros, 1 = vector load, 2 = per-element carry, 3 = straddle.
+template <typename T>
+struct VecSrc {
+    const T *cur;      // unshifted row base for this vector (frame t), stride `ld`
+    const T *prev;     // shifted-slice source: frame t-1 row base (stride ld) or carry (stride cs)
+    int ld, pstride, c, cs, mode;
+
+    __device__ __forceinline__ void load(int p, float (&f)[8]) const {
+        if (mode == 1) {
+            load8(cur + (size_t)p * ld, f);
+        } else if (mode == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = 0.f;
+        } else if (mode == 2) {   // all 8 channels from the carry [HW][cs] (element loads)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[i] = Elem<T>::to_f(prev[(size_t)p * pstride + i]);
+        } else {                  // straddles the slice boundary: element-wise select
+            float g[8];
+            load8(cur + (size_t)p * ld, f);
+            if (prev == nullptr) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) g[i] = 0.f;
+            } else if (pstride == ld) {
+                load8(prev + (size_t)p * ld, g);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    g[i] = (c + i < cs) ? Elem<T>::to_f(prev[(size_t)p * pstride + i]) : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (c + i < cs) f[i] = g[i];
+        }
+    }
+};
+
+// raw 16-byte vector (8 x 16-bit, or the first half of 8 x fp32 when T is float)
+template <typename T>
+__device__ __forceinline__ void cvt8(const uint4 (&u)[sizeof(T) / 2], float (&f)[8]) {
+    const T *e = reinterpret_cast<const T *>(u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = Elem<T>::to_f(e[i]);
+}
+template <typename T>
+__device__ __forceinline__ void ldraw8(const T *p, uint4 (&u)[sizeof(T) / 2]) {
+#pragma unroll
+    for (int k = 0; k < (int)(sizeof(T) / 2); ++k) u[k] = __ldg(reinterpret_cast<const uint4 *>(p) + k);
+}
+
+// Resolve the source of vector `v` (channels 8v..8v+7) of frame t.
+template <typename T>
+__device__ __forceinline__ VecSrc<T> vec_src(const ShiftSrc<T> &X, int t, int v) {
+    VecSrc<T> s;
+    const int c = 8 * v;
+    const bool in_a = c < X.ca;
+    const T *base = in_a ? X.xa : X.xb;
+    const int ld = in_a ? X.ca : X.cb;
+    const int cc = in_a ? c : c - X.ca;
+    s.ld = ld;
+    s.c = c;
+    s.cs = X.cs;
+    s.cur = base + (size_t)t * X.HW * ld + cc;
+    s.prev = nullptr;
+    s.pstride = ld;
+    if (c >= X.cs) {
+        s.mode = 1;
+        return s;
+    }
+    // (part of) the shifted slice: frame t-1, or the carry at t == 0 (zeros if none)
+    if (t > 0) {
+        s.prev = base + (size_t)(t - 1) * X.HW * ld + cc;
+        if (c + 8 <= X.cs) {
+            s.cur = s.prev;
+            s.mode = 1;
+        } else {
+            s.mode = 3;
+        }
+    } else if (X.carry == nullptr) {
+        s.mode = c + 8 <= X.cs ? 0 : 3;
+    } else {
+        s.prev = X.carry + c;
+        s.pstride = X.cs;
+        s.mode = c + 8 <= X.cs ? 2 : 3;
+    }
+    return s;
+}
+
+// Partial sums per (frame, chunk, group): grid (nchunk, T), 256 threads.
 template <typename T>
 __global__ void __launch_bounds__(256) gn_partial_kernel(const ShiftSrc<T> X, int G, double2 *__restrict__ partial,
                                                          int nchunk) {
@@ -20,24 +118,48 @@ __global__ void __launch_bounds__(256) gn_partial_kernel(const ShiftSrc<T> X, in
     const int t = blockIdx.y, chunk = blockIdx.x;
     const int C = X.C(), nv = C >> 3, npl = 256 / nv;
     const int tid = threadIdx.x, v = tid % nv, pl = tid / nv;
-    const int p0 = chunk * kStatPix, p1 = min(X.HW, p0 + kStatPix);
+    const int cp = chunk_pix(C);
+    const int p0 = chunk * cp, p1 = min(X.HW, p0 + cp);
     if (pl < npl) {
-        double s[8], q[8];
+        const VecSrc<T> src = vec_src(X, t, v);
+        // fp32 partial over <= kPixPerThread values per channel; fp64 from the block merge on
+        float s[8], q[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s[i] = q[i] = 0.0;
-        for (int p = p0 + pl; p < p1; p += npl) {
+        for (int i = 0; i < 8; ++i) s[i] = q[i] = 0.f;
+        int p = p0 + pl;
+        if (src.mode == 1) {   // hot path: plain strided vector loads, 4 in flight before any use
+            constexpr int NU = sizeof(T) / 2;
+            for (; p + 3 * npl < p1; p += 4 * npl) {
+                uint4 u0[NU], u1[NU], u2[NU], u3[NU];
+                ldraw8(src.cur + (size_t)p * src.ld, u0);
+                ldraw8(src.cur + (size_t)(p + npl) * src.ld, u1);
+                ldraw8(src.cur + (size_t)(p + 2 * npl) * src.ld, u2);
+                ldraw8(src.cur + (size_t)(p + 3 * npl) * src.ld, u3);
+                float f0[8], f1[8], f2[8], f3[8];
+                cvt8<T>(u0, f0);
+                cvt8<T>(u1, f1);
+                cvt8<T>(u2, f2);
+                cvt8<T>(u3, f3);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    s[i] += (f0[i] + f1[i]) + (f2[i] + f3[i]);
+                    q[i] = fmaf(f0[i], f0[i], fmaf(f1[i], f1[i], fmaf(f2[i], f2[i], fmaf(f3[i], f3[i], q[i]))));
+                }
+            }
+        }
+        for (; p < p1; p += npl) {
             float f[8];
-            X.shifted8(t, p, v * 8, f);
+            src.load(p, f);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                s[i] += (double)f[i];
-                q[i] = fma((double)f[i], (double)f[i], q[i]);
+                s[i] += f[i];
+                q[i] = fmaf(f[i], f[i], q[i]);
             }
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            s_sum[pl * C + v * 8 + i] = s[i];
-            s_sq[pl * C + v * 8 + i] = q[i];
+            s_sum[pl * C + v * 8 + i] = (double)s[i];
+            s_sq[pl * C + v * 8 + i] = (double)q[i];
         }
     }
     __syncthreads();
@@ -53,67 +175,127 @@ __global__ void __launch_bounds__(256) gn_partial_kernel(const ShiftSrc<T> X, in
     }
 }
 
-__global__ void gn_finalize_kernel(const double2 *__restrict__ partial, int nchunk, int G, int T, double n, double eps,
-                                   float2 *__restrict__ stats) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= T * G) return;
-    const int t = i / G, g = i % G;
-    double S = 0.0, Q = 0.0;
-    for (int c = 0; c < nchunk; ++c) {
-        double2 v = partial[((size_t)t * nchunk + c) * G + g];
-        S += v.x;
-        Q += v.y;
+// coef[t][c] = (mean of c's group, rstd * gamma[c]): grid (T), 256 threads.
+// One warp per group: lanes take chunks l, l+32, ... and a fixed xor-shuffle
+// tree merges them (deterministic for a given nchunk).
+template <typename T>
+__global__ void __launch_bounds__(256) gn_finalize_kernel(const double2 *__restrict__ partial, int nchunk, int G,
+                                                          int C, double n, double eps, const T *__restrict__ gamma,
+                                                          float2 *__restrict__ coef) {
+    __shared__ float s_mu[256], s_rs[256];
+    const int t = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int g = warp; g < G; g += blockDim.x >> 5) {
+        double S = 0.0, Q = 0.0;
+        for (int c = lane; c < nchunk; c += 32) {
+            const double2 v = partial[((size_t)t * nchunk + c) * G + g];
+            S += v.x;
+            Q += v.y;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            S += __shfl_xor_sync(0xffffffffu, S, o);
+            Q += __shfl_xor_sync(0xffffffffu, Q, o);
+        }
+        if (lane == 0) {
+            const double mu = S / n;
+            double var = Q / n - mu * mu;   // biased variance (R4)
+            if (var < 0.0) var = 0.0;
+            s_mu[g] = (float)mu;
+            s_rs[g] = (float)(1.0 / sqrt(var + eps));
+        }
     }
-    const double mu = S / n;
-    double var = Q / n - mu * mu;   // biased variance (R4)
-    if (var < 0.0) var = 0.0;
-    stats[i] = make_float2((float)mu, (float)(1.0 / sqrt(var + eps)));
+    __syncthreads();
+    const int cg = C / G;
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+        const int g = c / cg;
+        coef[(size_t)t * C + c] = make_float2(s_mu[g], s_rs[g] * Elem<T>::to_f(gamma[c]));
+    }
 }
 
-// out[t][p][c] = SiLU((Xs[t][p][c] - mu[t,g]) * rstd[t,g] * gamma[c] + beta[c])
+// SiLU(z) = z / (1 + e^-z).  16-bit outputs: one MUFU (ex2) per element and a
+// Newton reciprocal on the FMA pipe (rel. error < 1e-6, far below the 16-bit
+// rounding of the result); the MUFU pipe would otherwise bound this HBM kernel.
 template <typename T>
-__global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const float2 *__restrict__ stats, int G,
-                                                      const T *__restrict__ gamma, const T *__restrict__ beta,
-                                                      T *__restrict__ out, long nvec) {
-    const int C = X.C(), nv = C >> 3, cg = C / G;
-    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (long)gridDim.x * blockDim.x) {
-        const int v = (int)(i % nv);
-        const long pix = i / nv;
-        const int t = (int)(pix / X.HW), p = (int)(pix % X.HW);
-        float f[8];
-        X.shifted8(t, p, v * 8, f);
+__device__ __forceinline__ float silu_t(float z) {
+    if constexpr (sizeof(T) == 4) {
+        return z / (1.0f + expf(-z));   // validation mode: accurate
+    } else {
+        const float e = exp2f(fmaxf(z, -80.f) * -1.4426950408889634f);   // ex2.approx (fast-math free: exp2f)
+        const float d = 1.0f + e;                                          // in [1, 2^116)
+        float r = __int_as_float(0x7EF311C3 - __float_as_int(d));         // ~1/d to 4 bits
+        r = r * (2.0f - d * r);
+        r = r * (2.0f - d * r);
+        r = r * (2.0f - d * r);
+        return z * r;
+    }
+}
+
+// out[t][p][c] = SiLU((Xs[t][p][c] - mu) * (rstd*gamma[c]) + beta[c]): grid (nchunk, T).
+template <typename T>
+__global__ void __launch_bounds__(256, 4) gn_silu_kernel(const ShiftSrc<T> X, const float2 *__restrict__ coef,
+                                                      const T *__restrict__ beta, T *__restrict__ out) {
+    const int t = blockIdx.y, chunk = blockIdx.x;
+    const int C = X.C(), nv = C >> 3, npl = 256 / nv;
+    const int tid = threadIdx.x, v = tid % nv, pl = tid / nv;
+    if (pl >= npl) return;
+    const int cp = chunk_pix(C);
+    const int p0 = chunk * cp, p1 = min(X.HW, p0 + cp);
+    const VecSrc<T> src = vec_src(X, t, v);
+    float mu[8], sc[8], be[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int c = v * 8 + k;
-            const float2 st = stats[t * G + c / cg];
-            const float z = (f[k] - st.x) * st.y * Elem<T>::to_f(gamma[c]) + Elem<T>::to_f(beta[c]);
-            f[k] = silu_f(z);
+    for (int i = 0; i < 8; ++i) {
+        const float2 cf = coef[(size_t)t * C + 8 * v + i];
+        mu[i] = cf.x;
+        sc[i] = cf.y;
+        be[i] = Elem<T>::to_f(beta[8 * v + i]);
+    }
+    T *o = out + (size_t)t * X.HW * C + 8 * v;
+    int p = p0 + pl;
+    if (src.mode == 1) {   // hot path: 4 raw vector loads in flight, then compute + store
+        constexpr int NU = sizeof(T) / 2;
+        for (; p + 3 * npl < p1; p += 4 * npl) {
+            uint4 u[4][NU];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ldraw8(src.cur + (size_t)(p + j * npl) * src.ld, u[j]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float f[8];
+                cvt8<T>(u[j], f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] = silu_t<T>((f[i] - mu[i]) * sc[i] + be[i]);
+                store8(o + (size_t)(p + j * npl) * C, f);
+            }
         }
-        store8(out + pix * C + v * 8, f);
+    }
+    for (; p < p1; p += npl) {
+        float f[8];
+        src.load(p, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = silu_t<T>((f[i] - mu[i]) * sc[i] + be[i]);
+        store8(o + (size_t)p * C, f);
     }
 }
 
 // Test-only: materialise Xs with the same addressing (dvc_debug_shift_gather).
 template <typename T>
-__global__ void shift_gather_kernel(const ShiftSrc<T> X, T *__restrict__ out, long nvec) {
-    const int C = X.C(), nv = C >> 3;
-    for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (long)gridDim.x * blockDim.x) {
-        const int v = (int)(i % nv);
-        const long pix = i / nv;
+__global__ void __launch_bounds__(256) shift_gather_kernel(const ShiftSrc<T> X, T *__restrict__ out) {
+    const int t = blockIdx.y, chunk = blockIdx.x;
+    const int C = X.C(), nv = C >> 3, npl = 256 / nv;
+    const int tid = threadIdx.x, v = tid % nv, pl = tid / nv;
+    if (pl >= npl) return;
+    const int cp = chunk_pix(C);
+    const int p0 = chunk * cp, p1 = min(X.HW, p0 + cp);
+    const VecSrc<T> src = vec_src(X, t, v);
+    for (int p = p0 + pl; p < p1; p += npl) {
         float f[8];
-        X.shifted8((int)(pix / X.HW), (int)(pix % X.HW), v * 8, f);
-        store8(out + pix * C + v * 8, f);   // exact: 16-bit -> fp32 -> 16-bit round trip is the identity
+        src.load(p, f);
+        store8(out + ((size_t)t * X.HW + p) * C + 8 * v, f);   // exact: 16-bit -> fp32 -> 16-bit is the identity
     }
 }
 
-size_t gn_workspace_bytes(int T, int HW, int G) {
-    const int nchunk = (HW + kStatPix - 1) / kStatPix;
-    return align256((size_t)T * nchunk * G * sizeof(double2)) + align256((size_t)T * G * sizeof(float2));
-}
-
-static int grid_for(long nvec) {
-    long b = (nvec + 255) / 256;
-    return (int)(b < 148L * 16 ? b : 148L * 16);
+size_t gn_workspace_bytes(int T, int HW, int G, int C) {
+    const int nchunk = (HW + chunk_pix(C) - 1) / chunk_pix(C);
+    return align256((size_t)T * nchunk * G * sizeof(double2)) + align256((size_t)T * C * sizeof(float2));
 }
 
 template <typename T>
@@ -121,19 +303,17 @@ static dvc_status gn_silu_t(const NormArgs &a, cudaStream_t stream) {
     ShiftSrc<T> X{reinterpret_cast<const T *>(a.xa), reinterpret_cast<const T *>(a.xb),
                   reinterpret_cast<const T *>(a.carry), a.ca, a.cb, a.cs, a.HW};
     const int C = a.ca + a.cb;
-    const int nchunk = (a.HW + kStatPix - 1) / kStatPix;
+    const int nchunk = (a.HW + chunk_pix(C) - 1) / chunk_pix(C);
     double2 *partial = reinterpret_cast<double2 *>(a.ws);
-    float2 *stats = reinterpret_cast<float2 *>(reinterpret_cast<uint8_t *>(a.ws) +
-                                               align256((size_t)a.T * nchunk * a.G * sizeof(double2)));
+    float2 *coef = reinterpret_cast<float2 *>(reinterpret_cast<uint8_t *>(a.ws) +
+                                              align256((size_t)a.T * nchunk * a.G * sizeof(double2)));
     gn_partial_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, a.G, partial, nchunk);
     ++g_launches;
-    gn_finalize_kernel<<<(a.T * a.G + 127) / 128, 128, 0, stream>>>(partial, nchunk, a.G, a.T,
-                                                                    (double)(C / a.G) * a.HW, (double)a.eps, stats);
+    gn_finalize_kernel<T><<<a.T, 256, 0, stream>>>(partial, nchunk, a.G, C, (double)(C / a.G) * a.HW, (double)a.eps,
+                                                   reinterpret_cast<const T *>(a.gamma), coef);
     ++g_launches;
-    const long nvec = (long)a.T * a.HW * (C / 8);
-    gn_silu_kernel<T><<<grid_for(nvec), 256, 0, stream>>>(X, stats, a.G, reinterpret_cast<const T *>(a.gamma),
-                                                          reinterpret_cast<const T *>(a.beta),
-                                                          reinterpret_cast<T *>(a.out), nvec);
+    gn_silu_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, coef, reinterpret_cast<const T *>(a.beta),
+                                                             reinterpret_cast<T *>(a.out));
     ++g_launches;
     return check_launch("gn_silu");
 }
@@ -142,7 +322,7 @@ dvc_status gn_silu_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream) {
     const int C = a.ca + a.cb;
     DVC_CHECK_ARG(a.ca % 8 == 0 && a.cb % 8 == 0 && C / 8 <= 256, DVC_ERR_UNSUPPORTED,
                   "GN: channel counts must be multiples of 8 and at most 2048");
-    DVC_CHECK_ARG(a.G >= 1 && C % a.G == 0, DVC_ERR_DIVISIBILITY, "GN: G=%d must divide C=%d", a.G, C);
+    DVC_CHECK_ARG(a.G >= 1 && a.G <= 256 && C % a.G == 0, DVC_ERR_DIVISIBILITY, "GN: G=%d must divide C=%d", a.G, C);
     DVC_CHECK_ARG(a.cs <= a.ca, DVC_ERR_UNSUPPORTED, "shift slice must lie in the first source");
     switch (dt) {
         case DVC_BF16: return gn_silu_t<__nv_bfloat16>(a, stream);
@@ -155,20 +335,45 @@ template <typename T>
 static dvc_status gather_t(const NormArgs &a, cudaStream_t stream) {
     ShiftSrc<T> X{reinterpret_cast<const T *>(a.xa), reinterpret_cast<const T *>(a.xb),
                   reinterpret_cast<const T *>(a.carry), a.ca, a.cb, a.cs, a.HW};
-    const long nvec = (long)a.T * a.HW * ((a.ca + a.cb) / 8);
-    shift_gather_kernel<T><<<grid_for(nvec), 256, 0, stream>>>(X, reinterpret_cast<T *>(a.out), nvec);
+    const int nchunk = (a.HW + chunk_pix(a.ca + a.cb) - 1) / chunk_pix(a.ca + a.cb);
+    shift_gather_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, reinterpret_cast<T *>(a.out));
     ++g_launches;
     return check_launch("shift_gather");
 }
 
 dvc_status shift_gather_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream) {
-    DVC_CHECK_ARG(a.ca % 8 == 0 && a.cb % 8 == 0, DVC_ERR_UNSUPPORTED, "gather: channels must be multiples of 8");
+    DVC_CHECK_ARG(a.ca % 8 == 0 && a.cb % 8 == 0 && (a.ca + a.cb) / 8 <= 256, DVC_ERR_UNSUPPORTED,
+                  "gather: channels must be multiples of 8, at most 2048");
     DVC_CHECK_ARG(a.cs <= a.ca, DVC_ERR_UNSUPPORTED, "shift slice must lie in the first source");
     switch (dt) {
         case DVC_BF16: return gather_t<__nv_bfloat16>(a, stream);
         case DVC_F16: return gather_t<__half>(a, stream);
         default: return gather_t<float>(a, stream);
     }
+}
+
+// ----------------------------------------------------------------- nearest resize (R11)
+// U[t][y][x][c] = V[t][floor(y*hi/ho)][floor(x*wi/wo)][c]: materialises the
+// up-sampler's operand so its 3x3 conv runs on the TMA engine.  Exact copy.
+__global__ void __launch_bounds__(256) nearest_kernel(const uint4 *__restrict__ V, uint4 *__restrict__ U, int hi,
+                                                      int wi, int ho, int wo, int nvec) {
+    const int y = blockIdx.y, t = blockIdx.z;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;   // x * nvec + v within the output row
+    if (i >= wo * nvec) return;
+    const int x = i / nvec, v = i - x * nvec;
+    const int sy = (int)(((long)y * hi) / ho), sx = (int)(((long)x * wi) / wo);
+    U[(((size_t)t * ho + y) * wo) * nvec + i] = __ldg(V + (((size_t)t * hi + sy) * wi + sx) * nvec + v);
+}
+
+dvc_status nearest_run(const void *src, void *dst, int T, int hi, int wi, int ho, int wo, int C, dvc_dtype dt,
+                       cudaStream_t stream) {
+    DVC_CHECK_ARG((C * dt_size(dt)) % 16 == 0, DVC_ERR_UNSUPPORTED, "nearest: rows must be 16-byte multiples");
+    const int nvec = (int)(C * dt_size(dt) / 16);
+    dim3 grid((wo * nvec + 255) / 256, ho, T);
+    nearest_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const uint4 *>(src), reinterpret_cast<uint4 *>(dst), hi, wi,
+                                             ho, wo, nvec);
+    ++g_launches;
+    return check_launch("nearest");
 }
 
 }  // namespace dvc

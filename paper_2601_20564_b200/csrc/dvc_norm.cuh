@@ -17,7 +17,9 @@ struct NormArgs {
     void *ws;                // gn_workspace_bytes(T, HW, G)
 };
 
-size_t gn_workspace_bytes(int T, int HW, int G);
+size_t gn_workspace_bytes(int T, int HW, int G, int C);
+dvc_status nearest_run(const void *src, void *dst, int T, int hi, int wi, int ho, int wo, int C, dvc_dtype dt,
+                       cudaStream_t stream);
 dvc_status gn_silu_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream);
 dvc_status shift_gather_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream);
 

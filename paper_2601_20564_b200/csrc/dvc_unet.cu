@@ -204,7 +204,7 @@ size_t plan_workspace(const dvc_unet &n, int T, size_t *offs /* 16 regions */) {
         const int l = n.blevel[b];
         rbws = std::max(rbws, resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, (int)hw(l), c.dt));
     }
-    rbws = std::max(rbws, align256(gn_workspace_bytes(T, (int)hw(0), c.groups)) + T * hw(0) * W[0] * es);
+    rbws = std::max(rbws, align256(gn_workspace_bytes(T, (int)hw(0), c.groups, W[0])) + T * hw(0) * W[0] * es);
     size_t total = 0;
     for (int i = 0; i < 16; ++i) {
         size_t bytes = i == 14 ? rbws : i == 15 ? (n.carry_total * 2 + 2 * hw(0) * 2048) * es : sz[i] * es;
@@ -463,9 +463,18 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
             pp ^= 1;
         }
         if (u < 3) {
-            if ((st = conv3(h, W[l], SEG_UPNEAREST, n->lh[l], n->lw[l], n->us[u], W[l], n->lh[l - 1], n->lw[l - 1],
-                            hb[pp])) != DVC_OK)
-                return st;
+            if (g_ws_cg != 0) {
+                // materialise nearest_to(h, next skip size) (exact copy) so the 3x3 conv runs on the TMA engine
+                if ((st = nearest_run(h, rbws, T, n->lh[l], n->lw[l], n->lh[l - 1], n->lw[l - 1], W[l], dt, s)) !=
+                    DVC_OK)
+                    return st;
+                st = conv3(rbws, W[l], SEG_SAME, n->lh[l - 1], n->lw[l - 1], n->us[u], W[l], n->lh[l - 1],
+                           n->lw[l - 1], hb[pp]);
+            } else {
+                st = conv3(h, W[l], SEG_UPNEAREST, n->lh[l], n->lw[l], n->us[u], W[l], n->lh[l - 1], n->lw[l - 1],
+                           hb[pp]);
+            }
+            if (st != DVC_OK) return st;
             h = hb[pp];
             pp ^= 1;
         }
@@ -473,7 +482,7 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     // out = conv_out(SiLU(GN_out(h)))
     {
         uint8_t *gnws = reinterpret_cast<uint8_t *>(rbws);
-        void *op = gnws + align256(gn_workspace_bytes(T, hw(0), c.groups));
+        void *op = gnws + align256(gn_workspace_bytes(T, hw(0), c.groups, W[0]));
         NormArgs na{h, nullptr, nullptr, W[0], 0, 0, T, hw(0), c.groups, c.eps, n->gno_w, n->gno_b, op, gnws};
         if ((st = gn_silu_run(na, dt, s)) != DVC_OK) return st;
         if ((st = conv3(op, W[0], SEG_SAME, n->lh[0], n->lw[0], n->conv_out, c.c_lat, n->lh[0], n->lw[0], out)) !=
