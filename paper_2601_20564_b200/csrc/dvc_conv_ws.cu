@@ -35,6 +35,7 @@ struct WsParams {
     const void *bias0, *bias1, *residual;
     void *out;
     uint32_t idesc;
+    int dbg;   // perf experiments only (DVC_DEBUG_CONV): 1 skip A TMA, 2 skip B TMA, 4 skip MMA, 8 skip stores
 };
 
 constexpr int kWsThreads = 256;
@@ -110,19 +111,21 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         const int dx = p.seg_taps[s] == 9 ? tap % 3 - 1 : 0;
                         const int col = p.seg_col0[s] + tap * p.seg_tapstride[s];
                         for (int ch = 0; ch < nch; ++ch) {
-                            mbar_wait(&empty[stage], phase ^ 1);
+                            mbar_wait_spin(&empty[stage], phase ^ 1);
                             const uint32_t fb = smem_u32(&full[stage]);
                             const uint32_t dA = smem_u32(sA + stage * A_STAGE);
                             const uint32_t dB = smem_u32(sB + stage * B_STAGE);
+                            const bool la = !(p.dbg & 1), lbb = !(p.dbg & 2);
+                            const uint32_t txs = (uint32_t)CG * ((la ? a_bytes : 0u) + (lbb ? (uint32_t)B_STAGE : 0u));
                             if constexpr (CG == 1) {
-                                mbar_arrive_expect_tx_addr(fb, tx);
-                                tma_load_4d(dA, &p.amap[s], fb, ch * 64, x0 + dx, y0 + dy, t);
-                                tma_load_2d_a(dB, bm, fb, col + ch * 64, n0);
+                                mbar_arrive_expect_tx_addr(fb, txs);
+                                if (la) tma_load_4d(dA, &p.amap[s], fb, ch * 64, x0 + dx, y0 + dy, t);
+                                if (lbb) tma_load_2d_a(dB, bm, fb, col + ch * 64, n0);
                             } else {
-                                if (rank == 0) mbar_arrive_expect_tx_addr(fb, tx);
+                                if (rank == 0) mbar_arrive_expect_tx_addr(fb, txs);
                                 const uint32_t lb = mapa_shared(fb, 0);   // leader's barrier
-                                tma_load_4d_cg2(dA, &p.amap[s], lb, ch * 64, x0 + dx, y0 + dy, t);
-                                tma_load_2d_cg2(dB, bm, lb, col + ch * 64, n0);
+                                if (la) tma_load_4d_cg2(dA, &p.amap[s], lb, ch * 64, x0 + dx, y0 + dy, t);
+                                if (lbb) tma_load_2d_cg2(dB, bm, lb, col + ch * 64, n0);
                             }
                             if (++stage == STAGES) {
                                 stage = 0;
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                     const int nch = (p.seg_c[s] + 63) >> 6;
                     for (int tap = 0; tap < p.seg_taps[s]; ++tap) {
                         for (int ch = 0; ch < nch; ++ch) {
-                            mbar_wait(&full[stage], phase);
+                            mbar_wait_spin(&full[stage], phase);
                             tc_fence_after();
                             const int ksteps = min(64, p.seg_c[s] - ch * 64) >> 4;
                             const uint32_t a0 = smem_u32(sA + stage * A_STAGE);
@@ -158,8 +161,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                             for (int k = 0; k < ksteps; ++k) {
                                 const uint64_t ad = sdesc_sw128(a0 + k * 32);
                                 const uint64_t bd = sdesc_sw128(b0 + k * 32);
-                                if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, first ? 0u : 1u);
-                                else tc_mma_cg2(d, ad, bd, p.idesc, first ? 0u : 1u);
+                                if (!(p.dbg & 4) || first) {
+                                    if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, first ? 0u : 1u);
+                                    else tc_mma_cg2(d, ad, bd, p.idesc, first ? 0u : 1u);
+                                }
                                 first = false;
                             }
                             if constexpr (CG == 1) tc_commit(&empty[stage]);
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                 uint32_t v[16];
                 tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
                 const int n = nt * BN + cc;
-                if (m >= 0) {
+                if (m >= 0 && !(p.dbg & 8)) {
                     float f[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
@@ -336,7 +341,12 @@ static int engine_from_env() {
     if (e && (e[0] == '0' || e[0] == '1' || e[0] == '2') && e[1] == 0) return e[0] - '0';
     return 2;
 }
-int g_ws_cg = engine_from_env();   // 2: CTA-pair MMA (default), 1: single-CTA MMA, 0: gather engine only
+int g_ws_cg = engine_from_env();
+static int dbg_from_env() {
+    const char *e = getenv("DVC_DEBUG_CONV");
+    return e ? atoi(e) : 0;
+}
+static int g_ws_dbg = dbg_from_env();   // 2: CTA-pair MMA (default), 1: single-CTA MMA, 0: gather engine only
 
 bool conv_ws_applicable(const ConvDesc &d) {
     if (g_ws_cg == 0 || d.dt == DVC_F32) return false;
@@ -401,6 +411,7 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
     }
     const int bf = d.dt == DVC_BF16;
     p.idesc = make_idesc(bf, 128 * CG, bn);
+    p.dbg = g_ws_dbg;
     if (CG == 2) {
         if (bf) return launch_ws<__nv_bfloat16, 2, 6>(p, stream);
         return launch_ws<__half, 2, 6>(p, stream);

@@ -16,13 +16,14 @@
 
 namespace dvc {
 
-constexpr int kPixPerThread = 16;   // pixels per thread per statistics / apply block
+constexpr int kPixPerThread = 32;   // pixels per thread per statistics / apply block
 
 // pixels per block: every thread owns one 8-channel vector and kPixPerThread pixels
 __host__ __device__ __forceinline__ int chunk_pix(int C) { return (256 / (C >> 3)) * kPixPerThread; }
 
 // Source of one thread's 8-channel vector of the (shifted, concatenated) operand
-// for frame t.  mode: 0 = zeros, 1 = vector load, 2 = per-element carry, 3 = straddle.
+// for frame t.  mode: 0 = zeros, 1 = vector load, 2 = per-element carry,
+// 3 = straddle with zeros / carry (frame 0), 4 = straddle with frame t-1 (vector loads).
 template <typename T>
 struct VecSrc {
     const T *cur;      // unshifted row base for this vector (frame t), stride `ld`
@@ -38,7 +39,7 @@ struct VecSrc {
         } else if (mode == 2) {   // all 8 channels from the carry [HW][cs] (element loads)
 #pragma unroll
             for (int i = 0; i < 8; ++i) f[i] = Elem<T>::to_f(prev[(size_t)p * pstride + i]);
-        } else {                  // straddles the slice boundary: element-wise select
+        } else {                  // modes 3/4: straddles the slice boundary, element-wise select
             float g[8];
             load8(cur + (size_t)p * ld, f);
             if (prev == nullptr) {
@@ -71,6 +72,34 @@ __device__ __forceinline__ void ldraw8(const T *p, uint4 (&u)[sizeof(T) / 2]) {
     for (int k = 0; k < (int)(sizeof(T) / 2); ++k) u[k] = __ldg(reinterpret_cast<const uint4 *>(p) + k);
 }
 
+// Fast path for modes 1 and 4: issue the raw loads of NP pixels first, convert after.
+template <typename T, int NP, bool STRADDLE>
+__device__ __forceinline__ void load_fast(const VecSrc<T> &src, int p, int step, float (&f)[NP][8]) {
+    constexpr int NU = sizeof(T) / 2;
+    uint4 u[NP][NU];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) ldraw8(src.cur + (size_t)(p + j * step) * src.ld, u[j]);
+    if constexpr (STRADDLE) {
+        uint4 w[NP][NU];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) ldraw8(src.prev + (size_t)(p + j * step) * src.ld, w[j]);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) cvt8<T>(u[j], f[j]);
+        const int k = src.cs - src.c;   // first k channels come from frame t-1
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            float g[8];
+            cvt8<T>(w[j], g);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (i < k) f[j][i] = g[i];
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) cvt8<T>(u[j], f[j]);
+    }
+}
+
 // Resolve the source of vector `v` (channels 8v..8v+7) of frame t.
 template <typename T>
 __device__ __forceinline__ VecSrc<T> vec_src(const ShiftSrc<T> &X, int t, int v) {
@@ -97,7 +126,7 @@ __device__ __forceinline__ VecSrc<T> vec_src(const ShiftSrc<T> &X, int t, int v)
             s.cur = s.prev;
             s.mode = 1;
         } else {
-            s.mode = 3;
+            s.mode = 4;
         }
     } else if (X.carry == nullptr) {
         s.mode = c + 8 <= X.cs ? 0 : 3;
@@ -111,7 +140,7 @@ __device__ __forceinline__ VecSrc<T> vec_src(const ShiftSrc<T> &X, int t, int v)
 
 // Partial sums per (frame, chunk, group): grid (nchunk, T), 256 threads.
 template <typename T>
-__global__ void __launch_bounds__(256) gn_partial_kernel(const ShiftSrc<T> X, int G, double2 *__restrict__ partial,
+__global__ void __launch_bounds__(256, 3) gn_partial_kernel(const ShiftSrc<T> X, int G, double2 *__restrict__ partial,
                                                          int nchunk) {
     __shared__ double s_sum[2048];
     __shared__ double s_sq[2048];
@@ -126,24 +155,24 @@ __global__ void __launch_bounds__(256) gn_partial_kernel(const ShiftSrc<T> X, in
         float s[8], q[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) s[i] = q[i] = 0.f;
+        // identical arithmetic for every source mode and every T (bit-exact batch == online, H4):
+        // pixels are accumulated one at a time in increasing p.
+        constexpr int NU = sizeof(T) / 2;
         int p = p0 + pl;
-        if (src.mode == 1) {   // hot path: plain strided vector loads, 4 in flight before any use
-            constexpr int NU = sizeof(T) / 2;
+        if (src.mode == 1) {   // hot path: raw loads of 4 pixels in flight before any use
             for (; p + 3 * npl < p1; p += 4 * npl) {
-                uint4 u0[NU], u1[NU], u2[NU], u3[NU];
-                ldraw8(src.cur + (size_t)p * src.ld, u0);
-                ldraw8(src.cur + (size_t)(p + npl) * src.ld, u1);
-                ldraw8(src.cur + (size_t)(p + 2 * npl) * src.ld, u2);
-                ldraw8(src.cur + (size_t)(p + 3 * npl) * src.ld, u3);
-                float f0[8], f1[8], f2[8], f3[8];
-                cvt8<T>(u0, f0);
-                cvt8<T>(u1, f1);
-                cvt8<T>(u2, f2);
-                cvt8<T>(u3, f3);
+                uint4 u[4][NU];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    s[i] += (f0[i] + f1[i]) + (f2[i] + f3[i]);
-                    q[i] = fmaf(f0[i], f0[i], fmaf(f1[i], f1[i], fmaf(f2[i], f2[i], fmaf(f3[i], f3[i], q[i]))));
+                for (int j = 0; j < 4; ++j) ldraw8(src.cur + (size_t)(p + j * npl) * src.ld, u[j]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    float f[8];
+                    cvt8<T>(u[j], f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        s[i] += f[i];
+                        q[i] = fmaf(f[i], f[i], q[i]);
+                    }
                 }
             }
         }
@@ -232,7 +261,7 @@ __device__ __forceinline__ float silu_t(float z) {
 
 // out[t][p][c] = SiLU((Xs[t][p][c] - mu) * (rstd*gamma[c]) + beta[c]): grid (nchunk, T).
 template <typename T>
-__global__ void __launch_bounds__(256, 4) gn_silu_kernel(const ShiftSrc<T> X, const float2 *__restrict__ coef,
+__global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const float2 *__restrict__ coef,
                                                       const T *__restrict__ beta, T *__restrict__ out) {
     const int t = blockIdx.y, chunk = blockIdx.x;
     const int C = X.C(), nv = C >> 3, npl = 256 / nv;
@@ -251,19 +280,26 @@ __global__ void __launch_bounds__(256, 4) gn_silu_kernel(const ShiftSrc<T> X, co
     }
     T *o = out + (size_t)t * X.HW * C + 8 * v;
     int p = p0 + pl;
-    if (src.mode == 1) {   // hot path: 4 raw vector loads in flight, then compute + store
-        constexpr int NU = sizeof(T) / 2;
+    if (src.mode == 1) {   // hot path: 4 pixels' raw loads in flight, then compute + store
         for (; p + 3 * npl < p1; p += 4 * npl) {
-            uint4 u[4][NU];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) ldraw8(src.cur + (size_t)(p + j * npl) * src.ld, u[j]);
+            float f[4][8];
+            load_fast<T, 4, false>(src, p, npl, f);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                float f[8];
-                cvt8<T>(u[j], f);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) f[i] = silu_t<T>((f[i] - mu[i]) * sc[i] + be[i]);
-                store8(o + (size_t)(p + j * npl) * C, f);
+                for (int i = 0; i < 8; ++i) f[j][i] = silu_t<T>((f[j][i] - mu[i]) * sc[i] + be[i]);
+                store8(o + (size_t)(p + j * npl) * C, f[j]);
+            }
+        }
+    } else if (src.mode == 4) {   // vector straddling the shifted slice: two sources, 2 pixels in flight
+        for (; p + npl < p1; p += 2 * npl) {
+            float f[2][8];
+            load_fast<T, 2, true>(src, p, npl, f);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[j][i] = silu_t<T>((f[j][i] - mu[i]) * sc[i] + be[i]);
+                store8(o + (size_t)(p + j * npl) * C, f[j]);
             }
         }
     }

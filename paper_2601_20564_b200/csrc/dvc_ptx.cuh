@@ -28,6 +28,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// latency-critical wait (pipeline producer / MMA issuer): poll without a suspend hint
+__device__ __forceinline__ bool mbar_try_wait_nohint(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *b, uint32_t parity) {
+    uint32_t a = smem_u32(b);
+    while (!mbar_try_wait_nohint(a, parity)) {
+    }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
     uint32_t a = smem_u32(b);
     while (!mbar_try_wait(a, parity)) {
