@@ -71,11 +71,17 @@ void prof_end(ProfSlot s, cudaStream_t stream, double flops) {
 }
 
 // ----------------------------------------------------------------- ResBlock (a3-a8)
-size_t resblock_ws_bytes(int ca, int cb, int cout, int G, int T, int HW, dvc_dtype dt) {
+static bool box_mode(const RB &b) {
+    const int cin = b.ca + b.cb, cs = cin / b.P, cg = cin / b.G;
+    return cs % cg == 0;   // the shifted slice is whole GN groups: statistics from box partials
+}
+
+size_t resblock_ws_bytes(int ca, int cb, int cout, int G, int T, int H, int W, dvc_dtype dt) {
     const size_t es = dt_size(dt);
-    const int cin = ca + cb;
+    const int cin = ca + cb, HW = H * W;
     return align256(gn_workspace_bytes(T, HW, G, cin > cout ? cin : cout)) + align256((size_t)T * HW * cin * es) +
-           2 * align256((size_t)T * HW * cout * es);
+           2 * align256((size_t)T * HW * cout * es) + box_stats_bytes(T, H, W, ca) + box_stats_bytes(T, H, W, cb) +
+           box_stats_bytes(1, H, W, cin) + box_stats_bytes(T, H, W, cout) + 4 * 256;
 }
 
 dvc_status resblock_validate(const RB &b, int T, int H, int W) {
@@ -101,9 +107,13 @@ dvc_status resblock_validate(const RB &b, int T, int H, int W) {
     return DVC_OK;
 }
 
-// The block as a launch sequence.  ws holds GN scratch, H1 [T][HW][C_in], Y1 and H2 [T][HW][C_out].
+// The block as a launch sequence.  ws holds GN scratch, H1 [T][HW][C_in], Y1 and H2
+// [T][HW][C_out] and the box statistics.  stats_a / stats_b: box statistics of x_a /
+// x_b if the caller has them (produced by the previous conv's epilogue), else they
+// are computed here; stats_y: where to put the box statistics of y (or null).
 dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, int H, int W, const void *carry_in,
-                           void *carry_out, void *y, void *ws, cudaStream_t stream) {
+                           void *carry_out, void *y, void *ws, cudaStream_t stream, const void *stats_a,
+                           const void *stats_b, void *stats_y) {
     const int HW = H * W, cin = b.ca + b.cb, cs = cin / b.P;
     const size_t es = dt_size(b.dt);
     uint8_t *p = reinterpret_cast<uint8_t *>(ws);
@@ -114,6 +124,14 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
     void *y1 = p;
     p += align256((size_t)T * HW * b.cout * es);
     void *h2 = p;
+    p += align256((size_t)T * HW * b.cout * es);
+    void *st_a = p;
+    p += box_stats_bytes(T, H, W, b.ca);
+    void *st_b = p;
+    p += box_stats_bytes(T, H, W, b.cb);
+    void *st_k = p;
+    p += box_stats_bytes(1, H, W, cin);
+    void *st_y1 = p;
     dvc_status st;
     // carry_out = X[T-1][..., 0:C_in/P] (raw input, before this block overwrites nothing; y never aliases x)
     if (carry_out) {
@@ -121,10 +139,32 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
                                                            (size_t)(T - 1) * HW * b.ca * es,
                                    b.ca * es, cs * es, HW, cudaMemcpyDeviceToDevice, stream));
     }
+    const bool boxed = box_mode(b);
     // a3 + a4: H1 = SiLU(GN1(shift(X, carry)))
     NormArgs n1{xa, xb, carry_in, b.ca, b.cb, cs, T, HW, b.G, b.eps, b.gn1_w, b.gn1_b, h1, gnws};
-    if ((st = gn_silu_run(n1, b.dt, stream)) != DVC_OK) return st;
-    // a5: Y1 = conv3x3(H1) + b1
+    if (boxed) {
+        if (!stats_a) {
+            if ((st = box_stats_run(xa, T, H, W, b.ca, b.dt, reinterpret_cast<float *>(st_a), stream)) != DVC_OK)
+                return st;
+            stats_a = st_a;
+        }
+        if (b.cb > 0 && !stats_b) {
+            if ((st = box_stats_run(xb, T, H, W, b.cb, b.dt, reinterpret_cast<float *>(st_b), stream)) != DVC_OK)
+                return st;
+            stats_b = st_b;
+        }
+        const void *stats_k = nullptr;
+        if (carry_in) {
+            if ((st = box_stats_run(carry_in, 1, H, W, cs, b.dt, reinterpret_cast<float *>(st_k), stream)) != DVC_OK)
+                return st;
+            stats_k = st_k;
+        }
+        st = gn_silu_box_run(n1, BoxStatsIn{stats_a, b.cb > 0 ? stats_b : nullptr, stats_k}, H, W, b.dt, stream);
+    } else {
+        st = gn_silu_run(n1, b.dt, stream);
+    }
+    if (st != DVC_OK) return st;
+    // a5: Y1 = conv3x3(H1) + b1   (+ box statistics of Y1 from the epilogue)
     ConvDesc c1{};
     c1.seg[0] = ConvSeg{h1, cin, SEG_SAME, H, W, 9, b.conv1_w, 9 * cin, 0, cin};
     c1.nseg = 1;
@@ -134,11 +174,14 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
     c1.cout = b.cout;
     c1.bias0 = b.conv1_b;
     c1.out = y1;
+    c1.stats_out = boxed ? st_y1 : nullptr;
     c1.dt = b.dt;
     if ((st = conv_run(c1, stream)) != DVC_OK) return st;
     // a6: H2 = SiLU(GN2(Y1))
     NormArgs n2{y1, nullptr, nullptr, b.cout, 0, 0, T, HW, b.G, b.eps, b.gn2_w, b.gn2_b, h2, gnws};
-    if ((st = gn_silu_run(n2, b.dt, stream)) != DVC_OK) return st;
+    st = boxed ? gn_silu_box_run(n2, BoxStatsIn{st_y1, nullptr, nullptr}, H, W, b.dt, stream)
+               : gn_silu_run(n2, b.dt, stream);
+    if (st != DVC_OK) return st;
     // a7 + a8: Out = S(X) + conv3x3(H2) + b2; the 1x1 shortcut on the UNSHIFTED X is
     // extra K segments of the same GEMM (same fp32 accumulator), identity = epilogue add.
     ConvDesc c2{};
@@ -157,6 +200,7 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
     c2.cout = b.cout;
     c2.bias0 = b.conv2_b;
     c2.out = y;
+    c2.stats_out = stats_y;
     c2.dt = b.dt;
     return conv_run(c2, stream);
 }
@@ -289,7 +333,7 @@ dvc_status dvc_resblock_workspace_size(const dvc_resblock *b, int T, int H, int 
     RB r = rb_from_abi(b);
     DVC_CHECK_ARG(r.G >= 1 && r.ca >= 0 && r.cb >= 0 && r.cout >= 0 && T >= 1 && H >= 1 && W >= 1, DVC_ERR_ARG,
                   "bad sizes");
-    *bytes = resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, H * W, r.dt);
+    *bytes = resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, H, W, r.dt);
     return DVC_OK;
 }
 
@@ -301,7 +345,7 @@ dvc_status dvc_resblock_tsm_forward(const dvc_resblock *b, const void *x_a, cons
     dvc_status st = resblock_validate(r, T, H, W);
     if (st != DVC_OK) return st;
     DVC_CHECK_ARG(r.cb == 0 || x_b != nullptr, DVC_ERR_ARG, "x_b is null but c_b > 0");
-    DVC_CHECK_ARG(ws_bytes >= resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, H * W, r.dt), DVC_ERR_WORKSPACE,
+    DVC_CHECK_ARG(ws_bytes >= resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, H, W, r.dt), DVC_ERR_WORKSPACE,
                   "workspace too small");
     DVC_CHECK_ARG(((uintptr_t)workspace & 255) == 0, DVC_ERR_ARG, "workspace must be 256-byte aligned");
     if ((st = check_device()) != DVC_OK) return st;

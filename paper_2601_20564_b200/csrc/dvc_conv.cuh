@@ -36,9 +36,20 @@ struct ConvDesc {
     const void *bias0, *bias1;   // [cout] or null
     const void *residual;        // [M][cout] or null
     void *out;                   // [M][cout]
+    void *stats_out;             // per-channel box statistics of out (dvc_boxstats.cuh) or null
     dvc_dtype dt;
     long M() const { return (long)T * ho * wo; }
 };
+
+// spatial box of the TMA engine / box statistics for an H x W frame
+void choose_box(int H, int W, int *BX, int *BY);
+inline int boxes_per_frame(int H, int W) {
+    int bx = 1, by = 1;
+    choose_box(H, W, &bx, &by);
+    return ((H + by - 1) / by) * ((W + bx - 1) / bx);
+}
+// standalone box statistics of a [T][H][W][C] tensor (same bits as the conv epilogue)
+dvc_status box_stats_run(const void *x, int T, int H, int W, int C, dvc_dtype dt, float *stats, cudaStream_t stream);
 
 // live per-launch event timing (dvc_profile_begin/end)
 struct ProfSlot {

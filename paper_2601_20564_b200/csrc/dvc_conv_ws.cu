@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include "dvc_conv.cuh"
 #include "dvc_ptx.cuh"
+#include "dvc_boxstats.cuh"
 
 namespace dvc {
 
@@ -35,7 +36,8 @@ struct WsParams {
     const void *bias0, *bias1, *residual;
     void *out;
     uint32_t idesc;
-    int dbg;   // perf experiments only (DVC_DEBUG_CONV): 1 skip A TMA, 2 skip B TMA, 4 skip MMA, 8 skip stores
+    float *stats;   // per-channel box statistics of the output (dvc_boxstats.cuh), or null
+    int dbg;   // perf experiments only (DVC_DEBUG_CONV): 1 skip A TMA, 2 skip B TMA, 4 skip MMA, 8 skip stores, 16 skip epilogue
 };
 
 constexpr int kWsThreads = 256;
@@ -54,6 +56,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][4][32] box-statistics staging
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -83,7 +86,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
-        if (lane == 0) {
+        // the whole warp walks the (warp-uniform) loop; one elected lane issues
+        {
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t a_bytes = (uint32_t)(p.BX * p.BY * 128);
@@ -111,15 +115,17 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         const int dx = p.seg_taps[s] == 9 ? tap % 3 - 1 : 0;
                         const int col = p.seg_col0[s] + tap * p.seg_tapstride[s];
                         for (int ch = 0; ch < nch; ++ch) {
-                            mbar_wait_spin(&empty[stage], phase ^ 1);
+                            if (!(p.dbg & 32)) mbar_wait_spin(&empty[stage], phase ^ 1);
                             const uint32_t fb = smem_u32(&full[stage]);
                             const uint32_t dA = smem_u32(sA + stage * A_STAGE);
                             const uint32_t dB = smem_u32(sB + stage * B_STAGE);
                             const bool la = !(p.dbg & 1), lbb = !(p.dbg & 2);
                             const uint32_t txs = (uint32_t)CG * ((la ? a_bytes : 0u) + (lbb ? (uint32_t)B_STAGE : 0u));
-                            if constexpr (CG == 1) {
+                            if (!elect_one()) {
+                            } else if constexpr (CG == 1) {
                                 mbar_arrive_expect_tx_addr(fb, txs);
                                 if (la) tma_load_4d(dA, &p.amap[s], fb, ch * 64, x0 + dx, y0 + dy, t);
+                            if (p.dbg & 32) { /* timing experiment: no pipeline handshakes */ }
                                 if (lbb) tma_load_2d_a(dB, bm, fb, col + ch * 64, n0);
                             } else {
                                 if (rank == 0) mbar_arrive_expect_tx_addr(fb, txs);
@@ -138,14 +144,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
-        if (lane == 0 && rank == 0) {
+        // the whole warp walks the loop (warp-uniform descriptors live in uniform
+        // registers); one elected lane issues tcgen05.mma / commit
+        if (rank == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
             for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
                 const int buf = it & 1;
                 const uint32_t use = (uint32_t)(it >> 1) & 1;
-                mbar_wait(&tempty[buf], use ^ 1);   // epilogues of both CTAs drained this buffer
+                mbar_wait_spin(&tempty[buf], use ^ 1);   // epilogues of both CTAs drained this buffer
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(buf * BN);
                 bool first = true;
@@ -153,22 +161,29 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                     const int nch = (p.seg_c[s] + 63) >> 6;
                     for (int tap = 0; tap < p.seg_taps[s]; ++tap) {
                         for (int ch = 0; ch < nch; ++ch) {
-                            mbar_wait_spin(&full[stage], phase);
+                            if (!(p.dbg & 32)) mbar_wait_spin(&full[stage], phase);
                             tc_fence_after();
                             const int ksteps = min(64, p.seg_c[s] - ch * 64) >> 4;
                             const uint32_t a0 = smem_u32(sA + stage * A_STAGE);
                             const uint32_t b0 = smem_u32(sB + stage * B_STAGE);
-                            for (int k = 0; k < ksteps; ++k) {
-                                const uint64_t ad = sdesc_sw128(a0 + k * 32);
-                                const uint64_t bd = sdesc_sw128(b0 + k * 32);
-                                if (!(p.dbg & 4) || first) {
-                                    if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, first ? 0u : 1u);
-                                    else tc_mma_cg2(d, ad, bd, p.idesc, first ? 0u : 1u);
+                            const uint64_t ad0 = sdesc_sw128(a0), bd0 = sdesc_sw128(b0);
+                            if (elect_one()) {
+                                for (int k = 0; k < ksteps; ++k) {
+                                    // K advance inside the 128-byte swizzled row: +32 B = +2 in the address field
+                                    const uint64_t ad = ad0 + (uint64_t)(2 * k);
+                                    const uint64_t bd = bd0 + (uint64_t)(2 * k);
+                                    if (!(p.dbg & 4) || (first && k == 0)) {
+                                        if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, (first && k == 0) ? 0u : 1u);
+                                        else tc_mma_cg2(d, ad, bd, p.idesc, (first && k == 0) ? 0u : 1u);
+                                    }
                                 }
-                                first = false;
+                                if (!(p.dbg & 32)) {
+                                    if constexpr (CG == 1) tc_commit(&empty[stage]);
+                                    else tc_commit_cg2_mc(smem_u32(&empty[stage]), 0x3);
+                                }
                             }
-                            if constexpr (CG == 1) tc_commit(&empty[stage]);
-                            else tc_commit_cg2_mc(smem_u32(&empty[stage]), 0x3);
+                            __syncwarp();
+                            first = false;
                             if (++stage == STAGES) {
                                 stage = 0;
                                 phase ^= 1;
@@ -176,8 +191,11 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         }
                     }
                 }
-                if constexpr (CG == 1) tc_commit(&tfull[buf]);
-                else tc_commit_cg2_mc(smem_u32(&tfull[buf]), 0x3);
+                if (elect_one()) {
+                    if constexpr (CG == 1) tc_commit(&tfull[buf]);
+                    else tc_commit_cg2_mc(smem_u32(&tfull[buf]), 0x3);
+                }
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {
@@ -203,15 +221,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                 const int y = (rem / p.tiles_x) * p.BY + by, x = (rem % p.tiles_x) * p.BX + bx;
                 if (y < p.H && x < p.W) m = ((long)t * p.H + y) * p.W + x;
             }
-            mbar_wait(&tfull[buf], use);
+            mbar_wait_spin(&tfull[buf], use);
             tc_fence_after();
+            const bool want_stats = p.stats != nullptr && box < p.nbox;   // warp-uniform
 #pragma unroll 1
-            for (int cc = 0; cc < BN; cc += 16) {
+            for (int cc = 0, par = 0; cc < ((p.dbg & 16) ? 0 : BN); cc += 16, par ^= 1) {
                 uint32_t v[16];
                 tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
                 const int n = nt * BN + cc;
+                float f[16];
                 if (m >= 0 && !(p.dbg & 8)) {
-                    float f[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
                     float e[8];
@@ -239,14 +258,28 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
 #pragma unroll
                         for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
                     }
-                    float lo[8], hi[8];
+                    Vec8<T> lo, hi;
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        lo[i] = f[i];
-                        hi[i] = f[8 + i];
+                        lo.v[i] = Elem<T>::from_f(f[i]);
+                        hi.v[i] = Elem<T>::from_f(f[8 + i]);
+                        f[i] = Elem<T>::to_f(lo.v[i]);       // statistics of the stored values (R17)
+                        f[8 + i] = Elem<T>::to_f(hi.v[i]);
                     }
-                    store8(out + m * p.cout + n, lo);
-                    store8(out + m * p.cout + n + 8, hi);
+                    *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n) = lo;
+                    *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n + 8) = hi;
+                }
+                if (want_stats) {
+                    float x[32];
+                    box_row_values(f, m >= 0, x);
+                    red[(par * 4 + q4) * 32 + lane] = box_reduce_scatter32(x, lane);
+                    asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
+                    if (q4 == 0) {
+                        const int per = p.tiles_x * p.tiles_y;
+                        const int t = box / per, bi = box - t * per;
+                        const float val = box_combine4(red + par * 128, lane);
+                        p.stats[(((size_t)t * per + bi) * p.cout + n + (lane & 15)) * 2 + (lane >> 4)] = val;
+                    }
                 }
             }
             tc_fence_before();
@@ -290,7 +323,7 @@ static dvc_status make_amap(CUtensorMap *map, const void *ptr, dvc_dtype dt, int
 dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
 
 // Spatial box minimising the number of 128-row MMA tiles per frame.
-static void choose_box(int H, int W, int *BX, int *BY) {
+void choose_box(int H, int W, int *BX, int *BY) {
     long best = -1;
     for (int bx = 1; bx <= W && bx <= 128; ++bx) {
         int by = 128 / bx;
@@ -309,7 +342,7 @@ static int g_num_sms = 0;
 
 template <typename T, int CG, int STAGES>
 static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
-    const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16;
+    const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16 + 1024;
     auto kern = conv_ws_kernel<T, CG, STAGES>;
     DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (g_num_sms == 0) {
@@ -412,6 +445,7 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
     const int bf = d.dt == DVC_BF16;
     p.idesc = make_idesc(bf, 128 * CG, bn);
     p.dbg = g_ws_dbg;
+    p.stats = reinterpret_cast<float *>(d.stats_out);
     if (CG == 2) {
         if (bf) return launch_ws<__nv_bfloat16, 2, 6>(p, stream);
         return launch_ws<__half, 2, 6>(p, stream);

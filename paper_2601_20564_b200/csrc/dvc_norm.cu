@@ -13,6 +13,8 @@
 // fixed order (per-thread fp64 sums over a fixed pixel stride, fixed-order
 // smem merge per 256-pixel chunk, fixed-order merge over chunks).
 #include "dvc_norm.cuh"
+#include "dvc_boxstats.cuh"
+#include "dvc_conv.cuh"
 
 namespace dvc {
 
@@ -251,10 +253,10 @@ __device__ __forceinline__ float silu_t(float z) {
     } else {
         const float e = exp2f(fmaxf(z, -80.f) * -1.4426950408889634f);   // ex2.approx (fast-math free: exp2f)
         const float d = 1.0f + e;                                          // in [1, 2^116)
-        float r = __int_as_float(0x7EF311C3 - __float_as_int(d));         // ~1/d to 4 bits
-        r = r * (2.0f - d * r);
-        r = r * (2.0f - d * r);
-        r = r * (2.0f - d * r);
+        float r = __int_as_float(0x7EF127EA - __float_as_int(d));         // ~1/d, |rel err| < 0.06
+        r = r * (2.0f - d * r);                                             // < 3.6e-3
+        r = r * (2.0f - d * r);                                             // < 1.3e-5
+        r = r * (2.0f - d * r);                                             // < 2e-10 (fp32 rounding)
         return z * r;
     }
 }
@@ -274,9 +276,13 @@ __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const float2 cf = coef[(size_t)t * C + 8 * v + i];
-        mu[i] = cf.x;
         sc[i] = cf.y;
+        mu[i] = cf.x;
         be[i] = Elem<T>::to_f(beta[8 * v + i]);
+        if (sizeof(T) == 2) {   // 16-bit outputs: z = f*sc + (beta - mu*sc), one FMA per element
+            be[i] = be[i] - mu[i] * sc[i];
+            mu[i] = 0.f;
+        }
     }
     T *o = out + (size_t)t * X.HW * C + 8 * v;
     int p = p0 + pl;
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) f[j][i] = silu_t<T>((f[j][i] - mu[i]) * sc[i] + be[i]);
+                for (int i = 0; i < 8; ++i) f[j][i] = silu_t<T>(sizeof(T) == 2 ? fmaf(f[j][i], sc[i], be[i]) : (f[j][i] - mu[i]) * sc[i] + be[i]);
                 store8(o + (size_t)(p + j * npl) * C, f[j]);
             }
         }
@@ -298,7 +304,7 @@ __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) f[j][i] = silu_t<T>((f[j][i] - mu[i]) * sc[i] + be[i]);
+                for (int i = 0; i < 8; ++i) f[j][i] = silu_t<T>(sizeof(T) == 2 ? fmaf(f[j][i], sc[i], be[i]) : (f[j][i] - mu[i]) * sc[i] + be[i]);
                 store8(o + (size_t)(p + j * npl) * C, f[j]);
             }
         }
@@ -307,7 +313,7 @@ __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const
         float f[8];
         src.load(p, f);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) f[i] = silu_t<T>((f[i] - mu[i]) * sc[i] + be[i]);
+        for (int i = 0; i < 8; ++i) f[i] = silu_t<T>(sizeof(T) == 2 ? fmaf(f[i], sc[i], be[i]) : (f[i] - mu[i]) * sc[i] + be[i]);
         store8(o + (size_t)p * C, f);
     }
 }
@@ -410,6 +416,160 @@ dvc_status nearest_run(const void *src, void *dst, int T, int hi, int wi, int ho
                                              ho, wo, nvec);
     ++g_launches;
     return check_launch("nearest");
+}
+
+// ----------------------------------------------------------------- box statistics (standalone)
+// Same partials, same bits as the TMA engine's epilogue (dvc_boxstats.cuh).  grid (nbox, T), 128 threads.
+template <typename T>
+__global__ void __launch_bounds__(128) box_stats_kernel(const T *__restrict__ x, int H, int W, int C, int BX, int BY,
+                                                        int tiles_x, int vec_ok, float *__restrict__ stats) {
+    __shared__ float red[2][4][32];
+    const int b = blockIdx.x, t = blockIdx.y, per = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, r = threadIdx.x;
+    const int y = (b / tiles_x) * BY + r / BX, xx = (b % tiles_x) * BX + r % BX;
+    const bool valid = r < BX * BY && y < H && xx < W;
+    const T *row = x + (((size_t)t * H + (valid ? y : 0)) * W + (valid ? xx : 0)) * C;
+    for (int c0 = 0, par = 0; c0 < C; c0 += 16, par ^= 1) {
+        float v[16];
+        if (vec_ok) {   // 16-byte aligned rows: vector loads
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float e[8];
+                if (valid && c0 + 8 * h < C) load8(row + c0 + 8 * h, e);
+                else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) e[i] = 0.f;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[8 * h + i] = e[i];
+            }
+        } else {              // e.g. a carry slice of C_in/P = 30 channels: element loads
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = (valid && c0 + i < C) ? Elem<T>::to_f(row[c0 + i]) : 0.f;
+        }
+        float xs[32];
+        box_row_values(v, valid, xs);
+        red[par][warp][lane] = box_reduce_scatter32(xs, lane);
+        __syncthreads();
+        if (warp == 0 && c0 + (lane & 15) < C)
+            stats[(((size_t)t * per + b) * C + c0 + (lane & 15)) * 2 + (lane >> 4)] = box_combine4(&red[par][0][0], lane);
+    }
+}
+
+dvc_status box_stats_run(const void *x, int T, int H, int W, int C, dvc_dtype dt, float *stats, cudaStream_t stream) {
+    DVC_CHECK_ARG(C >= 1, DVC_ERR_ARG, "box statistics: C must be >= 1");
+    int BX = 1, BY = 1;
+    choose_box(H, W, &BX, &BY);
+    const int tx = (W + BX - 1) / BX, ty = (H + BY - 1) / BY;
+    dim3 grid(tx * ty, T);
+    // e.g. a packed carry slice may start at any element offset: vector loads only when aligned
+    const int vec_ok = (C % 8 == 0) && ((uintptr_t)x % 16 == 0) && ((C * dt_size(dt)) % 16 == 0);
+    switch (dt) {
+        case DVC_BF16:
+            box_stats_kernel<__nv_bfloat16><<<grid, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16 *>(x), H, W,
+                                                                      C, BX, BY, tx, vec_ok, stats);
+            break;
+        case DVC_F16:
+            box_stats_kernel<__half><<<grid, 128, 0, stream>>>(reinterpret_cast<const __half *>(x), H, W, C, BX, BY, tx,
+                                                               vec_ok, stats);
+            break;
+        default:
+            box_stats_kernel<float><<<grid, 128, 0, stream>>>(reinterpret_cast<const float *>(x), H, W, C, BX, BY, tx,
+                                                              vec_ok, stats);
+    }
+    ++g_launches;
+    return check_launch("box_stats");
+}
+
+// GN coefficients of the (shifted, concatenated) operand from box statistics:
+// group g of frame t takes frame t-1's statistics when its channels lie in the
+// shifted slice [0, cs) (carry statistics at t = 0, zeros without a carry),
+// else frame t's.  Requires cs % (C/G) == 0.  grid (T), 256 threads, warp per
+// group, lanes stride over boxes, fixed xor tree (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(256) gn_finalize_box_kernel(const float2 *__restrict__ pa, int ca,
+                                                              const float2 *__restrict__ pb, int cb,
+                                                              const float2 *__restrict__ pk, int cs, int nbox, int G,
+                                                              double n, double eps, const T *__restrict__ gamma,
+                                                              float2 *__restrict__ coef) {
+    __shared__ double s_S[8], s_Q[8];
+    __shared__ float s_mu, s_rs;
+    const int g = blockIdx.x, t = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int C = ca + cb, cg = C / G;
+    const bool shifted = (g + 1) * cg <= cs;
+    const int tf = shifted ? t - 1 : t;
+    double S = 0.0, Q = 0.0;
+    if (tf >= 0 || pk != nullptr) {
+        // the 256 threads stride over the group's (box, channel) items: a fixed order per thread
+        const int n_items = nbox * cg;
+        for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
+            const int b = i / cg, c = g * cg + (i - b * cg);
+            float2 v;
+            if (tf < 0) v = pk[(size_t)b * cs + c];
+            else if (c < ca) v = pa[((size_t)tf * nbox + b) * ca + c];
+            else v = pb[((size_t)tf * nbox + b) * cb + (c - ca)];
+            S += (double)v.x;
+            Q += (double)v.y;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        Q += __shfl_xor_sync(0xffffffffu, Q, o);
+    }
+    if (lane == 0) {
+        s_S[warp] = S;
+        s_Q[warp] = Q;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double SS = 0.0, QQ = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            SS += s_S[w];
+            QQ += s_Q[w];
+        }
+        const double mu = SS / n;
+        double var = QQ / n - mu * mu;   // biased variance (R4)
+        if (var < 0.0) var = 0.0;
+        s_mu = (float)mu;
+        s_rs = (float)(1.0 / sqrt(var + eps));
+    }
+    __syncthreads();
+    for (int c = g * cg + threadIdx.x; c < (g + 1) * cg; c += blockDim.x)
+        coef[(size_t)t * C + c] = make_float2(s_mu, s_rs * Elem<T>::to_f(gamma[c]));
+}
+
+size_t box_stats_bytes(int T, int H, int W, int C) { return align256((size_t)T * boxes_per_frame(H, W) * C * 8); }
+
+template <typename T>
+static dvc_status gn_silu_box_t(const NormArgs &a, const BoxStatsIn &bs, int H, int W, cudaStream_t stream) {
+    ShiftSrc<T> X{reinterpret_cast<const T *>(a.xa), reinterpret_cast<const T *>(a.xb),
+                  reinterpret_cast<const T *>(a.carry), a.ca, a.cb, a.cs, a.HW};
+    const int C = a.ca + a.cb;
+    const int nchunk = (a.HW + chunk_pix(C) - 1) / chunk_pix(C);
+    float2 *coef = reinterpret_cast<float2 *>(a.ws);
+    gn_finalize_box_kernel<T><<<dim3(a.G, a.T), 256, 0, stream>>>(
+        reinterpret_cast<const float2 *>(bs.a), a.ca, reinterpret_cast<const float2 *>(bs.b), a.cb,
+        reinterpret_cast<const float2 *>(bs.carry), a.cs, boxes_per_frame(H, W), a.G, (double)(C / a.G) * a.HW,
+        (double)a.eps, reinterpret_cast<const T *>(a.gamma), coef);
+    ++g_launches;
+    gn_silu_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, coef, reinterpret_cast<const T *>(a.beta),
+                                                             reinterpret_cast<T *>(a.out));
+    ++g_launches;
+    return check_launch("gn_silu_box");
+}
+
+dvc_status gn_silu_box_run(const NormArgs &a, const BoxStatsIn &bs, int H, int W, dvc_dtype dt, cudaStream_t stream) {
+    const int C = a.ca + a.cb;
+    DVC_CHECK_ARG(a.ca % 8 == 0 && a.cb % 8 == 0 && C / 8 <= 256, DVC_ERR_UNSUPPORTED,
+                  "GN: channel counts must be multiples of 8 and at most 2048");
+    DVC_CHECK_ARG(a.G >= 1 && a.G <= 256 && C % a.G == 0, DVC_ERR_DIVISIBILITY, "GN: G=%d must divide C=%d", a.G, C);
+    DVC_CHECK_ARG(a.cs <= a.ca && a.cs % (C / a.G) == 0, DVC_ERR_UNSUPPORTED, "box GN: slice must be whole groups");
+    switch (dt) {
+        case DVC_BF16: return gn_silu_box_t<__nv_bfloat16>(a, bs, H, W, stream);
+        case DVC_F16: return gn_silu_box_t<__half>(a, bs, H, W, stream);
+        default: return gn_silu_box_t<float>(a, bs, H, W, stream);
+    }
 }
 
 }  // namespace dvc

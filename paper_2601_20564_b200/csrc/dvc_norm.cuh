@@ -18,6 +18,15 @@ struct NormArgs {
 };
 
 size_t gn_workspace_bytes(int T, int HW, int G, int C);
+
+// Box statistics (dvc_boxstats.cuh) of the sources of a GN operand.
+struct BoxStatsIn {
+    const void *a, *b;   // [T][nbox][C_a] / [T][nbox][C_b] float2 (b may be null when C_b == 0)
+    const void *carry;   // [nbox][cs] float2 of the carry slice, or null (zeros)
+};
+size_t box_stats_bytes(int T, int H, int W, int C);
+// GN1/GN2 + SiLU from box statistics (no statistics pass over the operand); ws >= T*C*8 bytes
+dvc_status gn_silu_box_run(const NormArgs &a, const BoxStatsIn &bs, int H, int W, dvc_dtype dt, cudaStream_t stream);
 dvc_status nearest_run(const void *src, void *dst, int T, int hi, int wi, int ho, int wo, int C, dvc_dtype dt,
                        cudaStream_t stream);
 dvc_status gn_silu_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream);

@@ -28,6 +28,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// one elected lane of a converged warp (elect.sync)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // latency-critical wait (pipeline producer / MMA issuer): poll without a suspend hint
 __device__ __forceinline__ bool mbar_try_wait_nohint(uint32_t addr, uint32_t parity) {
     uint32_t ok;

@@ -11,9 +11,10 @@ struct RB {
     const void *gn1_w, *gn1_b, *conv1_w, *conv1_b, *gn2_w, *gn2_b, *conv2_w, *conv2_b, *sc_w, *sc_b;
 };
 
-size_t resblock_ws_bytes(int ca, int cb, int cout, int G, int T, int HW, dvc_dtype dt);
+size_t resblock_ws_bytes(int ca, int cb, int cout, int G, int T, int H, int W, dvc_dtype dt);
 dvc_status resblock_validate(const RB &b, int T, int H, int W);
 dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, int H, int W, const void *carry_in,
-                           void *carry_out, void *y, void *ws, cudaStream_t stream);
+                           void *carry_out, void *y, void *ws, cudaStream_t stream, const void *stats_a = nullptr,
+                           const void *stats_b = nullptr, void *stats_y = nullptr);
 
 }  // namespace dvc

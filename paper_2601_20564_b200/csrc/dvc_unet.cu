@@ -179,37 +179,57 @@ dvc_status validate_cfg(const dvc_unet_config *c) {
     return DVC_OK;
 }
 
-size_t plan_workspace(const dvc_unet &n, int T, size_t *offs /* 16 regions */) {
-    // regions: 0..11 skips, 12,13 ping-pong h, 14 ResBlock scratch (also GN_out operand), 15 halo send/recv
+// Workspace regions: 0..11 skips, 12/13 ping-pong h, 14 ResBlock scratch (also the
+// GN_out operand and the nearest-resize operand), 15 halo send/recv, 16..27 box
+// statistics of the skips, 28/29 box statistics of the ping-pong buffers.
+constexpr int kRegions = 30;
+
+size_t plan_workspace(const dvc_unet &n, int T, size_t *offs /* kRegions */) {
     const dvc_unet_config &c = n.cfg;
     const size_t es = dt_size(c.dt);
     const int *W = c.width;
-    size_t sz[16] = {};
+    size_t sz[kRegions] = {};
     auto hw = [&](int l) { return (size_t)n.lh[l] * n.lw[l]; };
+    auto bst = [&](int l, int C) { return box_stats_bytes(T, n.lh[l], n.lw[l], C); };
     int k = 0;
-    sz[k++] = T * hw(0) * W[0];
+    sz[k] = T * hw(0) * W[0] * es;
+    sz[16 + k++] = bst(0, W[0]);
     for (int l = 0; l < 4; ++l) {
-        sz[k++] = T * hw(l) * W[l];
-        sz[k++] = T * hw(l) * W[l];
-        if (l < 3) sz[k++] = T * hw(l + 1) * W[l];
+        for (int r = 0; r < 2; ++r) {
+            sz[k] = T * hw(l) * W[l] * es;
+            sz[16 + k++] = bst(l, W[l]);
+        }
+        if (l < 3) {
+            sz[k] = T * hw(l + 1) * W[l] * es;
+            sz[16 + k++] = bst(l + 1, W[l]);
+        }
     }
-    size_t hmax = 0;
-    for (int l = 0; l < 4; ++l) hmax = std::max(hmax, T * hw(l) * (size_t)W[l]);
-    for (int l = 1; l < 4; ++l) hmax = std::max(hmax, T * hw(l - 1) * (size_t)W[l]);
+    size_t hmax = 0, smax = 0;
+    for (int l = 0; l < 4; ++l) {
+        hmax = std::max(hmax, T * hw(l) * (size_t)W[l]);
+        smax = std::max(smax, bst(l, W[l]));
+    }
+    for (int l = 1; l < 4; ++l) {
+        hmax = std::max(hmax, T * hw(l - 1) * (size_t)W[l]);
+        smax = std::max(smax, bst(l - 1, W[l]));
+    }
     hmax = std::max(hmax, T * hw(0) * (size_t)c.c_lat);
-    sz[12] = sz[13] = hmax;
+    sz[12] = sz[13] = hmax * es;
+    sz[28] = sz[29] = smax;
     size_t rbws = 0;
     for (int b = 0; b < 22; ++b) {
         const RB &r = n.blk[b];
         const int l = n.blevel[b];
-        rbws = std::max(rbws, resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, (int)hw(l), c.dt));
+        rbws = std::max(rbws, resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, n.lh[l], n.lw[l], c.dt));
     }
     rbws = std::max(rbws, align256(gn_workspace_bytes(T, (int)hw(0), c.groups, W[0])) + T * hw(0) * W[0] * es);
+    for (int l = 1; l < 4; ++l) rbws = std::max(rbws, T * hw(l - 1) * (size_t)W[l] * es);
+    sz[14] = rbws;
+    sz[15] = (n.carry_total * 2 + 2 * hw(0) * 2048) * es;
     size_t total = 0;
-    for (int i = 0; i < 16; ++i) {
-        size_t bytes = i == 14 ? rbws : i == 15 ? (n.carry_total * 2 + 2 * hw(0) * 2048) * es : sz[i] * es;
+    for (int i = 0; i < kRegions; ++i) {
         offs[i] = total;
-        total += align256(bytes);
+        total += align256(sz[i]);
     }
     return total;
 }
@@ -343,7 +363,7 @@ dvc_status dvc_unet_carry_size(const dvc_unet *n, size_t *elems) {
 
 dvc_status dvc_unet_workspace_size(const dvc_unet *n, int T, size_t *bytes) {
     DVC_CHECK_ARG(n && bytes && T >= 1 && T <= n->cfg.max_T, DVC_ERR_ARG, "bad arguments (1 <= T <= max_T)");
-    size_t offs[16];
+    size_t offs[kRegions];
     *bytes = plan_workspace(*n, T, offs);
     return DVC_OK;
 }
@@ -354,7 +374,7 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     DVC_CHECK_ARG(n && lat && ctx && out && workspace, DVC_ERR_ARG, "null argument");
     DVC_CHECK_ARG(T >= 1 && T <= n->cfg.max_T, DVC_ERR_ARG, "T_local=%d outside [1, max_T=%d]", T, n->cfg.max_T);
     DVC_CHECK_ARG(((uintptr_t)workspace & 255) == 0, DVC_ERR_ARG, "workspace must be 256-byte aligned");
-    size_t offs[16];
+    size_t offs[kRegions];
     const size_t need = plan_workspace(*n, T, offs);
     DVC_CHECK_ARG(ws_bytes >= need, DVC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
     const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
@@ -367,9 +387,13 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     const size_t es = dt_size(dt);
     const int *W = c.width;
     uint8_t *ws = reinterpret_cast<uint8_t *>(workspace);
-    void *skip[12];
-    for (int i = 0; i < 12; ++i) skip[i] = ws + offs[i];
+    void *skip[12], *skst[12];
+    for (int i = 0; i < 12; ++i) {
+        skip[i] = ws + offs[i];
+        skst[i] = ws + offs[16 + i];
+    }
     void *hb[2] = {ws + offs[12], ws + offs[13]};
+    void *hbst[2] = {ws + offs[28], ws + offs[29]};
     void *rbws = ws + offs[14];
     uint8_t *halo = ws + offs[15];
     uint8_t *recv = halo;                                    // packed received carries
@@ -377,8 +401,9 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     auto hw = [&](int l) { return n->lh[l] * n->lw[l]; };
 
     int bi = 0;
-    // one ResBlock with its halo exchange
-    auto run_block = [&](const void *xa, const void *xb, void *y) -> dvc_status {
+    // one ResBlock with its halo exchange; sa/sb/sy: box statistics of x_a, x_b, y
+    auto run_block = [&](const void *xa, const void *xb, void *y, const void *sa, const void *sb,
+                         void *sy) -> dvc_status {
         const RB &r = n->blk[bi];
         const int l = n->blevel[bi];
         const int H = n->lh[l], Wd = n->lw[l];
@@ -400,12 +425,12 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         }
         void *cout_ptr = nullptr;
         if (carry_out && (world == 1 || rank == world - 1)) cout_ptr = reinterpret_cast<uint8_t *>(carry_out) + off;
-        dvc_status e = resblock_launch(r, xa, xb, T, H, Wd, cin_ptr, cout_ptr, y, rbws, s);
+        dvc_status e = resblock_launch(r, xa, xb, T, H, Wd, cin_ptr, cout_ptr, y, rbws, s, sa, sb, sy);
         ++bi;
         return e;
     };
     auto conv3 = [&](const void *src, int cin, int mode, int hi, int wi, const ConvW &cw, int cout, int ho, int wo,
-                     void *dst) {
+                     void *dst, void *dst_stats) {
         ConvDesc d{};
         d.seg[0] = ConvSeg{src, cin, mode, hi, wi, 9, cw.w, 9 * cin, 0, cin};
         d.nseg = 1;
@@ -415,6 +440,7 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         d.cout = cout;
         d.bias0 = cw.b;
         d.out = dst;
+        d.stats_out = dst_stats;
         d.dt = dt;
         return conv_run(d, s);
     };
@@ -432,50 +458,59 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         d.cout = W[0];
         d.bias0 = n->conv_in.b;
         d.out = skip[0];
+        d.stats_out = skst[0];
         d.dt = dt;
         if ((st = conv_run(d, s)) != DVC_OK) return st;
     }
     int k = 1;
     const void *h = skip[0];
+    const void *hs = skst[0];
     for (int l = 0; l < 4; ++l) {
         for (int r = 0; r < 2; ++r) {
-            if ((st = run_block(h, nullptr, skip[k])) != DVC_OK) return st;
-            h = skip[k++];
+            if ((st = run_block(h, nullptr, skip[k], hs, nullptr, skst[k])) != DVC_OK) return st;
+            h = skip[k];
+            hs = skst[k++];
         }
         if (l < 3) {
             if ((st = conv3(h, W[l], SEG_STRIDE2, n->lh[l], n->lw[l], n->ds[l], W[l], n->lh[l + 1], n->lw[l + 1],
-                            skip[k])) != DVC_OK)
+                            skip[k], skst[k])) != DVC_OK)
                 return st;
-            h = skip[k++];
+            h = skip[k];
+            hs = skst[k++];
         }
     }
     int pp = 0;
     for (int r = 0; r < 2; ++r) {
-        if ((st = run_block(h, nullptr, hb[pp])) != DVC_OK) return st;
+        if ((st = run_block(h, nullptr, hb[pp], hs, nullptr, hbst[pp])) != DVC_OK) return st;
         h = hb[pp];
+        hs = hbst[pp];
         pp ^= 1;
     }
     for (int u = 0; u < 4; ++u) {
         const int l = 3 - u;
         for (int r = 0; r < 3; ++r) {
-            if ((st = run_block(h, skip[--k], hb[pp])) != DVC_OK) return st;
+            --k;
+            if ((st = run_block(h, skip[k], hb[pp], hs, skst[k], hbst[pp])) != DVC_OK) return st;
             h = hb[pp];
+            hs = hbst[pp];
             pp ^= 1;
         }
         if (u < 3) {
+            void *nst = (u < 3) ? hbst[pp] : nullptr;
             if (g_ws_cg != 0) {
                 // materialise nearest_to(h, next skip size) (exact copy) so the 3x3 conv runs on the TMA engine
                 if ((st = nearest_run(h, rbws, T, n->lh[l], n->lw[l], n->lh[l - 1], n->lw[l - 1], W[l], dt, s)) !=
                     DVC_OK)
                     return st;
                 st = conv3(rbws, W[l], SEG_SAME, n->lh[l - 1], n->lw[l - 1], n->us[u], W[l], n->lh[l - 1],
-                           n->lw[l - 1], hb[pp]);
+                           n->lw[l - 1], hb[pp], nst);
             } else {
                 st = conv3(h, W[l], SEG_UPNEAREST, n->lh[l], n->lw[l], n->us[u], W[l], n->lh[l - 1], n->lw[l - 1],
-                           hb[pp]);
+                           hb[pp], nst);
             }
             if (st != DVC_OK) return st;
             h = hb[pp];
+            hs = hbst[pp];
             pp ^= 1;
         }
     }
@@ -484,9 +519,10 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         uint8_t *gnws = reinterpret_cast<uint8_t *>(rbws);
         void *op = gnws + align256(gn_workspace_bytes(T, hw(0), c.groups, W[0]));
         NormArgs na{h, nullptr, nullptr, W[0], 0, 0, T, hw(0), c.groups, c.eps, n->gno_w, n->gno_b, op, gnws};
-        if ((st = gn_silu_run(na, dt, s)) != DVC_OK) return st;
-        if ((st = conv3(op, W[0], SEG_SAME, n->lh[0], n->lw[0], n->conv_out, c.c_lat, n->lh[0], n->lw[0], out)) !=
-            DVC_OK)
+        if ((st = gn_silu_box_run(na, BoxStatsIn{hs, nullptr, nullptr}, n->lh[0], n->lw[0], dt, s)) != DVC_OK)
+            return st;
+        if ((st = conv3(op, W[0], SEG_SAME, n->lh[0], n->lw[0], n->conv_out, c.c_lat, n->lh[0], n->lw[0], out,
+                        nullptr)) != DVC_OK)
             return st;
     }
     if (world > 1 && nccl().CommGetAsyncError) {
