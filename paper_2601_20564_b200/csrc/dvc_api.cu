@@ -140,6 +140,92 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
                                    b.ca * es, cs * es, HW, cudaMemcpyDeviceToDevice, stream));
     }
     const bool boxed = box_mode(b);
+    if (boxed && conv_fz_applicable(H, W, b.dt)) {
+        // ---- fused path: GN statistics from box partials, GN-apply + SiLU + shift inside the convs
+        if (!stats_a) {
+            if ((st = box_stats_run(xa, T, H, W, b.ca, b.dt, reinterpret_cast<float *>(st_a), stream)) != DVC_OK)
+                return st;
+            stats_a = st_a;
+        }
+        if (b.cb > 0 && !stats_b) {
+            if ((st = box_stats_run(xb, T, H, W, b.cb, b.dt, reinterpret_cast<float *>(st_b), stream)) != DVC_OK)
+                return st;
+            stats_b = st_b;
+        }
+        const void *stats_k = nullptr;
+        void *carry_pad = nullptr;
+        const int cs_pad = (cs + 7) & ~7;
+        if (carry_in) {
+            if ((st = box_stats_run(carry_in, 1, H, W, cs, b.dt, reinterpret_cast<float *>(st_k), stream)) != DVC_OK)
+                return st;
+            stats_k = st_k;
+            carry_pad = h1;   // [HW][cs_pad]: 16-byte rows for the TMA halo map (h1 is not used on this path)
+            if (cs_pad != cs) DVC_CUDA(cudaMemsetAsync(carry_pad, 0, (size_t)HW * cs_pad * es, stream));
+            DVC_CUDA(cudaMemcpy2DAsync(carry_pad, cs_pad * es, carry_in, cs * es, cs * es, HW,
+                                       cudaMemcpyDeviceToDevice, stream));
+        }
+        void *coef = gnws;
+        NormArgs n1{xa, xb, carry_in, b.ca, b.cb, cs, T, HW, b.G, b.eps, b.gn1_w, b.gn1_b, coef, nullptr};
+        if ((st = gn_coef_box_run(n1, BoxStatsIn{stats_a, b.cb > 0 ? stats_b : nullptr, stats_k}, H, W, b.dt,
+                                  stream)) != DVC_OK)
+            return st;
+        FzDesc f1{};
+        f1.seg[0] = FzDesc::Seg{xa, b.ca, 0, 9, 1, 1, b.conv1_w, 9 * cin, 0, cin};
+        f1.nseg = 1;
+        if (b.cb > 0) f1.seg[f1.nseg++] = FzDesc::Seg{xb, b.cb, b.ca, 9, 1, 0, b.conv1_w, 9 * cin, b.ca, cin};
+        f1.T = T;
+        f1.H = H;
+        f1.W = W;
+        f1.cout = b.cout;
+        f1.cs = cs;
+        f1.cs_pad = cs_pad;
+        f1.carry_pad = carry_pad;
+        f1.coef = coef;
+        f1.cop = cin;
+        f1.bias0 = b.conv1_b;
+        f1.out = y1;
+        f1.stats_out = st_y1;
+        f1.dt = b.dt;
+        {
+            ConvDesc prof{};
+            prof.seg[0] = ConvSeg{xa, cin, SEG_SAME, H, W, 9, b.conv1_w, 9 * cin, 0, cin};
+            prof.nseg = 1, prof.T = T, prof.ho = H, prof.wo = W, prof.cout = b.cout;
+            ProfSlot slot = prof_begin(stream);
+            st = conv_fz_run(f1, stream);
+            prof_end(slot, stream, conv_flops(prof));
+            if (st != DVC_OK) return st;
+        }
+        NormArgs n2{y1, nullptr, nullptr, b.cout, 0, 0, T, HW, b.G, b.eps, b.gn2_w, b.gn2_b, coef, nullptr};
+        if ((st = gn_coef_box_run(n2, BoxStatsIn{st_y1, nullptr, nullptr}, H, W, b.dt, stream)) != DVC_OK) return st;
+        FzDesc f2{};
+        f2.seg[0] = FzDesc::Seg{y1, b.cout, 0, 9, 1, 0, b.conv2_w, 9 * b.cout, 0, b.cout};
+        f2.nseg = 1;
+        if (b.sc_w) {
+            f2.seg[f2.nseg++] = FzDesc::Seg{xa, b.ca, 0, 1, 0, 0, b.sc_w, cin, 0, 0};
+            if (b.cb > 0) f2.seg[f2.nseg++] = FzDesc::Seg{xb, b.cb, 0, 1, 0, 0, b.sc_w, cin, b.ca, 0};
+            f2.bias1 = b.sc_b;
+        } else {
+            f2.residual = xa;
+        }
+        f2.T = T;
+        f2.H = H;
+        f2.W = W;
+        f2.cout = b.cout;
+        f2.coef = coef;
+        f2.cop = b.cout;
+        f2.bias0 = b.conv2_b;
+        f2.out = y;
+        f2.stats_out = stats_y;
+        f2.dt = b.dt;
+        ConvDesc prof{};
+        prof.seg[0] = ConvSeg{y1, b.cout, SEG_SAME, H, W, 9, b.conv2_w, 9 * b.cout, 0, b.cout};
+        prof.nseg = 1, prof.T = T, prof.ho = H, prof.wo = W, prof.cout = b.cout;
+        if (b.sc_w) prof.seg[prof.nseg++] = ConvSeg{xa, cin, SEG_SAME, H, W, 1, b.sc_w, cin, 0, 0};
+        ProfSlot slot = prof_begin(stream);
+        st = conv_fz_run(f2, stream);
+        prof_end(slot, stream, conv_flops(prof));
+        return st;
+    }
     // a3 + a4: H1 = SiLU(GN1(shift(X, carry)))
     NormArgs n1{xa, xb, carry_in, b.ca, b.cb, cs, T, HW, b.G, b.eps, b.gn1_w, b.gn1_b, h1, gnws};
     if (boxed) {

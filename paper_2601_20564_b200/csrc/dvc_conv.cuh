@@ -41,6 +41,29 @@ struct ConvDesc {
     long M() const { return (long)T * ho * wo; }
 };
 
+// Convolution with the GN-apply + SiLU (+ temporal shift) operand producer fused in
+// (dvc_conv_fz.cu).  Segments read raw NHWC tensors through 10x18 halo boxes.
+struct FzDesc {
+    struct Seg {
+        const void *src;   // raw operand tensor [T][H][W][c]
+        int c, cglob0, taps, transform, shift;
+        const void *w;
+        int w_ld, col0, tapstride;
+    };
+    Seg seg[4];
+    int nseg;
+    int T, H, W, cout;
+    int cs, cs_pad;              // shifted slice width; padded carry row length (multiple of 8)
+    const void *carry_pad;       // [H][W][cs_pad] carry slice (16-byte rows) or null = zeros
+    const void *coef;            // float2 [T][cop]: (scale, shift) of GN-apply (beta, mean folded)
+    int cop;
+    const void *bias0, *bias1, *residual;
+    void *out, *stats_out;
+    dvc_dtype dt;
+};
+dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream);
+bool conv_fz_applicable(int H, int W, dvc_dtype dt);
+
 // spatial box of the TMA engine / box statistics for an H x W frame
 void choose_box(int H, int W, int *BX, int *BY);
 inline int boxes_per_frame(int H, int W) {

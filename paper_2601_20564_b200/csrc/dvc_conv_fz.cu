@@ -1,0 +1,572 @@
+// dvc_conv_fz.cu -- tcgen05 implicit-GEMM 3x3 convolution whose A operand
+// producer is fused with GroupNorm-apply + SiLU and the Batch-dimension
+// temporal shift (SURVEY a3/a4/a5 and a6/a7/a8 in one kernel).
+//
+// Output tiles are 8-wide x 16-tall pixel boxes (128 MMA rows).  For every
+// 64-channel chunk of the operand the transform warps read the raw 10 x 18 halo
+// of the box once from global memory (128-bit loads, L2-resident neighbours) and write
+//     H = SiLU(X * sc[t][c] + b[t][c])   (0 outside the frame: conv padding after
+//                                          the transform, H3)
+// into a no-swizzle K-major tile (8-channel core matrices of 180 halo rows).  The
+// nine taps are then nine UMMA descriptors into that one tile: row offset
+// (1+dy)*10 + (1+dx), 8-row groups 160 B apart (one image row each) -- the halo
+// is transformed once instead of nine times and no H tensor reaches HBM.
+// The temporal shift is load addressing: channels [0, C_in/P) of frame t are
+// read from frame t-1, or from the carry slice at t = 0.
+// The 1x1 shortcut segments (raw, unshifted X) use the same halo path with an
+// identity transform and only the centre tap.
+//
+// Warps (512 threads): 1 TMEM allocator + MMA issuer (leader CTA), 2 weight TMA
+// producer, 4-7 epilogue (bias / residual / 16-bit store / box statistics),
+// 8-15 transform (load + GN-apply + SiLU + store into the UMMA tile).  CTA pairs (cta_group::2, M=256),
+// double-buffered TMEM accumulators, as in dvc_conv_ws.cu.
+#include <cuda.h>
+#include <cstdlib>
+#include "dvc_conv.cuh"
+#include "dvc_ptx.cuh"
+#include "dvc_boxstats.cuh"
+
+namespace dvc {
+
+constexpr int FZ_BX = 8, FZ_BY = 16;
+constexpr int FZ_HX = FZ_BX + 2, FZ_HY = FZ_BY + 2;
+constexpr int FZ_HROWS = FZ_HX * FZ_HY;      // 180 halo pixels
+constexpr int FZ_BOX_BYTES = FZ_HROWS * 128;  // raw halo box, SW128
+constexpr int FZ_SLOT = 23552;                // 1024-aligned slot (>= 23040)
+constexpr int FZ_LBO = FZ_HROWS * 16;         // between 8-channel core-matrix columns
+constexpr int FZ_SBO = FZ_HX * 16;            // between 8-row groups (image rows)
+constexpr int FZ_BSTAGES = 6;
+constexpr int kFzThreads = 512;
+
+struct FzSeg {
+    const void *src;   // raw operand tensor [T][H][W][c]
+    int c;          // channels of this segment
+    int cglob0;     // first operand channel (coef index) of this segment
+    int taps;       // 9 (GN/SiLU operand) or 1 (raw shortcut)
+    int transform;  // 1: GN-apply + SiLU + padding zero; 0: copy
+    int shift;      // 1: channels [0, cs) of the segment come from frame t-1 / carry
+    int bidx, col0, tapstride;
+};
+
+struct FzParams {
+    CUtensorMap bmap[2];   // weights, box {64, BN/CG}
+    CUtensorMap rmap;      // residual [T][H][W][cout], box {BN, 8, 16, 1}, no swizzle (if residual)
+    FzSeg seg[4];
+    int nseg, cs, has_carry, cs_pad;
+    const void *carry_pad; // [H][W][cs_pad] (16-byte rows)
+    const float2 *coef;    // [T][C_op] = (scale, shift) of the GN affine, beta and mean folded in
+    int cop;               // channels of the fused operand
+    int T, H, W, cout, bn, tiles_x, tiles_y, nbox, ntile_n, nwork;
+    const void *bias0, *bias1, *residual;
+    void *out;
+    float *stats;
+    uint32_t idesc;
+};
+
+// UMMA descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B
+__device__ __forceinline__ uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;   // version; layout type 0 = SWIZZLE_NONE
+    return d;
+}
+
+__device__ __forceinline__ float fz_silu(float z) { return silu_fast(z); }
+
+struct FzBox {
+    int t, y0, x0;
+    bool valid;
+};
+__device__ __forceinline__ FzBox fz_box(const FzParams &p, int box) {
+    FzBox b;
+    b.valid = box < p.nbox;
+    if (!b.valid) {
+        b.t = p.T;   // fully out of bounds: TMA zero fill
+        b.y0 = b.x0 = 0;
+        return b;
+    }
+    const int per = p.tiles_x * p.tiles_y;
+    b.t = box / per;
+    const int rem = box - b.t * per;
+    b.y0 = (rem / p.tiles_x) * FZ_BY;
+    b.x0 = (rem % p.tiles_x) * FZ_BX;
+    return b;
+}
+
+template <typename T, int CG>
+__global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_constant__ FzParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int BN = p.bn, BNH = p.bn / CG;
+    const int B_STAGE = BNH * 128;
+    uint8_t *sTf = smem;                        // [2] transformed tiles
+    uint8_t *sB = sTf + 2 * FZ_SLOT;            // [FZ_BSTAGES] weight tiles
+    uint8_t *sRes = sB + FZ_BSTAGES * B_STAGE;  // residual tile of the current output box [128][BN]
+    uint64_t *tf_full = reinterpret_cast<uint64_t *>(sRes + (p.residual ? 128 * BN * 2 : 0));
+    uint64_t *tf_empty = tf_full + 2;
+    uint64_t *b_full = tf_empty + 2;
+    uint64_t *b_empty = b_full + FZ_BSTAGES;
+    uint64_t *tfull = b_empty + FZ_BSTAGES;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *res_full = tempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(res_full + 1);
+    float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][4][32] box-statistics staging
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const int cluster_id = blockIdx.x / CG, nclusters = gridDim.x / CG;
+    const uint32_t ncols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tf_full[i], CG);
+            mbar_init(&tf_empty[i], 1);
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], CG * 4);
+        }
+        for (int s = 0; s < FZ_BSTAGES; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        mbar_init(res_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+    }
+    if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), ncols);
+    tc_fence_before();
+    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 2) {
+        // ===================== weight producer =====================
+        int bs = 0;
+        uint32_t bph = 0;
+        const uint32_t tx = (uint32_t)CG * (uint32_t)B_STAGE;
+        for (int w = cluster_id; w < p.nwork; w += nclusters) {
+            const int nt = w % p.ntile_n;
+            const int n0 = nt * BN + (int)rank * BNH;
+            for (int s = 0; s < p.nseg; ++s) {
+                const FzSeg &sg = p.seg[s];
+                const int nch = (sg.c + 63) >> 6;
+                const CUtensorMap *bm = &p.bmap[sg.bidx];
+                for (int ch = 0; ch < nch; ++ch) {
+                    for (int tap = 0; tap < sg.taps; ++tap) {
+                        mbar_wait_spin(&b_empty[bs], bph ^ 1);
+                        if (elect_one()) {
+                            const uint32_t fb = smem_u32(&b_full[bs]);
+                            const uint32_t dB = smem_u32(sB + bs * B_STAGE);
+                            const int col = sg.col0 + tap * sg.tapstride + ch * 64;
+                            if constexpr (CG == 1) {
+                                mbar_arrive_expect_tx_addr(fb, tx);
+                                tma_load_2d_a(dB, bm, fb, col, n0);
+                            } else {
+                                if (rank == 0) mbar_arrive_expect_tx_addr(fb, tx);
+                                tma_load_2d_cg2(dB, bm, mapa_shared(fb, 0), col, n0);
+                            }
+                        }
+                        __syncwarp();
+                        if (++bs == FZ_BSTAGES) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp >= 8) {
+        // ===================== transform warps: raw halo -> H tile =====================
+        const int kg = warp - 8;   // 8-channel core-matrix column of this warp
+        int tb = 0;
+        uint32_t tph = 0;
+        const uint32_t tf_full_leader = CG == 2 ? mapa_shared(smem_u32(&tf_full[0]), 0) : smem_u32(&tf_full[0]);
+        for (int w = cluster_id; w < p.nwork; w += nclusters) {
+            const FzBox bx = fz_box(p, (w / p.ntile_n) * CG + (int)rank);
+            for (int s = 0; s < p.nseg; ++s) {
+                const FzSeg &sg = p.seg[s];
+                const int nch = (sg.c + 63) >> 6;
+                for (int ch = 0; ch < nch; ++ch) {
+                    const int cl = ch * 64 + kg * 8;           // first channel (segment-local) of this warp
+                    const int cgl = sg.cglob0 + cl;            // operand channel (coef index)
+                    const bool cval = cl < sg.c;
+                    // per-channel GN affine of frame t and the shift selection (8 channels)
+                    float sc[8], sh[8];
+                    int from_prev = 0;   // bit i: channel i comes from the previous frame / carry
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        sc[i] = 1.f;
+                        sh[i] = 0.f;
+                        if (sg.transform && cval && bx.valid) {
+                            const float2 cf = p.coef[(size_t)bx.t * p.cop + cgl + i];
+                            sc[i] = cf.x;
+                            sh[i] = cf.y;
+                        }
+                        if (sg.shift && cl + i < p.cs) from_prev |= 1 << i;
+                    }
+                    const bool prev_zero = from_prev && bx.t == 0 && !p.has_carry;
+                    // sources of this warp's 8 channels: frame t, and frame t-1 / the padded carry
+                    const T *srcT = reinterpret_cast<const T *>(sg.src);
+                    const bool prev_carry = from_prev && bx.t == 0;
+                    mbar_wait(&tf_empty[tb], tph ^ 1);
+                    uint8_t *tf = sTf + tb * FZ_SLOT + kg * FZ_LBO;
+                    constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane
+                    uint4 cu[NR], pv[NR];
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) {   // issue every load before any use
+                        const int r = lane + 32 * k;
+                        const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
+                        const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
+                        const bool ok = r < FZ_HROWS && bx.valid && cval && y >= 0 && y < p.H && x >= 0 && x < p.W;
+                        cu[k] = make_uint4(0, 0, 0, 0);
+                        pv[k] = make_uint4(0, 0, 0, 0);
+                        if (ok) {
+                            const size_t pix = ((size_t)bx.t * p.H + y) * p.W + x;
+                            if (from_prev != 0xFF)
+                                cu[k] = __ldg(reinterpret_cast<const uint4 *>(srcT + pix * sg.c + cl));
+                            if (from_prev && !prev_zero) {
+                                if (prev_carry)
+                                    pv[k] = __ldg(reinterpret_cast<const uint4 *>(
+                                        reinterpret_cast<const T *>(p.carry_pad) + ((size_t)y * p.W + x) * p.cs_pad + cl));
+                                else
+                                    pv[k] = __ldg(reinterpret_cast<const uint4 *>(srcT + (pix - (size_t)p.H * p.W) * sg.c + cl));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) {
+                        const int r = lane + 32 * k;
+                        if (r >= FZ_HROWS) break;
+                        const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
+                        const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
+                        const bool inframe = bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
+                        uint4 out;
+                        if (!cval) {
+                            out = make_uint4(0, 0, 0, 0);
+                        } else {
+                            const T *ec = reinterpret_cast<const T *>(&cu[k]);
+                            const T *ep = reinterpret_cast<const T *>(&pv[k]);
+                            Vec8<T> o;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const float v = Elem<T>::to_f(((from_prev >> i) & 1) ? ep[i] : ec[i]);
+                                float h = v;
+                                if (sg.transform) h = inframe ? fz_silu(fmaf(v, sc[i], sh[i])) : 0.f;
+                                o.v[i] = Elem<T>::from_f(h);
+                            }
+                            out = *reinterpret_cast<uint4 *>(&o);
+                        }
+                        *reinterpret_cast<uint4 *>(tf + r * 16) = out;
+                    }
+                    fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
+                    asm volatile("bar.sync 2, 256;" ::: "memory");   // the 8 transform warps
+                    if (warp == 8 && elect_one()) {
+                        if constexpr (CG == 1)
+                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tf_full[tb]))
+                                         : "memory");
+                        else mbar_arrive_cluster(tf_full_leader + (uint32_t)(tb * 8));
+                    }
+                    __syncwarp();
+                    if (++tb == 2) {
+                        tb = 0;
+                        tph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader CTA) =====================
+        if (rank == 0) {
+            int bs = 0, tb = 0, it = 0;
+            uint32_t bph = 0, tph = 0;
+            for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
+                const int buf = it & 1;
+                const uint32_t use = (uint32_t)(it >> 1) & 1;
+                mbar_wait_spin(&tempty[buf], use ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(buf * BN);
+                bool first = true;
+                for (int s = 0; s < p.nseg; ++s) {
+                    const FzSeg &sg = p.seg[s];
+                    const int nch = (sg.c + 63) >> 6;
+                    for (int ch = 0; ch < nch; ++ch) {
+                        const int ksteps = min(64, sg.c - ch * 64) >> 4;
+                        mbar_wait_spin(&tf_full[tb], tph);
+                        tc_fence_after();
+                        const uint32_t a_base = smem_u32(sTf + tb * FZ_SLOT);
+                        for (int tap = 0; tap < sg.taps; ++tap) {
+                            const int dy = sg.taps == 9 ? tap / 3 - 1 : 0, dx = sg.taps == 9 ? tap % 3 - 1 : 0;
+                            mbar_wait_spin(&b_full[bs], bph);
+                            tc_fence_after();
+                            const uint32_t a0 = a_base + (uint32_t)(((1 + dy) * FZ_HX + (1 + dx)) * 16);
+                            const uint32_t b0 = smem_u32(sB + bs * B_STAGE);
+                            if (elect_one()) {
+                                for (int k = 0; k < ksteps; ++k) {
+                                    // K step of 16 channels = two 8-channel core-matrix columns
+                                    const uint64_t ad = sdesc_noswz(a0 + (uint32_t)(2 * k * FZ_LBO), FZ_LBO, FZ_SBO);
+                                    const uint64_t bd = sdesc_sw128(b0 + k * 32);
+                                    const uint32_t acc = (first && k == 0) ? 0u : 1u;
+                                    if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, acc);
+                                    else tc_mma_cg2(d, ad, bd, p.idesc, acc);
+                                }
+                                if constexpr (CG == 1) tc_commit(&b_empty[bs]);
+                                else tc_commit_cg2_mc(smem_u32(&b_empty[bs]), 0x3);
+                            }
+                            __syncwarp();
+                            first = false;
+                            if (++bs == FZ_BSTAGES) {
+                                bs = 0;
+                                bph ^= 1;
+                            }
+                        }
+                        if (elect_one()) {   // the transformed tile is free once its taps retire
+                            if constexpr (CG == 1) tc_commit(&tf_empty[tb]);
+                            else tc_commit_cg2_mc(smem_u32(&tf_empty[tb]), 0x3);
+                        }
+                        __syncwarp();
+                        if (++tb == 2) {
+                            tb = 0;
+                            tph ^= 1;
+                        }
+                    }
+                }
+                if (elect_one()) {
+                    if constexpr (CG == 1) tc_commit(&tfull[buf]);
+                    else tc_commit_cg2_mc(smem_u32(&tfull[buf]), 0x3);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ===================== epilogue (both CTAs) =====================
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;
+        const int by = r / FZ_BX, bxp = r - by * FZ_BX;
+        const T *b0 = reinterpret_cast<const T *>(p.bias0);
+        const T *b1 = reinterpret_cast<const T *>(p.bias1);
+        const T *res = reinterpret_cast<const T *>(p.residual);
+        T *out = reinterpret_cast<T *>(p.out);
+        const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
+        // residual tile of box w via TMA (coalesced, latency hidden behind the mainloop)
+        auto load_res = [&](int w) {
+            if (res && w < p.nwork && q4 == 0 && elect_one()) {
+                const int qq = w / p.ntile_n, ntt = w - qq * p.ntile_n;
+                const FzBox bb = fz_box(p, qq * CG + (int)rank);
+                const uint32_t fb = smem_u32(res_full);
+                mbar_arrive_expect_tx_addr(fb, (uint32_t)(128 * BN * 2));
+                tma_load_4d(smem_u32(sRes), &p.rmap, fb, ntt * BN, bb.x0, bb.y0, bb.t);
+            }
+            __syncwarp();
+        };
+        load_res(cluster_id);
+        int it = 0;
+        for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
+            const int buf = it & 1;
+            const uint32_t use = (uint32_t)(it >> 1) & 1;
+            const int q = w / p.ntile_n, nt = w - q * p.ntile_n;
+            const int box = q * CG + (int)rank;
+            const FzBox bx = fz_box(p, box);
+            long m = -1;
+            if (bx.valid) {
+                const int y = bx.y0 + by, x = bx.x0 + bxp;
+                if (y < p.H && x < p.W) m = ((long)bx.t * p.H + y) * p.W + x;
+            }
+            if (res) mbar_wait(res_full, (uint32_t)it & 1);
+            mbar_wait(&tfull[buf], use);
+            tc_fence_after();
+            const bool want_stats = p.stats != nullptr && bx.valid;
+#pragma unroll 1
+            for (int cc = 0, par = 0; cc < BN; cc += 16, par ^= 1) {
+                uint32_t v[16];
+                tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
+                const int n = nt * BN + cc;
+                float f[16];
+                if (m >= 0) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
+                    float e[8];
+                    if (b0) {
+                        load8(b0 + n, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] += e[i];
+                        load8(b0 + n + 8, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                    }
+                    if (b1) {
+                        load8(b1 + n, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[i] += e[i];
+                        load8(b1 + n + 8, e);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                    }
+                    if (res) {   // from the TMA-staged residual tile (row r of the box)
+                        const Vec8<T> *rr = reinterpret_cast<const Vec8<T> *>(sRes + ((size_t)r * BN + cc) * 2);
+                        const Vec8<T> ra = rr[0], rb = rr[1];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            f[i] += Elem<T>::to_f(ra.v[i]);
+                            f[8 + i] += Elem<T>::to_f(rb.v[i]);
+                        }
+                    }
+                    Vec8<T> lo, hi;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        lo.v[i] = Elem<T>::from_f(f[i]);
+                        hi.v[i] = Elem<T>::from_f(f[8 + i]);
+                        f[i] = Elem<T>::to_f(lo.v[i]);
+                        f[8 + i] = Elem<T>::to_f(hi.v[i]);
+                    }
+                    *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n) = lo;
+                    *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n + 8) = hi;
+                }
+                if (want_stats) {
+                    float x[32];
+                    box_row_values(f, m >= 0, x);
+                    red[(par * 4 + q4) * 32 + lane] = box_reduce_scatter32(x, lane);
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (q4 == 0) {
+                        const int per = p.tiles_x * p.tiles_y;
+                        const int bi = box - bx.t * per;
+                        const float val = box_combine4(red + par * 128, lane);
+                        p.stats[(((size_t)bx.t * per + bi) * p.cout + n + (lane & 15)) * 2 + (lane >> 4)] = val;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (CG == 1) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                                        smem_u32(&tempty[buf]))
+                                                    : "memory");
+                else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+            }
+            if (res) {   // all 4 warps are done with the residual tile: fetch the next one
+                asm volatile("bar.sync 3, 128;" ::: "memory");
+                load_res(w + nclusters);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<CG>(tmem, ncols);
+    }
+}
+
+// ----------------------------------------------------------------- host side
+PFN_encodeTiled_t get_encode_fn();
+dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
+extern int g_ws_cg;
+
+bool conv_fz_applicable(int H, int W, dvc_dtype dt) { return g_ws_cg == 2 && dt != DVC_F32 && H >= 32 && W >= 8; }
+
+static int g_fz_sms = 0;
+
+dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
+    DVC_CHECK_ARG(d.nseg >= 1 && d.nseg <= 4 && d.T >= 1 && d.T < 256 && d.cout % 16 == 0, DVC_ERR_UNSUPPORTED,
+                  "fused conv: bad descriptor");
+    FzParams p;
+    memset(&p, 0, sizeof(p));
+    constexpr int CG = 2;
+    int bn = d.cout;
+    if (bn > 256) {
+        bn = 0;
+        for (int c = 256; c >= 16; c -= 16)
+            if (d.cout % c == 0 && (c / CG) % 8 == 0) {
+                bn = c;
+                break;
+            }
+    }
+    DVC_CHECK_ARG(bn >= 16 && (bn / CG) % 8 == 0, DVC_ERR_UNSUPPORTED, "no N tile for cout=%d", d.cout);
+    p.bn = bn;
+    p.T = d.T;
+    p.H = d.H;
+    p.W = d.W;
+    p.cout = d.cout;
+    p.tiles_x = (d.W + FZ_BX - 1) / FZ_BX;
+    p.tiles_y = (d.H + FZ_BY - 1) / FZ_BY;
+    p.nbox = d.T * p.tiles_x * p.tiles_y;
+    p.ntile_n = d.cout / bn;
+    p.nwork = ((p.nbox + CG - 1) / CG) * p.ntile_n;
+    p.bias0 = d.bias0;
+    p.bias1 = d.bias1;
+    p.residual = d.residual;
+    p.out = d.out;
+    p.stats = reinterpret_cast<float *>(d.stats_out);
+    p.coef = reinterpret_cast<const float2 *>(d.coef);
+    p.cop = d.cop;
+    p.cs = d.cs;
+    p.has_carry = d.carry_pad != nullptr;
+    p.carry_pad = d.carry_pad;
+    p.cs_pad = d.cs_pad;
+    p.nseg = d.nseg;
+    dvc_status st;
+    DVC_CHECK_ARG(!p.has_carry || (((uintptr_t)d.carry_pad & 15) == 0 && d.cs_pad % 8 == 0), DVC_ERR_ARG,
+                  "fused conv: padded carry must have 16-byte rows");
+    int nb = 0;
+    const void *bw[2] = {nullptr, nullptr};
+    for (int s = 0; s < d.nseg; ++s) {
+        const FzDesc::Seg &g = d.seg[s];
+        DVC_CHECK_ARG(g.c % 16 == 0 && g.src != nullptr && ((uintptr_t)g.src & 15) == 0, DVC_ERR_UNSUPPORTED,
+                      "fused conv: segment channels / alignment");
+        int idx = -1;
+        for (int k = 0; k < nb; ++k)
+            if (bw[k] == g.w) idx = k;
+        if (idx < 0) {
+            DVC_CHECK_ARG(nb < 2, DVC_ERR_UNSUPPORTED, "at most two weight matrices per conv");
+            idx = nb++;
+            bw[idx] = g.w;
+            st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
+            if (st != DVC_OK) return st;
+        }
+        p.seg[s] = FzSeg{g.src, g.c, g.cglob0, g.taps, g.transform, g.shift, idx, g.col0, g.tapstride};
+    }
+    if (d.residual) {
+        PFN_encodeTiled_t enc = get_encode_fn();
+        DVC_CHECK_ARG(enc != nullptr && ((uintptr_t)d.residual & 15) == 0, DVC_ERR_ARG, "fused conv: residual map");
+        cuuint64_t gdim[4] = {(cuuint64_t)d.cout, (cuuint64_t)d.W, (cuuint64_t)d.H, (cuuint64_t)d.T};
+        cuuint64_t gstride[3] = {(cuuint64_t)d.cout * 2, (cuuint64_t)d.W * d.cout * 2, (cuuint64_t)d.H * d.W * d.cout * 2};
+        cuuint32_t box[4] = {(cuuint32_t)bn, (cuuint32_t)FZ_BX, (cuuint32_t)FZ_BY, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = enc(&p.rmap, d.dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                         4, const_cast<void *>(d.residual), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (residual) failed (%d)", (int)r);
+    }
+    p.idesc = make_idesc(d.dt == DVC_BF16, 128 * CG, bn);
+    const size_t smem = 1024 + 2 * (size_t)FZ_SLOT + (size_t)FZ_BSTAGES * (bn / CG) * 128 +
+                        (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (9 + 2 * FZ_BSTAGES) + 16 + 1024;
+    auto kern = d.dt == DVC_BF16 ? conv_fz_kernel<__nv_bfloat16, 2> : conv_fz_kernel<__half, 2>;
+    DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (g_fz_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_fz_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int clusters = g_fz_sms / CG;
+    if (clusters > p.nwork) clusters = p.nwork;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * CG);
+    cfg.blockDim = dim3(kFzThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DVC_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    ++g_launches;
+    return check_launch("conv_fz_kernel");
+}
+
+}  // namespace dvc

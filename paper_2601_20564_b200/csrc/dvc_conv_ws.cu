@@ -322,8 +322,15 @@ static dvc_status make_amap(CUtensorMap *map, const void *ptr, dvc_dtype dt, int
 
 dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
 
-// Spatial box minimising the number of 128-row MMA tiles per frame.
+// Spatial box minimising the number of 128-row MMA tiles per frame.  Frames
+// with H >= 32 use the fused engine's 8 x 16 box (dvc_conv_fz.cu) so that every
+// producer of a tensor shares one box decomposition (box statistics).
 void choose_box(int H, int W, int *BX, int *BY) {
+    if (H >= 32 && W >= 8) {
+        *BX = 8;
+        *BY = 16;
+        return;
+    }
     long best = -1;
     for (int bx = 1; bx <= W && bx <= 128; ++bx) {
         int by = 128 / bx;

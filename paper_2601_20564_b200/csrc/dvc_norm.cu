@@ -251,13 +251,7 @@ __device__ __forceinline__ float silu_t(float z) {
     if constexpr (sizeof(T) == 4) {
         return z / (1.0f + expf(-z));   // validation mode: accurate
     } else {
-        const float e = exp2f(fmaxf(z, -80.f) * -1.4426950408889634f);   // ex2.approx (fast-math free: exp2f)
-        const float d = 1.0f + e;                                          // in [1, 2^116)
-        float r = __int_as_float(0x7EF127EA - __float_as_int(d));         // ~1/d, |rel err| < 0.06
-        r = r * (2.0f - d * r);                                             // < 3.6e-3
-        r = r * (2.0f - d * r);                                             // < 1.3e-5
-        r = r * (2.0f - d * r);                                             // < 2e-10 (fp32 rounding)
-        return z * r;
+        return silu_fast(z);
     }
 }
 
@@ -491,7 +485,7 @@ __global__ void __launch_bounds__(256) gn_finalize_box_kernel(const float2 *__re
                                                               const float2 *__restrict__ pb, int cb,
                                                               const float2 *__restrict__ pk, int cs, int nbox, int G,
                                                               double n, double eps, const T *__restrict__ gamma,
-                                                              float2 *__restrict__ coef) {
+                                                              const T *__restrict__ beta, float2 *__restrict__ coef) {
     __shared__ double s_S[8], s_Q[8];
     __shared__ float s_mu, s_rs;
     const int g = blockIdx.x, t = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -535,8 +529,11 @@ __global__ void __launch_bounds__(256) gn_finalize_box_kernel(const float2 *__re
         s_rs = (float)(1.0 / sqrt(var + eps));
     }
     __syncthreads();
-    for (int c = g * cg + threadIdx.x; c < (g + 1) * cg; c += blockDim.x)
-        coef[(size_t)t * C + c] = make_float2(s_mu, s_rs * Elem<T>::to_f(gamma[c]));
+    for (int c = g * cg + threadIdx.x; c < (g + 1) * cg; c += blockDim.x) {
+        const float sc = s_rs * Elem<T>::to_f(gamma[c]);
+        // beta == null: (mean, scale) for gn_silu; else the folded affine (scale, beta - mean * scale)
+        coef[(size_t)t * C + c] = beta ? make_float2(sc, Elem<T>::to_f(beta[c]) - s_mu * sc) : make_float2(s_mu, sc);
+    }
 }
 
 size_t box_stats_bytes(int T, int H, int W, int C) { return align256((size_t)T * boxes_per_frame(H, W) * C * 8); }
@@ -551,12 +548,34 @@ static dvc_status gn_silu_box_t(const NormArgs &a, const BoxStatsIn &bs, int H, 
     gn_finalize_box_kernel<T><<<dim3(a.G, a.T), 256, 0, stream>>>(
         reinterpret_cast<const float2 *>(bs.a), a.ca, reinterpret_cast<const float2 *>(bs.b), a.cb,
         reinterpret_cast<const float2 *>(bs.carry), a.cs, boxes_per_frame(H, W), a.G, (double)(C / a.G) * a.HW,
-        (double)a.eps, reinterpret_cast<const T *>(a.gamma), coef);
+        (double)a.eps, reinterpret_cast<const T *>(a.gamma), nullptr, coef);
     ++g_launches;
     gn_silu_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, coef, reinterpret_cast<const T *>(a.beta),
                                                              reinterpret_cast<T *>(a.out));
     ++g_launches;
     return check_launch("gn_silu_box");
+}
+
+template <typename T>
+static dvc_status gn_coef_t(const NormArgs &a, const BoxStatsIn &bs, int H, int W, cudaStream_t stream) {
+    const int C = a.ca + a.cb;
+    gn_finalize_box_kernel<T><<<dim3(a.G, a.T), 256, 0, stream>>>(
+        reinterpret_cast<const float2 *>(bs.a), a.ca, reinterpret_cast<const float2 *>(bs.b), a.cb,
+        reinterpret_cast<const float2 *>(bs.carry), a.cs, boxes_per_frame(H, W), a.G, (double)(C / a.G) * a.HW,
+        (double)a.eps, reinterpret_cast<const T *>(a.gamma), reinterpret_cast<const T *>(a.beta),
+        reinterpret_cast<float2 *>(a.out));
+    ++g_launches;
+    return check_launch("gn_coef");
+}
+
+dvc_status gn_coef_box_run(const NormArgs &a, const BoxStatsIn &bs, int H, int W, dvc_dtype dt, cudaStream_t stream) {
+    const int C = a.ca + a.cb;
+    DVC_CHECK_ARG(a.G >= 1 && C % a.G == 0 && a.cs % (C / a.G) == 0, DVC_ERR_UNSUPPORTED, "GN coef: bad groups");
+    switch (dt) {
+        case DVC_BF16: return gn_coef_t<__nv_bfloat16>(a, bs, H, W, stream);
+        case DVC_F16: return gn_coef_t<__half>(a, bs, H, W, stream);
+        default: return gn_coef_t<float>(a, bs, H, W, stream);
+    }
 }
 
 dvc_status gn_silu_box_run(const NormArgs &a, const BoxStatsIn &bs, int H, int W, dvc_dtype dt, cudaStream_t stream) {

@@ -25,6 +25,8 @@ struct BoxStatsIn {
     const void *carry;   // [nbox][cs] float2 of the carry slice, or null (zeros)
 };
 size_t box_stats_bytes(int T, int H, int W, int C);
+// GN coefficients only: a.out <- float2 [T][C] (scale, beta - mean*scale) for the fused conv
+dvc_status gn_coef_box_run(const NormArgs &a, const BoxStatsIn &bs, int H, int W, dvc_dtype dt, cudaStream_t stream);
 // GN1/GN2 + SiLU from box statistics (no statistics pass over the operand); ws >= T*C*8 bytes
 dvc_status gn_silu_box_run(const NormArgs &a, const BoxStatsIn &bs, int H, int W, dvc_dtype dt, cudaStream_t stream);
 dvc_status nearest_run(const void *src, void *dst, int T, int hi, int wi, int ho, int wo, int C, dvc_dtype dt,

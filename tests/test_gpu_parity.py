@@ -127,7 +127,10 @@ def test_resblock_fp32_config1(dvc, orc, with_carry):   # C1: T=8, 64 ch, 32x32,
 @pytest.mark.parametrize("dtype", [torch.float32] + DTYPES)
 @pytest.mark.parametrize("cin,cout,cb,T,H,W", [(32, 32, 0, 3, 9, 17), (48, 32, 0, 2, 16, 16), (64, 32, 32, 2, 7, 11),
                                                  (240, 240, 0, 2, 10, 13), (720, 240, 240, 1, 6, 9),
-                                                 (1920, 960, 960, 2, 3, 5), (240, 480, 0, 1, 12, 20)])
+                                                 (1920, 960, 960, 2, 3, 5), (240, 480, 0, 1, 12, 20),
+                                                 # H >= 32: the fused GN/SiLU/shift conv engine (8x16 halo boxes)
+                                                 (240, 240, 0, 3, 40, 24), (720, 240, 240, 2, 34, 20),
+                                                 (64, 32, 32, 2, 33, 9), (480, 480, 0, 2, 45, 16)])
 def test_resblock_parity(dvc, orc, dtype, cin, cout, cb, T, H, W):
     G = 8 if cin < 240 else 24
     w = synthgen.resblock_weights(cin, cout, seed=cin + cout)
@@ -145,28 +148,40 @@ def test_resblock_parity(dvc, orc, dtype, cin, cout, cb, T, H, W):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_resblock_identity_when_conv2_zero(dvc, dtype):   # P7 on the GPU, bit-exact
+@pytest.mark.parametrize("H,W", [(8, 8), (36, 16)])
+def test_resblock_identity_when_conv2_zero(dvc, dtype, H, W):   # P7 on the GPU, bit-exact
     w = synthgen.resblock_weights(64, 64)
     w["conv2_w"][:] = 0
     w["conv2_b"][:] = 0
     wd, _ = rb_device(w, dtype)
-    x, _ = dev(synthgen.normal((3, 8, 8, 64)), dtype)
+    x, _ = dev(synthgen.normal((3, H, W, 64)), dtype)
     out = _run_block(dvc, wd, x)
     assert torch.equal(out, x)
 
 
+def test_resblock_legacy_gn_path(dvc, orc):   # G % P != 0: slice not whole groups -> per-element shifted GN pass
+    dtype = torch.bfloat16
+    w = synthgen.resblock_weights(240, 240, seed=11)
+    wd, w64 = rb_device(w, dtype)
+    x, x64 = dev(synthgen.normal((3, 40, 16, 240), seed=12), dtype)
+    out = _run_block(dvc, wd, x, G=30)
+    ref, _ = orc.resblock(x64, None, w64, 30, 8, mode="bf16")
+    assert rel_l2(host64(out), ref) <= 1e-2
+
+
 @pytest.mark.parametrize("dtype", DTYPES + [torch.float32])
-def test_resblock_batch_equals_online_and_deterministic(dvc, dtype):   # P9 / G10 / G12, bit-exact
+@pytest.mark.parametrize("H,W", [(10, 12), (40, 17)])
+def test_resblock_batch_equals_online_and_deterministic(dvc, dtype, H, W):   # P9 / G10 / G12, bit-exact
     w = synthgen.resblock_weights(240, 240)
     wd, _ = rb_device(w, dtype)
     T = 6
-    x, _ = dev(synthgen.normal((T, 10, 12, 240)), dtype)
+    x, _ = dev(synthgen.normal((T, H, W, 240)), dtype)
     full = _run_block(dvc, wd, x, G=24)
     again = _run_block(dvc, wd, x, G=24)
     assert torch.equal(full, again)
     carry, parts = None, []
     for t in range(T):
-        ko = torch.empty((10, 12, 30), dtype=dtype, device="cuda")
+        ko = torch.empty((H, W, 30), dtype=dtype, device="cuda")
         parts.append(_run_block(dvc, wd, x[t:t + 1].contiguous(), carry=carry, carry_out=ko, G=24))
         carry = ko
     assert torch.equal(torch.cat(parts), full)

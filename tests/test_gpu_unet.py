@@ -32,7 +32,7 @@ def _net(dvc, dtype, width, c_lat, h, w, max_T, G, seed=0):
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("h,w,T", [(12, 20, 3), (9, 14, 2)])
+@pytest.mark.parametrize("h,w,T", [(12, 20, 3), (9, 14, 2), (64, 40, 2)])
 def test_skeleton_small_parity(dvc, orc, dtype, h, w, T):
     net, wts = _net(dvc, dtype, SMALL, 32, h, w, 4, 8)
     lat, lat64 = dev(synthgen.normal((T, h, w, 32), 1), dtype)
@@ -48,8 +48,9 @@ def test_skeleton_small_parity(dvc, orc, dtype, h, w, T):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-def test_skeleton_batch_equals_online_and_chunks(dvc, dtype):   # G10, G11 (loopback), G12: bit-exact
-    h, w, T = 12, 20, 6
+@pytest.mark.parametrize("h,w", [(12, 20), (66, 36)])
+def test_skeleton_batch_equals_online_and_chunks(dvc, dtype, h, w):   # G10, G11 (loopback), G12: bit-exact
+    T = 6
     net, _ = _net(dvc, dtype, SMALL, 32, h, w, T, 8)
     lat, _ = dev(synthgen.normal((T, h, w, 32), 1), dtype)
     ctx, _ = dev(synthgen.normal((T, h, w, 32), 5), dtype)
