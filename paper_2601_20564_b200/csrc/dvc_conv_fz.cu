@@ -51,6 +51,7 @@ struct FzSeg {
 struct FzParams {
     CUtensorMap bmap[2];   // weights, box {64, BN/CG}
     CUtensorMap rmap;      // residual [T][H][W][cout], box {BN, 8, 16, 1}, no swizzle (if residual)
+    CUtensorMap smap[4];   // raw (transform == 0) segments: box {64, 8, 16, 1}, SW128 -> straight into a tile slot
     FzSeg seg[4];
     int nseg, cs, has_carry, cs_pad;
     const void *carry_pad; // [H][W][cs_pad] (16-byte rows)
@@ -189,6 +190,28 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 const FzSeg &sg = p.seg[s];
                 const int nch = (sg.c + 63) >> 6;
                 for (int ch = 0; ch < nch; ++ch) {
+                    if (!sg.transform) {
+                        // raw 1x1 segment: no transform -- TMA the box (SW128) straight into the tile slot;
+                        // each CTA signals its bytes to the leader's tf_full
+                        mbar_wait(&tf_empty[tb], tph ^ 1);
+                        if (warp == 8 && elect_one()) {
+                            const uint32_t fb = CG == 2 ? tf_full_leader + (uint32_t)(tb * 8) : smem_u32(&tf_full[tb]);
+                            if constexpr (CG == 1) {
+                                mbar_arrive_expect_tx_addr(fb, 128 * 128);
+                                tma_load_4d(smem_u32(sTf + tb * FZ_SLOT), &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
+                            } else {
+                                mbar_arrive_expect_tx_cluster(fb, 128 * 128);
+                                tma_load_4d_cg2(smem_u32(sTf + tb * FZ_SLOT), &p.smap[s], fb, ch * 64, bx.x0, bx.y0,
+                                                bx.t);
+                            }
+                        }
+                        __syncwarp();
+                        if (++tb == 2) {
+                            tb = 0;
+                            tph ^= 1;
+                        }
+                        continue;
+                    }
                     const int cl = ch * 64 + kg * 8;           // first channel (segment-local) of this warp
                     const int cgl = sg.cglob0 + cl;            // operand channel (coef index)
                     const bool cval = cl < sg.c;
@@ -304,8 +327,11 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                             const uint32_t b0 = smem_u32(sB + bs * B_STAGE);
                             if (elect_one()) {
                                 for (int k = 0; k < ksteps; ++k) {
-                                    // K step of 16 channels = two 8-channel core-matrix columns
-                                    const uint64_t ad = sdesc_noswz(a0 + (uint32_t)(2 * k * FZ_LBO), FZ_LBO, FZ_SBO);
+                                    // transformed tile: K step of 16 channels = two 8-channel core-matrix
+                                    // columns of the halo layout; raw segment: the TMA box in SW128
+                                    const uint64_t ad = sg.transform
+                                                            ? sdesc_noswz(a0 + (uint32_t)(2 * k * FZ_LBO), FZ_LBO, FZ_SBO)
+                                                            : sdesc_sw128(a_base + k * 32);
                                     const uint64_t bd = sdesc_sw128(b0 + k * 32);
                                     const uint32_t acc = (first && k == 0) ? 0u : 1u;
                                     if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, acc);
@@ -464,6 +490,8 @@ PFN_encodeTiled_t get_encode_fn();
 dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
 extern int g_ws_cg;
 
+dvc_status make_box_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX, int BY);
+
 bool conv_fz_applicable(int H, int W, dvc_dtype dt) { return g_ws_cg == 2 && dt != DVC_F32 && H >= 32 && W >= 8; }
 
 static int g_fz_sms = 0;
@@ -526,6 +554,11 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
             if (st != DVC_OK) return st;
         }
         p.seg[s] = FzSeg{g.src, g.c, g.cglob0, g.taps, g.transform, g.shift, idx, g.col0, g.tapstride};
+        if (!g.transform) {
+            DVC_CHECK_ARG(g.taps == 1, DVC_ERR_UNSUPPORTED, "fused conv: raw segments are 1x1");
+            st = make_box_map(&p.smap[s], g.src, d.dt, d.T, d.H, d.W, g.c, FZ_BX, FZ_BY);
+            if (st != DVC_OK) return st;
+        }
     }
     if (d.residual) {
         PFN_encodeTiled_t enc = get_encode_fn();

@@ -304,8 +304,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
 // ----------------------------------------------------------------- host side
 PFN_encodeTiled_t get_encode_fn();
 
+dvc_status make_box_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX, int BY);
 static dvc_status make_amap(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX,
                             int BY) {
+    return make_box_map(map, ptr, dt, T, H, W, C, BX, BY);
+}
+dvc_status make_box_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX, int BY) {
     PFN_encodeTiled_t enc = get_encode_fn();
     DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && (C * 2) % 16 == 0, DVC_ERR_ARG, "activation must be 16-byte aligned");
