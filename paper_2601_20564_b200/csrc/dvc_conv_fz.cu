@@ -102,12 +102,14 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int BN = p.bn, BNH = p.bn / CG;
     const int B_STAGE = BNH * 128;
-    uint8_t *sTf = smem;                        // [2] transformed tiles
-    uint8_t *sB = sTf + 2 * FZ_SLOT;            // [FZ_BSTAGES] weight tiles
+    // tile slots: 4 (2 when the residual tile needs the shared memory)
+    const int NTF = p.residual ? 2 : 4;
+    uint8_t *sTf = smem;                        // [NTF] transformed / raw operand tiles
+    uint8_t *sB = sTf + NTF * FZ_SLOT;          // [FZ_BSTAGES] weight tiles
     uint8_t *sRes = sB + FZ_BSTAGES * B_STAGE;  // residual tile of the current output box [128][BN]
     uint64_t *tf_full = reinterpret_cast<uint64_t *>(sRes + (p.residual ? 128 * BN * 2 : 0));
-    uint64_t *tf_empty = tf_full + 2;
-    uint64_t *b_full = tf_empty + 2;
+    uint64_t *tf_empty = tf_full + 4;
+    uint64_t *b_full = tf_empty + 4;
     uint64_t *b_empty = b_full + FZ_BSTAGES;
     uint64_t *tfull = b_empty + FZ_BSTAGES;
     uint64_t *tempty = tfull + 2;
@@ -121,9 +123,11 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     const uint32_t ncols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             mbar_init(&tf_full[i], CG);
             mbar_init(&tf_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], CG * 4);
         }
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                             }
                         }
                         __syncwarp();
-                        if (++tb == 2) {
+                        if (++tb == NTF) {
                             tb = 0;
                             tph ^= 1;
                         }
@@ -292,7 +296,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         else mbar_arrive_cluster(tf_full_leader + (uint32_t)(tb * 8));
                     }
                     __syncwarp();
-                    if (++tb == 2) {
+                    if (++tb == NTF) {
                         tb = 0;
                         tph ^= 1;
                     }
@@ -352,7 +356,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                             else tc_commit_cg2_mc(smem_u32(&tf_empty[tb]), 0x3);
                         }
                         __syncwarp();
-                        if (++tb == 2) {
+                        if (++tb == NTF) {
                             tb = 0;
                             tph ^= 1;
                         }
@@ -574,8 +578,8 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (residual) failed (%d)", (int)r);
     }
     p.idesc = make_idesc(d.dt == DVC_BF16, 128 * CG, bn);
-    const size_t smem = 1024 + 2 * (size_t)FZ_SLOT + (size_t)FZ_BSTAGES * (bn / CG) * 128 +
-                        (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (9 + 2 * FZ_BSTAGES) + 16 + 1024;
+    const size_t smem = 1024 + (d.residual ? 2 : 4) * (size_t)FZ_SLOT + (size_t)FZ_BSTAGES * (bn / CG) * 128 +
+                        (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (13 + 2 * FZ_BSTAGES) + 16 + 1024;
     auto kern = d.dt == DVC_BF16 ? conv_fz_kernel<__nv_bfloat16, 2> : conv_fz_kernel<__half, 2>;
     DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (g_fz_sms == 0) {
