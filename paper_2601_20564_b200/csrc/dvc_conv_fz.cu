@@ -35,7 +35,7 @@ constexpr int FZ_BOX_BYTES = FZ_HROWS * 128;  // raw halo box, SW128
 constexpr int FZ_SLOT = 23552;                // 1024-aligned slot (>= 23040)
 constexpr int FZ_LBO = FZ_HROWS * 16;         // between 8-channel core-matrix columns
 constexpr int FZ_SBO = FZ_HX * 16;            // between 8-row groups (image rows)
-constexpr int FZ_BSTAGES = 6;
+constexpr int FZ_MAX_BSTAGES = 16;
 constexpr int kFzThreads = 512;
 
 struct FzSeg {
@@ -62,6 +62,8 @@ struct FzParams {
     void *out;
     float *stats;
     uint32_t idesc;
+    int ntf, nb;   // tile slots, weight stages (sized from the shared-memory budget)
+    int dbg;   // perf experiments (DVC_DEBUG_CONV): 1 skip transform work, 4 skip MMAs, 16 skip epilogue
 };
 
 // UMMA descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B
@@ -103,7 +105,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     const int BN = p.bn, BNH = p.bn / CG;
     const int B_STAGE = BNH * 128;
     // tile slots: 4 (2 when the residual tile needs the shared memory)
-    const int NTF = p.residual ? 2 : 4;
+    const int NTF = p.ntf, FZ_BSTAGES = p.nb;
     uint8_t *sTf = smem;                        // [NTF] transformed / raw operand tiles
     uint8_t *sB = sTf + NTF * FZ_SLOT;          // [FZ_BSTAGES] weight tiles
     uint8_t *sRes = sB + FZ_BSTAGES * B_STAGE;  // residual tile of the current output box [128][BN]
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                     uint8_t *tf = sTf + tb * FZ_SLOT + kg * FZ_LBO;
                     constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane
                     uint4 cu[NR], pv[NR];
+                    if (!(p.dbg & 1))
 #pragma unroll
                     for (int k = 0; k < NR; ++k) {   // issue every load before any use
                         const int r = lane + 32 * k;
@@ -262,6 +265,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                             }
                         }
                     }
+                    if (!(p.dbg & 1))
 #pragma unroll
                     for (int k = 0; k < NR; ++k) {
                         const int r = lane + 32 * k;
@@ -338,8 +342,10 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                                                             : sdesc_sw128(a_base + k * 32);
                                     const uint64_t bd = sdesc_sw128(b0 + k * 32);
                                     const uint32_t acc = (first && k == 0) ? 0u : 1u;
-                                    if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, acc);
-                                    else tc_mma_cg2(d, ad, bd, p.idesc, acc);
+                                    if (!(p.dbg & 4) || acc == 0) {
+                                        if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, acc);
+                                        else tc_mma_cg2(d, ad, bd, p.idesc, acc);
+                                    }
                                 }
                                 if constexpr (CG == 1) tc_commit(&b_empty[bs]);
                                 else tc_commit_cg2_mc(smem_u32(&b_empty[bs]), 0x3);
@@ -408,7 +414,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
             tc_fence_after();
             const bool want_stats = p.stats != nullptr && bx.valid;
 #pragma unroll 1
-            for (int cc = 0, par = 0; cc < BN; cc += 16, par ^= 1) {
+            for (int cc = 0, par = 0; cc < ((p.dbg & 16) ? 0 : BN); cc += 16, par ^= 1) {
                 uint32_t v[16];
                 tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
                 const int n = nt * BN + cc;
@@ -578,8 +584,28 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (residual) failed (%d)", (int)r);
     }
     p.idesc = make_idesc(d.dt == DVC_BF16, 128 * CG, bn);
-    const size_t smem = 1024 + (d.residual ? 2 : 4) * (size_t)FZ_SLOT + (size_t)FZ_BSTAGES * (bn / CG) * 128 +
-                        (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (13 + 2 * FZ_BSTAGES) + 16 + 1024;
+    {
+        const char *e = getenv("DVC_DEBUG_CONV");
+        p.dbg = e ? atoi(e) : 0;
+    }
+    // shared memory: tile slots, weight stages, residual tile; fill the 227 KB budget with weight stages
+    {
+        const char *e = getenv("DVC_FZ_NTF");
+        p.ntf = e ? atoi(e) : (d.residual ? 2 : 4);
+        if (p.ntf < 2 || p.ntf > 4) p.ntf = 2;
+    }
+    const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (13 + 2 * FZ_MAX_BSTAGES) +
+                         16 + 1024 + 1024 /* static */;
+    const size_t bstage = (size_t)(bn / CG) * 128;
+    int nbst = (int)((227 * 1024 - fixed) / bstage);
+    {
+        const char *e = getenv("DVC_FZ_NB");
+        if (e && atoi(e) >= 2 && atoi(e) < nbst) nbst = atoi(e);
+    }
+    if (nbst > FZ_MAX_BSTAGES) nbst = FZ_MAX_BSTAGES;
+    DVC_CHECK_ARG(nbst >= 2, DVC_ERR_UNSUPPORTED, "fused conv: shared memory too small");
+    p.nb = nbst;
+    const size_t smem = fixed - 1024 + (size_t)nbst * bstage;
     auto kern = d.dt == DVC_BF16 ? conv_fz_kernel<__nv_bfloat16, 2> : conv_fz_kernel<__half, 2>;
     DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (g_fz_sms == 0) {
