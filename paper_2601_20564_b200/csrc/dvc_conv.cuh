@@ -27,7 +27,16 @@ struct ConvSeg {
     int w_ld;          // row length of w (elements)
     int w_col0;        // first column of this segment
     int w_tapstride;   // columns between taps
+    int packed;        // 1: w is a packed K-chunk-major image (pack_weights_run): B tile (tap, chunk) =
+                       //    rows [w_col0 + (tap*nchunks + chunk)*cout + n0, +BN) of a [rows][64] matrix,
+                       //    one contiguous block; w_col0 = this segment's row base, w_ld = 64
 };
+
+// Pack a conv weight matrix W [cout][taps][cin_total] (OHWI) segment [off, off+cs) into the
+// K-chunk-major image [taps][ceil(cs/64)][cout][64] (zero-padded channels).  Returns elements written.
+size_t packed_elems(int cout, int taps, int cs);
+dvc_status pack_weights_run(const void *W, dvc_dtype dt, int cout, int taps, int cin_total, int off, int cs, void *out,
+                            cudaStream_t stream);
 
 struct ConvDesc {
     ConvSeg seg[4];
@@ -49,6 +58,7 @@ struct FzDesc {
         int c, cglob0, taps, transform, shift;
         const void *w;
         int w_ld, col0, tapstride;
+        int packed;   // as ConvSeg::packed
     };
     Seg seg[4];
     int nseg;

@@ -45,7 +45,7 @@ struct FzSeg {
     int taps;       // 9 (GN/SiLU operand) or 1 (raw shortcut)
     int transform;  // 1: GN-apply + SiLU + padding zero; 0: copy
     int shift;      // 1: channels [0, cs) of the segment come from frame t-1 / carry
-    int bidx, col0, tapstride;
+    int bidx, col0, tapstride, packed;
 };
 
 struct FzParams {
@@ -166,13 +166,15 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         if (elect_one()) {
                             const uint32_t fb = smem_u32(&b_full[bs]);
                             const uint32_t dB = smem_u32(sB + bs * B_STAGE);
-                            const int col = sg.col0 + tap * sg.tapstride + ch * 64;
+                            // packed weights: the (tap, chunk) tile is one contiguous row block
+                            const int col = sg.packed ? 0 : sg.col0 + tap * sg.tapstride + ch * 64;
+                            const int row = sg.packed ? sg.col0 + (tap * nch + ch) * p.cout + n0 : n0;
                             if constexpr (CG == 1) {
                                 mbar_arrive_expect_tx_addr(fb, tx);
-                                tma_load_2d_a(dB, bm, fb, col, n0);
+                                tma_load_2d_a(dB, bm, fb, col, row);
                             } else {
                                 if (rank == 0) mbar_arrive_expect_tx_addr(fb, tx);
-                                tma_load_2d_cg2(dB, bm, mapa_shared(fb, 0), col, n0);
+                                tma_load_2d_cg2(dB, bm, mapa_shared(fb, 0), col, row);
                             }
                         }
                         __syncwarp();
@@ -560,10 +562,19 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
             DVC_CHECK_ARG(nb < 2, DVC_ERR_UNSUPPORTED, "at most two weight matrices per conv");
             idx = nb++;
             bw[idx] = g.w;
-            st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
+            if (g.packed) {
+                long rows = 0;   // the map covers every segment sharing this packed block
+                for (int s2 = 0; s2 < d.nseg; ++s2)
+                    if (d.seg[s2].w == g.w) {
+                        const long r = d.seg[s2].col0 + (long)d.seg[s2].taps * ((d.seg[s2].c + 63) / 64) * d.cout;
+                        if (r > rows) rows = r;
+                    }
+                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, rows, 64, bn / CG);
+            } else
+                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
             if (st != DVC_OK) return st;
         }
-        p.seg[s] = FzSeg{g.src, g.c, g.cglob0, g.taps, g.transform, g.shift, idx, g.col0, g.tapstride};
+        p.seg[s] = FzSeg{g.src, g.c, g.cglob0, g.taps, g.transform, g.shift, idx, g.col0, g.tapstride, g.packed};
         if (!g.transform) {
             DVC_CHECK_ARG(g.taps == 1, DVC_ERR_UNSUPPORTED, "fused conv: raw segments are 1x1");
             st = make_box_map(&p.smap[s], g.src, d.dt, d.T, d.H, d.W, g.c, FZ_BX, FZ_BY);

@@ -29,7 +29,7 @@ namespace dvc {
 struct WsParams {
     CUtensorMap amap[4];   // per segment: 4D {C, W, H, T}, box {64, BX, BY, 1}, SW128, OOB zero
     CUtensorMap bmap[2];   // weights 2D {K, C_out}, box {64, BN/CG}, SW128
-    int bidx[4], seg_c[4], seg_taps[4], seg_col0[4], seg_tapstride[4];
+    int bidx[4], seg_c[4], seg_taps[4], seg_col0[4], seg_tapstride[4], seg_packed[4];
     int nseg;
     int T, H, W, cout, bn;
     int BX, BY, tiles_x, tiles_y, nbox, ntile_n, nwork;
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         const int dy = p.seg_taps[s] == 9 ? tap / 3 - 1 : 0;
                         const int dx = p.seg_taps[s] == 9 ? tap % 3 - 1 : 0;
                         const int col = p.seg_col0[s] + tap * p.seg_tapstride[s];
+                        const int prow = p.seg_col0[s] + tap * nch * p.cout;   // packed weights: row block of this tap
                         for (int ch = 0; ch < nch; ++ch) {
                             if (!(p.dbg & 32)) mbar_wait_spin(&empty[stage], phase ^ 1);
                             const uint32_t fb = smem_u32(&full[stage]);
@@ -126,12 +127,18 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                                 mbar_arrive_expect_tx_addr(fb, txs);
                                 if (la) tma_load_4d(dA, &p.amap[s], fb, ch * 64, x0 + dx, y0 + dy, t);
                             if (p.dbg & 32) { /* timing experiment: no pipeline handshakes */ }
-                                if (lbb) tma_load_2d_a(dB, bm, fb, col + ch * 64, n0);
+                                if (lbb) {
+                                    if (p.seg_packed[s]) tma_load_2d_a(dB, bm, fb, 0, prow + ch * p.cout + n0);
+                                    else tma_load_2d_a(dB, bm, fb, col + ch * 64, n0);
+                                }
                             } else {
                                 if (rank == 0) mbar_arrive_expect_tx_addr(fb, txs);
                                 const uint32_t lb = mapa_shared(fb, 0);   // leader's barrier
                                 if (la) tma_load_4d_cg2(dA, &p.amap[s], lb, ch * 64, x0 + dx, y0 + dy, t);
-                                if (lbb) tma_load_2d_cg2(dB, bm, lb, col + ch * 64, n0);
+                                if (lbb) {
+                                    if (p.seg_packed[s]) tma_load_2d_cg2(dB, bm, lb, 0, prow + ch * p.cout + n0);
+                                    else tma_load_2d_cg2(dB, bm, lb, col + ch * 64, n0);
+                                }
                             }
                             if (++stage == STAGES) {
                                 stage = 0;
@@ -444,10 +451,20 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
             DVC_CHECK_ARG(nb < 2, DVC_ERR_UNSUPPORTED, "at most two weight matrices per conv");
             idx = nb++;
             bw[idx] = g.w;
-            st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
+            if (g.packed) {
+                long rows = 0;   // the map covers every segment sharing this packed block
+                for (int s2 = 0; s2 < d.nseg; ++s2)
+                    if (d.seg[s2].w == g.w) {
+                        const long r = d.seg[s2].w_col0 + (long)d.seg[s2].taps * ((d.seg[s2].c_src + 63) / 64) * d.cout;
+                        if (r > rows) rows = r;
+                    }
+                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, rows, 64, bn / CG);
+            } else
+                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
             if (st != DVC_OK) return st;
         }
         p.bidx[s] = idx;
+        p.seg_packed[s] = g.packed;
         p.seg_c[s] = g.c_src;
         p.seg_taps[s] = g.taps;
         p.seg_col0[s] = g.w_col0;
