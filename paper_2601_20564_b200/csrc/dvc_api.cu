@@ -170,9 +170,16 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
                                   stream)) != DVC_OK)
             return st;
         FzDesc f1{};
-        f1.seg[0] = FzDesc::Seg{xa, b.ca, 0, 9, 1, 1, b.conv1_w, 9 * cin, 0, cin};
-        f1.nseg = 1;
-        if (b.cb > 0) f1.seg[f1.nseg++] = FzDesc::Seg{xb, b.cb, b.ca, 9, 1, 0, b.conv1_w, 9 * cin, b.ca, cin};
+        if (b.conv1_pk) {
+            const int rows_a = 9 * ((b.ca + 63) / 64) * b.cout;
+            f1.seg[0] = FzDesc::Seg{xa, b.ca, 0, 9, 1, 1, b.conv1_pk, 64, 0, 0, 1};
+            f1.nseg = 1;
+            if (b.cb > 0) f1.seg[f1.nseg++] = FzDesc::Seg{xb, b.cb, b.ca, 9, 1, 0, b.conv1_pk, 64, rows_a, 0, 1};
+        } else {
+            f1.seg[0] = FzDesc::Seg{xa, b.ca, 0, 9, 1, 1, b.conv1_w, 9 * cin, 0, cin, 0};
+            f1.nseg = 1;
+            if (b.cb > 0) f1.seg[f1.nseg++] = FzDesc::Seg{xb, b.cb, b.ca, 9, 1, 0, b.conv1_w, 9 * cin, b.ca, cin, 0};
+        }
         f1.T = T;
         f1.H = H;
         f1.W = W;
@@ -198,11 +205,18 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
         NormArgs n2{y1, nullptr, nullptr, b.cout, 0, 0, T, HW, b.G, b.eps, b.gn2_w, b.gn2_b, coef, nullptr};
         if ((st = gn_coef_box_run(n2, BoxStatsIn{st_y1, nullptr, nullptr}, H, W, b.dt, stream)) != DVC_OK) return st;
         FzDesc f2{};
-        f2.seg[0] = FzDesc::Seg{y1, b.cout, 0, 9, 1, 0, b.conv2_w, 9 * b.cout, 0, b.cout};
+        if (b.conv2_pk) f2.seg[0] = FzDesc::Seg{y1, b.cout, 0, 9, 1, 0, b.conv2_pk, 64, 0, 0, 1};
+        else f2.seg[0] = FzDesc::Seg{y1, b.cout, 0, 9, 1, 0, b.conv2_w, 9 * b.cout, 0, b.cout, 0};
         f2.nseg = 1;
         if (b.sc_w) {
-            f2.seg[f2.nseg++] = FzDesc::Seg{xa, b.ca, 0, 1, 0, 0, b.sc_w, cin, 0, 0};
-            if (b.cb > 0) f2.seg[f2.nseg++] = FzDesc::Seg{xb, b.cb, 0, 1, 0, 0, b.sc_w, cin, b.ca, 0};
+            if (b.sc_pk) {
+                const int rows_a = ((b.ca + 63) / 64) * b.cout;
+                f2.seg[f2.nseg++] = FzDesc::Seg{xa, b.ca, 0, 1, 0, 0, b.sc_pk, 64, 0, 0, 1};
+                if (b.cb > 0) f2.seg[f2.nseg++] = FzDesc::Seg{xb, b.cb, 0, 1, 0, 0, b.sc_pk, 64, rows_a, 0, 1};
+            } else {
+                f2.seg[f2.nseg++] = FzDesc::Seg{xa, b.ca, 0, 1, 0, 0, b.sc_w, cin, 0, 0, 0};
+                if (b.cb > 0) f2.seg[f2.nseg++] = FzDesc::Seg{xb, b.cb, 0, 1, 0, 0, b.sc_w, cin, b.ca, 0, 0};
+            }
             f2.bias1 = b.sc_b;
         } else {
             f2.residual = xa;
@@ -252,7 +266,9 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
     if (st != DVC_OK) return st;
     // a5: Y1 = conv3x3(H1) + b1   (+ box statistics of Y1 from the epilogue)
     ConvDesc c1{};
-    c1.seg[0] = ConvSeg{h1, cin, SEG_SAME, H, W, 9, b.conv1_w, 9 * cin, 0, cin};
+    const bool pk = b.dt != DVC_F32 && conv_ws_applicable_dims(b.dt);
+    if (pk && b.conv1_pk && b.cb == 0) c1.seg[0] = ConvSeg{h1, cin, SEG_SAME, H, W, 9, b.conv1_pk, 64, 0, 0, 1};
+    else c1.seg[0] = ConvSeg{h1, cin, SEG_SAME, H, W, 9, b.conv1_w, 9 * cin, 0, cin};
     c1.nseg = 1;
     c1.T = T;
     c1.ho = H;
@@ -271,11 +287,18 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
     // a7 + a8: Out = S(X) + conv3x3(H2) + b2; the 1x1 shortcut on the UNSHIFTED X is
     // extra K segments of the same GEMM (same fp32 accumulator), identity = epilogue add.
     ConvDesc c2{};
-    c2.seg[0] = ConvSeg{h2, b.cout, SEG_SAME, H, W, 9, b.conv2_w, 9 * b.cout, 0, b.cout};
+    if (pk && b.conv2_pk) c2.seg[0] = ConvSeg{h2, b.cout, SEG_SAME, H, W, 9, b.conv2_pk, 64, 0, 0, 1};
+    else c2.seg[0] = ConvSeg{h2, b.cout, SEG_SAME, H, W, 9, b.conv2_w, 9 * b.cout, 0, b.cout};
     c2.nseg = 1;
     if (b.sc_w) {
-        c2.seg[c2.nseg++] = ConvSeg{xa, b.ca, SEG_SAME, H, W, 1, b.sc_w, cin, 0, 0};
-        if (b.cb > 0) c2.seg[c2.nseg++] = ConvSeg{xb, b.cb, SEG_SAME, H, W, 1, b.sc_w, cin, b.ca, 0};
+        if (pk && b.sc_pk) {
+            const int rows_a = ((b.ca + 63) / 64) * b.cout;
+            c2.seg[c2.nseg++] = ConvSeg{xa, b.ca, SEG_SAME, H, W, 1, b.sc_pk, 64, 0, 0, 1};
+            if (b.cb > 0) c2.seg[c2.nseg++] = ConvSeg{xb, b.cb, SEG_SAME, H, W, 1, b.sc_pk, 64, rows_a, 0, 1};
+        } else {
+            c2.seg[c2.nseg++] = ConvSeg{xa, b.ca, SEG_SAME, H, W, 1, b.sc_w, cin, 0, 0};
+            if (b.cb > 0) c2.seg[c2.nseg++] = ConvSeg{xb, b.cb, SEG_SAME, H, W, 1, b.sc_w, cin, b.ca, 0};
+        }
         c2.bias1 = b.sc_b;
     } else {
         c2.residual = xa;

@@ -100,6 +100,7 @@ dvc_status conv_tc_run(const ConvDesc &d, cudaStream_t stream);
 dvc_status conv_simt_run(const ConvDesc &d, cudaStream_t stream);
 dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream);   // TMA + CTA-pair persistent engine
 bool conv_ws_applicable(const ConvDesc &d);
+inline bool conv_ws_applicable_dims(dvc_dtype dt) { extern int g_ws_cg; return g_ws_cg != 0 && dt != DVC_F32; }
 extern int g_ws_cg;   // 2 (default): CTA pairs; 1: single CTA; 0: gather engine only
 
 // Row-address helper shared by both engines: source pixel index of output

@@ -9,6 +9,8 @@ struct RB {
     float eps;
     dvc_dtype dt;
     const void *gn1_w, *gn1_b, *conv1_w, *conv1_b, *gn2_w, *gn2_b, *conv2_w, *conv2_b, *sc_w, *sc_b;
+    // optional packed weight images (dvc_pack.cu) for the TMA engines; null = use the OHWI weights
+    const void *conv1_pk = nullptr, *conv2_pk = nullptr, *sc_pk = nullptr;
 };
 
 size_t resblock_ws_bytes(int ca, int cb, int cout, int G, int T, int H, int W, dvc_dtype dt);

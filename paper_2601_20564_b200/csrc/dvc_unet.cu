@@ -16,6 +16,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
@@ -83,11 +84,13 @@ struct dvc_comm {
 // ----------------------------------------------------------------- the network
 struct ConvW {
     const void *w, *b;
+    const void *pk = nullptr;   // packed image (dvc_pack.cu) for the TMA engines, or null
 };
 
 struct dvc_unet {
     dvc_unet_config cfg;
     void *dweights = nullptr;
+    void *dpacked = nullptr;   // packed weight images (16-bit configs)
     size_t welems = 0;
     ConvW conv_in, ds[3], us[3], conv_out;
     const void *gno_w = nullptr, *gno_b = nullptr;
@@ -234,6 +237,54 @@ size_t plan_workspace(const dvc_unet &n, int T, size_t *offs /* kRegions */) {
     return total;
 }
 
+// Packed K-chunk-major weight images for every same-resolution conv (TMA engines): one
+// contiguous block per (tap, 64-channel chunk) weight tile.  Multi-segment convs (concat
+// inputs) pack segment a's rows then segment b's rows in one block.
+dvc_status pack_all(dvc_unet &n) {
+    const dvc_unet_config &c = n.cfg;
+    const size_t es = dt_size(c.dt);
+    struct Job {
+        const void *w;
+        int cout, taps, cin, off, cs;
+        const void **dst;
+        size_t base;   // element offset of this segment inside its block
+        size_t block;  // element offset of the block
+    };
+    std::vector<Job> jobs;
+    size_t total = 0;
+    auto add = [&](const void *w, int cout, int taps, int ca, int cb, const void **dst) {
+        const size_t a = packed_elems(cout, taps, ca);
+        const size_t blk = total;
+        jobs.push_back(Job{w, cout, taps, ca + cb, 0, ca, dst, 0, blk});
+        if (cb > 0) jobs.push_back(Job{w, cout, taps, ca + cb, ca, cb, nullptr, a, blk});
+        total += a + (cb > 0 ? packed_elems(cout, taps, cb) : 0);
+        total = (total + 127) & ~size_t(127);   // 256-byte aligned blocks
+    };
+    const int *W = c.width;
+    add(n.conv_in.w, W[0], 9, c.c_lat, c.c_ctx, &n.conv_in.pk);
+    for (int b = 0; b < 22; ++b) {
+        RB &r = n.blk[b];
+        add(r.conv1_w, r.cout, 9, r.ca, r.cb, &r.conv1_pk);
+        add(r.conv2_w, r.cout, 9, r.cout, 0, &r.conv2_pk);
+        if (r.sc_w) add(r.sc_w, r.cout, 1, r.ca, r.cb, &r.sc_pk);
+    }
+    for (int u = 0; u < 3; ++u) add(n.us[u].w, W[3 - u], 9, W[3 - u], 0, &n.us[u].pk);
+    add(n.conv_out.w, c.c_lat, 9, W[0], 0, &n.conv_out.pk);
+    if (cudaMalloc(&n.dpacked, total * es) != cudaSuccess) {
+        set_error("cudaMalloc of %zu packed weight bytes failed", total * es);
+        return DVC_ERR_CUDA;
+    }
+    uint8_t *base = reinterpret_cast<uint8_t *>(n.dpacked);
+    for (const Job &j : jobs) {
+        void *dst = base + (j.block + j.base) * es;
+        dvc_status st = pack_weights_run(j.w, c.dt, j.cout, j.taps, j.cin, j.off, j.cs, dst, 0);
+        if (st != DVC_OK) return st;
+        if (j.dst) *j.dst = base + j.block * es;
+    }
+    DVC_CUDA(cudaDeviceSynchronize());
+    return DVC_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -344,6 +395,18 @@ dvc_status dvc_unet_create(const dvc_unet_config *cfg, const void *host_weights,
         n->carry_total += (size_t)n->lh[l] * n->lw[l] * ((r.ca + r.cb) / r.P);
     }
     n->welems = elems;
+    // Packed weight images (contiguous weight tiles) measured slower than the OHWI rows on B200
+    // (r1 profiles), so they are opt-in: DVC_PACK_WEIGHTS=1.
+    const char *pe = getenv("DVC_PACK_WEIGHTS");
+    if (cfg->dt != DVC_F32 && pe && pe[0] == '1') {
+        st = pack_all(*n);
+        if (st != DVC_OK) {
+            cudaFree(n->dweights);
+            cudaFree(n->dpacked);
+            delete n;
+            return st;
+        }
+    }
     *out = n;
     return DVC_OK;
 }
@@ -351,6 +414,7 @@ dvc_status dvc_unet_create(const dvc_unet_config *cfg, const void *host_weights,
 dvc_status dvc_unet_destroy(dvc_unet *n) {
     if (!n) return DVC_OK;
     cudaFree(n->dweights);
+    cudaFree(n->dpacked);
     delete n;
     return DVC_OK;
 }
@@ -432,7 +496,10 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     auto conv3 = [&](const void *src, int cin, int mode, int hi, int wi, const ConvW &cw, int cout, int ho, int wo,
                      void *dst, void *dst_stats) {
         ConvDesc d{};
-        d.seg[0] = ConvSeg{src, cin, mode, hi, wi, 9, cw.w, 9 * cin, 0, cin};
+        if (mode == SEG_SAME && cw.pk && conv_ws_applicable_dims(dt))
+            d.seg[0] = ConvSeg{src, cin, mode, hi, wi, 9, cw.pk, 64, 0, 0, 1};
+        else
+            d.seg[0] = ConvSeg{src, cin, mode, hi, wi, 9, cw.w, 9 * cin, 0, cin};
         d.nseg = 1;
         d.T = T;
         d.ho = ho;
@@ -449,8 +516,14 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     {
         ConvDesc d{};
         const int cc = c.c_lat + c.c_ctx;
-        d.seg[0] = ConvSeg{lat, c.c_lat, SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_in.w, 9 * cc, 0, cc};
-        d.seg[1] = ConvSeg{ctx, c.c_ctx, SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_in.w, 9 * cc, c.c_lat, cc};
+        if (n->conv_in.pk && conv_ws_applicable_dims(dt)) {
+            const int rows_a = 9 * ((c.c_lat + 63) / 64) * W[0];
+            d.seg[0] = ConvSeg{lat, c.c_lat, SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_in.pk, 64, 0, 0, 1};
+            d.seg[1] = ConvSeg{ctx, c.c_ctx, SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_in.pk, 64, rows_a, 0, 1};
+        } else {
+            d.seg[0] = ConvSeg{lat, c.c_lat, SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_in.w, 9 * cc, 0, cc};
+            d.seg[1] = ConvSeg{ctx, c.c_ctx, SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_in.w, 9 * cc, c.c_lat, cc};
+        }
         d.nseg = 2;
         d.T = T;
         d.ho = n->lh[0];
