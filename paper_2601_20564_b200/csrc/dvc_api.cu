@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <vector>
+#include <mutex>
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
 #include "dvc_resblock.cuh"
@@ -19,6 +20,28 @@ void set_error(const char *fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
+}
+
+bool smem_attr_ok(const void *kern, int smem) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    static const void *keys[64];
+    static int vals[64];
+    static int n = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const void *key = reinterpret_cast<const char *>(kern) + dev;   // per device
+    for (int i = 0; i < n; ++i)
+        if (keys[i] == key) {
+            if (vals[i] >= smem) return true;
+            vals[i] = smem;
+            return false;
+        }
+    if (n < 64) {
+        keys[n] = key;
+        vals[n++] = smem;
+    }
+    return false;
 }
 
 dvc_status check_launch(const char *what) {

@@ -98,6 +98,9 @@ __device__ __forceinline__ float silu_fast(float z) {
 
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 
+// true if `kern` already allows >= smem bytes of dynamic shared memory (records the new size otherwise)
+bool smem_attr_ok(const void *kern, int smem);
+
 // ----------------------------------------------------------------- shifted-operand addressing (a3)
 // One ResBlock input X = concat(xa[ca], xb[cb]) over frames [T][HW].  The
 // Batch-dimension temporal shift is pure addressing:

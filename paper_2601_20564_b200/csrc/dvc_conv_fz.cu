@@ -63,7 +63,6 @@ struct FzParams {
     float *stats;
     uint32_t idesc;
     int ntf, nb;   // tile slots, weight stages (sized from the shared-memory budget)
-    int dbg;   // perf experiments (DVC_DEBUG_CONV): 1 skip transform work, 4 skip MMAs, 16 skip epilogue
 };
 
 // UMMA descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B
@@ -150,9 +149,13 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
 
     if (warp == 2) {
         // ===================== weight producer =====================
+        // converged warp; lane 0 issues through guard predicates (no divergent region per stage)
         int bs = 0;
         uint32_t bph = 0;
         const uint32_t tx = (uint32_t)CG * (uint32_t)B_STAGE;
+        const uint32_t issue = lane == 0, expect = issue && rank == 0;
+        const uint32_t bfull0 = smem_u32(b_full), bempty0 = smem_u32(b_empty), sB0 = smem_u32(sB);
+        const uint32_t lead_bfull0 = CG == 2 ? mapa_shared(bfull0, 0) : bfull0;
         for (int w = cluster_id; w < p.nwork; w += nclusters) {
             const int nt = w % p.ntile_n;
             const int n0 = nt * BN + (int)rank * BNH;
@@ -162,22 +165,12 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 const CUtensorMap *bm = &p.bmap[sg.bidx];
                 for (int ch = 0; ch < nch; ++ch) {
                     for (int tap = 0; tap < sg.taps; ++tap) {
-                        mbar_wait_spin(&b_empty[bs], bph ^ 1);
-                        if (elect_one()) {
-                            const uint32_t fb = smem_u32(&b_full[bs]);
-                            const uint32_t dB = smem_u32(sB + bs * B_STAGE);
-                            // packed weights: the (tap, chunk) tile is one contiguous row block
-                            const int col = sg.packed ? 0 : sg.col0 + tap * sg.tapstride + ch * 64;
-                            const int row = sg.packed ? sg.col0 + (tap * nch + ch) * p.cout + n0 : n0;
-                            if constexpr (CG == 1) {
-                                mbar_arrive_expect_tx_addr(fb, tx);
-                                tma_load_2d_a(dB, bm, fb, col, row);
-                            } else {
-                                if (rank == 0) mbar_arrive_expect_tx_addr(fb, tx);
-                                tma_load_2d_cg2(dB, bm, mapa_shared(fb, 0), col, row);
-                            }
-                        }
-                        __syncwarp();
+                        mbar_wait_spin_addr(bempty0 + 8 * bs, bph ^ 1);
+                        // packed weights: the (tap, chunk) tile is one contiguous row block
+                        const int col = sg.packed ? 0 : sg.col0 + tap * sg.tapstride + ch * 64;
+                        const int row = sg.packed ? sg.col0 + (tap * nch + ch) * p.cout + n0 : n0;
+                        mbar_expect_tx_if(expect, bfull0 + 8 * bs, tx);
+                        tma_load_2d_if<CG>(issue, sB0 + bs * B_STAGE, bm, lead_bfull0 + 8 * bs, col, row);
                         if (++bs == FZ_BSTAGES) {
                             bs = 0;
                             bph ^= 1;
@@ -245,7 +238,6 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                     uint8_t *tf = sTf + tb * FZ_SLOT + kg * FZ_LBO;
                     constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane
                     uint4 cu[NR], pv[NR];
-                    if (!(p.dbg & 1))
 #pragma unroll
                     for (int k = 0; k < NR; ++k) {   // issue every load before any use
                         const int r = lane + 32 * k;
@@ -267,7 +259,6 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                             }
                         }
                     }
-                    if (!(p.dbg & 1))
 #pragma unroll
                     for (int k = 0; k < NR; ++k) {
                         const int r = lane + 32 * k;
@@ -311,70 +302,56 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
+        // converged warp; mma_stage() elects the issuing lane inside its asm
         if (rank == 0) {
             int bs = 0, tb = 0, it = 0;
             uint32_t bph = 0, tph = 0;
+            const uint32_t bfull0 = smem_u32(b_full), bempty0 = smem_u32(b_empty);
+            const uint32_t tffull0 = smem_u32(tf_full), tfempty0 = smem_u32(tf_empty);
+            const uint32_t b_lo0 = desc_lo(smem_u32(sB), 16), sT0 = smem_u32(sTf);
             for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
                 const int buf = it & 1;
                 const uint32_t use = (uint32_t)(it >> 1) & 1;
                 mbar_wait_spin(&tempty[buf], use ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(buf * BN);
-                bool first = true;
+                uint32_t acc = 0;
                 for (int s = 0; s < p.nseg; ++s) {
                     const FzSeg &sg = p.seg[s];
-                    const int nch = (sg.c + 63) >> 6;
+                    const int nch = (sg.c + 63) >> 6, taps = sg.taps;
+                    const uint32_t klast = (uint32_t)(sg.c - 64 * (nch - 1)) >> 4;
+                    // transformed tile: K step of 16 channels = two 8-channel core-matrix columns of
+                    // the halo layout (no swizzle); raw segment: the TMA box in SW128
+                    const bool tf = sg.transform != 0;
+                    const uint32_t a_hi = tf ? desc_hi_noswz(FZ_SBO) : kDescHiSw128;
+                    const uint32_t a_step = tf ? (uint32_t)(2 * FZ_LBO) >> 4 : 2u;
+                    const uint32_t a_lbo = tf ? (uint32_t)FZ_LBO : 16u;
                     for (int ch = 0; ch < nch; ++ch) {
-                        const int ksteps = min(64, sg.c - ch * 64) >> 4;
-                        mbar_wait_spin(&tf_full[tb], tph);
+                        const uint32_t ks = ch == nch - 1 ? klast : 4u;
+                        mbar_wait_spin_addr(tffull0 + 8 * tb, tph);
                         tc_fence_after();
-                        const uint32_t a_base = smem_u32(sTf + tb * FZ_SLOT);
-                        for (int tap = 0; tap < sg.taps; ++tap) {
-                            const int dy = sg.taps == 9 ? tap / 3 - 1 : 0, dx = sg.taps == 9 ? tap % 3 - 1 : 0;
-                            mbar_wait_spin(&b_full[bs], bph);
+                        const uint32_t a_base = sT0 + (uint32_t)(tb * FZ_SLOT);
+                        for (int tap = 0; tap < taps; ++tap) {
+                            const int dy = taps == 9 ? tap / 3 - 1 : 0, dx = taps == 9 ? tap % 3 - 1 : 0;
+                            const uint32_t a0 = tf ? a_base + (uint32_t)(((1 + dy) * FZ_HX + (1 + dx)) * 16) : a_base;
+                            mbar_wait_spin_addr(bfull0 + 8 * bs, bph);
                             tc_fence_after();
-                            const uint32_t a0 = a_base + (uint32_t)(((1 + dy) * FZ_HX + (1 + dx)) * 16);
-                            const uint32_t b0 = smem_u32(sB + bs * B_STAGE);
-                            if (elect_one()) {
-                                for (int k = 0; k < ksteps; ++k) {
-                                    // transformed tile: K step of 16 channels = two 8-channel core-matrix
-                                    // columns of the halo layout; raw segment: the TMA box in SW128
-                                    const uint64_t ad = sg.transform
-                                                            ? sdesc_noswz(a0 + (uint32_t)(2 * k * FZ_LBO), FZ_LBO, FZ_SBO)
-                                                            : sdesc_sw128(a_base + k * 32);
-                                    const uint64_t bd = sdesc_sw128(b0 + k * 32);
-                                    const uint32_t acc = (first && k == 0) ? 0u : 1u;
-                                    if (!(p.dbg & 4) || acc == 0) {
-                                        if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, acc);
-                                        else tc_mma_cg2(d, ad, bd, p.idesc, acc);
-                                    }
-                                }
-                                if constexpr (CG == 1) tc_commit(&b_empty[bs]);
-                                else tc_commit_cg2_mc(smem_u32(&b_empty[bs]), 0x3);
-                            }
-                            __syncwarp();
-                            first = false;
+                            mma_stage<CG>(d, desc_lo(a0, a_lbo), a_hi, a_step, b_lo0 + (uint32_t)(bs * (B_STAGE >> 4)),
+                                          kDescHiSw128, p.idesc, ks, acc, bempty0 + 8 * bs);
+                            acc = 1;
                             if (++bs == FZ_BSTAGES) {
                                 bs = 0;
                                 bph ^= 1;
                             }
                         }
-                        if (elect_one()) {   // the transformed tile is free once its taps retire
-                            if constexpr (CG == 1) tc_commit(&tf_empty[tb]);
-                            else tc_commit_cg2_mc(smem_u32(&tf_empty[tb]), 0x3);
-                        }
-                        __syncwarp();
+                        commit_elected<CG>(tfempty0 + 8 * tb);   // the tile slot is free once its taps retire
                         if (++tb == NTF) {
                             tb = 0;
                             tph ^= 1;
                         }
                     }
                 }
-                if (elect_one()) {
-                    if constexpr (CG == 1) tc_commit(&tfull[buf]);
-                    else tc_commit_cg2_mc(smem_u32(&tfull[buf]), 0x3);
-                }
-                __syncwarp();
+                commit_elected<CG>(smem_u32(&tfull[buf]));
             }
         }
     } else if (warp >= 4 && warp < 8) {
@@ -416,7 +393,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
             tc_fence_after();
             const bool want_stats = p.stats != nullptr && bx.valid;
 #pragma unroll 1
-            for (int cc = 0, par = 0; cc < ((p.dbg & 16) ? 0 : BN); cc += 16, par ^= 1) {
+            for (int cc = 0, par = 0; cc < BN; cc += 16, par ^= 1) {
                 uint32_t v[16];
                 tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
                 const int n = nt * BN + cc;
@@ -595,10 +572,6 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (residual) failed (%d)", (int)r);
     }
     p.idesc = make_idesc(d.dt == DVC_BF16, 128 * CG, bn);
-    {
-        const char *e = getenv("DVC_DEBUG_CONV");
-        p.dbg = e ? atoi(e) : 0;
-    }
     // shared memory: tile slots, weight stages, residual tile; fill the 227 KB budget with weight stages
     {
         const char *e = getenv("DVC_FZ_NTF");
@@ -618,7 +591,8 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     p.nb = nbst;
     const size_t smem = fixed - 1024 + (size_t)nbst * bstage;
     auto kern = d.dt == DVC_BF16 ? conv_fz_kernel<__nv_bfloat16, 2> : conv_fz_kernel<__half, 2>;
-    DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
+        DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (g_fz_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);

@@ -30,6 +30,7 @@ struct WsParams {
     CUtensorMap amap[4];   // per segment: 4D {C, W, H, T}, box {64, BX, BY, 1}, SW128, OOB zero
     CUtensorMap bmap[2];   // weights 2D {K, C_out}, box {64, BN/CG}, SW128
     int bidx[4], seg_c[4], seg_taps[4], seg_col0[4], seg_tapstride[4], seg_packed[4];
+    int seg_nch[4], seg_klast[4];   // 64-channel stages per tap; K=16 steps in the last one
     int nseg;
     int T, H, W, cout, bn;
     int BX, BY, tiles_x, tiles_y, nbox, ntile_n, nwork;
@@ -37,7 +38,6 @@ struct WsParams {
     void *out;
     uint32_t idesc;
     float *stats;   // per-channel box statistics of the output (dvc_boxstats.cuh), or null
-    int dbg;   // perf experiments only (DVC_DEBUG_CONV): 1 skip A TMA, 2 skip B TMA, 4 skip MMA, 8 skip stores, 16 skip epilogue
 };
 
 constexpr int kWsThreads = 256;
@@ -86,64 +86,53 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
-        // the whole warp walks the (warp-uniform) loop; one elected lane issues
-        {
-            int stage = 0;
-            uint32_t phase = 0;
-            const uint32_t a_bytes = (uint32_t)(p.BX * p.BY * 128);
-            const uint32_t tx = (uint32_t)CG * (a_bytes + (uint32_t)B_STAGE);
-            for (int w = cluster_id; w < p.nwork; w += nclusters) {
-                const int q = w / p.ntile_n, nt = w - q * p.ntile_n;
-                const int n0 = nt * BN + (int)rank * BNH;
-                int box = q * CG + (int)rank;
-                int t, y0, x0;
-                if (box < p.nbox) {
-                    const int per = p.tiles_x * p.tiles_y;
-                    t = box / per;
-                    const int rem = box - t * per;
-                    y0 = (rem / p.tiles_x) * p.BY;
-                    x0 = (rem % p.tiles_x) * p.BX;
-                } else {   // padding box of the last pair: fully out of bounds -> zeros
-                    t = p.T;
-                    y0 = x0 = 0;
-                }
-                for (int s = 0; s < p.nseg; ++s) {
-                    const int nch = (p.seg_c[s] + 63) >> 6;
-                    const CUtensorMap *bm = &p.bmap[p.bidx[s]];
-                    for (int tap = 0; tap < p.seg_taps[s]; ++tap) {
-                        const int dy = p.seg_taps[s] == 9 ? tap / 3 - 1 : 0;
-                        const int dx = p.seg_taps[s] == 9 ? tap % 3 - 1 : 0;
-                        const int col = p.seg_col0[s] + tap * p.seg_tapstride[s];
-                        const int prow = p.seg_col0[s] + tap * nch * p.cout;   // packed weights: row block of this tap
-                        for (int ch = 0; ch < nch; ++ch) {
-                            if (!(p.dbg & 32)) mbar_wait_spin(&empty[stage], phase ^ 1);
-                            const uint32_t fb = smem_u32(&full[stage]);
-                            const uint32_t dA = smem_u32(sA + stage * A_STAGE);
-                            const uint32_t dB = smem_u32(sB + stage * B_STAGE);
-                            const bool la = !(p.dbg & 1), lbb = !(p.dbg & 2);
-                            const uint32_t txs = (uint32_t)CG * ((la ? a_bytes : 0u) + (lbb ? (uint32_t)B_STAGE : 0u));
-                            if (!elect_one()) {
-                            } else if constexpr (CG == 1) {
-                                mbar_arrive_expect_tx_addr(fb, txs);
-                                if (la) tma_load_4d(dA, &p.amap[s], fb, ch * 64, x0 + dx, y0 + dy, t);
-                            if (p.dbg & 32) { /* timing experiment: no pipeline handshakes */ }
-                                if (lbb) {
-                                    if (p.seg_packed[s]) tma_load_2d_a(dB, bm, fb, 0, prow + ch * p.cout + n0);
-                                    else tma_load_2d_a(dB, bm, fb, col + ch * 64, n0);
-                                }
-                            } else {
-                                if (rank == 0) mbar_arrive_expect_tx_addr(fb, txs);
-                                const uint32_t lb = mapa_shared(fb, 0);   // leader's barrier
-                                if (la) tma_load_4d_cg2(dA, &p.amap[s], lb, ch * 64, x0 + dx, y0 + dy, t);
-                                if (lbb) {
-                                    if (p.seg_packed[s]) tma_load_2d_cg2(dB, bm, lb, 0, prow + ch * p.cout + n0);
-                                    else tma_load_2d_cg2(dB, bm, lb, col + ch * 64, n0);
-                                }
-                            }
-                            if (++stage == STAGES) {
-                                stage = 0;
-                                phase ^= 1;
-                            }
+        // the whole warp walks the (warp-uniform) loop; lane 0 issues through guard
+        // predicates (no divergent region per stage)
+        int stage = 0;
+        uint32_t phase = 0;
+        const uint32_t a_bytes = (uint32_t)(p.BX * p.BY * 128);
+        const uint32_t tx = (uint32_t)CG * (a_bytes + (uint32_t)B_STAGE);
+        const uint32_t issue = lane == 0;
+        const uint32_t expect = issue && rank == 0;   // the leader's barrier counts both CTAs' bytes
+        const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+        const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
+        const uint32_t lead_full0 = CG == 2 ? mapa_shared(full0, 0) : full0;
+        for (int w = cluster_id; w < p.nwork; w += nclusters) {
+            const int q = w / p.ntile_n, nt = w - q * p.ntile_n;
+            const int n0 = nt * BN + (int)rank * BNH;
+            const int box = q * CG + (int)rank;
+            int t, y0, x0;
+            if (box < p.nbox) {
+                const int per = p.tiles_x * p.tiles_y;
+                t = box / per;
+                const int rem = box - t * per;
+                y0 = (rem / p.tiles_x) * p.BY;
+                x0 = (rem % p.tiles_x) * p.BX;
+            } else {   // padding box of the last pair: fully out of bounds -> zeros
+                t = p.T;
+                y0 = x0 = 0;
+            }
+            for (int s = 0; s < p.nseg; ++s) {
+                const int nch = p.seg_nch[s], taps = p.seg_taps[s];
+                const CUtensorMap *am = &p.amap[s];
+                const CUtensorMap *bm = &p.bmap[p.bidx[s]];
+                const bool packed = p.seg_packed[s] != 0;
+                for (int tap = 0; tap < taps; ++tap) {
+                    const int dy = taps == 9 ? tap / 3 - 1 : 0;
+                    const int dx = taps == 9 ? tap % 3 - 1 : 0;
+                    // weight tile origin: column block of this tap, or (packed) its row block
+                    const int bc0 = packed ? 0 : p.seg_col0[s] + tap * p.seg_tapstride[s];
+                    const int br0 = packed ? p.seg_col0[s] + tap * nch * p.cout + n0 : n0;
+                    const int bcs = packed ? 0 : 64, brs = packed ? p.cout : 0;
+                    for (int ch = 0; ch < nch; ++ch) {
+                        mbar_wait_spin_addr(empty0 + 8 * stage, phase ^ 1);
+                        const uint32_t lb = CG == 2 ? lead_full0 + 8 * stage : full0 + 8 * stage;
+                        mbar_expect_tx_if(expect, full0 + 8 * stage, tx);
+                        tma_load_4d_if<CG>(issue, sA0 + stage * A_STAGE, am, lb, ch * 64, x0 + dx, y0 + dy, t);
+                        tma_load_2d_if<CG>(issue, sB0 + stage * B_STAGE, bm, lb, bc0 + ch * bcs, br0 + ch * brs);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
                         }
                     }
                 }
@@ -151,46 +140,31 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
-        // the whole warp walks the loop (warp-uniform descriptors live in uniform
-        // registers); one elected lane issues tcgen05.mma / commit
+        // converged warp; mma_stage() elects the issuing lane inside its asm
         if (rank == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
+            const uint32_t full0 = smem_u32(full), empty0 = smem_u32(empty);
+            const uint32_t a_lo0 = desc_lo(smem_u32(sA), 16), b_lo0 = desc_lo(smem_u32(sB), 16);
             for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
                 const int buf = it & 1;
                 const uint32_t use = (uint32_t)(it >> 1) & 1;
                 mbar_wait_spin(&tempty[buf], use ^ 1);   // epilogues of both CTAs drained this buffer
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(buf * BN);
-                bool first = true;
+                uint32_t acc = 0;
                 for (int s = 0; s < p.nseg; ++s) {
-                    const int nch = (p.seg_c[s] + 63) >> 6;
-                    for (int tap = 0; tap < p.seg_taps[s]; ++tap) {
+                    const int nch = p.seg_nch[s], taps = p.seg_taps[s];
+                    const uint32_t klast = (uint32_t)p.seg_klast[s];
+                    for (int tap = 0; tap < taps; ++tap) {
                         for (int ch = 0; ch < nch; ++ch) {
-                            if (!(p.dbg & 32)) mbar_wait_spin(&full[stage], phase);
+                            mbar_wait_spin_addr(full0 + 8 * stage, phase);
                             tc_fence_after();
-                            const int ksteps = min(64, p.seg_c[s] - ch * 64) >> 4;
-                            const uint32_t a0 = smem_u32(sA + stage * A_STAGE);
-                            const uint32_t b0 = smem_u32(sB + stage * B_STAGE);
-                            const uint64_t ad0 = sdesc_sw128(a0), bd0 = sdesc_sw128(b0);
-                            if (elect_one()) {
-                                for (int k = 0; k < ksteps; ++k) {
-                                    // K advance inside the 128-byte swizzled row: +32 B = +2 in the address field
-                                    const uint64_t ad = ad0 + (uint64_t)(2 * k);
-                                    const uint64_t bd = bd0 + (uint64_t)(2 * k);
-                                    if (!(p.dbg & 4) || (first && k == 0)) {
-                                        if constexpr (CG == 1) tc_mma(d, ad, bd, p.idesc, (first && k == 0) ? 0u : 1u);
-                                        else tc_mma_cg2(d, ad, bd, p.idesc, (first && k == 0) ? 0u : 1u);
-                                    }
-                                }
-                                if (!(p.dbg & 32)) {
-                                    if constexpr (CG == 1) tc_commit(&empty[stage]);
-                                    else tc_commit_cg2_mc(smem_u32(&empty[stage]), 0x3);
-                                }
-                            }
-                            __syncwarp();
-                            first = false;
+                            mma_stage<CG>(d, a_lo0 + (uint32_t)stage * (A_STAGE >> 4), kDescHiSw128, 2u,
+                                          b_lo0 + (uint32_t)(stage * (B_STAGE >> 4)), kDescHiSw128, p.idesc,
+                                          ch == nch - 1 ? klast : 4u, acc, empty0 + 8 * stage);
+                            acc = 1;
                             if (++stage == STAGES) {
                                 stage = 0;
                                 phase ^= 1;
@@ -198,11 +172,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         }
                     }
                 }
-                if (elect_one()) {
-                    if constexpr (CG == 1) tc_commit(&tfull[buf]);
-                    else tc_commit_cg2_mc(smem_u32(&tfull[buf]), 0x3);
-                }
-                __syncwarp();
+                commit_elected<CG>(smem_u32(&tfull[buf]));
             }
         }
     } else if (warp >= 4) {
@@ -228,16 +198,16 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                 const int y = (rem / p.tiles_x) * p.BY + by, x = (rem % p.tiles_x) * p.BX + bx;
                 if (y < p.H && x < p.W) m = ((long)t * p.H + y) * p.W + x;
             }
-            mbar_wait_spin(&tfull[buf], use);
+            mbar_wait(&tfull[buf], use);   // long wait (a whole main loop): sleep, leave the issue slots
             tc_fence_after();
             const bool want_stats = p.stats != nullptr && box < p.nbox;   // warp-uniform
 #pragma unroll 1
-            for (int cc = 0, par = 0; cc < ((p.dbg & 16) ? 0 : BN); cc += 16, par ^= 1) {
+            for (int cc = 0, par = 0; cc < BN; cc += 16, par ^= 1) {
                 uint32_t v[16];
                 tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
                 const int n = nt * BN + cc;
                 float f[16];
-                if (m >= 0 && !(p.dbg & 8)) {
+                if (m >= 0) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
                     float e[8];
@@ -362,7 +332,8 @@ template <typename T, int CG, int STAGES>
 static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
     const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16 + 1024;
     auto kern = conv_ws_kernel<T, CG, STAGES>;
-    DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
+        DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (g_num_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -392,12 +363,7 @@ static int engine_from_env() {
     if (e && (e[0] == '0' || e[0] == '1' || e[0] == '2') && e[1] == 0) return e[0] - '0';
     return 2;
 }
-int g_ws_cg = engine_from_env();
-static int dbg_from_env() {
-    const char *e = getenv("DVC_DEBUG_CONV");
-    return e ? atoi(e) : 0;
-}
-static int g_ws_dbg = dbg_from_env();   // 2: CTA-pair MMA (default), 1: single-CTA MMA, 0: gather engine only
+int g_ws_cg = engine_from_env();   // 2: CTA-pair MMA (default), 1: single-CTA MMA, 0: gather engine only
 
 bool conv_ws_applicable(const ConvDesc &d) {
     if (g_ws_cg == 0 || d.dt == DVC_F32) return false;
@@ -466,13 +432,14 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
         p.bidx[s] = idx;
         p.seg_packed[s] = g.packed;
         p.seg_c[s] = g.c_src;
+        p.seg_nch[s] = (g.c_src + 63) / 64;
+        p.seg_klast[s] = (g.c_src - 64 * (p.seg_nch[s] - 1)) / 16;
         p.seg_taps[s] = g.taps;
         p.seg_col0[s] = g.w_col0;
         p.seg_tapstride[s] = g.w_tapstride;
     }
     const int bf = d.dt == DVC_BF16;
     p.idesc = make_idesc(bf, 128 * CG, bn);
-    p.dbg = g_ws_dbg;
     p.stats = reinterpret_cast<float *>(d.stats_out);
     if (CG == 2) {
         if (bf) return launch_ws<__nv_bfloat16, 2, 6>(p, stream);

@@ -230,6 +230,123 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
     else
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+// ----------------------------------------------------------------- branch-free stage issue
+// The MMA-issuing warp walks its loop converged; these helpers run in all 32 lanes and
+// elect ONE lane inside the asm (guard predicates, no divergent region), so a 64-channel
+// K stage costs a handful of uniform-datapath instructions instead of a BSSY/ELECT/BRA
+// region per stage (measured: the branchy issue loop was as slow as the MMAs it fed).
+//
+// UMMA smem descriptors as two 32-bit words: lo = start address >> 4 (14 bits) | LBO << 16,
+// hi = SBO | version (bit 46) | layout (bits 61-63).  A K step of 16 elements adds
+// `a_step` / 2 (16-byte units) to lo; the start field never carries (smem < 256 KB).
+constexpr uint32_t kDescHiSw128 = 0x40004040u;   // SBO 1024 B, version 1, SWIZZLE_128B
+__host__ __device__ constexpr uint32_t desc_lo(uint32_t saddr, uint32_t lbo_bytes) {
+    return ((saddr >> 4) & 0x3FFFu) | (((lbo_bytes >> 4) & 0x3FFFu) << 16);
+}
+__host__ __device__ constexpr uint32_t desc_hi_noswz(uint32_t sbo_bytes) {
+    return ((sbo_bytes >> 4) & 0x3FFFu) | (1u << 14);
+}
+
+#define DVC_MMA_STAGE_ASM(CGS)                                                         \
+    "{\n\t.reg .pred e, q, acc, one;\n\t.reg .b32 al, bl;\n\t.reg .b64 ad, bd;\n\t"    \
+    "elect.sync _|e, 0xffffffff;\n\t"                                                  \
+    "setp.ne.b32 acc, %8, 0;\n\t"                                                      \
+    "setp.eq.u32 one, %7, %7;\n\t"                                                     \
+    "mov.b64 ad, {%1, %2};\n\t"                                                        \
+    "mov.b64 bd, {%4, %5};\n\t"                                                        \
+    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ad, bd, %6, acc;\n\t"           \
+    "setp.gt.u32 q, %7, 1;\n\tand.pred q, q, e;\n\t"                                   \
+    "add.u32 al, %1, %3;\n\tadd.u32 bl, %4, 2;\n\t"                                    \
+    "mov.b64 ad, {al, %2};\n\tmov.b64 bd, {bl, %5};\n\t"                               \
+    "@q tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ad, bd, %6, one;\n\t"           \
+    "setp.gt.u32 q, %7, 2;\n\tand.pred q, q, e;\n\t"                                   \
+    "add.u32 al, al, %3;\n\tadd.u32 bl, bl, 2;\n\t"                                    \
+    "mov.b64 ad, {al, %2};\n\tmov.b64 bd, {bl, %5};\n\t"                               \
+    "@q tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ad, bd, %6, one;\n\t"           \
+    "setp.gt.u32 q, %7, 3;\n\tand.pred q, q, e;\n\t"                                   \
+    "add.u32 al, al, %3;\n\tadd.u32 bl, bl, 2;\n\t"                                    \
+    "mov.b64 ad, {al, %2};\n\tmov.b64 bd, {bl, %5};\n\t"                               \
+    "@q tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ad, bd, %6, one;\n\t"
+
+// ks (1..4) K=16 MMAs over one 64-channel stage (first one overwrites D iff accum == 0),
+// then a commit arriving on `bar` (every CTA of the pair for CG = 2).
+template <int CG>
+__device__ __forceinline__ void mma_stage(uint32_t d, uint32_t a_lo, uint32_t a_hi, uint32_t a_step, uint32_t b_lo,
+                                          uint32_t b_hi, uint32_t idesc, uint32_t ks, uint32_t accum, uint32_t bar) {
+    if constexpr (CG == 1) {
+        asm volatile(DVC_MMA_STAGE_ASM("1")
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}\n" ::"r"(d),
+                     "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(ks), "r"(accum),
+                     "r"(bar)
+                     : "memory");
+    } else {
+        asm volatile(DVC_MMA_STAGE_ASM("2")
+                     "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+                     "[%9], %10;\n\t}\n" ::"r"(d),
+                     "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(ks), "r"(accum),
+                     "r"(bar), "h"((uint16_t)3)
+                     : "memory");
+    }
+}
+// commit (all prior MMAs of the elected lane) from a converged warp
+template <int CG>
+__device__ __forceinline__ void commit_elected(uint32_t bar) {
+    if constexpr (CG == 1)
+        asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
+                     : "memory");
+    else
+        asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                     "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+                     "[%0], %1;\n\t}\n" ::"r"(bar),
+                     "h"((uint16_t)3)
+                     : "memory");
+}
+__device__ __forceinline__ void mbar_wait_spin_addr(uint32_t a, uint32_t parity) {
+    while (!mbar_try_wait_nohint(a, parity)) {
+    }
+}
+
+// predicated (branch-free) TMA issue: only lanes with pred != 0 issue
+__device__ __forceinline__ void mbar_expect_tx_if(uint32_t pred, uint32_t addr, uint32_t bytes) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t"
+                 "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n\t}\n" ::"r"(pred),
+                 "r"(addr), "r"(bytes)
+                 : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load_4d_if(uint32_t pred, uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0,
+                                               int c1, int c2, int c3) {
+    if constexpr (CG == 1)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %7, 0;\n\t"
+                     "@p cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                     " [%0], [%1, {%3, %4, %5, %6}], [%2];\n\t}\n" ::"r"(dst),
+                     "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(pred)
+                     : "memory");
+    else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %7, 0;\n\t"
+                     "@p cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                     " [%0], [%1, {%3, %4, %5, %6}], [%2];\n\t}\n" ::"r"(dst),
+                     "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(pred)
+                     : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load_2d_if(uint32_t pred, uint32_t dst, const CUtensorMap *map, uint32_t bar, int c0,
+                                               int c1) {
+    if constexpr (CG == 1)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+                     "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                     " [%0], [%1, {%3, %4}], [%2];\n\t}\n" ::"r"(dst),
+                     "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(pred)
+                     : "memory");
+    else
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+                     "@p cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                     " [%0], [%1, {%3, %4}], [%2];\n\t}\n" ::"r"(dst),
+                     "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(pred)
+                     : "memory");
+}
+
 __device__ __forceinline__ uint32_t mbar_try_wait_addr(uint32_t addr, uint32_t parity) {
     return mbar_try_wait(addr, parity);
 }
