@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <vector>
+#include <string>
 #include <mutex>
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
@@ -76,7 +77,9 @@ struct Prof {
     bool on = false;
     int cap = 0, used = 0;
     std::vector<cudaEvent_t> ev;   // 2 per launch
-    std::vector<double> flops;
+    std::vector<double> flops, ms;
+    std::vector<std::string> label;
+    int done = 0;   // records kept by dvc_profile_end for dvc_profile_record
 } g_prof;
 }  // namespace
 
@@ -87,10 +90,15 @@ ProfSlot prof_begin(cudaStream_t stream) {
     return ProfSlot{i};
 }
 
-void prof_end(ProfSlot s, cudaStream_t stream, double flops) {
+void prof_end(ProfSlot s, cudaStream_t stream, double flops, const char *engine, const ConvDesc &d) {
     if (s.idx < 0) return;
     cudaEventRecord(g_prof.ev[2 * s.idx + 1], stream);
     g_prof.flops[s.idx] = flops;
+    char buf[128];
+    int k = 0;
+    for (int i = 0; i < d.nseg; ++i) k += d.seg[i].taps * d.seg[i].c_src;
+    snprintf(buf, sizeof(buf), "%s T=%d %dx%d K=%d N=%d segs=%d", engine, d.T, d.ho, d.wo, k, d.cout, d.nseg);
+    g_prof.label[s.idx] = buf;
 }
 
 // ----------------------------------------------------------------- ResBlock (a3-a8)
@@ -222,7 +230,7 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
             prof.nseg = 1, prof.T = T, prof.ho = H, prof.wo = W, prof.cout = b.cout;
             ProfSlot slot = prof_begin(stream);
             st = conv_fz_run(f1, stream);
-            prof_end(slot, stream, conv_flops(prof));
+            prof_end(slot, stream, conv_flops(prof), "fz1", prof);
             if (st != DVC_OK) return st;
         }
         NormArgs n2{y1, nullptr, nullptr, b.cout, 0, 0, T, HW, b.G, b.eps, b.gn2_w, b.gn2_b, coef, nullptr};
@@ -260,7 +268,7 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
         if (b.sc_w) prof.seg[prof.nseg++] = ConvSeg{xa, cin, SEG_SAME, H, W, 1, b.sc_w, cin, 0, 0};
         ProfSlot slot = prof_begin(stream);
         st = conv_fz_run(f2, stream);
-        prof_end(slot, stream, conv_flops(prof));
+        prof_end(slot, stream, conv_flops(prof), "fz2", prof);
         return st;
     }
     // a3 + a4: H1 = SiLU(GN1(shift(X, carry)))
@@ -395,6 +403,9 @@ dvc_status dvc_profile_begin(int max_launches) {
         for (size_t i = old; i < g_prof.ev.size(); ++i) DVC_CUDA(cudaEventCreate(&g_prof.ev[i]));
     }
     g_prof.flops.assign(max_launches, 0.0);
+    g_prof.ms.assign(max_launches, 0.0);
+    g_prof.label.assign(max_launches, std::string());
+    g_prof.done = 0;
     g_prof.cap = max_launches;
     g_prof.used = 0;
     g_prof.on = true;
@@ -411,11 +422,20 @@ dvc_status dvc_profile_end(double *conv_ms, double *conv_flops, int *conv_launch
         DVC_CUDA(cudaEventElapsedTime(&t, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]));
         ms += t;
         fl += g_prof.flops[i];
+        g_prof.ms[i] = t;
     }
+    g_prof.done = g_prof.used;
     *conv_ms = ms;
     *conv_flops = fl;
     *conv_launches = g_prof.used;
     g_prof.used = 0;
+    return DVC_OK;
+}
+dvc_status dvc_profile_record(int i, double *ms, double *flops, char *label, int label_cap) {
+    DVC_CHECK_ARG(i >= 0 && i < g_prof.done, DVC_ERR_ARG, "record %d not available (%d kept)", i, g_prof.done);
+    if (ms) *ms = g_prof.ms[i];
+    if (flops) *flops = g_prof.flops[i];
+    if (label && label_cap > 0) snprintf(label, (size_t)label_cap, "%s", g_prof.label[i].c_str());
     return DVC_OK;
 }
 int dvc_abi_version(void) { return DVC_ABI_VERSION; }

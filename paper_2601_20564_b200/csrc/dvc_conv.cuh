@@ -89,7 +89,8 @@ struct ProfSlot {
     int idx;   // -1 = not profiling
 };
 ProfSlot prof_begin(cudaStream_t stream);
-void prof_end(ProfSlot s, cudaStream_t stream, double flops);
+struct ConvDesc;
+void prof_end(ProfSlot s, cudaStream_t stream, double flops, const char *engine, const ConvDesc &d);
 double conv_flops(const ConvDesc &d);
 
 // Validates the descriptor for the given engine; returns DVC_OK or an error.

@@ -75,7 +75,47 @@ __device__ __forceinline__ uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo, ui
     return d;
 }
 
-__device__ __forceinline__ float fz_silu(float z) { return silu_fast(z); }
+// SiLU(z) = z / (1 + e^-z) given z and u = -z*log2(e) (computed by its own FFMA): two MUFU
+// ops (ex2.approx, rcp.approx; <= 2 ulp fp32 each), far below the 16-bit rounding of H (R23)
+__device__ __forceinline__ float fz_silu_pre(float z, float u) {
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(u));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+    return z * r;
+}
+// 16-byte read-only load if pred, else zeros (branch-free)
+__device__ __forceinline__ uint4 ldg_v4_if(uint32_t pred, const void *ptr) {
+    uint4 v;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
+        "@p ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}\n"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "r"(pred), "l"(ptr));
+    return v;
+}
+// two 16-bit elements in one 32-bit word (element 2j in the low half)
+template <typename T> struct Pk;
+template <> struct Pk<__nv_bfloat16> {
+    static __device__ __forceinline__ void unpack(uint32_t w, float &a, float &b) {
+        a = __uint_as_float(w << 16);
+        b = __uint_as_float(w & 0xFFFF0000u);
+    }
+    static __device__ __forceinline__ uint32_t pack(float a, float b) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+};
+template <> struct Pk<__half> {
+    static __device__ __forceinline__ void unpack(uint32_t w, float &a, float &b) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w));
+        a = f.x;
+        b = f.y;
+    }
+    static __device__ __forceinline__ uint32_t pack(float a, float b) {
+        __half2 h = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+};
 
 struct FzBox {
     int t, y0, x0;
@@ -117,6 +157,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     uint64_t *res_full = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(res_full + 1);
     float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][4][32] box-statistics staging
+    float *sbias = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(red + 256) + 15) & ~uintptr_t(15));
+    //              ^ [2][cout] bias0, bias1 in fp32 (16-byte aligned for float4 reads)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -141,6 +183,10 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         fence_proxy_async();
     }
     if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), ncols);
+    for (int i = tid; i < p.cout; i += kFzThreads) {
+        sbias[i] = p.bias0 ? Elem<T>::to_f(reinterpret_cast<const T *>(p.bias0)[i]) : 0.f;
+        sbias[p.cout + i] = p.bias1 ? Elem<T>::to_f(reinterpret_cast<const T *>(p.bias1)[i]) : 0.f;
+    }
     tc_fence_before();
     __syncthreads();
     if constexpr (CG == 2) cluster_sync_all();
@@ -215,49 +261,53 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                     }
                     const int cl = ch * 64 + kg * 8;           // first channel (segment-local) of this warp
                     const int cgl = sg.cglob0 + cl;            // operand channel (coef index)
-                    const bool cval = cl < sg.c;
-                    // per-channel GN affine of frame t and the shift selection (8 channels)
-                    float sc[8], sh[8];
-                    int from_prev = 0;   // bit i: channel i comes from the previous frame / carry
+                    const bool cval = cl < sg.c;               // warp-uniform
+                    // GN affine of frame t for the 8 channels, z = v*sc + sh, and the same affine
+                    // pre-scaled by -log2(e) so that e^-z = ex2(v*sc2 + sh2) costs one FFMA
+                    float sc[8], sh[8], sc2[8], sh2[8];
+                    if (cval && bx.valid) {
+                        const float4 *cf = reinterpret_cast<const float4 *>(p.coef + (size_t)bx.t * p.cop + cgl);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        sc[i] = 1.f;
-                        sh[i] = 0.f;
-                        if (sg.transform && cval && bx.valid) {
-                            const float2 cf = p.coef[(size_t)bx.t * p.cop + cgl + i];
-                            sc[i] = cf.x;
-                            sh[i] = cf.y;
+                        for (int i = 0; i < 4; ++i) {
+                            const float4 q = __ldg(cf + i);
+                            sc[2 * i] = q.x, sh[2 * i] = q.y, sc[2 * i + 1] = q.z, sh[2 * i + 1] = q.w;
                         }
-                        if (sg.shift && cl + i < p.cs) from_prev |= 1 << i;
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) sc[i] = 1.f, sh[i] = 0.f;
                     }
-                    const bool prev_zero = from_prev && bx.t == 0 && !p.has_carry;
-                    // sources of this warp's 8 channels: frame t, and frame t-1 / the padded carry
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) sc2[i] = sc[i] * -1.4426950408889634f, sh2[i] = sh[i] * -1.4426950408889634f;
+                    // temporal shift: the first nprev of these 8 channels come from frame t-1 (or the
+                    // carry at t = 0).  C_in/P is even (C_in % 16 == 0), so the split falls on a
+                    // 32-bit word: merge = (prev & m) | (cur & ~m) per word.
+                    const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
+                    uint32_t msk[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) msk[j] = 2 * j < nprev ? 0xFFFFFFFFu : 0u;
+                    // sources (warp-uniform): frame t, and frame t-1 or the padded carry at t = 0
                     const T *srcT = reinterpret_cast<const T *>(sg.src);
-                    const bool prev_carry = from_prev && bx.t == 0;
+                    const size_t HWs = (size_t)p.H * p.W;
+                    const bool prev_carry = bx.t == 0;
+                    const uint32_t lc = cval && bx.valid && nprev < 8;
+                    const uint32_t lp = cval && bx.valid && nprev > 0 && !(prev_carry && !p.has_carry);
+                    const T *cur_base = srcT + (size_t)bx.t * HWs * sg.c + cl;
+                    const T *prev_base = prev_carry ? reinterpret_cast<const T *>(p.carry_pad) + cl
+                                                    : srcT + ((size_t)bx.t - 1) * HWs * sg.c + cl;
+                    const int prev_ld = prev_carry ? p.cs_pad : sg.c;
                     mbar_wait(&tf_empty[tb], tph ^ 1);
                     uint8_t *tf = sTf + tb * FZ_SLOT + kg * FZ_LBO;
                     constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane
                     uint4 cu[NR], pv[NR];
 #pragma unroll
-                    for (int k = 0; k < NR; ++k) {   // issue every load before any use
+                    for (int k = 0; k < NR; ++k) {   // issue every load before any use (predicated, no branches)
                         const int r = lane + 32 * k;
                         const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
                         const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
-                        const bool ok = r < FZ_HROWS && bx.valid && cval && y >= 0 && y < p.H && x >= 0 && x < p.W;
-                        cu[k] = make_uint4(0, 0, 0, 0);
-                        pv[k] = make_uint4(0, 0, 0, 0);
-                        if (ok) {
-                            const size_t pix = ((size_t)bx.t * p.H + y) * p.W + x;
-                            if (from_prev != 0xFF)
-                                cu[k] = __ldg(reinterpret_cast<const uint4 *>(srcT + pix * sg.c + cl));
-                            if (from_prev && !prev_zero) {
-                                if (prev_carry)
-                                    pv[k] = __ldg(reinterpret_cast<const uint4 *>(
-                                        reinterpret_cast<const T *>(p.carry_pad) + ((size_t)y * p.W + x) * p.cs_pad + cl));
-                                else
-                                    pv[k] = __ldg(reinterpret_cast<const uint4 *>(srcT + (pix - (size_t)p.H * p.W) * sg.c + cl));
-                            }
-                        }
+                        const uint32_t ok = r < FZ_HROWS && y >= 0 && y < p.H && x >= 0 && x < p.W;
+                        const int pf = y * p.W + x;
+                        cu[k] = ldg_v4_if(ok & lc, cur_base + (ptrdiff_t)pf * sg.c);
+                        pv[k] = ldg_v4_if(ok & lp, prev_base + (ptrdiff_t)pf * prev_ld);
                     }
 #pragma unroll
                     for (int k = 0; k < NR; ++k) {
@@ -265,24 +315,21 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         if (r >= FZ_HROWS) break;
                         const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
                         const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
-                        const bool inframe = bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
-                        uint4 out;
-                        if (!cval) {
-                            out = make_uint4(0, 0, 0, 0);
-                        } else {
-                            const T *ec = reinterpret_cast<const T *>(&cu[k]);
-                            const T *ep = reinterpret_cast<const T *>(&pv[k]);
-                            Vec8<T> o;
+                        // conv zero padding applies AFTER the transform (H3): out of frame -> 0
+                        const bool live = cval && bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
+                        const uint32_t wc[4] = {cu[k].x, cu[k].y, cu[k].z, cu[k].w};
+                        const uint32_t wp[4] = {pv[k].x, pv[k].y, pv[k].z, pv[k].w};
+                        uint32_t o[4];
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const float v = Elem<T>::to_f(((from_prev >> i) & 1) ? ep[i] : ec[i]);
-                                float h = v;
-                                if (sg.transform) h = inframe ? fz_silu(fmaf(v, sc[i], sh[i])) : 0.f;
-                                o.v[i] = Elem<T>::from_f(h);
-                            }
-                            out = *reinterpret_cast<uint4 *>(&o);
+                        for (int j = 0; j < 4; ++j) {
+                            float v0, v1;
+                            Pk<T>::unpack((wp[j] & msk[j]) | (wc[j] & ~msk[j]), v0, v1);
+                            const float h0 = fz_silu_pre(fmaf(v0, sc[2 * j], sh[2 * j]), fmaf(v0, sc2[2 * j], sh2[2 * j]));
+                            const float h1 = fz_silu_pre(fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]),
+                                                         fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
+                            o[j] = live ? Pk<T>::pack(h0, h1) : 0u;
                         }
-                        *reinterpret_cast<uint4 *>(tf + r * 16) = out;
+                        *reinterpret_cast<uint4 *>(tf + r * 16) = make_uint4(o[0], o[1], o[2], o[3]);
                     }
                     fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
                     asm volatile("bar.sync 2, 256;" ::: "memory");   // the 8 transform warps
@@ -359,8 +406,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         const int q4 = warp & 3;
         const int r = q4 * 32 + lane;
         const int by = r / FZ_BX, bxp = r - by * FZ_BX;
-        const T *b0 = reinterpret_cast<const T *>(p.bias0);
-        const T *b1 = reinterpret_cast<const T *>(p.bias1);
+        const float *sb0 = p.bias0 ? sbias : nullptr;
+        const float *sb1 = p.bias1 ? sbias + p.cout : nullptr;
         const T *res = reinterpret_cast<const T *>(p.residual);
         T *out = reinterpret_cast<T *>(p.out);
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
@@ -392,31 +439,27 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
             mbar_wait(&tfull[buf], use);
             tc_fence_after();
             const bool want_stats = p.stats != nullptr && bx.valid;
-#pragma unroll 1
-            for (int cc = 0, par = 0; cc < BN; cc += 16, par ^= 1) {
-                uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
+            // one 16-column chunk: + bias (fp32, shared memory) + residual (staged tile), 16-bit
+            // store, box statistics of the stored values
+            auto chunk = [&](const uint32_t (&v)[16], int cc, int par) {
                 const int n = nt * BN + cc;
                 float f[16];
                 if (m >= 0) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
-                    float e[8];
-                    if (b0) {
-                        load8(b0 + n, e);
+                    if (sb0) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] += e[i];
-                        load8(b0 + n + 8, e);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                        for (int i = 0; i < 16; i += 4) {
+                            const float4 e = *reinterpret_cast<const float4 *>(sb0 + n + i);
+                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
+                        }
                     }
-                    if (b1) {
-                        load8(b1 + n, e);
+                    if (sb1) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] += e[i];
-                        load8(b1 + n + 8, e);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                        for (int i = 0; i < 16; i += 4) {
+                            const float4 e = *reinterpret_cast<const float4 *>(sb1 + n + i);
+                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
+                        }
                     }
                     if (res) {   // from the TMA-staged residual tile (row r of the box)
                         const Vec8<T> *rr = reinterpret_cast<const Vec8<T> *>(sRes + ((size_t)r * BN + cc) * 2);
@@ -432,7 +475,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                     for (int i = 0; i < 8; ++i) {
                         lo.v[i] = Elem<T>::from_f(f[i]);
                         hi.v[i] = Elem<T>::from_f(f[8 + i]);
-                        f[i] = Elem<T>::to_f(lo.v[i]);
+                        f[i] = Elem<T>::to_f(lo.v[i]);       // statistics of the stored values (R17)
                         f[8 + i] = Elem<T>::to_f(hi.v[i]);
                     }
                     *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n) = lo;
@@ -450,6 +493,23 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         p.stats[(((size_t)bx.t * per + bi) * p.cout + n + (lane & 15)) * 2 + (lane >> 4)] = val;
                     }
                 }
+            };
+            // TMEM -> registers two chunks at a time: the next chunk's tcgen05.ld is in flight
+            // while the current one is processed
+            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
+            uint32_t va[16], vb[16];
+            tmem_ld16_nowait(taddr, va);
+            tmem_wait16(va);
+#pragma unroll 1
+            for (int cc = 0; cc < BN; cc += 32) {
+                const bool more = cc + 16 < BN;
+                if (more) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
+                chunk(va, cc, 0);
+                if (!more) break;
+                tmem_wait16(vb);
+                if (cc + 32 < BN) tmem_ld16_nowait(taddr + (uint32_t)(cc + 32), va);
+                chunk(vb, cc + 16, 1);
+                if (cc + 32 < BN) tmem_wait16(va);
             }
             tc_fence_before();
             __syncwarp();
@@ -579,7 +639,7 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         if (p.ntf < 2 || p.ntf > 4) p.ntf = 2;
     }
     const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (13 + 2 * FZ_MAX_BSTAGES) +
-                         16 + 1024 + 1024 /* static */;
+                         16 + 1024 + 1024 /* static */ + (size_t)2 * d.cout * 4 /* bias */;
     const size_t bstage = (size_t)(bn / CG) * 128;
     int nbst = (int)((227 * 1024 - fixed) / bstage);
     {

@@ -169,7 +169,7 @@ dvc_status conv_run(const ConvDesc &d, cudaStream_t stream) {
     ProfSlot slot = prof_begin(stream);
     const bool ws = d.dt != DVC_F32 && conv_ws_applicable(d);
     dvc_status st = d.dt == DVC_F32 ? conv_simt_run(d, stream) : ws ? conv_ws_run(d, stream) : conv_tc_run(d, stream);
-    prof_end(slot, stream, conv_flops(d));
+    prof_end(slot, stream, conv_flops(d), d.dt == DVC_F32 ? "simt" : ws ? "ws" : "tc", d);
     if (st == DVC_OK && d.stats_out != nullptr && !ws)   // engines without the fused epilogue statistics
         st = box_stats_run(d.out, d.T, d.ho, d.wo, d.cout, d.dt, reinterpret_cast<float *>(d.stats_out), stream);
     return st;

@@ -66,6 +66,16 @@ def profile_end():
     return ms.value, fl.value, n.value
 
 
+def profile_records(n: int):
+    """-> [(label, ms, flops)] for the n launches of the last profile window."""
+    out = []
+    for i in range(n):
+        ms, fl, lab = ctypes.c_double(), ctypes.c_double(), ctypes.create_string_buffer(128)
+        check(lib().dvc_profile_record(i, ctypes.byref(ms), ctypes.byref(fl), lab, 128))
+        out.append((lab.value.decode(), ms.value, fl.value))
+    return out
+
+
 # ------------------------------------------------------------------ a1 + a2
 def dvc_encode_pixelunshuffle(frames: torch.Tensor, w_exp=None, b_exp=None, s: int = 8, out=None, stream=None):
     """frames [T,3,H,W] -> latent [T,H/s,W/s,c_lat] (c_lat = 3 s^2 without expansion)."""
