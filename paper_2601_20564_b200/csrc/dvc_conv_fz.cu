@@ -3,22 +3,25 @@
 // temporal shift (SURVEY a3/a4/a5 and a6/a7/a8 in one kernel).
 //
 // Output tiles are 8-wide x 16-tall pixel boxes (128 MMA rows).  For every
-// 64-channel chunk of the operand the transform warps read the raw 10 x 18 halo
-// of the box once from global memory (128-bit loads, L2-resident neighbours) and write
+// 64-channel chunk of the operand a producer warp TMA-loads the raw 10 x 18 halo
+// of the box as eight 8-channel boxes {8, 10, 18} (no swizzle, out-of-bounds zero
+// fill) -- each lands as one 180-row core-matrix column of a K-major UMMA tile --
+// together with the chunk's 64 GN coefficients.  The transform warps then rewrite
+// the tile in place (shared memory only, no global-load latency on their path):
 //     H = SiLU(X * sc[t][c] + b[t][c])   (0 outside the frame: conv padding after
 //                                          the transform, H3)
-// into a no-swizzle K-major tile (8-channel core matrices of 180 halo rows).  The
-// nine taps are then nine UMMA descriptors into that one tile: row offset
+// The nine taps are nine UMMA descriptors into that one tile: row offset
 // (1+dy)*10 + (1+dx), 8-row groups 160 B apart (one image row each) -- the halo
 // is transformed once instead of nine times and no H tensor reaches HBM.
-// The temporal shift is load addressing: channels [0, C_in/P) of frame t are
-// read from frame t-1, or from the carry slice at t = 0.
-// The 1x1 shortcut segments (raw, unshifted X) use the same halo path with an
-// identity transform and only the centre tap.
+// The temporal shift is addressing of those TMA boxes: channels [0, C_in/P) of
+// frame t come from frame t-1, from the carry at t = 0, or (no carry) from an
+// out-of-bounds box = zeros; the one 8-channel group straddling C_in/P is merged
+// from a side buffer.  The 1x1 shortcut segments (raw, unshifted X) are TMA'd as
+// SW128 boxes straight into a slot (centre tap only).
 //
 // Warps (512 threads): 1 TMEM allocator + MMA issuer (leader CTA), 2 weight TMA
-// producer, 4-7 epilogue (bias / residual / 16-bit store / box statistics),
-// 8-15 transform (load + GN-apply + SiLU + store into the UMMA tile).  CTA pairs (cta_group::2, M=256),
+// producer, 3 operand-tile TMA producer, 4-7 epilogue (bias / residual / 16-bit
+// store / box statistics), 8-15 transform.  CTA pairs (cta_group::2, M=256),
 // double-buffered TMEM accumulators, as in dvc_conv_ws.cu.
 #include <cuda.h>
 #include <cstdlib>
@@ -31,9 +34,12 @@ namespace dvc {
 constexpr int FZ_BX = 8, FZ_BY = 16;
 constexpr int FZ_HX = FZ_BX + 2, FZ_HY = FZ_BY + 2;
 constexpr int FZ_HROWS = FZ_HX * FZ_HY;      // 180 halo pixels
-constexpr int FZ_BOX_BYTES = FZ_HROWS * 128;  // raw halo box, SW128
-constexpr int FZ_SLOT = 23552;                // 1024-aligned slot (>= 23040)
-constexpr int FZ_LBO = FZ_HROWS * 16;         // between 8-channel core-matrix columns
+constexpr int FZ_COLB = FZ_HROWS * 16;        // one 8-channel halo column (TMA box bytes, 2880)
+constexpr int FZ_LBO = 2944;                  // column stride: 2880 rounded up to the TMA's 128-B alignment
+// tile slot: [8][FZ_LBO] halo tile | [FZ_LBO] shift side buffer | [64] float2 GN coefficients
+constexpr int FZ_SIDE = 8 * FZ_LBO;           // 23552
+constexpr int FZ_COEF = FZ_SIDE + FZ_LBO;     // 26496
+constexpr int FZ_SLOT = 27648;                // 1024-aligned (raw SW128 boxes land at the slot start)
 constexpr int FZ_SBO = FZ_HX * 16;            // between 8-row groups (image rows)
 constexpr int FZ_MAX_BSTAGES = 16;
 constexpr int kFzThreads = 512;
@@ -52,6 +58,8 @@ struct FzParams {
     CUtensorMap bmap[2];   // weights, box {64, BN/CG}
     CUtensorMap rmap;      // residual [T][H][W][cout], box {BN, 8, 16, 1}, no swizzle (if residual)
     CUtensorMap smap[4];   // raw (transform == 0) segments: box {64, 8, 16, 1}, SW128 -> straight into a tile slot
+    CUtensorMap hmap[4];   // transform segments: 8-channel halo box {8, 10, 18, 1}, no swizzle, OOB zero
+    CUtensorMap cmap;      // padded carry [1][H][W][cs_pad], same box (if has_carry)
     FzSeg seg[4];
     int nseg, cs, has_carry, cs_pad;
     const void *carry_pad; // [H][W][cs_pad] (16-byte rows)
@@ -82,16 +90,6 @@ __device__ __forceinline__ float fz_silu_pre(float z, float u) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(u));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
     return z * r;
-}
-// 16-byte read-only load if pred, else zeros (branch-free)
-__device__ __forceinline__ uint4 ldg_v4_if(uint32_t pred, const void *ptr) {
-    uint4 v;
-    asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\tmov.b32 %2, 0;\n\tmov.b32 %3, 0;\n\t"
-        "@p ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}\n"
-        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-        : "r"(pred), "l"(ptr));
-    return v;
 }
 // two 16-bit elements in one 32-bit word (element 2j in the low half)
 template <typename T> struct Pk;
@@ -155,7 +153,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     uint64_t *tfull = b_empty + FZ_BSTAGES;
     uint64_t *tempty = tfull + 2;
     uint64_t *res_full = tempty + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(res_full + 1);
+    uint64_t *raw_full = res_full + 1;   // [4] halo TMA (+ coefficients) landed in slot tb (local CTA)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(raw_full + 4);
     float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][4][32] box-statistics staging
     float *sbias = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(red + 256) + 15) & ~uintptr_t(15));
     //              ^ [2][cout] bias0, bias1 in fp32 (16-byte aligned for float4 reads)
@@ -179,6 +178,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
             mbar_init(&b_empty[s], 1);
         }
         mbar_init(res_full, 1);
+        for (int i = 0; i < 4; ++i) mbar_init(&raw_full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
@@ -225,11 +225,15 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 }
             }
         }
-    } else if (warp >= 8) {
-        // ===================== transform warps: raw halo -> H tile =====================
-        const int kg = warp - 8;   // 8-channel core-matrix column of this warp
+    } else if (warp == 3) {
+        // ===================== operand tile producer (TMA) =====================
+        // transform segments: per 8-channel group one halo box {8 ch, 10, 18} of frame t (or of
+        // frame t-1 / the carry / zeros for the shifted channels) straight into its core-matrix
+        // column, plus the 64 GN coefficients; raw 1x1 segments: one SW128 box into the slot,
+        // completing on the leader's tf_full.
         int tb = 0;
         uint32_t tph = 0;
+        const uint32_t issue = lane == 0;
         const uint32_t tf_full_leader = CG == 2 ? mapa_shared(smem_u32(&tf_full[0]), 0) : smem_u32(&tf_full[0]);
         for (int w = cluster_id; w < p.nwork; w += nclusters) {
             const FzBox bx = fz_box(p, (w / p.ntile_n) * CG + (int)rank);
@@ -237,99 +241,137 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 const FzSeg &sg = p.seg[s];
                 const int nch = (sg.c + 63) >> 6;
                 for (int ch = 0; ch < nch; ++ch) {
+                    mbar_wait(&tf_empty[tb], tph ^ 1);
+                    const uint32_t slot = smem_u32(sTf + tb * FZ_SLOT);
                     if (!sg.transform) {
-                        // raw 1x1 segment: no transform -- TMA the box (SW128) straight into the tile slot;
-                        // each CTA signals its bytes to the leader's tf_full
-                        mbar_wait(&tf_empty[tb], tph ^ 1);
-                        if (warp == 8 && elect_one()) {
-                            const uint32_t fb = CG == 2 ? tf_full_leader + (uint32_t)(tb * 8) : smem_u32(&tf_full[tb]);
+                        if (issue) {
+                            const uint32_t fb = tf_full_leader + (uint32_t)(tb * 8);
                             if constexpr (CG == 1) {
                                 mbar_arrive_expect_tx_addr(fb, 128 * 128);
-                                tma_load_4d(smem_u32(sTf + tb * FZ_SLOT), &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
+                                tma_load_4d(slot, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
                             } else {
                                 mbar_arrive_expect_tx_cluster(fb, 128 * 128);
-                                tma_load_4d_cg2(smem_u32(sTf + tb * FZ_SLOT), &p.smap[s], fb, ch * 64, bx.x0, bx.y0,
-                                                bx.t);
+                                tma_load_4d_cg2(slot, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
                             }
                         }
-                        __syncwarp();
+                    } else if (issue) {
+                        const int c0 = ch * 64;
+                        const int ngrp = min(8, (sg.c - c0) >> 3);
+                        int nside = 0;
+                        for (int g = 0; g < ngrp; ++g) {
+                            const int nprev = sg.shift ? min(max(p.cs - (c0 + 8 * g), 0), 8) : 0;
+                            nside += nprev > 0 && nprev < 8;
+                        }
+                        const uint32_t rb = smem_u32(&raw_full[tb]);
+                        const uint32_t coef_bytes = bx.valid ? (uint32_t)ngrp * 64u : 0u;
+                        mbar_arrive_expect_tx_addr(rb, (uint32_t)(ngrp + nside) * FZ_COLB + coef_bytes);
+                        for (int g = 0; g < ngrp; ++g) {
+                            const int cl = c0 + 8 * g;
+                            const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
+                            const uint32_t dst = slot + (uint32_t)(g * FZ_LBO);
+                            if (nprev < 8)
+                                tma_load_4d(dst, &p.hmap[s], rb, cl, bx.x0 - 1, bx.y0 - 1, bx.t);
+                            if (nprev > 0) {
+                                // shifted channels: frame t-1, the carry at t = 0, or (no carry) a fully
+                                // out-of-bounds box = zeros
+                                const uint32_t pd = nprev < 8 ? slot + FZ_SIDE : dst;
+                                if (bx.t > 0 || !p.has_carry)
+                                    tma_load_4d(pd, &p.hmap[s], rb, cl, bx.x0 - 1, bx.y0 - 1, bx.t > 0 ? bx.t - 1 : -1);
+                                else
+                                    tma_load_4d(pd, &p.cmap, rb, cl, bx.x0 - 1, bx.y0 - 1, 0);
+                            }
+                        }
+                        if (coef_bytes)
+                            bulk_load(slot + FZ_COEF, p.coef + (size_t)bx.t * p.cop + sg.cglob0 + c0, coef_bytes, rb);
+                    }
+                    __syncwarp();
+                    if (++tb == NTF) {
+                        tb = 0;
+                        tph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp >= 8) {
+        // ===================== transform warps: in place, H = SiLU(GN(X)) =====================
+        const int kg = warp - 8;   // 8-channel core-matrix column of this warp
+        int tb = 0;
+        uint32_t tph = 0;
+        uint32_t rph = 0;   // raw_full phase per slot: only transform chunks complete raw_full
+        const uint32_t tf_full_leader = CG == 2 ? mapa_shared(smem_u32(&tf_full[0]), 0) : smem_u32(&tf_full[0]);
+        for (int w = cluster_id; w < p.nwork; w += nclusters) {
+            const FzBox bx = fz_box(p, (w / p.ntile_n) * CG + (int)rank);
+            for (int s = 0; s < p.nseg; ++s) {
+                const FzSeg &sg = p.seg[s];
+                const int nch = (sg.c + 63) >> 6;
+                for (int ch = 0; ch < nch; ++ch) {
+                    if (!sg.transform) {   // raw segment: the producer's TMA completes tf_full itself
                         if (++tb == NTF) {
                             tb = 0;
                             tph ^= 1;
                         }
                         continue;
                     }
-                    const int cl = ch * 64 + kg * 8;           // first channel (segment-local) of this warp
-                    const int cgl = sg.cglob0 + cl;            // operand channel (coef index)
-                    const bool cval = cl < sg.c;               // warp-uniform
-                    // GN affine of frame t for the 8 channels, z = v*sc + sh, and the same affine
-                    // pre-scaled by -log2(e) so that e^-z = ex2(v*sc2 + sh2) costs one FFMA
-                    float sc[8], sh[8], sc2[8], sh2[8];
-                    if (cval && bx.valid) {
-                        const float4 *cf = reinterpret_cast<const float4 *>(p.coef + (size_t)bx.t * p.cop + cgl);
+                    const int cl = ch * 64 + kg * 8;   // first channel (segment-local) of this warp
+                    uint8_t *slot = sTf + tb * FZ_SLOT;
+                    mbar_wait(&raw_full[tb], (rph >> tb) & 1u);
+                    rph ^= 1u << tb;
+                    if (cl < sg.c) {   // warp-uniform; groups past the segment are never read by the MMA
+                        // GN affine of frame t for the 8 channels, z = v*sc + sh, and the same affine
+                        // pre-scaled by -log2(e) so that e^-z = ex2(v*sc2 + sh2) costs one FFMA
+                        float sc[8], sh[8], sc2[8], sh2[8];
+                        if (bx.valid) {
+                            const float4 *cf = reinterpret_cast<const float4 *>(slot + FZ_COEF + kg * 64);
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const float4 q = __ldg(cf + i);
-                            sc[2 * i] = q.x, sh[2 * i] = q.y, sc[2 * i + 1] = q.z, sh[2 * i + 1] = q.w;
+                            for (int i = 0; i < 4; ++i) {
+                                const float4 q = cf[i];
+                                sc[2 * i] = q.x, sh[2 * i] = q.y, sc[2 * i + 1] = q.z, sh[2 * i + 1] = q.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) sc[i] = 1.f, sh[i] = 0.f;
                         }
-                    } else {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) sc[i] = 1.f, sh[i] = 0.f;
-                    }
+                        for (int i = 0; i < 8; ++i)
+                            sc2[i] = sc[i] * -1.4426950408889634f, sh2[i] = sh[i] * -1.4426950408889634f;
+                        // a group straddling C_in/P: its first nprev channels come from the side buffer.
+                        // C_in/P is even (C_in % 16 == 0): merge per 32-bit word.
+                        const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
+                        const bool straddle = nprev > 0 && nprev < 8;
+                        uint32_t msk[4];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) sc2[i] = sc[i] * -1.4426950408889634f, sh2[i] = sh[i] * -1.4426950408889634f;
-                    // temporal shift: the first nprev of these 8 channels come from frame t-1 (or the
-                    // carry at t = 0).  C_in/P is even (C_in % 16 == 0), so the split falls on a
-                    // 32-bit word: merge = (prev & m) | (cur & ~m) per word.
-                    const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
-                    uint32_t msk[4];
+                        for (int j = 0; j < 4; ++j) msk[j] = 2 * j < nprev ? 0xFFFFFFFFu : 0u;
+                        uint8_t *col = slot + kg * FZ_LBO;
+                        constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) msk[j] = 2 * j < nprev ? 0xFFFFFFFFu : 0u;
-                    // sources (warp-uniform): frame t, and frame t-1 or the padded carry at t = 0
-                    const T *srcT = reinterpret_cast<const T *>(sg.src);
-                    const size_t HWs = (size_t)p.H * p.W;
-                    const bool prev_carry = bx.t == 0;
-                    const uint32_t lc = cval && bx.valid && nprev < 8;
-                    const uint32_t lp = cval && bx.valid && nprev > 0 && !(prev_carry && !p.has_carry);
-                    const T *cur_base = srcT + (size_t)bx.t * HWs * sg.c + cl;
-                    const T *prev_base = prev_carry ? reinterpret_cast<const T *>(p.carry_pad) + cl
-                                                    : srcT + ((size_t)bx.t - 1) * HWs * sg.c + cl;
-                    const int prev_ld = prev_carry ? p.cs_pad : sg.c;
-                    mbar_wait(&tf_empty[tb], tph ^ 1);
-                    uint8_t *tf = sTf + tb * FZ_SLOT + kg * FZ_LBO;
-                    constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane
-                    uint4 cu[NR], pv[NR];
+                        for (int k = 0; k < NR; ++k) {
+                            const int r = lane + 32 * k;
+                            if (r >= FZ_HROWS) break;
+                            const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
+                            const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
+                            // conv zero padding applies AFTER the transform (H3): out of frame -> 0
+                            const bool live = bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
+                            uint4 cu = *reinterpret_cast<const uint4 *>(col + r * 16);
+                            if (straddle) {
+                                const uint4 pv = *reinterpret_cast<const uint4 *>(slot + FZ_SIDE + r * 16);
+                                cu.x = (pv.x & msk[0]) | (cu.x & ~msk[0]);
+                                cu.y = (pv.y & msk[1]) | (cu.y & ~msk[1]);
+                                cu.z = (pv.z & msk[2]) | (cu.z & ~msk[2]);
+                                cu.w = (pv.w & msk[3]) | (cu.w & ~msk[3]);
+                            }
+                            const uint32_t wc[4] = {cu.x, cu.y, cu.z, cu.w};
+                            uint32_t o[4];
 #pragma unroll
-                    for (int k = 0; k < NR; ++k) {   // issue every load before any use (predicated, no branches)
-                        const int r = lane + 32 * k;
-                        const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
-                        const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
-                        const uint32_t ok = r < FZ_HROWS && y >= 0 && y < p.H && x >= 0 && x < p.W;
-                        const int pf = y * p.W + x;
-                        cu[k] = ldg_v4_if(ok & lc, cur_base + (ptrdiff_t)pf * sg.c);
-                        pv[k] = ldg_v4_if(ok & lp, prev_base + (ptrdiff_t)pf * prev_ld);
-                    }
-#pragma unroll
-                    for (int k = 0; k < NR; ++k) {
-                        const int r = lane + 32 * k;
-                        if (r >= FZ_HROWS) break;
-                        const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
-                        const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
-                        // conv zero padding applies AFTER the transform (H3): out of frame -> 0
-                        const bool live = cval && bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
-                        const uint32_t wc[4] = {cu[k].x, cu[k].y, cu[k].z, cu[k].w};
-                        const uint32_t wp[4] = {pv[k].x, pv[k].y, pv[k].z, pv[k].w};
-                        uint32_t o[4];
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            float v0, v1;
-                            Pk<T>::unpack((wp[j] & msk[j]) | (wc[j] & ~msk[j]), v0, v1);
-                            const float h0 = fz_silu_pre(fmaf(v0, sc[2 * j], sh[2 * j]), fmaf(v0, sc2[2 * j], sh2[2 * j]));
-                            const float h1 = fz_silu_pre(fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]),
-                                                         fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
-                            o[j] = live ? Pk<T>::pack(h0, h1) : 0u;
+                            for (int j = 0; j < 4; ++j) {
+                                float v0, v1;
+                                Pk<T>::unpack(wc[j], v0, v1);
+                                const float h0 = fz_silu_pre(fmaf(v0, sc[2 * j], sh[2 * j]), fmaf(v0, sc2[2 * j], sh2[2 * j]));
+                                const float h1 = fz_silu_pre(fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]),
+                                                             fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
+                                o[j] = live ? Pk<T>::pack(h0, h1) : 0u;
+                            }
+                            *reinterpret_cast<uint4 *>(col + r * 16) = make_uint4(o[0], o[1], o[2], o[3]);
                         }
-                        *reinterpret_cast<uint4 *>(tf + r * 16) = make_uint4(o[0], o[1], o[2], o[3]);
                     }
                     fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
                     asm volatile("bar.sync 2, 256;" ::: "memory");   // the 8 transform warps
@@ -545,6 +587,23 @@ bool conv_fz_applicable(int H, int W, dvc_dtype dt) { return g_ws_cg == 2 && dt 
 
 static int g_fz_sms = 0;
 
+// 8-channel halo box {8, 10, 18, 1} of a [T][H][W][C] tensor, no swizzle: lands as one 180-row
+// core-matrix column of the UMMA tile; out-of-bounds rows (and frames) are zero-filled
+static dvc_status make_halo_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && C % 8 == 0, DVC_ERR_ARG, "fused conv: halo source alignment");
+    cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
+    cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {8, (cuuint32_t)FZ_HX, (cuuint32_t)FZ_HY, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                     const_cast<void *>(ptr), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (halo) failed (%d)", (int)r);
+    return DVC_OK;
+}
+
 dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     DVC_CHECK_ARG(d.nseg >= 1 && d.nseg <= 4 && d.T >= 1 && d.T < 256 && d.cout % 16 == 0, DVC_ERR_UNSUPPORTED,
                   "fused conv: bad descriptor");
@@ -577,6 +636,7 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     p.out = d.out;
     p.stats = reinterpret_cast<float *>(d.stats_out);
     p.coef = reinterpret_cast<const float2 *>(d.coef);
+    DVC_CHECK_ARG(((uintptr_t)d.coef & 15) == 0 && d.cop % 2 == 0, DVC_ERR_ARG, "fused conv: coefficient alignment");
     p.cop = d.cop;
     p.cs = d.cs;
     p.has_carry = d.carry_pad != nullptr;
@@ -590,8 +650,8 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     const void *bw[2] = {nullptr, nullptr};
     for (int s = 0; s < d.nseg; ++s) {
         const FzDesc::Seg &g = d.seg[s];
-        DVC_CHECK_ARG(g.c % 16 == 0 && g.src != nullptr && ((uintptr_t)g.src & 15) == 0, DVC_ERR_UNSUPPORTED,
-                      "fused conv: segment channels / alignment");
+        DVC_CHECK_ARG(g.c % 16 == 0 && g.src != nullptr && ((uintptr_t)g.src & 15) == 0 && g.cglob0 % 2 == 0,
+                      DVC_ERR_UNSUPPORTED, "fused conv: segment channels / alignment");
         int idx = -1;
         for (int k = 0; k < nb; ++k)
             if (bw[k] == g.w) idx = k;
@@ -615,8 +675,14 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         if (!g.transform) {
             DVC_CHECK_ARG(g.taps == 1, DVC_ERR_UNSUPPORTED, "fused conv: raw segments are 1x1");
             st = make_box_map(&p.smap[s], g.src, d.dt, d.T, d.H, d.W, g.c, FZ_BX, FZ_BY);
-            if (st != DVC_OK) return st;
+        } else {
+            st = make_halo_map(&p.hmap[s], g.src, d.dt, d.T, d.H, d.W, g.c);
         }
+        if (st != DVC_OK) return st;
+    }
+    if (p.has_carry) {
+        st = make_halo_map(&p.cmap, d.carry_pad, d.dt, 1, d.H, d.W, d.cs_pad);
+        if (st != DVC_OK) return st;
     }
     if (d.residual) {
         PFN_encodeTiled_t enc = get_encode_fn();
@@ -638,7 +704,7 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         p.ntf = e ? atoi(e) : (d.residual ? 2 : 4);
         if (p.ntf < 2 || p.ntf > 4) p.ntf = 2;
     }
-    const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (13 + 2 * FZ_MAX_BSTAGES) +
+    const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (17 + 2 * FZ_MAX_BSTAGES) +
                          16 + 1024 + 1024 /* static */ + (size_t)2 * d.cout * 4 /* bias */;
     const size_t bstage = (size_t)(bn / CG) * 128;
     int nbst = (int)((227 * 1024 - fixed) / bstage);

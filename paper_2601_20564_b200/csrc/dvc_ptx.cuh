@@ -325,6 +325,12 @@ __device__ __forceinline__ void mbar_wait_spin_addr(uint32_t a, uint32_t parity)
     }
 }
 
+// 1D bulk copy global -> shared (16-byte aligned, bytes % 16 == 0), completing on a local mbarrier
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
 // predicated (branch-free) TMA issue: only lanes with pred != 0 issue
 __device__ __forceinline__ void mbar_expect_tx_if(uint32_t pred, uint32_t addr, uint32_t bytes) {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t"

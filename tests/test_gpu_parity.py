@@ -130,7 +130,9 @@ def test_resblock_fp32_config1(dvc, orc, with_carry):   # C1: T=8, 64 ch, 32x32,
                                                  (1920, 960, 960, 2, 3, 5), (240, 480, 0, 1, 12, 20),
                                                  # H >= 32: the fused GN/SiLU/shift conv engine (8x16 halo boxes)
                                                  (240, 240, 0, 3, 40, 24), (720, 240, 240, 2, 34, 20),
-                                                 (64, 32, 32, 2, 33, 9), (480, 480, 0, 2, 45, 16)])
+                                                 (64, 32, 32, 2, 33, 9), (480, 480, 0, 2, 45, 16),
+                                                 # > 74 CTA-pair tiles: slots cycle through raw and transformed chunks
+                                                 (96, 32, 32, 6, 64, 72)])
 def test_resblock_parity(dvc, orc, dtype, cin, cout, cb, T, H, W):
     G = 8 if cin < 240 else 24
     w = synthgen.resblock_weights(cin, cout, seed=cin + cout)
