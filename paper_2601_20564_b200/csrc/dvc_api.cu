@@ -7,6 +7,8 @@
 #include <vector>
 #include <string>
 #include <mutex>
+#include <map>
+#include <tuple>
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
 #include "dvc_resblock.cuh"
@@ -99,6 +101,32 @@ void prof_end(ProfSlot s, cudaStream_t stream, double flops, const char *engine,
     for (int i = 0; i < d.nseg; ++i) k += d.seg[i].taps * d.seg[i].c_src;
     snprintf(buf, sizeof(buf), "%s T=%d %dx%d K=%d N=%d segs=%d", engine, d.T, d.ho, d.wo, k, d.cout, d.nseg);
     g_prof.label[s.idx] = buf;
+}
+
+// ----------------------------------------------------------------- identity weights
+// [c][c] identity in dt, one per (device, c, dt), allocated on first use and kept for the
+// process lifetime (the fused conv's identity-skip segment).  First use synchronises
+// (cudaMalloc / cudaMemcpy): not inside stream capture.
+static const void *identity_weights(int c, dvc_dtype dt) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, int>, void *> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(dev, c, (int)dt);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    std::vector<uint16_t> h((size_t)c * c, 0);
+    const uint16_t one = dt == DVC_BF16 ? 0x3F80 : 0x3C00;
+    for (int i = 0; i < c; ++i) h[(size_t)i * c + i] = one;
+    void *d = nullptr;
+    if (cudaMalloc(&d, h.size() * 2) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    cache[key] = d;
+    return d;
 }
 
 // ----------------------------------------------------------------- ResBlock (a3-a8)
@@ -250,7 +278,12 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
             }
             f2.bias1 = b.sc_b;
         } else {
-            f2.residual = xa;
+            // identity skip (C_in == C_out): X . I as a 1x1 raw segment -- the tensor core adds the
+            // residual into the fp32 accumulator (exact products), no residual tile in the epilogue
+            DVC_CHECK_ARG(b.cb == 0 && b.ca == b.cout, DVC_ERR_UNSUPPORTED, "identity skip needs C_in == C_out");
+            const void *eye = identity_weights(b.cout, b.dt);
+            DVC_CHECK_ARG(eye != nullptr, DVC_ERR_CUDA, "identity weights: %s", "allocation failed");
+            f2.seg[f2.nseg++] = FzDesc::Seg{xa, b.ca, 0, 1, 0, 0, eye, b.cout, 0, 0, 0};
         }
         f2.T = T;
         f2.H = H;

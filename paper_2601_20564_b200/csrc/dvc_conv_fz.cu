@@ -20,10 +20,11 @@
 // SW128 boxes straight into a slot (centre tap only).
 //
 // Warps (512 threads): 1 TMEM allocator + MMA issuer (leader CTA), 2 weight TMA
-// producer, 3 operand-tile TMA producer, 4-7 epilogue (bias / residual / 16-bit
+// producer, 3 operand-tile TMA producer, 4-7 epilogue (bias / 16-bit
 // store / box statistics), 8-15 transform.  CTA pairs (cta_group::2, M=256),
 // double-buffered TMEM accumulators, as in dvc_conv_ws.cu.
 #include <cuda.h>
+#include <cstdio>
 #include <cstdlib>
 #include "dvc_conv.cuh"
 #include "dvc_ptx.cuh"
@@ -39,9 +40,11 @@ constexpr int FZ_LBO = 2944;                  // column stride: 2880 rounded up 
 // tile slot: [8][FZ_LBO] halo tile | [FZ_LBO] shift side buffer | [64] float2 GN coefficients
 constexpr int FZ_SIDE = 8 * FZ_LBO;           // 23552
 constexpr int FZ_COEF = FZ_SIDE + FZ_LBO;     // 26496
-constexpr int FZ_SLOT = 27648;                // 1024-aligned (raw SW128 boxes land at the slot start)
+constexpr int FZ_SLOT = 27648;                // 1024-aligned
+constexpr int FZ_RAW_SLOT = 128 * 128;        // one raw SW128 box {64, 8, 16}
 constexpr int FZ_SBO = FZ_HX * 16;            // between 8-row groups (image rows)
 constexpr int FZ_MAX_BSTAGES = 16;
+constexpr int FZ_MAX_NTF = 6;   // even: keeps the barrier block a multiple of 16 B
 constexpr int kFzThreads = 512;
 
 struct FzSeg {
@@ -56,9 +59,9 @@ struct FzSeg {
 
 struct FzParams {
     CUtensorMap bmap[2];   // weights, box {64, BN/CG}
-    CUtensorMap rmap;      // residual [T][H][W][cout], box {BN, 8, 16, 1}, no swizzle (if residual)
     CUtensorMap smap[4];   // raw (transform == 0) segments: box {64, 8, 16, 1}, SW128 -> straight into a tile slot
     CUtensorMap hmap[4];   // transform segments: 8-channel halo box {8, 10, 18, 1}, no swizzle, OOB zero
+    CUtensorMap wmap[4];   // transform segments: 64-channel halo box {64, 10, 18, 1}, SW128, OOB zero
     CUtensorMap cmap;      // padded carry [1][H][W][cs_pad], same box (if has_carry)
     FzSeg seg[4];
     int nseg, cs, has_carry, cs_pad;
@@ -66,11 +69,13 @@ struct FzParams {
     const float2 *coef;    // [T][C_op] = (scale, shift) of the GN affine, beta and mean folded in
     int cop;               // channels of the fused operand
     int T, H, W, cout, bn, tiles_x, tiles_y, nbox, ntile_n, nwork;
-    const void *bias0, *bias1, *residual;
+    const void *bias0, *bias1;
     void *out;
     float *stats;
     uint32_t idesc;
-    int ntf, nb;   // tile slots, weight stages (sized from the shared-memory budget)
+    int ntf, nraw, nb;   // tile slots, raw slots (0 or 2), weight stages (sized from the shared-memory budget)
+    unsigned long long *prof;   // [6][4] wait/total cycles per role (PROF kernels only)
+    int sw_mode;                // 0: 8-channel no-swizzle boxes only; 1/2: SW128 whole-chunk box for unshifted chunks (2: base offset)
 };
 
 // UMMA descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B
@@ -83,15 +88,24 @@ __device__ __forceinline__ uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo, ui
     return d;
 }
 
-// SiLU(z) = z / (1 + e^-z) given z and u = -z*log2(e) (computed by its own FFMA): two MUFU
-// ops (ex2.approx, rcp.approx; <= 2 ulp fp32 each), far below the 16-bit rounding of H (R23)
-__device__ __forceinline__ float fz_silu_pre(float z, float u) {
-    float e, r;
+// SiLU(z) = z * rcp(1 + ex2(u)) with u = -z*log2(e) from its own FFMA: two MUFU ops
+// (ex2.approx, rcp.approx; <= 2 ulp fp32 each), far below the 16-bit rounding of H (R23)
+__device__ __forceinline__ float fz_ex2(float u) {
+    float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(u));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
-    return z * r;
+    return e;
+}
+__device__ __forceinline__ float fz_rcp(float d) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+    return r;
 }
 // two 16-bit elements in one 32-bit word (element 2j in the low half)
+// an unshifted transform chunk is one SW128 halo box {64, 10, 18} (rows of 128 B); chunks holding
+// shifted channels keep the 8-channel no-swizzle columns (per-group source selection)
+__device__ __forceinline__ bool fz_sw_chunk(const FzParams &p, const FzSeg &sg, int c0) {
+    return p.sw_mode != 0 && (!sg.shift || c0 >= p.cs);
+}
 template <typename T> struct Pk;
 template <> struct Pk<__nv_bfloat16> {
     static __device__ __forceinline__ void unpack(uint32_t w, float &a, float &b) {
@@ -135,29 +149,35 @@ __device__ __forceinline__ FzBox fz_box(const FzParams &p, int box) {
     return b;
 }
 
-template <typename T, int CG>
+// PROF: clock64 accounting of the pipeline waits per warp role (DVC_FZ_PROF=1; diagnostics only)
+template <typename T, int CG, bool PROF>
 __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_constant__ FzParams p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-aligned, derived from smem_raw by pointer arithmetic so the compiler keeps the
+    // shared address space (an integer round trip would turn every access generic)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int BN = p.bn, BNH = p.bn / CG;
     const int B_STAGE = BNH * 128;
-    // tile slots: 4 (2 when the residual tile needs the shared memory)
-    const int NTF = p.ntf, FZ_BSTAGES = p.nb;
-    uint8_t *sTf = smem;                        // [NTF] transformed / raw operand tiles
-    uint8_t *sB = sTf + NTF * FZ_SLOT;          // [FZ_BSTAGES] weight tiles
-    uint8_t *sRes = sB + FZ_BSTAGES * B_STAGE;  // residual tile of the current output box [128][BN]
-    uint64_t *tf_full = reinterpret_cast<uint64_t *>(sRes + (p.residual ? 128 * BN * 2 : 0));
-    uint64_t *tf_empty = tf_full + 4;
-    uint64_t *b_full = tf_empty + 4;
+    // transform tile slots (4 unless overridden), a separate 2-slot ring for the raw 1x1 segments
+    // (so short raw chunks never hold back the transform prefetch), weight stages filling the
+    // rest of the 227 KB
+    const int NTF = p.ntf, NRAW = p.nraw, FZ_BSTAGES = p.nb;
+    uint8_t *sTf = smem;                        // [NTF] transformed operand tiles
+    uint8_t *sRaw = sTf + NTF * FZ_SLOT;        // [NRAW] raw SW128 boxes (16 KB)
+    uint8_t *sB = sRaw + NRAW * FZ_RAW_SLOT;    // [FZ_BSTAGES] weight tiles
+    uint64_t *tf_full = reinterpret_cast<uint64_t *>(sB + FZ_BSTAGES * B_STAGE);
+    uint64_t *tf_empty = tf_full + FZ_MAX_NTF;
+    uint64_t *b_full = tf_empty + FZ_MAX_NTF;
     uint64_t *b_empty = b_full + FZ_BSTAGES;
     uint64_t *tfull = b_empty + FZ_BSTAGES;
     uint64_t *tempty = tfull + 2;
-    uint64_t *res_full = tempty + 2;
-    uint64_t *raw_full = res_full + 1;   // [4] halo TMA (+ coefficients) landed in slot tb (local CTA)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(raw_full + 4);
-    float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][4][32] box-statistics staging
-    float *sbias = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(red + 256) + 15) & ~uintptr_t(15));
-    //              ^ [2][cout] bias0, bias1 in fp32 (16-byte aligned for float4 reads)
+    uint64_t *raw_full = tempty + 2;   // [4] halo TMA (+ coefficients) landed in slot tb (local CTA)
+    uint64_t *rw_full = raw_full + FZ_MAX_NTF;  // [2] raw box landed (leader; both CTAs' bytes)
+    uint64_t *rw_empty = rw_full + 2;  // [2] raw slot free (MMA commit, both CTAs)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rw_empty + 2);
+    float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][2][4][32] box-statistics staging
+    float *sbias = red + 512;   // [2][cout] bias0, bias1 in fp32 (16-byte aligned: the barrier block is
+                                // 1024-aligned and holds an even number of 8-byte barriers)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -165,7 +185,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     const uint32_t ncols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < FZ_MAX_NTF; ++i) {
             mbar_init(&tf_full[i], CG);
             mbar_init(&tf_empty[i], 1);
         }
@@ -177,8 +197,11 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
             mbar_init(&b_full[s], 1);
             mbar_init(&b_empty[s], 1);
         }
-        mbar_init(res_full, 1);
-        for (int i = 0; i < 4; ++i) mbar_init(&raw_full[i], 1);
+        for (int i = 0; i < FZ_MAX_NTF; ++i) mbar_init(&raw_full[i], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&rw_full[i], CG);
+            mbar_init(&rw_empty[i], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
@@ -192,6 +215,14 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     if constexpr (CG == 2) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    unsigned long long pacc[4] = {0, 0, 0, 0};
+    const long long tstart = PROF ? clock64() : 0;
+#define FZ_TIMED(slot, stmt)                                  \
+    do {                                                      \
+        const long long t0_ = PROF ? clock64() : 0;           \
+        stmt;                                                 \
+        if constexpr (PROF) pacc[slot] += clock64() - t0_;    \
+    } while (0)
 
     if (warp == 2) {
         // ===================== weight producer =====================
@@ -211,7 +242,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 const CUtensorMap *bm = &p.bmap[sg.bidx];
                 for (int ch = 0; ch < nch; ++ch) {
                     for (int tap = 0; tap < sg.taps; ++tap) {
-                        mbar_wait_spin_addr(bempty0 + 8 * bs, bph ^ 1);
+                        FZ_TIMED(0, mbar_wait_spin_addr(bempty0 + 8 * bs, bph ^ 1));
                         // packed weights: the (tap, chunk) tile is one contiguous row block
                         const int col = sg.packed ? 0 : sg.col0 + tap * sg.tapstride + ch * 64;
                         const int row = sg.packed ? sg.col0 + (tap * nch + ch) * p.cout + n0 : n0;
@@ -225,45 +256,66 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 }
             }
         }
-    } else if (warp == 3) {
-        // ===================== operand tile producer (TMA) =====================
+    } else if (warp == 3 || warp == 0) {
+        // ===================== operand tile producers (TMA) =====================
+        // warp 3: transformed segments (tf ring); warp 0: raw 1x1 segments (raw ring).  Two
+        // producers so that neither ring's back-pressure holds up the other's prefetch.
         // transform segments: per 8-channel group one halo box {8 ch, 10, 18} of frame t (or of
         // frame t-1 / the carry / zeros for the shifted channels) straight into its core-matrix
         // column, plus the 64 GN coefficients; raw 1x1 segments: one SW128 box into the slot,
         // completing on the leader's tf_full.
-        int tb = 0;
-        uint32_t tph = 0;
+        int tb = 0, rb = 0;
+        uint32_t tph = 0, rph = 0;
         const uint32_t issue = lane == 0;
-        const uint32_t tf_full_leader = CG == 2 ? mapa_shared(smem_u32(&tf_full[0]), 0) : smem_u32(&tf_full[0]);
+        const uint32_t rw_full_leader = CG == 2 ? mapa_shared(smem_u32(&rw_full[0]), 0) : smem_u32(&rw_full[0]);
+        const bool raw_role = warp == 0;
         for (int w = cluster_id; w < p.nwork; w += nclusters) {
             const FzBox bx = fz_box(p, (w / p.ntile_n) * CG + (int)rank);
             for (int s = 0; s < p.nseg; ++s) {
                 const FzSeg &sg = p.seg[s];
                 const int nch = (sg.c + 63) >> 6;
+                if (raw_role == (sg.transform != 0)) continue;   // the other producer's segment
                 for (int ch = 0; ch < nch; ++ch) {
-                    mbar_wait(&tf_empty[tb], tph ^ 1);
-                    const uint32_t slot = smem_u32(sTf + tb * FZ_SLOT);
-                    if (!sg.transform) {
+                    if (!sg.transform) {   // raw ring
+                        FZ_TIMED(0, mbar_wait(&rw_empty[rb], rph ^ 1));
                         if (issue) {
-                            const uint32_t fb = tf_full_leader + (uint32_t)(tb * 8);
+                            const uint32_t fb = rw_full_leader + (uint32_t)(rb * 8);
+                            const uint32_t dst = smem_u32(sRaw + rb * FZ_RAW_SLOT);
                             if constexpr (CG == 1) {
-                                mbar_arrive_expect_tx_addr(fb, 128 * 128);
-                                tma_load_4d(slot, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
+                                mbar_arrive_expect_tx_addr(fb, FZ_RAW_SLOT);
+                                tma_load_4d(dst, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
                             } else {
-                                mbar_arrive_expect_tx_cluster(fb, 128 * 128);
-                                tma_load_4d_cg2(slot, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
+                                mbar_arrive_expect_tx_cluster(fb, FZ_RAW_SLOT);
+                                tma_load_4d_cg2(dst, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
                             }
                         }
-                    } else if (issue) {
+                        __syncwarp();
+                        if (++rb == 2) {
+                            rb = 0;
+                            rph ^= 1;
+                        }
+                        continue;
+                    }
+                    FZ_TIMED(0, mbar_wait(&tf_empty[tb], tph ^ 1));
+                    const uint32_t slot = smem_u32(sTf + tb * FZ_SLOT);
+                    if (issue) {
                         const int c0 = ch * 64;
                         const int ngrp = min(8, (sg.c - c0) >> 3);
+                        const uint32_t rb = smem_u32(&raw_full[tb]);
+                        const uint32_t coef_bytes = bx.valid ? (uint32_t)ngrp * 64u : 0u;
+                        if (fz_sw_chunk(p, sg, c0)) {
+                            mbar_arrive_expect_tx_addr(rb, (uint32_t)FZ_HROWS * 128u + coef_bytes);
+                            tma_load_4d(slot, &p.wmap[s], rb, c0, bx.x0 - 1, bx.y0 - 1, bx.t);
+                            if (coef_bytes)
+                                bulk_load(slot + FZ_COEF, p.coef + (size_t)bx.t * p.cop + sg.cglob0 + c0, coef_bytes, rb);
+                            goto produced;
+                        }
+                        {
                         int nside = 0;
                         for (int g = 0; g < ngrp; ++g) {
                             const int nprev = sg.shift ? min(max(p.cs - (c0 + 8 * g), 0), 8) : 0;
                             nside += nprev > 0 && nprev < 8;
                         }
-                        const uint32_t rb = smem_u32(&raw_full[tb]);
-                        const uint32_t coef_bytes = bx.valid ? (uint32_t)ngrp * 64u : 0u;
                         mbar_arrive_expect_tx_addr(rb, (uint32_t)(ngrp + nside) * FZ_COLB + coef_bytes);
                         for (int g = 0; g < ngrp; ++g) {
                             const int cl = c0 + 8 * g;
@@ -283,6 +335,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         }
                         if (coef_bytes)
                             bulk_load(slot + FZ_COEF, p.coef + (size_t)bx.t * p.cop + sg.cglob0 + c0, coef_bytes, rb);
+                        }
+                    produced:;
                     }
                     __syncwarp();
                     if (++tb == NTF) {
@@ -305,16 +359,10 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 const FzSeg &sg = p.seg[s];
                 const int nch = (sg.c + 63) >> 6;
                 for (int ch = 0; ch < nch; ++ch) {
-                    if (!sg.transform) {   // raw segment: the producer's TMA completes tf_full itself
-                        if (++tb == NTF) {
-                            tb = 0;
-                            tph ^= 1;
-                        }
-                        continue;
-                    }
+                    if (!sg.transform) continue;   // raw segments use their own ring
                     const int cl = ch * 64 + kg * 8;   // first channel (segment-local) of this warp
                     uint8_t *slot = sTf + tb * FZ_SLOT;
-                    mbar_wait(&raw_full[tb], (rph >> tb) & 1u);
+                    FZ_TIMED(0, mbar_wait(&raw_full[tb], (rph >> tb) & 1u));
                     rph ^= 1u << tb;
                     if (cl < sg.c) {   // warp-uniform; groups past the segment are never read by the MMA
                         // GN affine of frame t for the 8 channels, z = v*sc + sh, and the same affine
@@ -341,40 +389,65 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         uint32_t msk[4];
 #pragma unroll
                         for (int j = 0; j < 4; ++j) msk[j] = 2 * j < nprev ? 0xFFFFFFFFu : 0u;
-                        uint8_t *col = slot + kg * FZ_LBO;
-                        constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane
+                        // row r of this warp's 8 channels: SW128 chunk -> 16-byte unit kg ^ (r & 7) of the
+                        // 128-byte row r (the TMA swizzle); else row r of core-matrix column kg
+                        const bool sw = fz_sw_chunk(p, sg, ch * 64);
+                        auto roff = [&](int r) -> int { return sw ? r * 128 + ((kg ^ (r & 7)) << 4) : kg * FZ_LBO + r * 16; };
+                        constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane (the last one partial)
+                        // all rows' words first (independent shared loads in flight), then two rows
+                        // (16 independent ex2 / rcp chains) per step
+                        uint32_t wv[NR][4];
 #pragma unroll
                         for (int k = 0; k < NR; ++k) {
                             const int r = lane + 32 * k;
-                            if (r >= FZ_HROWS) break;
-                            const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
-                            const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
-                            // conv zero padding applies AFTER the transform (H3): out of frame -> 0
-                            const bool live = bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
-                            uint4 cu = *reinterpret_cast<const uint4 *>(col + r * 16);
-                            if (straddle) {
-                                const uint4 pv = *reinterpret_cast<const uint4 *>(slot + FZ_SIDE + r * 16);
-                                cu.x = (pv.x & msk[0]) | (cu.x & ~msk[0]);
-                                cu.y = (pv.y & msk[1]) | (cu.y & ~msk[1]);
-                                cu.z = (pv.z & msk[2]) | (cu.z & ~msk[2]);
-                                cu.w = (pv.w & msk[3]) | (cu.w & ~msk[3]);
+                            uint4 cu = make_uint4(0, 0, 0, 0);
+                            if (r < FZ_HROWS) {
+                                cu = *reinterpret_cast<const uint4 *>(slot + roff(r));
+                                if (straddle) {
+                                    const uint4 pv = *reinterpret_cast<const uint4 *>(slot + FZ_SIDE + r * 16);
+                                    cu.x = (pv.x & msk[0]) | (cu.x & ~msk[0]);
+                                    cu.y = (pv.y & msk[1]) | (cu.y & ~msk[1]);
+                                    cu.z = (pv.z & msk[2]) | (cu.z & ~msk[2]);
+                                    cu.w = (pv.w & msk[3]) | (cu.w & ~msk[3]);
+                                }
                             }
-                            const uint32_t wc[4] = {cu.x, cu.y, cu.z, cu.w};
-                            uint32_t o[4];
+                            wv[k][0] = cu.x, wv[k][1] = cu.y, wv[k][2] = cu.z, wv[k][3] = cu.w;
+                        }
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                float v0, v1;
-                                Pk<T>::unpack(wc[j], v0, v1);
-                                const float h0 = fz_silu_pre(fmaf(v0, sc[2 * j], sh[2 * j]), fmaf(v0, sc2[2 * j], sh2[2 * j]));
-                                const float h1 = fz_silu_pre(fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]),
-                                                             fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
-                                o[j] = live ? Pk<T>::pack(h0, h1) : 0u;
+                        for (int k0 = 0; k0 < NR; k0 += 2) {
+                            float z[2][8], e[2][8];
+#pragma unroll
+                            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    float v0, v1;
+                                    Pk<T>::unpack(wv[k0 + k][j], v0, v1);
+                                    z[k][2 * j] = fmaf(v0, sc[2 * j], sh[2 * j]);
+                                    z[k][2 * j + 1] = fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]);
+                                    e[k][2 * j] = fz_ex2(fmaf(v0, sc2[2 * j], sh2[2 * j]));
+                                    e[k][2 * j + 1] = fz_ex2(fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
+                                }
+#pragma unroll
+                            for (int k = 0; k < 2; ++k) {
+                                const int r = lane + 32 * (k0 + k);
+                                if (r >= FZ_HROWS) continue;
+                                const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
+                                const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
+                                // conv zero padding applies AFTER the transform (H3): out of frame -> 0
+                                const bool live = bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
+                                uint32_t o[4];
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const float h0 = z[k][2 * j] * fz_rcp(1.0f + e[k][2 * j]);
+                                    const float h1 = z[k][2 * j + 1] * fz_rcp(1.0f + e[k][2 * j + 1]);
+                                    o[j] = live ? Pk<T>::pack(h0, h1) : 0u;
+                                }
+                                *reinterpret_cast<uint4 *>(slot + roff(r)) = make_uint4(o[0], o[1], o[2], o[3]);
                             }
-                            *reinterpret_cast<uint4 *>(col + r * 16) = make_uint4(o[0], o[1], o[2], o[3]);
                         }
                     }
-                    fence_proxy_async();   // generic-proxy smem writes -> visible to the tensor core
-                    asm volatile("bar.sync 2, 256;" ::: "memory");   // the 8 transform warps
+                    FZ_TIMED(2, fence_proxy_async());   // generic-proxy smem writes -> visible to the tensor core
+                    FZ_TIMED(1, asm volatile("bar.sync 2, 256;" ::: "memory"));   // the 8 transform warps
                     if (warp == 8 && elect_one()) {
                         if constexpr (CG == 1)
                             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tf_full[tb]))
@@ -393,44 +466,79 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         // ===================== MMA issuer (leader CTA) =====================
         // converged warp; mma_stage() elects the issuing lane inside its asm
         if (rank == 0) {
-            int bs = 0, tb = 0, it = 0;
-            uint32_t bph = 0, tph = 0;
+            int bs = 0, tb = 0, rb = 0, it = 0;
+            uint32_t bph = 0, tph = 0, rph = 0;
+            const uint32_t rwfull0 = smem_u32(rw_full), rwempty0 = smem_u32(rw_empty), sR0 = smem_u32(sRaw);
             const uint32_t bfull0 = smem_u32(b_full), bempty0 = smem_u32(b_empty);
             const uint32_t tffull0 = smem_u32(tf_full), tfempty0 = smem_u32(tf_empty);
             const uint32_t b_lo0 = desc_lo(smem_u32(sB), 16), sT0 = smem_u32(sTf);
+            const uint32_t b_inc = (uint32_t)(B_STAGE >> 4);
+            uint32_t b_lo = b_lo0;   // descriptor word of weight stage bs
             for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
                 const int buf = it & 1;
                 const uint32_t use = (uint32_t)(it >> 1) & 1;
-                mbar_wait_spin(&tempty[buf], use ^ 1);
+                FZ_TIMED(0, mbar_wait_spin(&tempty[buf], use ^ 1));
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(buf * BN);
                 uint32_t acc = 0;
                 for (int s = 0; s < p.nseg; ++s) {
                     const FzSeg &sg = p.seg[s];
-                    const int nch = (sg.c + 63) >> 6, taps = sg.taps;
+                    const int nch = (sg.c + 63) >> 6;
                     const uint32_t klast = (uint32_t)(sg.c - 64 * (nch - 1)) >> 4;
                     // transformed tile: K step of 16 channels = two 8-channel core-matrix columns of
                     // the halo layout (no swizzle); raw segment: the TMA box in SW128
                     const bool tf = sg.transform != 0;
-                    const uint32_t a_hi = tf ? desc_hi_noswz(FZ_SBO) : kDescHiSw128;
-                    const uint32_t a_step = tf ? (uint32_t)(2 * FZ_LBO) >> 4 : 2u;
-                    const uint32_t a_lbo = tf ? (uint32_t)FZ_LBO : 16u;
                     for (int ch = 0; ch < nch; ++ch) {
                         const uint32_t ks = ch == nch - 1 ? klast : 4u;
-                        mbar_wait_spin_addr(tffull0 + 8 * tb, tph);
-                        tc_fence_after();
-                        const uint32_t a_base = sT0 + (uint32_t)(tb * FZ_SLOT);
-                        for (int tap = 0; tap < taps; ++tap) {
-                            const int dy = taps == 9 ? tap / 3 - 1 : 0, dx = taps == 9 ? tap % 3 - 1 : 0;
-                            const uint32_t a0 = tf ? a_base + (uint32_t)(((1 + dy) * FZ_HX + (1 + dx)) * 16) : a_base;
-                            mbar_wait_spin_addr(bfull0 + 8 * bs, bph);
+                        if (!tf) {   // raw 1x1 chunk from the raw ring (SW128 box): one tap
+                            FZ_TIMED(1, mbar_wait_spin_addr(rwfull0 + 8 * rb, rph));
                             tc_fence_after();
-                            mma_stage<CG>(d, desc_lo(a0, a_lbo), a_hi, a_step, b_lo0 + (uint32_t)(bs * (B_STAGE >> 4)),
+                            FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
+                            tc_fence_after();
+                            mma_stage<CG>(d, desc_lo(sR0 + (uint32_t)(rb * FZ_RAW_SLOT), 16), kDescHiSw128, 2u, b_lo,
                                           kDescHiSw128, p.idesc, ks, acc, bempty0 + 8 * bs);
                             acc = 1;
+                            commit_elected<CG>(rwempty0 + 8 * rb);
+                            b_lo += b_inc;
                             if (++bs == FZ_BSTAGES) {
                                 bs = 0;
                                 bph ^= 1;
+                                b_lo = b_lo0;
+                            }
+                            if (++rb == 2) {
+                                rb = 0;
+                                rph ^= 1;
+                            }
+                            continue;
+                        }
+                        FZ_TIMED(1, mbar_wait_spin_addr(tffull0 + 8 * tb, tph));
+                        tc_fence_after();
+                        // transformed tile (no swizzle, 8-channel core-matrix columns FZ_LBO apart, image
+                        // rows FZ_SBO apart): tap (dy, dx) starts (1+dy)*10 + (1+dx) halo rows in; a K step
+                        // of 16 channels = two core-matrix columns
+                        // SW128 chunk: rows of 128 B, image rows FZ_HX * 128 B apart, tap offset in
+                        // whole rows, K step +32 B
+                        const bool sw = fz_sw_chunk(p, sg, ch * 64);
+                        const uint32_t a_base = sT0 + (uint32_t)(tb * FZ_SLOT);
+                        const uint32_t a_lo0 = sw ? desc_lo(a_base, 16) : desc_lo(a_base, FZ_LBO);
+                        const uint32_t a_hi = sw ? desc_hi_sw128(FZ_HX * 128) : desc_hi_noswz(FZ_SBO);
+                        const uint32_t a_step = sw ? 2u : (uint32_t)(2 * FZ_LBO) >> 4;
+                        const uint32_t a_row = sw ? 8u : 1u;   // one halo row in 16-byte units
+#pragma unroll
+                        for (int tap = 0; tap < 9; ++tap) {
+                            FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
+                            tc_fence_after();
+                            const uint32_t roff16 = (uint32_t)((tap / 3) * FZ_HX + tap % 3) * a_row;
+                            // optional matrix base offset (bits 49-51): the 1024-B pattern phase of the start
+                            const uint32_t bo = sw && p.sw_mode == 2 ? (((a_base >> 7) + roff16 / 8) & 7u) << 17 : 0u;
+                            mma_stage<CG>(d, a_lo0 + roff16, a_hi | bo, a_step, b_lo, kDescHiSw128, p.idesc, ks, acc,
+                                          bempty0 + 8 * bs);
+                            acc = 1;
+                            b_lo += b_inc;
+                            if (++bs == FZ_BSTAGES) {
+                                bs = 0;
+                                bph ^= 1;
+                                b_lo = b_lo0;
                             }
                         }
                         commit_elected<CG>(tfempty0 + 8 * tb);   // the tile slot is free once its taps retire
@@ -450,21 +558,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         const int by = r / FZ_BX, bxp = r - by * FZ_BX;
         const float *sb0 = p.bias0 ? sbias : nullptr;
         const float *sb1 = p.bias1 ? sbias + p.cout : nullptr;
-        const T *res = reinterpret_cast<const T *>(p.residual);
         T *out = reinterpret_cast<T *>(p.out);
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
-        // residual tile of box w via TMA (coalesced, latency hidden behind the mainloop)
-        auto load_res = [&](int w) {
-            if (res && w < p.nwork && q4 == 0 && elect_one()) {
-                const int qq = w / p.ntile_n, ntt = w - qq * p.ntile_n;
-                const FzBox bb = fz_box(p, qq * CG + (int)rank);
-                const uint32_t fb = smem_u32(res_full);
-                mbar_arrive_expect_tx_addr(fb, (uint32_t)(128 * BN * 2));
-                tma_load_4d(smem_u32(sRes), &p.rmap, fb, ntt * BN, bb.x0, bb.y0, bb.t);
-            }
-            __syncwarp();
-        };
-        load_res(cluster_id);
         int it = 0;
         for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
             const int buf = it & 1;
@@ -477,14 +572,14 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 const int y = bx.y0 + by, x = bx.x0 + bxp;
                 if (y < p.H && x < p.W) m = ((long)bx.t * p.H + y) * p.W + x;
             }
-            if (res) mbar_wait(res_full, (uint32_t)it & 1);
-            mbar_wait(&tfull[buf], use);
+            FZ_TIMED(1, mbar_wait(&tfull[buf], use));
             tc_fence_after();
             const bool want_stats = p.stats != nullptr && bx.valid;
-            // one 16-column chunk: + bias (fp32, shared memory) + residual (staged tile), 16-bit
-            // store, box statistics of the stored values
-            auto chunk = [&](const uint32_t (&v)[16], int cc, int par) {
-                const int n = nt * BN + cc;
+            const int per = p.tiles_x * p.tiles_y;
+            float *stats_box = want_stats ? p.stats + ((size_t)bx.t * per + (box - bx.t * per)) * p.cout * 2 : nullptr;
+            // one 16-column chunk: + bias (fp32, shared memory), 16-bit store; returns (in x) this
+            // row's statistics contribution of the stored values
+            auto chunk = [&](const uint32_t (&v)[16], int n, float (&x)[32]) {
                 float f[16];
                 if (m >= 0) {
 #pragma unroll
@@ -503,15 +598,6 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                             f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
                         }
                     }
-                    if (res) {   // from the TMA-staged residual tile (row r of the box)
-                        const Vec8<T> *rr = reinterpret_cast<const Vec8<T> *>(sRes + ((size_t)r * BN + cc) * 2);
-                        const Vec8<T> ra = rr[0], rb = rr[1];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            f[i] += Elem<T>::to_f(ra.v[i]);
-                            f[8 + i] += Elem<T>::to_f(rb.v[i]);
-                        }
-                    }
                     Vec8<T> lo, hi;
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
@@ -523,35 +609,36 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                     *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n) = lo;
                     *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n + 8) = hi;
                 }
+                if (want_stats) box_row_values(f, m >= 0, x);
+            };
+            // TMEM -> registers 32 columns at a time (two 16-column loads in flight); the box
+            // statistics of both chunks are reduced together (two independent butterflies, one
+            // barrier per 32 columns) and combined by warps 0 / 1 (canonical order, dvc_boxstats.cuh)
+            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
+            int par = 0;
+#pragma unroll 1
+            for (int cc = 0; cc < BN; cc += 32, par ^= 1) {
+                const bool two = cc + 16 < BN;   // warp-uniform
+                uint32_t va[16], vb[16];
+                tmem_ld16_nowait(taddr + (uint32_t)cc, va);
+                if (two) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
+                tmem_wait16(va);
+                float *rr = red + par * 256;   // [2 chunks][4 warps][32]
+                float x[32];
+                chunk(va, nt * BN + cc, x);
+                if (want_stats) rr[q4 * 32 + lane] = box_reduce_scatter32(x, lane);
+                if (two) {
+                    tmem_wait16(vb);
+                    chunk(vb, nt * BN + cc + 16, x);
+                    if (want_stats) rr[128 + q4 * 32 + lane] = box_reduce_scatter32(x, lane);
+                }
                 if (want_stats) {
-                    float x[32];
-                    box_row_values(f, m >= 0, x);
-                    red[(par * 4 + q4) * 32 + lane] = box_reduce_scatter32(x, lane);
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (q4 == 0) {
-                        const int per = p.tiles_x * p.tiles_y;
-                        const int bi = box - bx.t * per;
-                        const float val = box_combine4(red + par * 128, lane);
-                        p.stats[(((size_t)bx.t * per + bi) * p.cout + n + (lane & 15)) * 2 + (lane >> 4)] = val;
+                    FZ_TIMED(2, asm volatile("bar.sync 1, 128;" ::: "memory"));
+                    if (q4 < (two ? 2 : 1)) {
+                        const int n = nt * BN + cc + 16 * q4;
+                        stats_box[(n + (lane & 15)) * 2 + (lane >> 4)] = box_combine4(rr + q4 * 128, lane);
                     }
                 }
-            };
-            // TMEM -> registers two chunks at a time: the next chunk's tcgen05.ld is in flight
-            // while the current one is processed
-            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
-            uint32_t va[16], vb[16];
-            tmem_ld16_nowait(taddr, va);
-            tmem_wait16(va);
-#pragma unroll 1
-            for (int cc = 0; cc < BN; cc += 32) {
-                const bool more = cc + 16 < BN;
-                if (more) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
-                chunk(va, cc, 0);
-                if (!more) break;
-                tmem_wait16(vb);
-                if (cc + 32 < BN) tmem_ld16_nowait(taddr + (uint32_t)(cc + 32), va);
-                chunk(vb, cc + 16, 1);
-                if (cc + 32 < BN) tmem_wait16(va);
             }
             tc_fence_before();
             __syncwarp();
@@ -561,11 +648,16 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                                                     : "memory");
                 else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
             }
-            if (res) {   // all 4 warps are done with the residual tile: fetch the next one
-                asm volatile("bar.sync 3, 128;" ::: "memory");
-                load_res(w + nclusters);
-            }
         }
+    }
+#undef FZ_TIMED
+    if constexpr (PROF) {
+        const int role = warp == 1 ? 0 : warp == 4 ? 1 : warp == 8 ? 2 : warp == 3 ? 3 : warp == 2 ? 4 : -1;
+        if (role >= 0 && lane == 0 && !(role == 0 && rank != 0)) {
+            pacc[3] = clock64() - tstart;
+            for (int i = 0; i < 4; ++i) atomicAdd(p.prof + role * 4 + i, pacc[i]);
+        }
+        if (tid == 0) atomicAdd(p.prof + 20, 1ull);
     }
     tc_fence_before();
     __syncthreads();
@@ -589,24 +681,27 @@ static int g_fz_sms = 0;
 
 // 8-channel halo box {8, 10, 18, 1} of a [T][H][W][C] tensor, no swizzle: lands as one 180-row
 // core-matrix column of the UMMA tile; out-of-bounds rows (and frames) are zero-filled
-static dvc_status make_halo_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C) {
+static dvc_status make_halo_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C,
+                                 int box_c = 8) {
     PFN_encodeTiled_t enc = get_encode_fn();
     DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && C % 8 == 0, DVC_ERR_ARG, "fused conv: halo source alignment");
     cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
     cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {8, (cuuint32_t)FZ_HX, (cuuint32_t)FZ_HY, 1};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)FZ_HX, (cuuint32_t)FZ_HY, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
                      const_cast<void *>(ptr), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     box_c == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     box_c == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (halo) failed (%d)", (int)r);
     return DVC_OK;
 }
 
 dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
-    DVC_CHECK_ARG(d.nseg >= 1 && d.nseg <= 4 && d.T >= 1 && d.T < 256 && d.cout % 16 == 0, DVC_ERR_UNSUPPORTED,
-                  "fused conv: bad descriptor");
+    DVC_CHECK_ARG(d.nseg >= 1 && d.nseg <= 4 && d.T >= 1 && d.T < 256 && d.cout % 16 == 0 && d.residual == nullptr,
+                  DVC_ERR_UNSUPPORTED, "fused conv: bad descriptor (identity skips are 1x1 segments, not residuals)");
     FzParams p;
     memset(&p, 0, sizeof(p));
     constexpr int CG = 2;
@@ -632,9 +727,9 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     p.nwork = ((p.nbox + CG - 1) / CG) * p.ntile_n;
     p.bias0 = d.bias0;
     p.bias1 = d.bias1;
-    p.residual = d.residual;
     p.out = d.out;
     p.stats = reinterpret_cast<float *>(d.stats_out);
+    if (getenv("DVC_FZ_XNOSTATS")) p.stats = nullptr;   // timing experiment only: results are wrong
     p.coef = reinterpret_cast<const float2 *>(d.coef);
     DVC_CHECK_ARG(((uintptr_t)d.coef & 15) == 0 && d.cop % 2 == 0, DVC_ERR_ARG, "fused conv: coefficient alignment");
     p.cop = d.cop;
@@ -676,7 +771,9 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
             DVC_CHECK_ARG(g.taps == 1, DVC_ERR_UNSUPPORTED, "fused conv: raw segments are 1x1");
             st = make_box_map(&p.smap[s], g.src, d.dt, d.T, d.H, d.W, g.c, FZ_BX, FZ_BY);
         } else {
+            DVC_CHECK_ARG(g.taps == 9, DVC_ERR_UNSUPPORTED, "fused conv: transformed segments are 3x3");
             st = make_halo_map(&p.hmap[s], g.src, d.dt, d.T, d.H, d.W, g.c);
+            if (st == DVC_OK) st = make_halo_map(&p.wmap[s], g.src, d.dt, d.T, d.H, d.W, g.c, 64);
         }
         if (st != DVC_OK) return st;
     }
@@ -684,28 +781,23 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         st = make_halo_map(&p.cmap, d.carry_pad, d.dt, 1, d.H, d.W, d.cs_pad);
         if (st != DVC_OK) return st;
     }
-    if (d.residual) {
-        PFN_encodeTiled_t enc = get_encode_fn();
-        DVC_CHECK_ARG(enc != nullptr && ((uintptr_t)d.residual & 15) == 0, DVC_ERR_ARG, "fused conv: residual map");
-        cuuint64_t gdim[4] = {(cuuint64_t)d.cout, (cuuint64_t)d.W, (cuuint64_t)d.H, (cuuint64_t)d.T};
-        cuuint64_t gstride[3] = {(cuuint64_t)d.cout * 2, (cuuint64_t)d.W * d.cout * 2, (cuuint64_t)d.H * d.W * d.cout * 2};
-        cuuint32_t box[4] = {(cuuint32_t)bn, (cuuint32_t)FZ_BX, (cuuint32_t)FZ_BY, 1};
-        cuuint32_t estr[4] = {1, 1, 1, 1};
-        CUresult r = enc(&p.rmap, d.dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                         4, const_cast<void *>(d.residual), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (residual) failed (%d)", (int)r);
-    }
     p.idesc = make_idesc(d.dt == DVC_BF16, 128 * CG, bn);
+    {
+        static const int sw_env = getenv("DVC_FZ_SW") ? atoi(getenv("DVC_FZ_SW")) : 1;
+        p.sw_mode = sw_env;
+    }
     // shared memory: tile slots, weight stages, residual tile; fill the 227 KB budget with weight stages
     {
         const char *e = getenv("DVC_FZ_NTF");
-        p.ntf = e ? atoi(e) : (d.residual ? 2 : 4);
-        if (p.ntf < 2 || p.ntf > 4) p.ntf = 2;
+        p.ntf = e ? atoi(e) : 4;
+        if (p.ntf < 2 || p.ntf > FZ_MAX_NTF) p.ntf = 4;
     }
-    const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (d.residual ? (size_t)128 * bn * 2 : 0) + 8 * (17 + 2 * FZ_MAX_BSTAGES) +
-                         16 + 1024 + 1024 /* static */ + (size_t)2 * d.cout * 4 /* bias */;
+    p.nraw = 0;
+    for (int s = 0; s < d.nseg; ++s)
+        if (!d.seg[s].transform) p.nraw = 2;
+    const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (size_t)p.nraw * FZ_RAW_SLOT + 8 * (8 + 3 * FZ_MAX_NTF + 2 * FZ_MAX_BSTAGES) +
+                         16 + 2048 /* red */ +
+                         1024 /* static */ + 16 + (size_t)2 * d.cout * 4 /* bias */;
     const size_t bstage = (size_t)(bn / CG) * 128;
     int nbst = (int)((227 * 1024 - fixed) / bstage);
     {
@@ -716,7 +808,15 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     DVC_CHECK_ARG(nbst >= 2, DVC_ERR_UNSUPPORTED, "fused conv: shared memory too small");
     p.nb = nbst;
     const size_t smem = fixed - 1024 + (size_t)nbst * bstage;
-    auto kern = d.dt == DVC_BF16 ? conv_fz_kernel<__nv_bfloat16, 2> : conv_fz_kernel<__half, 2>;
+    static const bool prof = getenv("DVC_FZ_PROF") != nullptr && atoi(getenv("DVC_FZ_PROF")) != 0;
+    static unsigned long long *prof_buf = nullptr;
+    if (prof) {
+        if (!prof_buf) DVC_CUDA(cudaMalloc(&prof_buf, 24 * sizeof(unsigned long long)));
+        DVC_CUDA(cudaMemsetAsync(prof_buf, 0, 24 * sizeof(unsigned long long), stream));
+        p.prof = prof_buf;
+    }
+    auto kern = d.dt == DVC_BF16 ? (prof ? conv_fz_kernel<__nv_bfloat16, 2, true> : conv_fz_kernel<__nv_bfloat16, 2, false>)
+                                 : (prof ? conv_fz_kernel<__half, 2, true> : conv_fz_kernel<__half, 2, false>);
     if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (g_fz_sms == 0) {
@@ -740,6 +840,19 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     cfg.numAttrs = 1;
     DVC_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
     ++g_launches;
+    if (prof) {   // diagnostics: per-role wait / total cycles averaged over CTAs (stderr)
+        unsigned long long h[24];
+        DVC_CUDA(cudaMemcpyAsync(h, prof_buf, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        DVC_CUDA(cudaStreamSynchronize(stream));
+        const double n = (double)(h[20] ? h[20] : 1), nl = n / CG;
+        fprintf(stderr,
+                "fzprof T=%d %dx%d K=%d N=%d segs=%d | mma(leader) tempty %.0f tffull %.0f bfull %.0f tot %.0f | "
+                "epi resfull %.0f tfull %.0f statbar %.0f tot %.0f | tf rawfull %.0f bar %.0f fence %.0f tot %.0f | "
+                "prod tfempty %.0f tot %.0f | bprod bempty %.0f tot %.0f\n",
+                d.T, d.H, d.W, 0, d.cout, d.nseg, h[0] / nl, h[1] / nl, h[2] / nl, h[3] / nl,
+                h[4] / n, h[5] / n, h[6] / n, h[7] / n, h[8] / n, h[9] / n, h[10] / n, h[11] / n, h[12] / n, h[15] / n, h[16] / n,
+                h[19] / n);
+    }
     return check_launch("conv_fz_kernel");
 }
 

@@ -52,7 +52,9 @@ __device__ __forceinline__ int pack_row(long m, int ho, int wo) {
 template <typename T, int NACC, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ TcParams p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-aligned, derived from smem_raw by pointer arithmetic so the compiler keeps the
+    // shared address space (an integer round trip would turn every access generic)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int BN = p.bn;
     constexpr int A_TILE = 128 * 128;          // bytes per 128-row x 64-ch tile
     constexpr int A_STAGE = NACC * A_TILE;

@@ -45,7 +45,9 @@ constexpr int kWsThreads = 256;
 template <typename T, int CG, int STAGES>
 __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_constant__ WsParams p) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-aligned, derived from smem_raw by pointer arithmetic so the compiler keeps the
+    // shared address space (an integer round trip would turn every access generic)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int BN = p.bn, BNH = p.bn / CG;
     constexpr int A_STAGE = 128 * 128;
     const int B_STAGE = BNH * 128;

@@ -264,6 +264,9 @@ __host__ __device__ constexpr uint32_t desc_lo(uint32_t saddr, uint32_t lbo_byte
 __host__ __device__ constexpr uint32_t desc_hi_noswz(uint32_t sbo_bytes) {
     return ((sbo_bytes >> 4) & 0x3FFFu) | (1u << 14);
 }
+__host__ __device__ constexpr uint32_t desc_hi_sw128(uint32_t sbo_bytes) {
+    return ((sbo_bytes >> 4) & 0x3FFFu) | (1u << 14) | (2u << 29);
+}
 
 #define DVC_MMA_STAGE_ASM(CGS)                                                         \
     "{\n\t.reg .pred e, q, acc, one;\n\t.reg .b32 al, bl;\n\t.reg .b64 ad, bd;\n\t"    \
