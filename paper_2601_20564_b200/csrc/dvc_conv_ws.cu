@@ -30,7 +30,8 @@ struct WsParams {
     CUtensorMap amap[4];   // per segment: 4D {C, W, H, T}, box {64, BX, BY, 1}, SW128, OOB zero
     CUtensorMap bmap[2];   // weights 2D {K, C_out}, box {64, BN/CG}, SW128
     int bidx[4], seg_c[4], seg_taps[4], seg_col0[4], seg_tapstride[4], seg_packed[4];
-    int seg_nch[4], seg_klast[4];   // 64-channel stages per tap; K=16 steps in the last one
+    int seg_nch[4], seg_klast[4];
+    int seg_stride[4];   // 1: same resolution; 2: stride-2 conv (TMA element stride 2 over the input)   // 64-channel stages per tap; K=16 steps in the last one
     int nseg;
     int T, H, W, cout, bn;
     int BX, BY, tiles_x, tiles_y, nbox, ntile_n, nwork;
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                 y0 = x0 = 0;
             }
             for (int s = 0; s < p.nseg; ++s) {
-                const int nch = p.seg_nch[s], taps = p.seg_taps[s];
+                const int nch = p.seg_nch[s], taps = p.seg_taps[s], sst = p.seg_stride[s];
                 const CUtensorMap *am = &p.amap[s];
                 const CUtensorMap *bm = &p.bmap[p.bidx[s]];
                 const bool packed = p.seg_packed[s] != 0;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         mbar_wait_spin_addr(empty0 + 8 * stage, phase ^ 1);
                         const uint32_t lb = CG == 2 ? lead_full0 + 8 * stage : full0 + 8 * stage;
                         mbar_expect_tx_if(expect, full0 + 8 * stage, tx);
-                        tma_load_4d_if<CG>(issue, sA0 + stage * A_STAGE, am, lb, ch * 64, x0 + dx, y0 + dy, t);
+                        tma_load_4d_if<CG>(issue, sA0 + stage * A_STAGE, am, lb, ch * 64, sst * x0 + dx, sst * y0 + dy, t);
                         tma_load_2d_if<CG>(issue, sB0 + stage * B_STAGE, bm, lb, bc0 + ch * bcs, br0 + ch * brs);
                         if (++stage == STAGES) {
                             stage = 0;
@@ -284,9 +285,23 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
 PFN_encodeTiled_t get_encode_fn();
 
 dvc_status make_box_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX, int BY);
+// box {64, BX, BY} of output pixels over a [T][H][W][C] input; stride 2: the TMA walks the input
+// with element stride 2 (box {64, 2 BX, 2 BY}, every other pixel), i.e. the stride-2 conv's taps
 static dvc_status make_amap(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX,
-                            int BY) {
-    return make_box_map(map, ptr, dt, T, H, W, C, BX, BY);
+                            int BY, int stride) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && (C * 2) % 16 == 0 && (stride == 1 || stride == 2), DVC_ERR_ARG,
+                  "activation must be 16-byte aligned");
+    cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
+    cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)(BX * stride), (cuuint32_t)(BY * stride), 1};
+    cuuint32_t estr[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+    CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                     const_cast<void *>(ptr), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (activation) failed (%d)", (int)r);
+    return DVC_OK;
 }
 dvc_status make_box_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX, int BY) {
     PFN_encodeTiled_t enc = get_encode_fn();
@@ -369,8 +384,13 @@ int g_ws_cg = engine_from_env();   // 2: CTA-pair MMA (default), 1: single-CTA M
 
 bool conv_ws_applicable(const ConvDesc &d) {
     if (g_ws_cg == 0 || d.dt == DVC_F32) return false;
-    for (int s = 0; s < d.nseg; ++s)
-        if (d.seg[s].mode != SEG_SAME || d.seg[s].hi != d.ho || d.seg[s].wi != d.wo) return false;
+    for (int s = 0; s < d.nseg; ++s) {
+        const ConvSeg &g = d.seg[s];
+        const bool same = g.mode == SEG_SAME && g.hi == d.ho && g.wi == d.wo;
+        // 3x3 / stride 2 / pad 1: ho = ceil(hi / 2)
+        const bool down = g.mode == SEG_STRIDE2 && g.taps == 9 && (g.hi + 1) / 2 == d.ho && (g.wi + 1) / 2 == d.wo;
+        if (!same && !down) return false;
+    }
     return true;
 }
 
@@ -410,7 +430,8 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
     const void *bw[2] = {nullptr, nullptr};
     for (int s = 0; s < d.nseg; ++s) {
         const ConvSeg &g = d.seg[s];
-        st = make_amap(&p.amap[s], g.src, d.dt, d.T, d.ho, d.wo, g.c_src, p.BX, p.BY);
+        p.seg_stride[s] = g.mode == SEG_STRIDE2 ? 2 : 1;
+        st = make_amap(&p.amap[s], g.src, d.dt, d.T, g.hi, g.wi, g.c_src, p.BX, p.BY, p.seg_stride[s]);
         if (st != DVC_OK) return st;
         int idx = -1;
         for (int k = 0; k < nb; ++k)
