@@ -377,7 +377,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None if traffic is None else traffic.get("bytes_per_step"),
-                     "kernel": "conv_ws_kernel + conv_tc_kernel (all convolution launches of the step, summed)",
+                     "kernel": "conv_fz_kernel + conv_ws_kernel + conv_tc_kernel (all convolution launches of the step, summed)",
                      "conv_ms_per_step": conv_ms / args.steps, "conv_launches_per_step": conv_n / args.steps,
                      "conv_share_of_step": conv_ms / ms, "peak_source": peak_src},
         "clocks": clk.summary(),

@@ -100,7 +100,6 @@ __device__ __forceinline__ float fz_rcp(float d) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
     return r;
 }
-// two 16-bit elements in one 32-bit word (element 2j in the low half)
 // an unshifted transform chunk is one SW128 halo box {64, 10, 18} (rows of 128 B); chunks holding
 // shifted channels keep the 8-channel no-swizzle columns (per-group source selection)
 __device__ __forceinline__ bool fz_sw_chunk(const FzParams &p, const FzSeg &sg, int c0) {

@@ -56,32 +56,41 @@ json.dump({"bytes_per_step": conv_bytes, "conv_ns_per_step_ncu": conv_ns,
            "source": f"profiles/{rnd}_launches.txt (sum of dram__bytes_read+write over all conv launches of one step)"},
           open("profiles/traffic.json", "w"), indent=1)
 
-# ---- full capture of the conv kernel
-rep = f"{G}/prof_convws_{tag}.ncu-rep"
-if os.path.exists(rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    r = list(csv.reader(raw.splitlines()))
-    h = r[0]
-    keep = ("Duration", "SM Frequency", "DRAM Throughput", "Memory Throughput", "L2 Cache Throughput", "L1/TEX Cache Throughput",
-            "Compute (SM) Throughput", "Registers Per Thread", "Grid Size", "Block Size", "Dynamic Shared Memory Per Block",
-            "Achieved Occupancy", "L2 Hit Rate", "Issue Slots Busy")
-    with open(f"profiles/{rnd}_conv_ws_full.txt", "w") as f:
-        f.write(f"# ncu --set full --clock-control none --import-source on -k regex:conv_ws -s 0 -c 2 (launch 0 = conv_in, "
-                f"launch 1 = down0.r0 conv1, 720p T=32 bf16)\n")
-        for row in r[1:]:
-            d = dict(zip(h, row))
-            if d.get("Metric Name") in keep:
-                f.write(f"launch {d['ID']}  {d['Metric Name']:35s} {d['Metric Value']:>14s} {d['Metric Unit']}\n")
-        raw2 = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-        r2 = list(csv.reader(raw2.splitlines()))
-        for row in r2[2:]:
-            d = dict(zip(r2[0], row))
-            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-                      "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
-                      "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
-                      "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", "lts__t_bytes.sum"):
-                if m in d:
-                    f.write(f"raw {m:80s} {d[m]} {r2[1][r2[0].index(m)]}\n")
+# ---- full captures of the conv kernels
+for eng, what in (("ws", "launch 0 = conv_in, launch 1 = the first persistent-TMA ResBlock conv"),
+                  ("fz", "launch 0 = down0.r0 conv1 (fused GN/SiLU/shift), launch 1 = its conv2 (+ identity skip)")):
+  rep = f"{G}/prof_conv{eng}_{tag}.ncu-rep"
+  if os.path.exists(rep):
+      raw = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+      r = list(csv.reader(raw.splitlines()))
+      h = r[0]
+      keep = ("Duration", "SM Frequency", "DRAM Throughput", "Memory Throughput", "L2 Cache Throughput", "L1/TEX Cache Throughput",
+              "Compute (SM) Throughput", "Registers Per Thread", "Grid Size", "Block Size", "Dynamic Shared Memory Per Block",
+              "Achieved Occupancy", "L2 Hit Rate", "Issue Slots Busy")
+      with open(f"profiles/{rnd}_conv_{eng}_full.txt", "w") as f:
+          f.write(f"# ncu --set full --clock-control none --import-source on -k regex:conv_{eng} -s 0 -c 2 ({what}, "
+                  f"720p T=32 bf16)\n")
+          for row in r[1:]:
+              d = dict(zip(h, row))
+              if d.get("Metric Name") in keep:
+                  f.write(f"launch {d['ID']}  {d['Metric Name']:35s} {d['Metric Value']:>14s} {d['Metric Unit']}\n")
+          raw2 = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+          r2 = list(csv.reader(raw2.splitlines()))
+          for row in r2[2:]:
+              d = dict(zip(r2[0], row))
+              for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                        "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+                        "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum", "lts__t_bytes.sum"):
+                  if m in d:
+                      f.write(f"raw {m:80s} {d[m]} {r2[1][r2[0].index(m)]}\n")
+for extra in ("breakdown", "fzprof"):
+    src = f"{G}/{extra}_{tag}.txt"
+    if os.path.exists(src):
+        lines = open(src).read().splitlines()
+        if extra == "fzprof":
+            lines = lines[-20:]
+        open(f"profiles/{rnd}_{extra}.txt", "w").write("\n".join(lines) + "\n")
 bj = f"{G}/bench_{tag}.json"
 if os.path.exists(bj):
     line = [l for l in open(bj) if l.startswith("{")][-1]
