@@ -2,6 +2,7 @@
 // workspace carving and launch order.  No host sync and no allocation on the
 // forward path; every check happens before the first launch.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -500,6 +501,8 @@ dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype dt, int T, in
     }
     DVC_CHECK_ARG(s == 8, DVC_ERR_UNSUPPORTED, "fused expansion needs s == 8");
     DVC_CHECK_ARG(c_lat >= 16 && c_lat % 16 == 0, DVC_ERR_UNSUPPORTED, "c_lat must be a multiple of 16");
+    if (encode_tma_applicable(dt, H, W, s, c_lat) && !getenv("DVC_ENCODE_GATHER"))
+        return encode_tma_run(frames, dt, T, H, W, w_exp, b_exp, c_lat, latent, strm);
     ConvDesc d{};
     d.seg[0] = ConvSeg{frames, 192, SEG_UNSHUFFLE8, H, W, 1, w_exp, 192, 0, 0};
     d.nseg = 1;

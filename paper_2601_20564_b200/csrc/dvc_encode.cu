@@ -1,0 +1,251 @@
+// dvc_encode.cu -- a1 + a2 in one persistent tcgen05 kernel: PixelUnshuffle (s = 8) fused with the
+// Latent Channel Expansion 1x1 conv (192 -> c_lat, + bias), SURVEY a1/a2 (R12-R14).
+//
+// The unshuffle is pure TMA addressing.  The frames [T][3][H][W] are viewed as the 4D tensor
+//     (x: W, dy: 8, hb: H/8, tc: 3T)     (x fastest; strides 2 B, 2W B, 16W B, 2HW B)
+// and one box {64, 8, 16, 3} (no swizzle; 128-byte rows = 64 pixels = 8 latent columns) is the
+// 8 x 16 latent-pixel output box with all 192 unshuffled channels k = c*64 + dy*8 + dx.  With
+// x = 8 wb + dx it lands in shared memory as
+//     [c][hb][dy][wb][dx]
+// which IS the canonical K-major no-swizzle UMMA layout of the A tile: a core matrix (8 latent
+// pixels of one row x 8 consecutive k) is 128 contiguous bytes, core matrices adjacent in K (dy,
+// dy+1) are 128 B apart (LBO), adjacent in M (next latent row) 1024 B apart (SBO); channel c
+// starts 16 KB further.  So the 192-channel latent never exists in memory, and no thread touches
+// the A operand: the frames go HBM -> TMA -> tensor core.
+//
+// GEMM per tile: M = 128 latent pixels, N = c_lat (<= 256), K = 192 (12 MMAs of K = 16); the
+// expansion weights [c_lat][192] stay resident in shared memory (3 SW128 boxes).  Two TMEM
+// accumulators (2 x N fp32 columns) let the epilogue (bias, 16-bit store) of tile i overlap the
+// MMAs of tile i+1; two A stages overlap the next tile's TMA with the current tile's MMAs.
+// Warps (256 threads): 0 TMA producer, 1 TMEM allocator + MMA issuer, 4-7 epilogue.
+// HBM-bound by design: per tile 48 KB of frames in, 128 x c_lat x 2 B of latent out.
+#include <cuda.h>
+#include <cstdlib>
+#include "dvc_conv.cuh"
+#include "dvc_ptx.cuh"
+
+namespace dvc {
+
+constexpr int ENC_BX = 8, ENC_BY = 16;         // latent pixels per tile (128 MMA rows)
+constexpr int ENC_A_BYTES = 3 * 64 * 128 * 2;  // 49152: {64, 8, 16, 3} 16-bit box
+constexpr int ENC_THREADS = 256;
+
+struct EncParams {
+    CUtensorMap amap;   // 4D frames view, box {64, 8, 16, 3}, no swizzle
+    CUtensorMap bmap;   // expansion weights [c_lat][192], box {64, c_lat}, SW128
+    int T, h, w, c_lat;
+    int tiles_x, tiles_y, ntiles;
+    const void *bias;
+    void *out;          // latent [T][h][w][c_lat]
+    uint32_t idesc;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(ENC_THREADS, 1) encode_kernel(const __grid_constant__ EncParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int N = p.c_lat;
+    const int B_CHUNK = N * 128;               // one 64-column SW128 box of the weights
+    uint8_t *sA = smem;                        // [2][ENC_A_BYTES]
+    uint8_t *sB = sA + 2 * ENC_A_BYTES;        // [3][B_CHUNK]
+    uint64_t *a_full = reinterpret_cast<uint64_t *>(sB + 3 * B_CHUNK);
+    uint64_t *a_empty = a_full + 2;
+    uint64_t *tfull = a_empty + 2;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *b_full = tempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_full + 2);
+    float *sbias = reinterpret_cast<float *>(tmem_slot + 4);   // [c_lat]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t ncols = 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        mbar_init(&b_full[0], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+        tma_prefetch(&p.amap);
+        tma_prefetch(&p.bmap);
+    }
+    if (warp == 1) tmem_alloc<1>(smem_u32(tmem_slot), ncols);
+    for (int i = tid; i < N; i += ENC_THREADS) sbias[i] = Elem<T>::to_f(reinterpret_cast<const T *>(p.bias)[i]);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        const uint32_t issue = lane == 0;
+        if (issue) {
+            const uint32_t bb = smem_u32(&b_full[0]);
+            mbar_arrive_expect_tx_addr(bb, (uint32_t)(3 * B_CHUNK));
+            for (int kc = 0; kc < 3; ++kc) tma_load_2d_a(smem_u32(sB + kc * B_CHUNK), &p.bmap, bb, kc * 64, 0);
+        }
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            const int per = p.tiles_x * p.tiles_y;
+            const int t = tile / per, rem = tile - t * per;
+            const int by = rem / p.tiles_x, bx = rem - by * p.tiles_x;
+            mbar_wait_spin(&a_empty[stage], phase ^ 1);
+            if (issue) {
+                const uint32_t fb = smem_u32(&a_full[stage]);
+                mbar_arrive_expect_tx_addr(fb, ENC_A_BYTES);
+                tma_load_4d(smem_u32(sA + stage * ENC_A_BYTES), &p.amap, fb, bx * ENC_BX * 8, 0, by * ENC_BY, t * 3);
+            }
+            __syncwarp();
+            if (++stage == 2) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        mbar_wait(&b_full[0], 0);
+        tc_fence_after();
+        const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
+        int stage = 0, it = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+            const int buf = it & 1;
+            const uint32_t use = (uint32_t)(it >> 1) & 1;
+            mbar_wait_spin(&tempty[buf], use ^ 1);
+            mbar_wait_spin(&a_full[stage], phase);
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(buf * N);
+            const uint32_t a_base = sA0 + (uint32_t)(stage * ENC_A_BYTES);
+            // colour c = K block of 64: A at +16 KB per colour (K step of 16 = dy += 2 = +256 B),
+            // B = weight box c (K step = +32 B inside the swizzled 128-byte rows)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const uint32_t a_lo = desc_lo(a_base + (uint32_t)(c * 16384), 128);
+                const uint32_t b_lo = desc_lo(sB0 + (uint32_t)(c * B_CHUNK), 16);
+                if (c < 2)
+                    mma_stage_nc<1>(d, a_lo, desc_hi_noswz(1024), 16u, b_lo, kDescHiSw128, p.idesc, 4u, c ? 1u : 0u);
+                else
+                    mma_stage<1>(d, a_lo, desc_hi_noswz(1024), 16u, b_lo, kDescHiSw128, p.idesc, 4u, 1u,
+                                 smem_u32(&a_empty[stage]));
+            }
+            commit_elected<1>(smem_u32(&tfull[buf]));
+            if (++stage == 2) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ===================== epilogue: + bias, 16-bit store =====================
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;   // accumulator row = latent pixel (r / 8, r % 8) of the box
+        T *out = reinterpret_cast<T *>(p.out);
+        int it = 0;
+        for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+            const int buf = it & 1;
+            const uint32_t use = (uint32_t)(it >> 1) & 1;
+            const int per = p.tiles_x * p.tiles_y;
+            const int t = tile / per, rem = tile - t * per;
+            const int y = (rem / p.tiles_x) * ENC_BY + r / ENC_BX, x = (rem % p.tiles_x) * ENC_BX + r % ENC_BX;
+            const bool live = y < p.h && x < p.w;
+            T *orow = out + (((size_t)t * p.h + y) * p.w + x) * N;
+            mbar_wait(&tfull[buf], use);
+            tc_fence_after();
+            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * N);
+#pragma unroll 1
+            for (int cc = 0; cc < N; cc += 32) {
+                uint32_t va[16], vb[16];
+                const bool two = cc + 16 < N;
+                tmem_ld16_nowait(taddr + (uint32_t)cc, va);
+                if (two) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
+                tmem_wait16(va);
+                if (two) tmem_wait16(vb);
+                if (live) {
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        if (h2 == 1 && !two) break;
+                        const uint32_t *v = h2 ? vb : va;
+                        const int n = cc + 16 * h2;
+                        Vec8<T> lo, hi;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            lo.v[i] = Elem<T>::from_f(__uint_as_float(v[i]) + sbias[n + i]);
+                            hi.v[i] = Elem<T>::from_f(__uint_as_float(v[8 + i]) + sbias[n + 8 + i]);
+                        }
+                        *reinterpret_cast<Vec8<T> *>(orow + n) = lo;
+                        *reinterpret_cast<Vec8<T> *>(orow + n + 8) = hi;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<1>(tmem, ncols);
+    }
+}
+
+// ----------------------------------------------------------------- host side
+PFN_encodeTiled_t get_encode_fn();
+dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
+
+bool encode_tma_applicable(dvc_dtype dt, int H, int W, int s, int c_lat) {
+    return dt != DVC_F32 && s == 8 && H % 8 == 0 && W % 8 == 0 && c_lat >= 16 && c_lat <= 256 && c_lat % 16 == 0 &&
+           (W / 8) >= 1;
+}
+
+static int g_enc_sms = 0;
+
+dvc_status encode_tma_run(const void *frames, dvc_dtype dt, int T, int H, int W, const void *w_exp, const void *b_exp,
+                          int c_lat, void *latent, cudaStream_t stream) {
+    DVC_CHECK_ARG(encode_tma_applicable(dt, H, W, 8, c_lat), DVC_ERR_UNSUPPORTED, "encode: unsupported shape");
+    DVC_CHECK_ARG(((uintptr_t)frames & 15) == 0 && ((uintptr_t)latent & 15) == 0, DVC_ERR_ARG,
+                  "encode: frames / latent must be 16-byte aligned");
+    EncParams p;
+    memset(&p, 0, sizeof(p));
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    // frames [T][3][H][W] as (x, dy, hb, t*3 + c)
+    cuuint64_t gdim[4] = {(cuuint64_t)W, 8, (cuuint64_t)(H / 8), (cuuint64_t)T * 3};
+    cuuint64_t gstride[3] = {(cuuint64_t)W * 2, (cuuint64_t)W * 16, (cuuint64_t)H * W * 2};
+    cuuint32_t box[4] = {ENC_BX * 8, 8, ENC_BY, 3};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(&p.amap, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                     const_cast<void *>(frames), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (frames) failed (%d)", (int)r);
+    dvc_status st = make_bmap_rows(&p.bmap, w_exp, dt, c_lat, 192, c_lat);
+    if (st != DVC_OK) return st;
+    p.T = T;
+    p.h = H / 8;
+    p.w = W / 8;
+    p.c_lat = c_lat;
+    p.tiles_x = (p.w + ENC_BX - 1) / ENC_BX;
+    p.tiles_y = (p.h + ENC_BY - 1) / ENC_BY;
+    p.ntiles = T * p.tiles_x * p.tiles_y;
+    p.bias = b_exp;
+    p.out = latent;
+    p.idesc = make_idesc(dt == DVC_BF16, 128, c_lat);
+    const size_t smem = 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 8 * 10 + 16 + (size_t)c_lat * 4;
+    auto kern = dt == DVC_BF16 ? encode_kernel<__nv_bfloat16> : encode_kernel<__half>;
+    if (!smem_attr_ok((const void *)kern, (int)smem))
+        DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (g_enc_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_enc_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = p.ntiles < g_enc_sms ? p.ntiles : g_enc_sms;
+    kern<<<grid, ENC_THREADS, smem, stream>>>(p);
+    ++g_launches;
+    return check_launch("encode_kernel");
+}
+
+}  // namespace dvc

@@ -309,6 +309,19 @@ __device__ __forceinline__ void mma_stage(uint32_t d, uint32_t a_lo, uint32_t a_
                      : "memory");
     }
 }
+// the same K steps without a commit (the caller commits after a later stage)
+template <int CG>
+__device__ __forceinline__ void mma_stage_nc(uint32_t d, uint32_t a_lo, uint32_t a_hi, uint32_t a_step, uint32_t b_lo,
+                                             uint32_t b_hi, uint32_t idesc, uint32_t ks, uint32_t accum) {
+    if constexpr (CG == 1)
+        asm volatile(DVC_MMA_STAGE_ASM("1") "}\n" ::"r"(d), "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi),
+                     "r"(idesc), "r"(ks), "r"(accum)
+                     : "memory");
+    else
+        asm volatile(DVC_MMA_STAGE_ASM("2") "}\n" ::"r"(d), "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi),
+                     "r"(idesc), "r"(ks), "r"(accum)
+                     : "memory");
+}
 // commit (all prior MMAs of the elected lane) from a converged warp
 template <int CG>
 __device__ __forceinline__ void commit_elected(uint32_t bar) {
