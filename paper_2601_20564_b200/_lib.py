@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_PKG, "libdvc.so")
+# DVC_LIB: an alternative build of the same library (A/B timing experiments, tools/ab.sh)
+SO_PATH = os.environ.get("DVC_LIB") or os.path.join(_PKG, "libdvc.so")
 
 DVC_BF16, DVC_F16, DVC_F32 = 0, 1, 2
 STATUS = {0: "DVC_OK", 1: "DVC_ERR_ARG", 2: "DVC_ERR_DIVISIBILITY", 3: "DVC_ERR_SHAPE",

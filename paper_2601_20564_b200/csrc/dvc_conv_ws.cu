@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][4][32] box-statistics staging
+    float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][2][4][32] box-statistics staging
+    float *sbias = red + 512;   // [2][cout] bias0, bias1 in fp32 (16-byte aligned: even barrier count)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -81,6 +82,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
         tma_prefetch(&p.bmap[0]);
     }
     if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), ncols);
+    for (int i = tid; i < p.cout; i += kWsThreads) {
+        sbias[i] = p.bias0 ? Elem<T>::to_f(reinterpret_cast<const T *>(p.bias0)[i]) : 0.f;
+        sbias[p.cout + i] = p.bias1 ? Elem<T>::to_f(reinterpret_cast<const T *>(p.bias1)[i]) : 0.f;
+    }
     tc_fence_before();
     __syncthreads();
     if constexpr (CG == 2) cluster_sync_all();
@@ -183,8 +188,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
         const int q4 = warp & 3;                 // TMEM lane quadrant of this warp
         const int r = q4 * 32 + lane;            // accumulator row = pixel of this CTA's box
         const int by = r / p.BX, bx = r - by * p.BX;
-        const T *b0 = reinterpret_cast<const T *>(p.bias0);
-        const T *b1 = reinterpret_cast<const T *>(p.bias1);
+        const float *sb0 = p.bias0 ? sbias : nullptr;
+        const float *sb1 = p.bias1 ? sbias + p.cout : nullptr;
         const T *res = reinterpret_cast<const T *>(p.residual);
         T *out = reinterpret_cast<T *>(p.out);
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
@@ -194,9 +199,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
             const uint32_t use = (uint32_t)(it >> 1) & 1;
             const int q = w / p.ntile_n, nt = w - q * p.ntile_n;
             const int box = q * CG + (int)rank;
+            const int per = p.tiles_x * p.tiles_y;
             long m = -1;
             if (box < p.nbox && r < p.BX * p.BY) {
-                const int per = p.tiles_x * p.tiles_y;
                 const int t = box / per, rem = box - t * per;
                 const int y = (rem / p.tiles_x) * p.BY + by, x = (rem % p.tiles_x) * p.BX + bx;
                 if (y < p.H && x < p.W) m = ((long)t * p.H + y) * p.W + x;
@@ -204,39 +209,36 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
             mbar_wait(&tfull[buf], use);   // long wait (a whole main loop): sleep, leave the issue slots
             tc_fence_after();
             const bool want_stats = p.stats != nullptr && box < p.nbox;   // warp-uniform
-#pragma unroll 1
-            for (int cc = 0, par = 0; cc < BN; cc += 16, par ^= 1) {
-                uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN + cc), v);
-                const int n = nt * BN + cc;
+            float *stats_box = want_stats ? p.stats + (size_t)box * p.cout * 2 : nullptr;   // box = t * per + bi
+            // one 16-column chunk: + bias (fp32, shared memory) + residual, 16-bit store; x = this
+            // row's statistics contribution of the stored values
+            auto chunk = [&](const uint32_t (&v)[16], int n, float (&x)[32]) {
                 float f[16];
                 if (m >= 0) {
+                    float rv[16];
+                    if (res) {   // issue the residual loads first
+                        load8(res + m * p.cout + n, *reinterpret_cast<float(*)[8]>(&rv[0]));
+                        load8(res + m * p.cout + n + 8, *reinterpret_cast<float(*)[8]>(&rv[8]));
+                    }
 #pragma unroll
                     for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
-                    float e[8];
-                    if (b0) {
-                        load8(b0 + n, e);
+                    if (sb0) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] += e[i];
-                        load8(b0 + n + 8, e);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                        for (int i = 0; i < 16; i += 4) {
+                            const float4 e = *reinterpret_cast<const float4 *>(sb0 + n + i);
+                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
+                        }
                     }
-                    if (b1) {
-                        load8(b1 + n, e);
+                    if (sb1) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] += e[i];
-                        load8(b1 + n + 8, e);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                        for (int i = 0; i < 16; i += 4) {
+                            const float4 e = *reinterpret_cast<const float4 *>(sb1 + n + i);
+                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
+                        }
                     }
                     if (res) {
-                        load8(res + m * p.cout + n, e);
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) f[i] += e[i];
-                        load8(res + m * p.cout + n + 8, e);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) f[8 + i] += e[i];
+                        for (int i = 0; i < 16; ++i) f[i] += rv[i];
                     }
                     Vec8<T> lo, hi;
 #pragma unroll
@@ -249,16 +251,33 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                     *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n) = lo;
                     *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n + 8) = hi;
                 }
+                if (want_stats) box_row_values(f, m >= 0, x);
+            };
+            // 32 columns per step: two tcgen05.ld in flight, two butterflies, one barrier, and the
+            // combine split over warps 0 / 1 (canonical order, dvc_boxstats.cuh)
+            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
+            int par = 0;
+#pragma unroll 1
+            for (int cc = 0; cc < BN; cc += 32, par ^= 1) {
+                const bool two = cc + 16 < BN;   // warp-uniform
+                uint32_t va[16], vb[16];
+                tmem_ld16_nowait(taddr + (uint32_t)cc, va);
+                if (two) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
+                tmem_wait16(va);
+                float *rr = red + par * 256;   // [2 chunks][4 warps][32]
+                float x[32];
+                chunk(va, nt * BN + cc, x);
+                if (want_stats) rr[q4 * 32 + lane] = box_reduce_scatter32(x, lane);
+                if (two) {
+                    tmem_wait16(vb);
+                    chunk(vb, nt * BN + cc + 16, x);
+                    if (want_stats) rr[128 + q4 * 32 + lane] = box_reduce_scatter32(x, lane);
+                }
                 if (want_stats) {
-                    float x[32];
-                    box_row_values(f, m >= 0, x);
-                    red[(par * 4 + q4) * 32 + lane] = box_reduce_scatter32(x, lane);
                     asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
-                    if (q4 == 0) {
-                        const int per = p.tiles_x * p.tiles_y;
-                        const int t = box / per, bi = box - t * per;
-                        const float val = box_combine4(red + par * 128, lane);
-                        p.stats[(((size_t)t * per + bi) * p.cout + n + (lane & 15)) * 2 + (lane >> 4)] = val;
+                    if (q4 < (two ? 2 : 1)) {
+                        const int n = nt * BN + cc + 16 * q4;
+                        stats_box[(n + (lane & 15)) * 2 + (lane >> 4)] = box_combine4(rr + q4 * 128, lane);
                     }
                 }
             }
@@ -347,7 +366,8 @@ static int g_num_sms = 0;
 
 template <typename T, int CG, int STAGES>
 static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
-    const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16 + 1024;
+    const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16 + 2048 +
+                        (size_t)2 * p.cout * 4;
     auto kern = conv_ws_kernel<T, CG, STAGES>;
     if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
