@@ -22,9 +22,9 @@ def dvc():
     return m
 
 
-def _net(dvc, dtype, width, c_lat, h, w, max_T, G, seed=0):
+def _net(dvc, dtype, width, c_lat, h, w, max_T, G, seed=0, P=8):
     named = synthgen.unet_weights(width, c_lat, c_lat, seed=seed)
-    cfg = dvc.unet_config(width, c_lat, c_lat, G, 8, 1e-5, dtype, h, w, max_T)
+    cfg = dvc.unet_config(width, c_lat, c_lat, G, P, 1e-5, dtype, h, w, max_T)
     assert dvc.unet_weight_count(cfg) == sum(a.size for _, a in named)
     blob = dvc.pack_weights(named, dtype)
     exact = [(n, torch.from_numpy(a).to(dtype).double().numpy()) for n, a in named]
@@ -64,6 +64,45 @@ def test_skeleton_batch_equals_online_and_chunks(dvc, dtype, h, w):   # G10, G11
                                                  carry_in=carry, carry_out=ko))
             carry, t0 = ko, t0 + n
         assert torch.equal(torch.cat(parts), full), chunks
+
+
+# f4: the shift ratio P (Fig. 8a sweep).  P = 2, 4 keep the slice whole GroupNorm groups (fused
+# path); P = 16 does not (C_in/16 is not a multiple of C/G): the per-element shifted-statistics path.
+@pytest.mark.parametrize("P", [2, 4, 16])
+@pytest.mark.parametrize("h,w,T", [(12, 20, 3), (64, 40, 2)])
+def test_skeleton_shift_ratio_sweep(dvc, orc, P, h, w, T):
+    dtype = torch.bfloat16
+    net, wts = _net(dvc, dtype, SMALL, 32, h, w, 4, 8, P=P)
+    lat, lat64 = dev(synthgen.normal((T, h, w, 32), 1), dtype)
+    ctx, ctx64 = dev(synthgen.normal((T, h, w, 32), 5), dtype)
+    co = torch.empty(net.carry_elems, dtype=dtype, device="cuda")
+    out = dvc.dvc_unet_decode_gop(net, lat, ctx, carry_out=co)
+    ref, kref = orc.skeleton(lat64, ctx64, wts, SMALL, G=8, P=P, mode=MODE[dtype])
+    assert rel_l2(host64(out), ref) <= TOL[dtype]
+    # batch == online, bit-exact, at this P
+    parts, carry = [], None
+    for t in range(T):
+        ko = torch.empty(net.carry_elems, dtype=dtype, device="cuda")
+        parts.append(dvc.dvc_unet_decode_gop(net, lat[t:t + 1].contiguous(), ctx[t:t + 1].contiguous(),
+                                             carry_in=carry, carry_out=ko))
+        carry = ko
+    assert torch.equal(torch.cat(parts), out)
+    assert torch.equal(carry, co)
+
+
+@pytest.mark.parametrize("h,w", [(12, 20), (66, 36)])
+def test_streaming_decoder_graphs_bit_exact(dvc, h, w):   # f4: CUDA-graph online decode == batch decode
+    dtype = torch.bfloat16
+    T = 5
+    net, _ = _net(dvc, dtype, SMALL, 32, h, w, T, 8)
+    lat, _ = dev(synthgen.normal((T, h, w, 32), 1), dtype)
+    ctx, _ = dev(synthgen.normal((T, h, w, 32), 5), dtype)
+    full = dvc.dvc_unet_decode_gop(net, lat, ctx)
+    sd = dvc.StreamingDecoder(net)
+    for _ in range(2):   # a reset starts a new chain: the same outputs again
+        sd.reset()
+        outs = [sd.step(lat[t], ctx[t]).clone() for t in range(T)]
+        assert torch.equal(torch.cat(outs), full)
 
 
 def test_skeleton_real_widths_small_latent(dvc, orc):   # R1 widths 240/480/960 at a 16x24 latent, bf16

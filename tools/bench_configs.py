@@ -7,7 +7,9 @@
   C3  ResBlock skeleton decode, 720p, 16-frame batch, fp16 and bf16: frames/s
   C4  1080p 64-frame GOP on one GPU (the N=1 point of the sharded config): frames/s
   C5  online (N calls of T=1 passing the carries) vs batch (one call of T=N) for N = 1..64 at 720p:
-      frames/s of both, and whether the outputs are bit-identical (they must be)
+      frames/s of both, and whether the outputs are bit-identical (they must be); plus streaming
+      serving through CUDA-graph replays (StreamingDecoder, f4)
+  F4  decode frames/s vs the shift ratio P in {2, 4, 8, 16}
 The headline metric is bench.py; this script is evidence for the other configs.
 """
 import argparse
@@ -104,7 +106,35 @@ def c5(Ns, steps):
         ms_o = timed(online, max(1, steps // 2))
         rows.append({"N": N, "batch_fps": N / (ms_b / 1e3), "online_fps": N / (ms_o / 1e3),
                      "latency_frames": N - 1, "bit_identical": bool(torch.equal(outb, outo))})
+    # f4 streaming serving: one frame per step through CUDA-graph replays (StreamingDecoder)
+    sd = dvc.StreamingDecoder(net)
+    n = 64
+
+    def stream():
+        sd.reset()
+        for t in range(n):
+            sd.step(lat[t % Tmax], ctx[t % Tmax])
+    ms_g = timed(stream, max(1, steps // 2), warmup=1)
+    rows.append({"streaming_graph_fps": n / (ms_g / 1e3), "latency_frames": 0})
     return {"config": "C5 online vs batch, 720p bf16", "rows": rows}
+
+
+def f4_p_sweep(steps):   # f4: decode throughput vs the shift ratio P (Fig. 8a)
+    h, w, T = 90, 160, 32
+    rows = []
+    for P in (2, 4, 8, 16):
+        named = synthgen.unet_weights(WIDTH, 256, 256)
+        cfg = dvc.unet_config(WIDTH, 256, 256, 24, P, 1e-5, torch.bfloat16, h, w, T)
+        net = dvc.UNet(cfg, dvc.pack_weights(named, torch.bfloat16))
+        lat = torch.from_numpy(synthgen.normal((T, h, w, 256), 1)).to(torch.bfloat16).cuda()
+        ctx = torch.from_numpy(synthgen.normal((T, h, w, 256), 5)).to(torch.bfloat16).cuda()
+        out = torch.empty_like(lat)
+        ws = torch.empty(net.workspace_size(T), dtype=torch.uint8, device="cuda")
+        ms = timed(lambda: dvc.dvc_unet_decode_gop(net, lat, ctx, out=out, workspace=ws), steps)
+        rows.append({"P": P, "frames_per_s": T / (ms / 1e3), "shift_slice_frac": 1 / P,
+                     "fused_gn_path": (24 % P == 0)})
+        net.close()
+    return {"config": "F4 shift-ratio sweep, 720p T=32 bf16 (skeleton decode)", "rows": rows}
 
 
 def main():
@@ -119,6 +149,7 @@ def main():
     ms, fps = decode_fps(torch.bfloat16, 135, 240, 64, max(3, steps // 2))
     print(json.dumps({"config": "C4 1080p 64-frame GOP, 1 GPU, bf16", "ms": ms, "frames_per_s": fps}), flush=True)
     print(json.dumps(c5([1, 2, 4, 8, 16, 32, 64], steps)), flush=True)
+    print(json.dumps(f4_p_sweep(steps)), flush=True)
 
 
 if __name__ == "__main__":
