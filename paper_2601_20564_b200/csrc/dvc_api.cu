@@ -48,6 +48,11 @@ bool smem_attr_ok(const void *kern, int smem) {
     return false;
 }
 
+bool pdl_enabled() {
+    static const bool on = !(getenv("DVC_PDL") && atoi(getenv("DVC_PDL")) == 0);
+    return on;
+}
+
 dvc_status check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cstddef>
+#include <utility>
 #include "../../include/dvc.h"
 
 namespace dvc {
@@ -100,6 +101,45 @@ inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 
 // true if `kern` already allows >= smem bytes of dynamic shared memory (records the new size otherwise)
 bool smem_attr_ok(const void *kern, int smem);
+
+// Programmatic dependent launch (PDL): kernels of the decode chain are launched with
+// programmatic stream serialisation, so a kernel's CTAs may start (prologue: barriers, TMEM,
+// tensor-map prefetch, weight-side loads) while its predecessor drains.  griddep_wait() blocks
+// until the predecessor grid has completed and its memory is visible -- every kernel calls it
+// before its first access to activation data; without the launch attribute it is a no-op.
+// griddep_launch() lets the successor grid be scheduled (correctness never depends on it).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// PDL (programmatic dependent launch) for the decode chain; DVC_PDL=0 disables it
+bool pdl_enabled();
+// launch `kern` with programmatic stream serialisation (+ an optional cluster dimension)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, int cluster,
+                       Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (cluster > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = cluster;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    if (pdl_enabled()) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ----------------------------------------------------------------- shifted-operand addressing (a3)
 // One ResBlock input X = concat(xa[ca], xb[cb]) over frames [T][HW].  The

@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     if constexpr (CG == 2) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();     // predecessor grid complete: activations may be read / written
+    griddep_launch();   // the successor may be scheduled on SMs that free up
     unsigned long long pacc[4] = {0, 0, 0, 0};
     const long long tstart = PROF ? clock64() : 0;
 #define FZ_TIMED(slot, stmt)                                  \
@@ -825,19 +827,7 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     }
     int clusters = g_fz_sms / CG;
     if (clusters > p.nwork) clusters = p.nwork;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(clusters * CG);
-    cfg.blockDim = dim3(kFzThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    DVC_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    DVC_CUDA(launch_pdl(kern, dim3(clusters * CG), dim3(kFzThreads), smem, stream, CG, p));
     ++g_launches;
     if (prof) {   // diagnostics: per-role wait / total cycles averaged over CTAs (stderr)
         unsigned long long h[24];

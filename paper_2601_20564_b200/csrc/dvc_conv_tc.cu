@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();     // predecessor grid complete: activations may be read / written
+    griddep_launch();   // the successor may be scheduled on SMs that free up
 
     if (warp < 4) {
         // ===================== A producer (gather + cp.async) =====================
@@ -335,7 +337,7 @@ static dvc_status launch_tc(const TcParams &p, int grid_m, int grid_n, cudaStrea
     auto kern = conv_tc_kernel<T, NACC, STAGES>;
     if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<dim3(grid_m, grid_n), kThreads, smem, stream>>>(p);
+    DVC_CUDA(launch_pdl(kern, dim3(grid_m, grid_n), dim3(kThreads), smem, stream, 1, p));
     ++g_launches;
     return check_launch("conv_tc_kernel");
 }

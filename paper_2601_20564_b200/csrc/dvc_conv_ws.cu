@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
     if constexpr (CG == 2) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();     // predecessor grid complete: activations may be read / written
+    griddep_launch();   // the successor may be scheduled on SMs that free up
 
     if (warp == 0) {
         // ===================== TMA producer (both CTAs) =====================
@@ -378,19 +380,7 @@ static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
     }
     int clusters = g_num_sms / CG;
     if (clusters > p.nwork) clusters = p.nwork;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(clusters * CG);
-    cfg.blockDim = dim3(kWsThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    DVC_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    DVC_CUDA(launch_pdl(kern, dim3(clusters * CG), dim3(kWsThreads), smem, stream, CG, p));
     ++g_launches;
     return check_launch("conv_ws_kernel");
 }

@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(ENC_THREADS, 1) encode_kernel(const __grid_con
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    griddep_wait();     // predecessor grid complete: activations may be read / written
+    griddep_launch();   // the successor may be scheduled on SMs that free up
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -243,7 +245,7 @@ dvc_status encode_tma_run(const void *frames, dvc_dtype dt, int T, int H, int W,
         cudaDeviceGetAttribute(&g_enc_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = p.ntiles < g_enc_sms ? p.ntiles : g_enc_sms;
-    kern<<<grid, ENC_THREADS, smem, stream>>>(p);
+    DVC_CUDA(launch_pdl(kern, dim3(grid), dim3(ENC_THREADS), smem, stream, 1, p));
     ++g_launches;
     return check_launch("encode_kernel");
 }

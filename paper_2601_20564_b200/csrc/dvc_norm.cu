@@ -144,6 +144,7 @@ __device__ __forceinline__ VecSrc<T> vec_src(const ShiftSrc<T> &X, int t, int v)
 template <typename T>
 __global__ void __launch_bounds__(256, 3) gn_partial_kernel(const ShiftSrc<T> X, int G, double2 *__restrict__ partial,
                                                          int nchunk) {
+    griddep_wait();
     __shared__ double s_sum[2048];
     __shared__ double s_sq[2048];
     const int t = blockIdx.y, chunk = blockIdx.x;
@@ -213,6 +214,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) gn_finalize_kernel(const double2 *__restrict__ partial, int nchunk, int G,
                                                           int C, double n, double eps, const T *__restrict__ gamma,
                                                           float2 *__restrict__ coef) {
+    griddep_wait();
     __shared__ float s_mu[256], s_rs[256];
     const int t = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int g = warp; g < G; g += blockDim.x >> 5) {
@@ -259,6 +261,7 @@ __device__ __forceinline__ float silu_t(float z) {
 template <typename T>
 __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const float2 *__restrict__ coef,
                                                       const T *__restrict__ beta, T *__restrict__ out) {
+    griddep_wait();
     const int t = blockIdx.y, chunk = blockIdx.x;
     const int C = X.C(), nv = C >> 3, npl = 256 / nv;
     const int tid = threadIdx.x, v = tid % nv, pl = tid / nv;
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const
 // Test-only: materialise Xs with the same addressing (dvc_debug_shift_gather).
 template <typename T>
 __global__ void __launch_bounds__(256) shift_gather_kernel(const ShiftSrc<T> X, T *__restrict__ out) {
+    griddep_wait();
     const int t = blockIdx.y, chunk = blockIdx.x;
     const int C = X.C(), nv = C >> 3, npl = 256 / nv;
     const int tid = threadIdx.x, v = tid % nv, pl = tid / nv;
@@ -343,13 +347,13 @@ static dvc_status gn_silu_t(const NormArgs &a, cudaStream_t stream) {
     double2 *partial = reinterpret_cast<double2 *>(a.ws);
     float2 *coef = reinterpret_cast<float2 *>(reinterpret_cast<uint8_t *>(a.ws) +
                                               align256((size_t)a.T * nchunk * a.G * sizeof(double2)));
-    gn_partial_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, a.G, partial, nchunk);
+    DVC_CUDA(launch_pdl(gn_partial_kernel<T>, dim3(dim3(nchunk, a.T)), dim3(256), 0, stream, 1, X, a.G, partial, nchunk));
     ++g_launches;
-    gn_finalize_kernel<T><<<a.T, 256, 0, stream>>>(partial, nchunk, a.G, C, (double)(C / a.G) * a.HW, (double)a.eps,
-                                                   reinterpret_cast<const T *>(a.gamma), coef);
+    DVC_CUDA(launch_pdl(gn_finalize_kernel<T>, dim3(a.T), dim3(256), 0, stream, 1, partial, nchunk, a.G, C, (double)(C / a.G) * a.HW, (double)a.eps,
+                                                   reinterpret_cast<const T *>(a.gamma), coef));
     ++g_launches;
-    gn_silu_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, coef, reinterpret_cast<const T *>(a.beta),
-                                                             reinterpret_cast<T *>(a.out));
+    DVC_CUDA(launch_pdl(gn_silu_kernel<T>, dim3(dim3(nchunk, a.T)), dim3(256), 0, stream, 1, X, coef, reinterpret_cast<const T *>(a.beta),
+                                                             reinterpret_cast<T *>(a.out)));
     ++g_launches;
     return check_launch("gn_silu");
 }
@@ -372,7 +376,7 @@ static dvc_status gather_t(const NormArgs &a, cudaStream_t stream) {
     ShiftSrc<T> X{reinterpret_cast<const T *>(a.xa), reinterpret_cast<const T *>(a.xb),
                   reinterpret_cast<const T *>(a.carry), a.ca, a.cb, a.cs, a.HW};
     const int nchunk = (a.HW + chunk_pix(a.ca + a.cb) - 1) / chunk_pix(a.ca + a.cb);
-    shift_gather_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, reinterpret_cast<T *>(a.out));
+    DVC_CUDA(launch_pdl(shift_gather_kernel<T>, dim3(dim3(nchunk, a.T)), dim3(256), 0, stream, 1, X, reinterpret_cast<T *>(a.out)));
     ++g_launches;
     return check_launch("shift_gather");
 }
@@ -393,6 +397,7 @@ dvc_status shift_gather_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream
 // up-sampler's operand so its 3x3 conv runs on the TMA engine.  Exact copy.
 __global__ void __launch_bounds__(256) nearest_kernel(const uint4 *__restrict__ V, uint4 *__restrict__ U, int hi,
                                                       int wi, int ho, int wo, int nvec) {
+    griddep_wait();
     const int y = blockIdx.y, t = blockIdx.z;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;   // x * nvec + v within the output row
     if (i >= wo * nvec) return;
@@ -406,8 +411,8 @@ dvc_status nearest_run(const void *src, void *dst, int T, int hi, int wi, int ho
     DVC_CHECK_ARG((C * dt_size(dt)) % 16 == 0, DVC_ERR_UNSUPPORTED, "nearest: rows must be 16-byte multiples");
     const int nvec = (int)(C * dt_size(dt) / 16);
     dim3 grid((wo * nvec + 255) / 256, ho, T);
-    nearest_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const uint4 *>(src), reinterpret_cast<uint4 *>(dst), hi, wi,
-                                             ho, wo, nvec);
+    DVC_CUDA(launch_pdl(nearest_kernel, dim3(grid), dim3(256), 0, stream, 1, reinterpret_cast<const uint4 *>(src), reinterpret_cast<uint4 *>(dst), hi, wi,
+                                             ho, wo, nvec));
     ++g_launches;
     return check_launch("nearest");
 }
@@ -417,6 +422,7 @@ dvc_status nearest_run(const void *src, void *dst, int T, int hi, int wi, int ho
 template <typename T>
 __global__ void __launch_bounds__(128) box_stats_kernel(const T *__restrict__ x, int H, int W, int C, int BX, int BY,
                                                         int tiles_x, int vec_ok, float *__restrict__ stats) {
+    griddep_wait();
     __shared__ float red[2][4][32];
     const int b = blockIdx.x, t = blockIdx.y, per = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, r = threadIdx.x;
@@ -460,16 +466,16 @@ dvc_status box_stats_run(const void *x, int T, int H, int W, int C, dvc_dtype dt
     const int vec_ok = (C % 8 == 0) && ((uintptr_t)x % 16 == 0) && ((C * dt_size(dt)) % 16 == 0);
     switch (dt) {
         case DVC_BF16:
-            box_stats_kernel<__nv_bfloat16><<<grid, 128, 0, stream>>>(reinterpret_cast<const __nv_bfloat16 *>(x), H, W,
-                                                                      C, BX, BY, tx, vec_ok, stats);
+            DVC_CUDA(launch_pdl(box_stats_kernel<__nv_bfloat16>, dim3(grid), dim3(128), 0, stream, 1, reinterpret_cast<const __nv_bfloat16 *>(x), H, W,
+                                                                      C, BX, BY, tx, vec_ok, stats));
             break;
         case DVC_F16:
-            box_stats_kernel<__half><<<grid, 128, 0, stream>>>(reinterpret_cast<const __half *>(x), H, W, C, BX, BY, tx,
-                                                               vec_ok, stats);
+            DVC_CUDA(launch_pdl(box_stats_kernel<__half>, dim3(grid), dim3(128), 0, stream, 1, reinterpret_cast<const __half *>(x), H, W, C, BX, BY, tx,
+                                                               vec_ok, stats));
             break;
         default:
-            box_stats_kernel<float><<<grid, 128, 0, stream>>>(reinterpret_cast<const float *>(x), H, W, C, BX, BY, tx,
-                                                              vec_ok, stats);
+            DVC_CUDA(launch_pdl(box_stats_kernel<float>, dim3(grid), dim3(128), 0, stream, 1, reinterpret_cast<const float *>(x), H, W, C, BX, BY, tx,
+                                                              vec_ok, stats));
     }
     ++g_launches;
     return check_launch("box_stats");
@@ -486,6 +492,7 @@ __global__ void __launch_bounds__(256) gn_finalize_box_kernel(const float2 *__re
                                                               const float2 *__restrict__ pk, int cs, int nbox, int G,
                                                               double n, double eps, const T *__restrict__ gamma,
                                                               const T *__restrict__ beta, float2 *__restrict__ coef) {
+    griddep_wait();
     __shared__ double s_S[8], s_Q[8];
     __shared__ float s_mu, s_rs;
     const int g = blockIdx.x, t = blockIdx.y, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -545,13 +552,13 @@ static dvc_status gn_silu_box_t(const NormArgs &a, const BoxStatsIn &bs, int H, 
     const int C = a.ca + a.cb;
     const int nchunk = (a.HW + chunk_pix(C) - 1) / chunk_pix(C);
     float2 *coef = reinterpret_cast<float2 *>(a.ws);
-    gn_finalize_box_kernel<T><<<dim3(a.G, a.T), 256, 0, stream>>>(
+    DVC_CUDA(launch_pdl(gn_finalize_box_kernel<T>, dim3(dim3(a.G, a.T)), dim3(256), 0, stream, 1, 
         reinterpret_cast<const float2 *>(bs.a), a.ca, reinterpret_cast<const float2 *>(bs.b), a.cb,
         reinterpret_cast<const float2 *>(bs.carry), a.cs, boxes_per_frame(H, W), a.G, (double)(C / a.G) * a.HW,
-        (double)a.eps, reinterpret_cast<const T *>(a.gamma), nullptr, coef);
+        (double)a.eps, reinterpret_cast<const T *>(a.gamma), nullptr, coef));
     ++g_launches;
-    gn_silu_kernel<T><<<dim3(nchunk, a.T), 256, 0, stream>>>(X, coef, reinterpret_cast<const T *>(a.beta),
-                                                             reinterpret_cast<T *>(a.out));
+    DVC_CUDA(launch_pdl(gn_silu_kernel<T>, dim3(dim3(nchunk, a.T)), dim3(256), 0, stream, 1, X, coef, reinterpret_cast<const T *>(a.beta),
+                                                             reinterpret_cast<T *>(a.out)));
     ++g_launches;
     return check_launch("gn_silu_box");
 }
@@ -559,11 +566,11 @@ static dvc_status gn_silu_box_t(const NormArgs &a, const BoxStatsIn &bs, int H, 
 template <typename T>
 static dvc_status gn_coef_t(const NormArgs &a, const BoxStatsIn &bs, int H, int W, cudaStream_t stream) {
     const int C = a.ca + a.cb;
-    gn_finalize_box_kernel<T><<<dim3(a.G, a.T), 256, 0, stream>>>(
+    DVC_CUDA(launch_pdl(gn_finalize_box_kernel<T>, dim3(dim3(a.G, a.T)), dim3(256), 0, stream, 1, 
         reinterpret_cast<const float2 *>(bs.a), a.ca, reinterpret_cast<const float2 *>(bs.b), a.cb,
         reinterpret_cast<const float2 *>(bs.carry), a.cs, boxes_per_frame(H, W), a.G, (double)(C / a.G) * a.HW,
         (double)a.eps, reinterpret_cast<const T *>(a.gamma), reinterpret_cast<const T *>(a.beta),
-        reinterpret_cast<float2 *>(a.out));
+        reinterpret_cast<float2 *>(a.out)));
     ++g_launches;
     return check_launch("gn_coef");
 }
