@@ -45,7 +45,11 @@ constexpr int FZ_RAW_SLOT = 128 * 128;        // one raw SW128 box {64, 8, 16}
 constexpr int FZ_SBO = FZ_HX * 16;            // between 8-row groups (image rows)
 constexpr int FZ_MAX_BSTAGES = 16;
 constexpr int FZ_MAX_NTF = 6;   // even: keeps the barrier block a multiple of 16 B
-constexpr int kFzThreads = 512;
+#ifndef FZ_TFW
+#define FZ_TFW 8   // transform warps: 8 (one per 8-channel column) or 16 (two per column, rows split;
+                   // measured slower: 768 threads cap registers at 80 and the epilogue spills)
+#endif
+constexpr int kFzThreads = 256 + 32 * FZ_TFW;
 
 struct FzSeg {
     const void *src;   // raw operand tensor [T][H][W][c]
@@ -349,7 +353,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         }
     } else if (warp >= 8) {
         // ===================== transform warps: in place, H = SiLU(GN(X)) =====================
-        const int kg = warp - 8;   // 8-channel core-matrix column of this warp
+        const int kg = (warp - 8) & 7;                     // 8-channel core-matrix column of this warp
+        const int row0 = FZ_TFW == 16 ? ((warp - 8) >> 3) * 96 : 0;   // 16 warps: rows [0,96) / [96,180)
         int tb = 0;
         uint32_t tph = 0;
         uint32_t rph = 0;   // raw_full phase per slot: only transform chunks complete raw_full
@@ -394,13 +399,13 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         // 128-byte row r (the TMA swizzle); else row r of core-matrix column kg
                         const bool sw = fz_sw_chunk(p, sg, ch * 64);
                         auto roff = [&](int r) -> int { return sw ? r * 128 + ((kg ^ (r & 7)) << 4) : kg * FZ_LBO + r * 16; };
-                        constexpr int NR = (FZ_HROWS + 31) / 32;   // 6 halo rows per lane (the last one partial)
+                        constexpr int NR = FZ_TFW == 16 ? 3 : (FZ_HROWS + 31) / 32;   // halo rows per lane
                         // all rows' words first (independent shared loads in flight), then two rows
                         // (16 independent ex2 / rcp chains) per step
                         uint32_t wv[NR][4];
 #pragma unroll
                         for (int k = 0; k < NR; ++k) {
-                            const int r = lane + 32 * k;
+                            const int r = row0 + lane + 32 * k;
                             uint4 cu = make_uint4(0, 0, 0, 0);
                             if (r < FZ_HROWS) {
                                 cu = *reinterpret_cast<const uint4 *>(slot + roff(r));
@@ -419,19 +424,25 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                             float z[2][8], e[2][8];
 #pragma unroll
                             for (int k = 0; k < 2; ++k)
+                                if (k0 + k < NR)
 #pragma unroll
                                 for (int j = 0; j < 4; ++j) {
                                     float v0, v1;
                                     Pk<T>::unpack(wv[k0 + k][j], v0, v1);
                                     z[k][2 * j] = fmaf(v0, sc[2 * j], sh[2 * j]);
                                     z[k][2 * j + 1] = fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]);
-                                    e[k][2 * j] = fz_ex2(fmaf(v0, sc2[2 * j], sh2[2 * j]));
-                                    e[k][2 * j + 1] = fz_ex2(fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
+                                    if constexpr (FZ_TFW == 16) {   // register budget: u = -z log2(e) from z
+                                        e[k][2 * j] = fz_ex2(z[k][2 * j] * -1.4426950408889634f);
+                                        e[k][2 * j + 1] = fz_ex2(z[k][2 * j + 1] * -1.4426950408889634f);
+                                    } else {
+                                        e[k][2 * j] = fz_ex2(fmaf(v0, sc2[2 * j], sh2[2 * j]));
+                                        e[k][2 * j + 1] = fz_ex2(fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
+                                    }
                                 }
 #pragma unroll
                             for (int k = 0; k < 2; ++k) {
-                                const int r = lane + 32 * (k0 + k);
-                                if (r >= FZ_HROWS) continue;
+                                const int r = row0 + lane + 32 * (k0 + k);
+                                if (k0 + k >= NR || r >= FZ_HROWS) continue;
                                 const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
                                 const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
                                 // conv zero padding applies AFTER the transform (H3): out of frame -> 0
@@ -448,7 +459,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         }
                     }
                     FZ_TIMED(2, fence_proxy_async());   // generic-proxy smem writes -> visible to the tensor core
-                    FZ_TIMED(1, asm volatile("bar.sync 2, 256;" ::: "memory"));   // the 8 transform warps
+                    FZ_TIMED(1, asm volatile("bar.sync 2, %0;" ::"n"(32 * FZ_TFW) : "memory"));   // the transform warps
                     if (warp == 8 && elect_one()) {
                         if constexpr (CG == 1)
                             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tf_full[tb]))
