@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstddef>
 #include <utility>
+#include <type_traits>
 #include "../../include/dvc.h"
 
 namespace dvc {
@@ -83,6 +84,39 @@ __device__ __forceinline__ void store8(T *p, const float (&f)[8]) {
     } else {
         reinterpret_cast<float4 *>(p)[0] = reinterpret_cast<float4 *>(&u)[0];
         reinterpret_cast<float4 *>(p)[1] = reinterpret_cast<float4 *>(&u)[1];
+    }
+}
+
+// Round 16 fp32 values to the 16-bit storage type with packed conversions (one cvt per pair)
+// into two 8-element vectors, and replace f[] by the stored values (the box statistics use the
+// stored values, R17).  Same rounding as Elem<T>::from_f element by element.
+template <typename T>
+__device__ __forceinline__ void round_store16(float (&f)[16], Vec8<T> &lo, Vec8<T> &hi) {
+    if constexpr (sizeof(T) == 2) {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+                w[i] = *reinterpret_cast<uint32_t *>(&h);
+                f[2 * i] = __uint_as_float(w[i] << 16);
+                f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+            } else {
+                __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+                w[i] = *reinterpret_cast<uint32_t *>(&h);
+                const float2 b = __half22float2(h);
+                f[2 * i] = b.x;
+                f[2 * i + 1] = b.y;
+            }
+        }
+        *reinterpret_cast<uint4 *>(&lo) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4 *>(&hi) = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            lo.v[i] = Elem<T>::from_f(f[i]);
+            hi.v[i] = Elem<T>::from_f(f[8 + i]);
+        }
     }
 }
 

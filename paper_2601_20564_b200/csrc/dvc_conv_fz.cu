@@ -611,17 +611,14 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         }
                     }
                     Vec8<T> lo, hi;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        lo.v[i] = Elem<T>::from_f(f[i]);
-                        hi.v[i] = Elem<T>::from_f(f[8 + i]);
-                        f[i] = Elem<T>::to_f(lo.v[i]);       // statistics of the stored values (R17)
-                        f[8 + i] = Elem<T>::to_f(hi.v[i]);
-                    }
+                    round_store16<T>(f, lo, hi);   // f <- the stored values (statistics, R17)
                     *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n) = lo;
                     *reinterpret_cast<Vec8<T> *>(out + m * p.cout + n + 8) = hi;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) f[i] = 0.f;   // rows outside the frame count as 0
                 }
-                if (want_stats) box_row_values(f, m >= 0, x);
+                if (want_stats) box_row_values(f, true, x);
             };
             // TMEM -> registers 32 columns at a time (two 16-column loads in flight); the box
             // statistics of both chunks are reduced together (two independent butterflies, one
