@@ -5,6 +5,6 @@ for i in $(seq 1 ${1:-2}); do
   for v in A B; do
     echo "== $v"
     DVC_LIB=ab/libdvc_$v.so timeout 120 python tools/conv_breakdown.py 2>/dev/null | head -1
-    DVC_LIB=ab/libdvc_$v.so timeout 200 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('fps', round(d['value'],1))"
+    DVC_LIB=ab/libdvc_$v.so timeout 200 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('fps', round(d['value'],1))"
   done
 done
