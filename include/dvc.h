@@ -197,12 +197,16 @@ DVC_API dvc_status dvc_comm_destroy(dvc_comm *c);
  * the number of launches.  max_launches bounds the event pool. */
 DVC_API dvc_status dvc_profile_begin(int max_launches);
 DVC_API dvc_status dvc_profile_end(double *conv_ms, double *conv_flops, int *conv_launches);
-/* Record i (0 <= i < conv_launches of the last dvc_profile_end) of that window: the
+/* Record i (0 <= i < dvc_profile_record_count()) of the last dvc_profile_end window: the
  * launch's event time (ms), its algorithmic FLOPs and a label "<engine> T=.. HxW K=.. N=.."
  * (engine: fz1/fz2 fused GN/SiLU/shift convs, ws persistent TMA conv, tc gather conv,
  * simt fp32).  Any output pointer may be null; label is truncated to label_cap bytes.
  * DVC_ERR_ARG if i is out of range. */
 DVC_API dvc_status dvc_profile_record(int i, double *ms, double *flops, char *label, int label_cap);
+/* Records kept by the last dvc_profile_end: the convolution launches plus the other
+ * instrumented kernels of the path (GroupNorm coefficients / apply, box statistics, nearest,
+ * encoder; label "<kernel> ...", flops 0).  dvc_profile_end's sums cover convolutions only. */
+DVC_API int dvc_profile_record_count(void);
 
 /* Convolution engine selection (tuning / A-B testing; default 2, or the
  * DVC_CONV_ENGINE environment variable at load):

@@ -66,6 +66,7 @@ _SIGS = {
                          ctypes.POINTER(c_int)], c_int),
     "dvc_profile_record": ([c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                             ctypes.c_char_p, c_int], c_int),
+    "dvc_profile_record_count": ([], c_int),
     "dvc_comm_unique_id": ([c_void_p], c_int),
     "dvc_comm_create": ([c_int, c_int, c_void_p, ctypes.POINTER(c_void_p)], c_int),
     "dvc_comm_destroy": ([c_void_p], c_int),

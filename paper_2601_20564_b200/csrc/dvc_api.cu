@@ -86,6 +86,7 @@ struct Prof {
     int cap = 0, used = 0;
     std::vector<cudaEvent_t> ev;   // 2 per launch
     std::vector<double> flops, ms;
+    std::vector<char> conv;   // 1: convolution launch (summed by dvc_profile_end); 0: other kernel
     std::vector<std::string> label;
     int done = 0;   // records kept by dvc_profile_end for dvc_profile_record
 } g_prof;
@@ -102,11 +103,20 @@ void prof_end(ProfSlot s, cudaStream_t stream, double flops, const char *engine,
     if (s.idx < 0) return;
     cudaEventRecord(g_prof.ev[2 * s.idx + 1], stream);
     g_prof.flops[s.idx] = flops;
+    g_prof.conv[s.idx] = 1;
     char buf[128];
     int k = 0;
     for (int i = 0; i < d.nseg; ++i) k += d.seg[i].taps * d.seg[i].c_src;
     snprintf(buf, sizeof(buf), "%s T=%d %dx%d K=%d N=%d segs=%d", engine, d.T, d.ho, d.wo, k, d.cout, d.nseg);
     g_prof.label[s.idx] = buf;
+}
+
+void prof_end_aux(ProfSlot s, cudaStream_t stream, const char *label) {
+    if (s.idx < 0) return;
+    cudaEventRecord(g_prof.ev[2 * s.idx + 1], stream);
+    g_prof.flops[s.idx] = 0.0;
+    g_prof.conv[s.idx] = 0;
+    g_prof.label[s.idx] = label;
 }
 
 // ----------------------------------------------------------------- identity weights
@@ -443,6 +453,7 @@ dvc_status dvc_profile_begin(int max_launches) {
     }
     g_prof.flops.assign(max_launches, 0.0);
     g_prof.ms.assign(max_launches, 0.0);
+    g_prof.conv.assign(max_launches, 0);
     g_prof.label.assign(max_launches, std::string());
     g_prof.done = 0;
     g_prof.cap = max_launches;
@@ -455,21 +466,26 @@ dvc_status dvc_profile_end(double *conv_ms, double *conv_flops, int *conv_launch
     DVC_CHECK_ARG(conv_ms && conv_flops && conv_launches, DVC_ERR_ARG, "null output");
     g_prof.on = false;
     double ms = 0, fl = 0;
+    int nconv = 0;
     for (int i = 0; i < g_prof.used; ++i) {
         DVC_CUDA(cudaEventSynchronize(g_prof.ev[2 * i + 1]));
         float t = 0.f;
         DVC_CUDA(cudaEventElapsedTime(&t, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]));
-        ms += t;
-        fl += g_prof.flops[i];
+        if (g_prof.conv[i]) {
+            ms += t;
+            fl += g_prof.flops[i];
+            ++nconv;
+        }
         g_prof.ms[i] = t;
     }
     g_prof.done = g_prof.used;
     *conv_ms = ms;
     *conv_flops = fl;
-    *conv_launches = g_prof.used;
+    *conv_launches = nconv;
     g_prof.used = 0;
     return DVC_OK;
 }
+int dvc_profile_record_count(void) { return g_prof.done; }
 dvc_status dvc_profile_record(int i, double *ms, double *flops, char *label, int label_cap) {
     DVC_CHECK_ARG(i >= 0 && i < g_prof.done, DVC_ERR_ARG, "record %d not available (%d kept)", i, g_prof.done);
     if (ms) *ms = g_prof.ms[i];

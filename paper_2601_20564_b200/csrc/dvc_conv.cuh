@@ -91,6 +91,7 @@ struct ProfSlot {
 ProfSlot prof_begin(cudaStream_t stream);
 struct ConvDesc;
 void prof_end(ProfSlot s, cudaStream_t stream, double flops, const char *engine, const ConvDesc &d);
+void prof_end_aux(ProfSlot s, cudaStream_t stream, const char *label);   // non-conv kernel (not summed)
 double conv_flops(const ConvDesc &d);
 
 // Validates the descriptor for the given engine; returns DVC_OK or an error.

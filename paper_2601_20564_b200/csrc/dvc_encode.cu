@@ -245,8 +245,10 @@ dvc_status encode_tma_run(const void *frames, dvc_dtype dt, int T, int H, int W,
         cudaDeviceGetAttribute(&g_enc_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = p.ntiles < g_enc_sms ? p.ntiles : g_enc_sms;
+    ProfSlot s0 = prof_begin(stream);
     DVC_CUDA(launch_pdl(kern, dim3(grid), dim3(ENC_THREADS), smem, stream, 1, p));
     ++g_launches;
+    prof_end_aux(s0, stream, "encode");
     return check_launch("encode_kernel");
 }
 

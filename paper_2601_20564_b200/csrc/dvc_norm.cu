@@ -12,6 +12,7 @@
 // (mean, rstd) per group come only from frame t's shifted input, reduced in a
 // fixed order (per-thread fp64 sums over a fixed pixel stride, fixed-order
 // smem merge per 256-pixel chunk, fixed-order merge over chunks).
+#include <cstdio>
 #include "dvc_norm.cuh"
 #include "dvc_boxstats.cuh"
 #include "dvc_conv.cuh"
@@ -260,13 +261,12 @@ __device__ __forceinline__ float silu_t(float z) {
 // out[t][p][c] = SiLU((Xs[t][p][c] - mu) * (rstd*gamma[c]) + beta[c]): grid (nchunk, T).
 template <typename T>
 __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const float2 *__restrict__ coef,
-                                                      const T *__restrict__ beta, T *__restrict__ out) {
+                                                      const T *__restrict__ beta, T *__restrict__ out, int cp) {
     griddep_wait();
     const int t = blockIdx.y, chunk = blockIdx.x;
     const int C = X.C(), nv = C >> 3, npl = 256 / nv;
     const int tid = threadIdx.x, v = tid % nv, pl = tid / nv;
     if (pl >= npl) return;
-    const int cp = chunk_pix(C);
     const int p0 = chunk * cp, p1 = min(X.HW, p0 + cp);
     const VecSrc<T> src = vec_src(X, t, v);
     float mu[8], sc[8], be[8];
@@ -283,12 +283,12 @@ __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const
     }
     T *o = out + (size_t)t * X.HW * C + 8 * v;
     int p = p0 + pl;
-    if (src.mode == 1) {   // hot path: 4 pixels' raw loads in flight, then compute + store
-        for (; p + 3 * npl < p1; p += 4 * npl) {
-            float f[4][8];
-            load_fast<T, 4, false>(src, p, npl, f);
+    if (src.mode == 1) {   // hot path: 8 pixels' raw loads in flight, then compute + store
+        for (; p + 7 * npl < p1; p += 8 * npl) {
+            float f[8][8];
+            load_fast<T, 8, false>(src, p, npl, f);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < 8; ++j) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) f[j][i] = silu_t<T>(sizeof(T) == 2 ? fmaf(f[j][i], sc[i], be[i]) : (f[j][i] - mu[i]) * sc[i] + be[i]);
                 store8(o + (size_t)(p + j * npl) * C, f[j]);
@@ -353,7 +353,7 @@ static dvc_status gn_silu_t(const NormArgs &a, cudaStream_t stream) {
                                                    reinterpret_cast<const T *>(a.gamma), coef));
     ++g_launches;
     DVC_CUDA(launch_pdl(gn_silu_kernel<T>, dim3(dim3(nchunk, a.T)), dim3(256), 0, stream, 1, X, coef, reinterpret_cast<const T *>(a.beta),
-                                                             reinterpret_cast<T *>(a.out)));
+                                                             reinterpret_cast<T *>(a.out), chunk_pix(C)));
     ++g_launches;
     return check_launch("gn_silu");
 }
@@ -411,9 +411,15 @@ dvc_status nearest_run(const void *src, void *dst, int T, int hi, int wi, int ho
     DVC_CHECK_ARG((C * dt_size(dt)) % 16 == 0, DVC_ERR_UNSUPPORTED, "nearest: rows must be 16-byte multiples");
     const int nvec = (int)(C * dt_size(dt) / 16);
     dim3 grid((wo * nvec + 255) / 256, ho, T);
+    ProfSlot s0 = prof_begin(stream);
     DVC_CUDA(launch_pdl(nearest_kernel, dim3(grid), dim3(256), 0, stream, 1, reinterpret_cast<const uint4 *>(src), reinterpret_cast<uint4 *>(dst), hi, wi,
                                              ho, wo, nvec));
     ++g_launches;
+    if (s0.idx >= 0) {
+        char lab[96];
+        snprintf(lab, sizeof(lab), "nearest T=%d %dx%d->%dx%d C=%d", T, hi, wi, ho, wo, C);
+        prof_end_aux(s0, stream, lab);
+    }
     return check_launch("nearest");
 }
 
@@ -464,6 +470,7 @@ dvc_status box_stats_run(const void *x, int T, int H, int W, int C, dvc_dtype dt
     dim3 grid(tx * ty, T);
     // e.g. a packed carry slice may start at any element offset: vector loads only when aligned
     const int vec_ok = (C % 8 == 0) && ((uintptr_t)x % 16 == 0) && ((C * dt_size(dt)) % 16 == 0);
+    ProfSlot s0 = prof_begin(stream);
     switch (dt) {
         case DVC_BF16:
             DVC_CUDA(launch_pdl(box_stats_kernel<__nv_bfloat16>, dim3(grid), dim3(128), 0, stream, 1, reinterpret_cast<const __nv_bfloat16 *>(x), H, W,
@@ -478,6 +485,7 @@ dvc_status box_stats_run(const void *x, int T, int H, int W, int C, dvc_dtype dt
                                                               vec_ok, stats));
     }
     ++g_launches;
+    prof_end_aux(s0, stream, "box_stats");
     return check_launch("box_stats");
 }
 
@@ -550,28 +558,48 @@ static dvc_status gn_silu_box_t(const NormArgs &a, const BoxStatsIn &bs, int H, 
     ShiftSrc<T> X{reinterpret_cast<const T *>(a.xa), reinterpret_cast<const T *>(a.xb),
                   reinterpret_cast<const T *>(a.carry), a.ca, a.cb, a.cs, a.HW};
     const int C = a.ca + a.cb;
-    const int nchunk = (a.HW + chunk_pix(C) - 1) / chunk_pix(C);
+    // one pass of 8 pixels in flight per thread: many short CTAs, no dependent load chains
+    const int cp = (256 / (C / 8)) * 8;
+    const int nchunk = (a.HW + cp - 1) / cp;
     float2 *coef = reinterpret_cast<float2 *>(a.ws);
+    ProfSlot s0 = prof_begin(stream);
     DVC_CUDA(launch_pdl(gn_finalize_box_kernel<T>, dim3(dim3(a.G, a.T)), dim3(256), 0, stream, 1, 
         reinterpret_cast<const float2 *>(bs.a), a.ca, reinterpret_cast<const float2 *>(bs.b), a.cb,
         reinterpret_cast<const float2 *>(bs.carry), a.cs, boxes_per_frame(H, W), a.G, (double)(C / a.G) * a.HW,
         (double)a.eps, reinterpret_cast<const T *>(a.gamma), nullptr, coef));
     ++g_launches;
+    if (s0.idx >= 0) {
+        char lab[96];
+        snprintf(lab, sizeof(lab), "gn_finalize T=%d G=%d C=%d nbox=%d", a.T, a.G, C, boxes_per_frame(H, W));
+        prof_end_aux(s0, stream, lab);
+    }
+    ProfSlot s1 = prof_begin(stream);
     DVC_CUDA(launch_pdl(gn_silu_kernel<T>, dim3(dim3(nchunk, a.T)), dim3(256), 0, stream, 1, X, coef, reinterpret_cast<const T *>(a.beta),
-                                                             reinterpret_cast<T *>(a.out)));
+                                                             reinterpret_cast<T *>(a.out), cp));
     ++g_launches;
+    if (s1.idx >= 0) {
+        char lab[96];
+        snprintf(lab, sizeof(lab), "gn_silu T=%d HW=%d C=%d cs=%d", a.T, a.HW, C, a.cs);
+        prof_end_aux(s1, stream, lab);
+    }
     return check_launch("gn_silu_box");
 }
 
 template <typename T>
 static dvc_status gn_coef_t(const NormArgs &a, const BoxStatsIn &bs, int H, int W, cudaStream_t stream) {
     const int C = a.ca + a.cb;
+    ProfSlot s0 = prof_begin(stream);
     DVC_CUDA(launch_pdl(gn_finalize_box_kernel<T>, dim3(dim3(a.G, a.T)), dim3(256), 0, stream, 1, 
         reinterpret_cast<const float2 *>(bs.a), a.ca, reinterpret_cast<const float2 *>(bs.b), a.cb,
         reinterpret_cast<const float2 *>(bs.carry), a.cs, boxes_per_frame(H, W), a.G, (double)(C / a.G) * a.HW,
         (double)a.eps, reinterpret_cast<const T *>(a.gamma), reinterpret_cast<const T *>(a.beta),
         reinterpret_cast<float2 *>(a.out)));
     ++g_launches;
+    if (s0.idx >= 0) {
+        char lab[96];
+        snprintf(lab, sizeof(lab), "gn_coef T=%d G=%d C=%d nbox=%d", a.T, a.G, C, boxes_per_frame(H, W));
+        prof_end_aux(s0, stream, lab);
+    }
     return check_launch("gn_coef");
 }
 

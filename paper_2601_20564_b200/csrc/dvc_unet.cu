@@ -588,7 +588,34 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         }
     }
     // out = conv_out(SiLU(GN_out(h)))
-    {
+    if (conv_fz_applicable(n->lh[0], n->lw[0], dt) && (W[0] / c.groups) > 0) {
+        // fused: GN_out coefficients from h's box statistics, GN-apply + SiLU inside conv_out's
+        // operand producer (no GN_out tensor in HBM)
+        float2 *coef = reinterpret_cast<float2 *>(rbws);
+        NormArgs na{h, nullptr, nullptr, W[0], 0, 0, T, hw(0), c.groups, c.eps, n->gno_w, n->gno_b, coef, nullptr};
+        if ((st = gn_coef_box_run(na, BoxStatsIn{hs, nullptr, nullptr}, n->lh[0], n->lw[0], dt, s)) != DVC_OK)
+            return st;
+        FzDesc f{};
+        if (n->conv_out.pk) f.seg[0] = FzDesc::Seg{h, W[0], 0, 9, 1, 0, n->conv_out.pk, 64, 0, 0, 1};
+        else f.seg[0] = FzDesc::Seg{h, W[0], 0, 9, 1, 0, n->conv_out.w, 9 * W[0], 0, W[0], 0};
+        f.nseg = 1;
+        f.T = T;
+        f.H = n->lh[0];
+        f.W = n->lw[0];
+        f.cout = c.c_lat;
+        f.coef = coef;
+        f.cop = W[0];
+        f.bias0 = n->conv_out.b;
+        f.out = out;
+        f.dt = dt;
+        ConvDesc prof{};
+        prof.seg[0] = ConvSeg{h, W[0], SEG_SAME, n->lh[0], n->lw[0], 9, n->conv_out.w, 9 * W[0], 0, W[0]};
+        prof.nseg = 1, prof.T = T, prof.ho = n->lh[0], prof.wo = n->lw[0], prof.cout = c.c_lat;
+        ProfSlot slot = prof_begin(s);
+        st = conv_fz_run(f, s);
+        prof_end(slot, s, conv_flops(prof), "fz_out", prof);
+        if (st != DVC_OK) return st;
+    } else {
         uint8_t *gnws = reinterpret_cast<uint8_t *>(rbws);
         void *op = gnws + align256(gn_workspace_bytes(T, hw(0), c.groups, W[0]));
         NormArgs na{h, nullptr, nullptr, W[0], 0, 0, T, hw(0), c.groups, c.eps, n->gno_w, n->gno_b, op, gnws};

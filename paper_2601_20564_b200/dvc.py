@@ -66,10 +66,10 @@ def profile_end():
     return ms.value, fl.value, n.value
 
 
-def profile_records(n: int):
-    """-> [(label, ms, flops)] for the n launches of the last profile window."""
+def profile_records(n: int | None = None):
+    """-> [(label, ms, flops)] for the instrumented launches of the last profile window."""
     out = []
-    for i in range(n):
+    for i in range(lib().dvc_profile_record_count() if n is None else n):
         ms, fl, lab = ctypes.c_double(), ctypes.c_double(), ctypes.create_string_buffer(128)
         check(lib().dvc_profile_record(i, ctypes.byref(ms), ctypes.byref(fl), lab, 128))
         out.append((lab.value.decode(), ms.value, fl.value))

@@ -34,7 +34,7 @@ peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflo
 dvc.profile_begin(4096)
 dvc.dvc_unet_decode_gop(net, lat, ctx, out=out, workspace=ws)
 ms, fl, n = dvc.profile_end()
-rec = dvc.profile_records(n)
+rec = dvc.profile_records()
 g = collections.OrderedDict()
 for lab, t, f in rec:
     e = g.setdefault(lab, [0, 0.0, 0.0])
@@ -42,6 +42,8 @@ for lab, t, f in rec:
     e[1] += t
     e[2] += f
 print(f"conv total {ms:.3f} ms, {fl / ms / 1e9:.1f} TFLOP/s over {n} launches (peak {peak})")
+aux = sum(t for lab, (c, t, f) in g.items() if f == 0)
+print(f"other instrumented kernels {aux:.3f} ms")
 for lab, (c, t, f) in sorted(g.items(), key=lambda x: -x[1][1]):
     tf = f / t / 1e9
-    print(f"{lab:48s} x{c:2d} {t:7.3f} ms {tf:7.1f} TF/s {tf / peak:5.2f}")
+    print(f"{lab:48s} x{c:2d} {t:7.3f} ms {tf:7.1f} TF/s {tf / peak:5.2f}" if f else f"{lab:48s} x{c:2d} {t:7.3f} ms")
