@@ -254,6 +254,91 @@ def resblock(X, carry, w: dict, G: int, P: int, eps: float = 1e-5, mode=None,
 
 
 # --------------------------------------------------------------------------
+# f1. Self-attention Transformer2D blocks ("U-Net"; P:525 parameter count;
+# readings R21-R24 in DESIGN.md section 3).  SD-2.1's Transformer2DModel with
+# the text cross-attention removed: GN -> proj_in -> [LN -> self-attention ->
+# +res] -> [LN -> GEGLU FF -> +res] -> proj_out -> + block input.
+# --------------------------------------------------------------------------
+def layernorm(X, gamma, beta, eps: float = 1e-5):
+    """LayerNorm over the channels of every pixel, biased two-pass variance (R21)."""
+    X = _f64(X)
+    mu = X.mean(axis=-1, keepdims=True)
+    var = ((X - mu) ** 2).mean(axis=-1, keepdims=True)
+    return (X - mu) / np.sqrt(var + eps) * _f64(gamma) + _f64(beta)
+
+
+def gelu(X):
+    """Exact GELU x * Phi(x) = x/2 * (1 + erf(x / sqrt 2)) (GEGLU gate, R21)."""
+    from scipy.special import erf
+    X = _f64(X)
+    return 0.5 * X * (1.0 + erf(X / np.sqrt(2.0)))
+
+
+def attention(Q, K, V, head_dim: int, rows=None):
+    """Multi-head self-attention of every frame over its own h*w tokens (R22):
+    for each frame t and head j (channels [j*d, (j+1)*d)),
+        O_j = softmax(Q_j K_j^T / sqrt(d)) V_j   (row softmax).
+    Q, K, V [T,N,C]; rows: optional query indices (sampled check at large N).
+    Returns [T,N,C] (or [T,len(rows),C])."""
+    Q, K, V = _f64(Q), _f64(K), _f64(V)
+    T, N, C = Q.shape
+    if C % head_dim:
+        raise ValueError("divisibility error: head_dim must divide C")
+    if rows is not None:
+        Q = Q[:, rows]
+    O = np.empty_like(Q)
+    d = head_dim
+    for t in range(T):
+        for j in range(C // d):
+            sl = slice(j * d, (j + 1) * d)
+            S = Q[t, :, sl] @ K[t, :, sl].T / np.sqrt(d)
+            S = S - S.max(axis=1, keepdims=True)
+            Pm = np.exp(S)
+            Pm = Pm / Pm.sum(axis=1, keepdims=True)
+            O[t, :, sl] = Pm @ V[t, :, sl]
+    return O
+
+
+TF_ORDER = ("gn_w", "gn_b", "proj_in_w", "proj_in_b", "ln1_w", "ln1_b", "qkv_w", "out_w", "out_b",
+            "ln2_w", "ln2_b", "ff1_w", "ff1_b", "ff2_w", "ff2_b", "proj_out_w", "proj_out_b")
+
+
+def tf_shapes(C: int) -> dict:
+    """Tensor shapes of one Transformer2D block of width C (blob order TF_ORDER)."""
+    return {"gn_w": (C,), "gn_b": (C,), "proj_in_w": (C, C), "proj_in_b": (C,),
+            "ln1_w": (C,), "ln1_b": (C,), "qkv_w": (3 * C, C), "out_w": (C, C), "out_b": (C,),
+            "ln2_w": (C,), "ln2_b": (C,), "ff1_w": (8 * C, C), "ff1_b": (8 * C,),
+            "ff2_w": (C, 4 * C), "ff2_b": (C,), "proj_out_w": (C, C), "proj_out_b": (C,)}
+
+
+def transformer(X, w: dict, G: int, head_dim: int, eps_gn: float = 1e-6, eps_ln: float = 1e-5,
+                mode=None):
+    """One Transformer2D block over X [T,h,w,C] (R21-R24), frames independent:
+        a  = GN(X)                          (G groups, eps 1e-6, no SiLU)
+        h0 = proj_in(a)                     (1x1, C -> C, bias)
+        q,k,v = split(LN1(h0) W_qkv^T)      (no bias)
+        h1 = out(attention(q, k, v)) + h0   (1x1 + bias)
+        f  = ff1(LN2(h1))                   (C -> 8C, bias); g = f[:4C] * gelu(f[4C:])
+        h2 = ff2(g) + h1                    (4C -> C, bias)
+        Y  = proj_out(h2) + X               (1x1 + bias)
+    mode rounds every stored tensor to 16-bit (R24)."""
+    X = _f64(X)
+    T, H, W, C = X.shape
+    N = H * W
+    a = rnd(groupnorm(X, G, w["gn_w"], w["gn_b"], eps_gn), mode)
+    h0 = rnd(conv1x1(a, w["proj_in_w"], w["proj_in_b"]), mode)
+    l1 = rnd(layernorm(h0, w["ln1_w"], w["ln1_b"], eps_ln), mode)
+    qkv = rnd(conv1x1(l1, w["qkv_w"]), mode).reshape(T, N, 3 * C)
+    o = rnd(attention(qkv[..., :C], qkv[..., C:2 * C], qkv[..., 2 * C:], head_dim), mode)
+    h1 = rnd(conv1x1(o.reshape(T, H, W, C), w["out_w"], w["out_b"]) + h0, mode)
+    l2 = rnd(layernorm(h1, w["ln2_w"], w["ln2_b"], eps_ln), mode)
+    f = rnd(conv1x1(l2, w["ff1_w"], w["ff1_b"]), mode)
+    g = rnd(f[..., :4 * C] * gelu(f[..., 4 * C:]), mode)
+    h2 = rnd(conv1x1(g, w["ff2_w"], w["ff2_b"]) + h1, mode)
+    return rnd(conv1x1(h2, w["proj_out_w"], w["proj_out_b"]) + X, mode)
+
+
+# --------------------------------------------------------------------------
 # a9-a10. The pruned U-Net ResBlock skeleton (P:110, P:320; R1, R9-R11)
 # --------------------------------------------------------------------------
 def unet_blocks(width=(240, 480, 960, 960)):
@@ -326,8 +411,14 @@ def _rb_weights(it, cin, cout):
     return w
 
 
+def _tf_weights(it, C):
+    sh = tf_shapes(C)
+    return {k: _take(it, sh[k], k) for k in TF_ORDER}
+
+
 def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int = 8,
-             eps: float = 1e-5, carries=None, mode=None, record=None, shift="batch", halo=None):
+             eps: float = 1e-5, carries=None, mode=None, record=None, shift="batch", halo=None,
+             attention: bool = False, head_dim: int = 48):
     """The pruned U-Net's ResBlock skeleton over T frames of one chain (R1, R11):
         x0 = conv_in(concat(Lbar, Cm));  push x0
         for level l = 0..3: two ResBlocks (push each); if l < 3: conv3x3 stride 2 (push)
@@ -335,7 +426,10 @@ def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int 
         for u = 0..3 (level 3-u): three ResBlocks on concat(h, pop());
                                   if u < 3: nearest to the next skip's size, conv3x3
         out = conv_out(silu(gn_out(h)))
-    The 16 self-attention Transformer2D blocks are elided (identity; NEXT-1).
+    attention=False: the 16 self-attention Transformer2D blocks are elided (identity).
+    attention=True (f1, full U-Net, R23): a Transformer2D block follows every ResBlock of
+    down levels 0-2, mid.r0, and every ResBlock of up levels 2-0; its weights follow that
+    ResBlock's in the blob (TF_ORDER).
     weights: iterable of (name, array) in the blob order of include/dvc.h.
     carries: list of 22 slices [h_l, w_l, Cin_k/P] (None = chain start, zeros).
     record: optional list that receives every ResBlock output.
@@ -351,6 +445,11 @@ def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int 
         carries = [None] * len(blocks)
     k_out = []
     bi = 0
+
+    def run_tf(h):
+        if not attention:
+            return h
+        return transformer(h, _tf_weights(it, h.shape[-1]), G, head_dim, mode=mode)
 
     def run_block(h):
         nonlocal bi
@@ -373,6 +472,8 @@ def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int 
     for l in range(4):
         for _ in range(2):
             h = run_block(h)
+            if l < 3:
+                h = run_tf(h)
             skips.append(h)
         if l < 3:
             C = h.shape[-1]
@@ -380,11 +481,15 @@ def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int 
             bd = _take(it, (C,), "down_b")
             h = rnd(conv2d(h, wd, bd, stride=2, pad=1), mode)
             skips.append(h)
-    for _ in range(2):
+    for r in range(2):
         h = run_block(h)
+        if r == 0:
+            h = run_tf(h)
     for u in range(4):
         for _ in range(3):
             h = run_block(np.concatenate([h, skips.pop()], axis=-1))
+            if u > 0:
+                h = run_tf(h)
         if u < 3:
             C = h.shape[-1]
             Ho, Wo = skips[-1].shape[1], skips[-1].shape[2]

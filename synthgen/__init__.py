@@ -71,6 +71,36 @@ RB_ORDER = ("gn1_w", "gn1_b", "conv1_w", "conv1_b", "gn2_w", "gn2_b",
             "conv2_w", "conv2_b", "sc_w", "sc_b")
 
 
+def _linear(g, cout, cin, bias=True):
+    bound = 1.0 / np.sqrt(cin)
+    w = g.uniform(-bound, bound, size=(cout, cin)).astype(np.float32)
+    b = g.uniform(-bound, bound, size=(cout,)).astype(np.float32) if bias else None
+    return w, b
+
+
+TF_ORDER = ("gn_w", "gn_b", "proj_in_w", "proj_in_b", "ln1_w", "ln1_b", "qkv_w", "out_w", "out_b",
+            "ln2_w", "ln2_b", "ff1_w", "ff1_b", "ff2_w", "ff2_b", "proj_out_w", "proj_out_b")
+
+
+def transformer_weights(C: int, seed: int = SEED_WEIGHTS, g=None, qkv_scale: float = 1.0) -> dict:
+    """One Transformer2D block's parameters (reading R21; blob order TF_ORDER):
+    Linear layers PyTorch-default U(+-1/sqrt(fan_in)); norms gamma ~ U(0.5,1.5),
+    beta ~ U(-0.5,0.5).  qkv_scale > 1 sharpens the attention (test-only knob)."""
+    g = rng(seed) if g is None else g
+    d = {}
+    d["gn_w"], d["gn_b"] = _gn(g, C)
+    d["proj_in_w"], d["proj_in_b"] = _linear(g, C, C)
+    d["ln1_w"], d["ln1_b"] = _gn(g, C)
+    d["qkv_w"], _ = _linear(g, 3 * C, C, bias=False)
+    d["qkv_w"] = (d["qkv_w"] * qkv_scale).astype(np.float32)
+    d["out_w"], d["out_b"] = _linear(g, C, C)
+    d["ln2_w"], d["ln2_b"] = _gn(g, C)
+    d["ff1_w"], d["ff1_b"] = _linear(g, 8 * C, C)
+    d["ff2_w"], d["ff2_b"] = _linear(g, C, 4 * C)
+    d["proj_out_w"], d["proj_out_b"] = _linear(g, C, C)
+    return d
+
+
 def expansion_weights(c_lat: int = 256, c_in: int = 192, seed: int = SEED_WEIGHTS):
     """Encoder-side Latent Channel Expansion 1x1 conv (reading R13): W [c_lat, c_in], b."""
     w, b = _conv(rng(seed), c_lat, 1, c_in)
@@ -78,13 +108,15 @@ def expansion_weights(c_lat: int = 256, c_in: int = 192, seed: int = SEED_WEIGHT
 
 
 def unet_weights(width=(240, 480, 960, 960), c_lat: int = 256, c_ctx: int = 256,
-                 seed: int = SEED_WEIGHTS):
+                 seed: int = SEED_WEIGHTS, attention: bool = False, qkv_scale: float = 1.0):
     """All skeleton tensors as [(name, float32 array)] in the blob order that
     include/dvc.h documents for dvc_unet_create:
       conv_in{w,b}; the 22 ResBlocks in U-Net order, each
       {gn1_w,gn1_b,conv1_w,conv1_b,gn2_w,gn2_b,conv2_w,conv2_b[,sc_w,sc_b]}, with the
       stride-2 conv{w,b} after down_l.r1 (l<3) and the post-upsample conv{w,b}
-      after up_u.r2 (u<3); then gn_out{w,b}; conv_out{w,b}."""
+      after up_u.r2 (u<3); then gn_out{w,b}; conv_out{w,b}.
+    attention=True (full U-Net, f1): a Transformer2D block's tensors (TF_ORDER) follow
+      every ResBlock of down levels 0-2, mid.r0 and every ResBlock of up levels 2-0."""
     g = rng(seed)
     out = []
 
@@ -99,6 +131,12 @@ def unet_weights(width=(240, 480, 960, 960), c_lat: int = 256, c_ctx: int = 256,
             if d[k] is not None:
                 out.append((f"{name}.{k}", d[k]))
 
+    def tf(name, C):
+        if attention:
+            d = transformer_weights(C, g=g, qkv_scale=qkv_scale)
+            for k in TF_ORDER:
+                out.append((f"{name}.tf.{k}", d[k]))
+
     conv("conv_in", width[0], c_lat + c_ctx)
     skip_ch = [width[0]]
     cur = width[0]
@@ -106,17 +144,23 @@ def unet_weights(width=(240, 480, 960, 960), c_lat: int = 256, c_ctx: int = 256,
         for r in range(2):
             block(f"down{l}.r{r}", cur, width[l])
             cur = width[l]
+            if l < 3:
+                tf(f"down{l}.r{r}", cur)
             skip_ch.append(cur)
         if l < 3:
             conv(f"down{l}.ds", cur, cur)
             skip_ch.append(cur)
     for r in range(2):
         block(f"mid.r{r}", cur, cur)
+        if r == 0:
+            tf("mid.r0", cur)
     for u in range(4):
         lvl = 3 - u
         for r in range(3):
             block(f"up{u}.r{r}", cur + skip_ch.pop(), width[lvl])
             cur = width[lvl]
+            if u > 0:
+                tf(f"up{u}.r{r}", cur)
         if u < 3:
             conv(f"up{u}.us", cur, cur)
     gw, gb = _gn(g, cur)
