@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define DVC_ABI_VERSION 1
+#define DVC_ABI_VERSION 2
 
 typedef enum {
     DVC_OK = 0,
@@ -126,6 +126,46 @@ DVC_API dvc_status dvc_debug_shift_gather(const void *x_a, const void *x_b, int 
                                   void *xs, void *stream);
 
 /* ------------------------------------------------------------------------
+ * f1.  One self-attention Transformer2D block of the full U-Net (the
+ * U-Net of SD-2.1 via AdcSR; 444.78 M parameters with these blocks;
+ * readings R21-R24 in DESIGN.md): SD-2.1's Transformer2DModel with the text
+ * cross-attention removed, frames independent (no temporal shift):
+ *   a  = GN(x)             groups, eps_gn (1e-6), per frame, no SiLU
+ *   h0 = a proj_in_w^T + proj_in_b                  ([C][C])
+ *   q|k|v = LN1(h0) qkv_w^T                         ([3C][C], no bias)
+ *   o  = per head j (channels [j*d,(j+1)*d)): softmax(q_j k_j^T / sqrt d) v_j
+ *        over the H*W tokens of the frame (row-major y, x)
+ *   h1 = o out_w^T + out_b + h0                     ([C][C])
+ *   f  = LN2(h1) ff1_w^T + ff1_b                    ([8C][C]); g = f[:4C] * gelu(f[4C:])
+ *   h2 = g ff2_w^T + ff2_b + h1                     ([C][4C])
+ *   y  = h2 proj_out_w^T + proj_out_b + x           ([C][C])
+ * LayerNorms: eps_ln (1e-5), per-channel affine.  gelu is the exact erf form.
+ * x, y [T,H,W,C] NHWC device pointers in dt; y MAY alias x (in place).
+ * Requirements: C % 16 == 0, C <= 1024, C % groups == 0, head_dim in
+ * {16, 32, 48, 64} dividing C, 1 <= T < 256.  16-bit dt: tensor cores
+ * (tcgen05) for the linear layers and the attention; DVC_F32: SIMT validation
+ * path.  Errors return before any launch.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    int c, groups, head_dim;
+    float eps_gn, eps_ln;
+    dvc_dtype dt;
+    const void *gn_w, *gn_b, *proj_in_w, *proj_in_b, *ln1_w, *ln1_b, *qkv_w, *out_w, *out_b;
+    const void *ln2_w, *ln2_b, *ff1_w, *ff1_b, *ff2_w, *ff2_b, *proj_out_w, *proj_out_b;
+} dvc_transformer;
+
+DVC_API dvc_status dvc_transformer_workspace_size(const dvc_transformer *b, int T, int H, int W, size_t *bytes);
+DVC_API dvc_status dvc_transformer_forward(const dvc_transformer *b, const void *x, int T, int H, int W, void *y,
+                                           void *workspace, size_t ws_bytes, void *stream);
+
+/* The attention step alone: qkv [T,N,3C] (q | k | v channel blocks, head j at
+ * channels [j*d,(j+1)*d) of each) -> out [T,N,C], softmax(q k^T / sqrt d) v per
+ * frame and head.  workspace >= dvc_attention_workspace_size (the transposed V). */
+DVC_API dvc_status dvc_attention_workspace_size(int T, int N, int C, dvc_dtype dt, size_t *bytes);
+DVC_API dvc_status dvc_attention_forward(const void *qkv, int T, int N, int C, int head_dim, dvc_dtype dt, void *out,
+                                         void *workspace, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------
  * a9 + a10 + e.  The pruned U-Net's ResBlock skeleton over a group of frames
  * (reading R1):
  *   x0 = conv_in(concat(Lbar_t, Cm_t))                 (P:110, 512 -> width[0])
@@ -134,8 +174,13 @@ DVC_API dvc_status dvc_debug_shift_gather(const void *x_a, const void *x_b, int 
  *   up levels 3..0: 3 OTSM ResBlocks on concat(h, skip) each, nearest resize to
  *   the next skip's size + 3x3 conv after the first three (R11)
  *   out = conv_out(SiLU(GN_out(h)))                    (width[0] -> c_lat)
- * The 16 self-attention Transformer2D blocks are not part of this path (they
- * are the next row, NEXT-1) and are treated as identity.
+ * head_dim == 0: the 16 self-attention Transformer2D blocks are elided
+ * (identity; the ResBlock skeleton of SURVEY 8a).  head_dim > 0 (f1, the full
+ * U-Net): a Transformer2D block (dvc_transformer, groups/eps_gn 1e-6/eps_ln
+ * 1e-5) follows every ResBlock of down levels 0-2, mid.r0 and every ResBlock
+ * of up levels 2-0 (R23); its 17 tensors (gn_w, gn_b, proj_in_w, proj_in_b,
+ * ln1_w, ln1_b, qkv_w, out_w, out_b, ln2_w, ln2_b, ff1_w, ff1_b, ff2_w, ff2_b,
+ * proj_out_w, proj_out_b) follow that ResBlock's in the blob.
  *
  * Weight blob (host memory, dt elements, concatenated in this order):
  *   conv_in{w [W0][3][3][c_lat+c_ctx], b}
@@ -155,6 +200,7 @@ typedef struct {
     dvc_dtype dt;
     int h, w;          /* latent size, e.g. 90x160 (720p), 135x240 (1080p) */
     int max_T;         /* largest T_local per call; sizes the workspace */
+    int head_dim;      /* 0 = skeleton (attention elided); 16/32/48/64 = full U-Net (48: R22) */
 } dvc_unet_config;
 
 typedef struct dvc_unet dvc_unet;

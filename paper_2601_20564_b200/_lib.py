@@ -36,7 +36,17 @@ class dvc_resblock(ctypes.Structure):
 
 class dvc_unet_config(ctypes.Structure):
     _fields_ = [("width", c_int * 4), ("c_lat", c_int), ("c_ctx", c_int), ("groups", c_int), ("shift_p", c_int),
-                ("eps", c_float), ("dt", c_int), ("h", c_int), ("w", c_int), ("max_T", c_int)]
+                ("eps", c_float), ("dt", c_int), ("h", c_int), ("w", c_int), ("max_T", c_int),
+                ("head_dim", c_int)]
+
+
+TF_FIELDS = ("gn_w", "gn_b", "proj_in_w", "proj_in_b", "ln1_w", "ln1_b", "qkv_w", "out_w", "out_b",
+             "ln2_w", "ln2_b", "ff1_w", "ff1_b", "ff2_w", "ff2_b", "proj_out_w", "proj_out_b")
+
+
+class dvc_transformer(ctypes.Structure):
+    _fields_ = [("c", c_int), ("groups", c_int), ("head_dim", c_int), ("eps_gn", c_float), ("eps_ln", c_float),
+                ("dt", c_int)] + [(f, c_void_p) for f in TF_FIELDS]
 
 
 _SIGS = {
@@ -60,6 +70,13 @@ _SIGS = {
     "dvc_unet_workspace_size": ([c_void_p, c_int, ctypes.POINTER(c_size_t)], c_int),
     "dvc_unet_decode_gop": ([c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_size_t, c_void_p], c_int),
+    "dvc_transformer_workspace_size": ([ctypes.POINTER(dvc_transformer), c_int, c_int, c_int,
+                                        ctypes.POINTER(c_size_t)], c_int),
+    "dvc_transformer_forward": ([ctypes.POINTER(dvc_transformer), c_void_p, c_int, c_int, c_int, c_void_p,
+                                 c_void_p, c_size_t, c_void_p], c_int),
+    "dvc_attention_workspace_size": ([c_int, c_int, c_int, c_int, ctypes.POINTER(c_size_t)], c_int),
+    "dvc_attention_forward": ([c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_size_t,
+                               c_void_p], c_int),
     "dvc_set_conv_engine": ([c_int], c_int),
     "dvc_profile_begin": ([c_int], c_int),
     "dvc_profile_end": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),

@@ -21,6 +21,7 @@
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
 #include "dvc_resblock.cuh"
+#include "dvc_attn.cuh"
 
 using namespace dvc;
 
@@ -96,6 +97,9 @@ struct dvc_unet {
     const void *gno_w = nullptr, *gno_b = nullptr;
     RB blk[22];
     int blevel[22];
+    TF tf[16];      // f1: Transformer2D blocks (cfg.head_dim > 0)
+    int tf_of[22];  // index into tf of the block following ResBlock b, or -1
+    int ntf = 0;
     int lh[4], lw[4];
     size_t carry_off[22];
     size_t carry_total = 0;
@@ -140,7 +144,38 @@ void walk(dvc_unet &n, Take take) {
             r.sc_w = r.sc_b = nullptr;
         }
         n.blevel[bi] = level;
+        n.tf_of[bi] = -1;
         ++bi;
+    };
+    // f1 (R23): a Transformer2D block after the ResBlock just walked; tensors follow its weights
+    n.ntf = 0;
+    auto tfb = [&](int C) {
+        if (c.head_dim <= 0) return;
+        TF &t = n.tf[n.ntf];
+        t.c = C;
+        t.groups = c.groups;
+        t.head_dim = c.head_dim;
+        t.eps_gn = 1e-6f;
+        t.eps_ln = 1e-5f;
+        t.dt = c.dt;
+        t.gn_w = take(C);
+        t.gn_b = take(C);
+        t.proj_in_w = take((size_t)C * C);
+        t.proj_in_b = take(C);
+        t.ln1_w = take(C);
+        t.ln1_b = take(C);
+        t.qkv_w = take((size_t)3 * C * C);
+        t.out_w = take((size_t)C * C);
+        t.out_b = take(C);
+        t.ln2_w = take(C);
+        t.ln2_b = take(C);
+        t.ff1_w = take((size_t)8 * C * C);
+        t.ff1_b = take((size_t)8 * C);
+        t.ff2_w = take((size_t)4 * C * C);
+        t.ff2_b = take(C);
+        t.proj_out_w = take((size_t)C * C);
+        t.proj_out_b = take(C);
+        n.tf_of[bi - 1] = n.ntf++;
     };
     n.conv_in = conv(W[0], c.c_lat + c.c_ctx, 3);
     std::vector<int> skips{W[0]};
@@ -149,6 +184,7 @@ void walk(dvc_unet &n, Take take) {
         for (int r = 0; r < 2; ++r) {
             block(cur, W[l], l, 0);
             cur = W[l];
+            if (l < 3) tfb(cur);
             skips.push_back(cur);
         }
         if (l < 3) {
@@ -156,7 +192,10 @@ void walk(dvc_unet &n, Take take) {
             skips.push_back(cur);
         }
     }
-    for (int r = 0; r < 2; ++r) block(cur, cur, 3, 0);
+    for (int r = 0; r < 2; ++r) {
+        block(cur, cur, 3, 0);
+        if (r == 0) tfb(cur);
+    }
     for (int u = 0; u < 4; ++u) {
         const int l = 3 - u;
         for (int r = 0; r < 3; ++r) {
@@ -164,6 +203,7 @@ void walk(dvc_unet &n, Take take) {
             skips.pop_back();
             block(cur + sk, W[l], l, sk);
             cur = W[l];
+            if (u > 0) tfb(cur);
         }
         if (u < 3) n.us[u] = conv(cur, cur, 3);
     }
@@ -179,6 +219,8 @@ dvc_status validate_cfg(const dvc_unet_config *c) {
                   "latent size >= 8x8 and 1 <= max_T < 256 required");
     DVC_CHECK_ARG(c->groups >= 1 && c->shift_p >= 1 && c->c_lat > 0 && c->c_ctx > 0, DVC_ERR_ARG, "bad config");
     for (int i = 0; i < 4; ++i) DVC_CHECK_ARG(c->width[i] > 0, DVC_ERR_ARG, "bad width");
+    DVC_CHECK_ARG(c->head_dim == 0 || c->head_dim == 16 || c->head_dim == 32 || c->head_dim == 48 || c->head_dim == 64,
+                  DVC_ERR_UNSUPPORTED, "head_dim must be 0 (attention elided) or 16/32/48/64");
     return DVC_OK;
 }
 
@@ -227,6 +269,8 @@ size_t plan_workspace(const dvc_unet &n, int T, size_t *offs /* kRegions */) {
     }
     rbws = std::max(rbws, align256(gn_workspace_bytes(T, (int)hw(0), c.groups, W[0])) + T * hw(0) * W[0] * es);
     for (int l = 1; l < 4; ++l) rbws = std::max(rbws, T * hw(l - 1) * (size_t)W[l] * es);
+    if (c.head_dim > 0)
+        for (int l = 0; l < 4; ++l) rbws = std::max(rbws, transformer_ws_bytes(W[l], T, n.lh[l], n.lw[l], c.dt));
     sz[14] = rbws;
     sz[15] = (n.carry_total * 2 + 2 * hw(0) * 2048) * es;
     size_t total = 0;
@@ -391,6 +435,11 @@ dvc_status dvc_unet_create(const dvc_unet_config *cfg, const void *host_weights,
             delete n;
             return st;
         }
+        if (n->tf_of[b] >= 0 && (st = transformer_validate(n->tf[n->tf_of[b]], 1, n->lh[l], n->lw[l])) != DVC_OK) {
+            cudaFree(n->dweights);
+            delete n;
+            return st;
+        }
         n->carry_off[b] = n->carry_total;
         n->carry_total += (size_t)n->lh[l] * n->lw[l] * ((r.ca + r.cb) / r.P);
     }
@@ -490,6 +539,9 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         void *cout_ptr = nullptr;
         if (carry_out && (world == 1 || rank == world - 1)) cout_ptr = reinterpret_cast<uint8_t *>(carry_out) + off;
         dvc_status e = resblock_launch(r, xa, xb, T, H, Wd, cin_ptr, cout_ptr, y, rbws, s, sa, sb, sy);
+        // f1: the Transformer2D block after this ResBlock, in place on y (its statistics refreshed)
+        if (e == DVC_OK && n->tf_of[bi] >= 0)
+            e = transformer_launch(n->tf[n->tf_of[bi]], y, T, H, Wd, y, rbws, s, sy, sy);
         ++bi;
         return e;
     };

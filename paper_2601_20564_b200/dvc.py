@@ -135,11 +135,57 @@ def dvc_debug_shift_gather(x_a, x_b=None, shift_p: int = 8, carry_in=None, out=N
     return out
 
 
+# ------------------------------------------------------------------ f1 Transformer2D block
+class TransformerParams:
+    """Device-side parameters of one Transformer2D block (keeps the tensors alive)."""
+
+    def __init__(self, tensors: dict, groups: int, head_dim: int, eps_gn: float = 1e-6, eps_ln: float = 1e-5):
+        self.t = {k: tensors[k].contiguous() for k in _lib.TF_FIELDS}
+        self.c = self.t["proj_in_w"].shape[0]
+        dt = self.t["proj_in_w"].dtype
+        self.struct = _lib.dvc_transformer(self.c, groups, head_dim, eps_gn, eps_ln, dtype_code(dt),
+                                           *[self.t[k].data_ptr() for k in _lib.TF_FIELDS])
+
+    def workspace_size(self, T, H, W) -> int:
+        n = ctypes.c_size_t()
+        check(lib().dvc_transformer_workspace_size(ctypes.byref(self.struct), T, H, W, ctypes.byref(n)))
+        return n.value
+
+
+def dvc_transformer_forward(params: TransformerParams, x, out=None, workspace=None, stream=None):
+    """x [T,H,W,C] -> y [T,H,W,C] (out may be x: in place)."""
+    T, H, W, _ = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    if workspace is None:
+        workspace = _ws(params.workspace_size(T, H, W), x.device)
+    check(lib().dvc_transformer_forward(ctypes.byref(params.struct), _ptr(x), T, H, W, _ptr(out), _ptr(workspace),
+                                        workspace.numel() * workspace.element_size(), _stream(stream)))
+    return out
+
+
+def dvc_attention_forward(qkv, head_dim: int, out=None, workspace=None, stream=None):
+    """qkv [T,N,3C] -> out [T,N,C] (multi-head softmax attention per frame)."""
+    T, N, C3 = qkv.shape
+    C = C3 // 3
+    if out is None:
+        out = torch.empty((T, N, C), dtype=qkv.dtype, device=qkv.device)
+    if workspace is None:
+        n = ctypes.c_size_t()
+        check(lib().dvc_attention_workspace_size(T, N, C, dtype_code(qkv.dtype), ctypes.byref(n)))
+        workspace = _ws(n.value, qkv.device)
+    check(lib().dvc_attention_forward(_ptr(qkv), T, N, C, head_dim, dtype_code(qkv.dtype), _ptr(out),
+                                      _ptr(workspace), workspace.numel() * workspace.element_size(),
+                                      _stream(stream)))
+    return out
+
+
 # ------------------------------------------------------------------ a9 + a10 + e
 def unet_config(width=(240, 480, 960, 960), c_lat=256, c_ctx=256, groups=24, shift_p=8, eps=1e-5,
-                dtype=torch.bfloat16, h=90, w=160, max_T=32):
+                dtype=torch.bfloat16, h=90, w=160, max_T=32, head_dim=0):
+    """head_dim 0: ResBlock skeleton (attention elided); 16/32/48/64: full U-Net (f1)."""
     return _lib.dvc_unet_config((ctypes.c_int * 4)(*width), c_lat, c_ctx, groups, shift_p, eps,
-                                dtype_code(dtype), h, w, max_T)
+                                dtype_code(dtype), h, w, max_T, head_dim)
 
 
 def unet_weight_count(cfg) -> int:

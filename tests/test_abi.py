@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version_and_status_strings(L):
-    assert L.dvc_abi_version() == 1
+    assert L.dvc_abi_version() == 2
     assert L.dvc_status_string(2) == b"DVC_ERR_DIVISIBILITY"
 
 
