@@ -111,10 +111,10 @@ void prof_end(ProfSlot s, cudaStream_t stream, double flops, const char *engine,
     g_prof.label[s.idx] = buf;
 }
 
-void prof_end_aux(ProfSlot s, cudaStream_t stream, const char *label) {
+void prof_end_aux(ProfSlot s, cudaStream_t stream, const char *label, double flops) {
     if (s.idx < 0) return;
     cudaEventRecord(g_prof.ev[2 * s.idx + 1], stream);
-    g_prof.flops[s.idx] = 0.0;
+    g_prof.flops[s.idx] = flops;
     g_prof.conv[s.idx] = 0;
     g_prof.label[s.idx] = label;
 }

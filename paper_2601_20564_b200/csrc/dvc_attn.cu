@@ -26,6 +26,7 @@
 // All operands use the no-swizzle canonical layout: 8-row x 16-byte core matrices, core
 // matrices adjacent in K 128 B apart (LBO), 8-row groups SBO apart.
 #include <cuda.h>
+#include <cstdio>
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
 #include "dvc_ptx.cuh"
@@ -191,28 +192,50 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const float *__restrict_
 }
 
 // ----------------------------------------------------------------- attention, tcgen05
-constexpr int kAttnThreads = 128;
+// One CTA = two 128-query tiles (256 queries) of one (frame, head), 10 warps:
+//   warps 0-3  softmax group 0 (tile 0; thread r owns query row r = TMEM lane r)
+//   warps 4-7  softmax group 1 (tile 1)
+//   warp 8     MMA issuer (one elected lane): S_t = Q_t K_j^T, PV_t = P_t V_j
+//   warp 9     TMA producer: Q tiles once, then a 3-stage ring of (K_j, V_j^T) tiles
+// TMEM (512 columns): S_0 [0,128), S_1 [128,256), PV_0 [256 + 64 b), PV_1 [384 + 64 b), b = j & 1.
+// The MMA warp issues PV_t(j) then S_t(j+1) as soon as group t has released S_t(j) and
+// written P_t(j), so the two groups drift half an iteration apart and the exp2 units (the
+// bound for head_dim 48: 192 FLOP per exp) stay busy while the other group waits.
+// All tiles are TMA'd with 3D views whose first dim is one 16-byte core-matrix row, which lands
+// them directly in the canonical no-swizzle K-major UMMA layout:
+//   Q/K [rows][D]:  box {8, 128, D/8}   -> core (r8, kc) at kc*2048 + r8*128   (LBO 2048, SBO 128)
+//   V^T [D][keys]:  box {8, D, 16}      -> core (d8, kc) at kc*D*16 + d8*128   (LBO D*16, SBO 128)
+//   P   [128][128]: written by the softmax threads in the same kc*2048 + r8*128 form
+constexpr int kAttnThreads = 320;
+constexpr int kAttnStages = 3;
 template <int D>
 struct AttnSmem {
-    static constexpr int Q = 128 * D * 2;        // [128 q][D]      SBO = D*16
-    static constexpr int K = 128 * D * 2;        // [128 keys][D]   SBO = D*16
-    static constexpr int V = D * 128 * 2;        // [D][128 keys]   SBO = 2048
-    static constexpr int P = 128 * 128 * 2;      // [128 q][128 keys] SBO = 2048
-    static constexpr int off_q = 0, off_k = Q, off_v = off_k + 2 * K, off_p = off_v + 2 * V;
-    static constexpr int off_bar = off_p + P;
-    static constexpr int bytes = off_bar + 64;
+    static constexpr int Q = 128 * D * 2;        // one query tile
+    static constexpr int K = 128 * D * 2;        // one key tile
+    static constexpr int V = D * 128 * 2;        // one transposed value tile
+    static constexpr int P = 128 * 128 * 2;      // one probability tile
+    static constexpr int off_q = 0, off_k = 2 * Q, off_v = off_k + kAttnStages * K;
+    static constexpr int off_p = off_v + kAttnStages * V;
+    static constexpr int off_bar = off_p + 2 * P;
+    // barriers: q_full, kv_full[3], kv_empty[3], s_full[2], s_free[2], p_full[2], o_full[2][2]
+    static constexpr int nbar = 1 + 2 * kAttnStages + 2 + 2 + 2 + 4;
+    static constexpr int bytes = off_bar + nbar * 8 + 16 + 1024;   // + TMEM slot + alignment slack
+};
+
+struct AttnMaps {
+    CUtensorMap q, k, v;   // q and k: the same qkv view at different channel offsets
 };
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ float ex2f(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
 }
 template <typename T>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -226,172 +249,202 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(kAttnThreads, 1) attn_tc_kernel(const T *__restrict__ qkv, const T *__restrict__ vt,
-                                                                  T *__restrict__ out, int N, int Npad, int C,
-                                                                  float scale_log2, uint32_t idesc_s,
-                                                                  uint32_t idesc_o) {
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_tc_kernel(const __grid_constant__ AttnMaps maps, T *__restrict__ out, int N, int C, float scale_log2,
+                   uint32_t idesc_s, uint32_t idesc_o) {
     using L = AttnSmem<D>;
-    extern __shared__ __align__(1024) uint8_t smem[];
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(smem);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::off_bar);
-    uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + L::off_bar + 16);
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int t = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * 128;
+    const uint32_t bar0 = sb + L::off_bar;
+    const uint32_t q_full = bar0, kv_full = bar0 + 8, kv_empty = kv_full + 8 * kAttnStages;
+    const uint32_t s_full = kv_empty + 8 * kAttnStages, s_free = s_full + 16, p_full = s_free + 16;
+    const uint32_t o_full = p_full + 16;   // [t][b] at o_full + 8 * (2 t + b)
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + L::off_bar + L::nbar * 8);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int t = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * 256;
+    const int nkt = (N + 127) / 128;
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        uint64_t *b = reinterpret_cast<uint64_t *>(smem + L::off_bar);
+        mbar_init(&b[0], 1);
+        for (int i = 0; i < kAttnStages; ++i) {
+            mbar_init(&b[1 + i], 1);
+            mbar_init(&b[1 + kAttnStages + i], 1);
+        }
+        const int sf = 1 + 2 * kAttnStages;
+        mbar_init(&b[sf], 1), mbar_init(&b[sf + 1], 1);          // s_full (tcgen05.commit)
+        mbar_init(&b[sf + 2], 4), mbar_init(&b[sf + 3], 4);      // s_free (one arrive per softmax warp)
+        mbar_init(&b[sf + 4], 4), mbar_init(&b[sf + 5], 4);      // p_full
+        for (int i = 0; i < 4; ++i) mbar_init(&b[sf + 6 + i], 1);   // o_full
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) tmem_alloc<1>(smem_u32(tslot), 256);
+    if (warp == 9 && lane == 0) {
+        tma_prefetch(&maps.q);
+        tma_prefetch(&maps.k);
+        tma_prefetch(&maps.v);
+    }
+    if (warp == 8) tmem_alloc<1>(smem_u32(tslot), 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    const uint32_t tS = tmem, tO = tmem + 128;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     griddep_wait();
 
-    const size_t ld = 3 * (size_t)C;
-    const T *qbase = qkv + (size_t)t * N * ld + h * D;
-    const T *kbase = qbase + C;
-    const T *vbase = vt + ((size_t)t * C + h * D) * Npad;
-    constexpr int DC = D / 8;   // 16-byte chunks per Q/K row
-    // Q tile
-    for (int i = tid; i < 128 * DC; i += kAttnThreads) {
-        const int r = i / DC, kc = i - r * DC;
-        const int n = q0 + r;
-        const T *src = qbase + (size_t)(n < N ? n : 0) * ld + kc * 8;
-        cp_async_16(sb + L::off_q + (r >> 3) * (D * 16) + kc * 128 + (r & 7) * 16, src, n < N ? 16u : 0u);
-    }
-    auto load_kv = [&](int j, int buf) {
-        const int k0 = j * 128;
-        for (int i = tid; i < 128 * DC; i += kAttnThreads) {
-            const int r = i / DC, kc = i - r * DC;
-            const int n = k0 + r;
-            const T *src = kbase + (size_t)(n < N ? n : 0) * ld + kc * 8;
-            cp_async_16(sb + L::off_k + buf * L::K + (r >> 3) * (D * 16) + kc * 128 + (r & 7) * 16, src,
-                        n < N ? 16u : 0u);
+    if (warp == 9) {
+        // ===================== TMA producer =====================
+        if (elect_one()) {
+            const int row_q = t * N + q0, row_k = t * N;
+            mbar_arrive_expect_tx_addr(q_full, 2 * L::Q);
+            tma_load_3d(sb + L::off_q, &maps.q, q_full, 0, row_q, h * D / 8);
+            tma_load_3d(sb + L::off_q + L::Q, &maps.q, q_full, 0, row_q + 128, h * D / 8);
+            for (int j = 0; j < nkt; ++j) {
+                const int st = j % kAttnStages;
+                if (j >= kAttnStages) mbar_wait_spin_addr(kv_empty + 8 * st, ((j / kAttnStages) - 1) & 1);
+                mbar_arrive_expect_tx_addr(kv_full + 8 * st, L::K + L::V);
+                tma_load_3d(sb + L::off_k + st * L::K, &maps.k, kv_full + 8 * st, 0, row_k + j * 128,
+                            (C + h * D) / 8);
+                tma_load_3d(sb + L::off_v + st * L::V, &maps.v, kv_full + 8 * st, 0, t * C + h * D, j * 16);
+            }
         }
-        for (int i = tid; i < D * 16; i += kAttnThreads) {
-            const int r = i >> 4, kc = i & 15;
-            const T *src = vbase + (size_t)r * Npad + k0 + kc * 8;
-            cp_async_16(sb + L::off_v + buf * L::V + (r >> 3) * 2048 + kc * 128 + (r & 7) * 16, src, 16u);
-        }
-    };
-    load_kv(0, 0);
-    cp_async_commit();
-
-    const int nkt = (N + 127) / 128;
-    float o[D];
-#pragma unroll
-    for (int i = 0; i < D; ++i) o[i] = 0.f;
-    float m = -INFINITY, l = 0.f;
-    uint32_t ph_s = 0, ph_o = 0;
-    const int row = tid;
-    const uint32_t p_row = sb + L::off_p + (row >> 3) * 2048 + (row & 7) * 16;
-
-    for (int j = 0; j < nkt; ++j) {
-        const int buf = j & 1;
-        if (j + 1 < nkt) {
-            load_kv(j + 1, buf ^ 1);
-            cp_async_commit();
-            cp_async_wait_1();
-        } else {
-            cp_async_wait_all();
-        }
-        fence_proxy_async();
-        __syncthreads();
-        if (tid == 0) {
+    } else if (warp == 8) {
+        // ===================== MMA issuer =====================
+        if (elect_one()) {
+            mbar_wait_spin_addr(q_full, 0);
             tc_fence_after();
-            const uint32_t qa = sb + L::off_q, ka = sb + L::off_k + buf * L::K;
+            auto issue_s = [&](int tt, int j) {
+                const int st = j % kAttnStages;
+                const uint32_t qa = sb + L::off_q + tt * L::Q, ka = sb + L::off_k + st * L::K;
 #pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-                const uint64_t ad = ((uint64_t)desc_hi_noswz(D * 16) << 32) | desc_lo(qa + ks * 256, 128);
-                const uint64_t bd = ((uint64_t)desc_hi_noswz(D * 16) << 32) | desc_lo(ka + ks * 256, 128);
-                tc_mma(tS, ad, bd, idesc_s, ks > 0);
-            }
-            tc_commit(&bars[0]);
-        }
-        mbar_wait(&bars[0], ph_s);
-        ph_s ^= 1;
-        tc_fence_after();
-        // ---- softmax of row `row` over this key tile
-        const int kvalid = N - j * 128;   // keys >= kvalid are padding
-        float mx = -INFINITY;
+                for (int ks = 0; ks < D / 16; ++ks) {
+                    const uint64_t ad = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(qa + ks * 4096, 2048);
+                    const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(ka + ks * 4096, 2048);
+                    tc_mma(tmem + tt * 128, ad, bd, idesc_s, ks > 0);
+                }
+                tc_commit_addr(s_full + 8 * tt);
+            };
+            auto issue_pv = [&](int tt, int j) {
+                const int st = j % kAttnStages;
+                const uint32_t pa = sb + L::off_p + tt * L::P, va = sb + L::off_v + st * L::V;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            uint32_t r[16];
-            tmem_ld16(tS + lane_off + c * 16, r);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float s = __uint_as_float(r[i]);
-                mx = (c * 16 + i < kvalid) ? fmaxf(mx, s) : mx;
-            }
-        }
-        const float m_new = fmaxf(m, mx * scale_log2);
-        const float alpha = ex2f(m - m_new);
-        float rs = 0.f;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            uint32_t r[16];
-            tmem_ld16(tS + lane_off + c * 16, r);
-            float p[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float e = ex2f(fmaf(__uint_as_float(r[i]), scale_log2, -m_new));
-                p[i] = (c * 16 + i < kvalid) ? e : 0.f;
-                rs += p[i];
-            }
-            st_shared_v4(p_row + (2 * c) * 128, pack2<T>(p[0], p[1]), pack2<T>(p[2], p[3]), pack2<T>(p[4], p[5]),
-                         pack2<T>(p[6], p[7]));
-            st_shared_v4(p_row + (2 * c + 1) * 128, pack2<T>(p[8], p[9]), pack2<T>(p[10], p[11]),
-                         pack2<T>(p[12], p[13]), pack2<T>(p[14], p[15]));
-        }
-        l = l * alpha + rs;
-        m = m_new;
-        fence_proxy_async();
-        tc_fence_before();
-        __syncthreads();
-        if (tid == 0) {
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint64_t ad = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(pa + ks * 4096, 2048);
+                    const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(va + ks * 2 * D * 16, D * 16);
+                    tc_mma(tmem + 256 + tt * 128 + (j & 1) * 64, ad, bd, idesc_o, ks > 0);
+                }
+                tc_commit_addr(o_full + 8 * (2 * tt + (j & 1)));
+            };
+            mbar_wait_spin_addr(kv_full, 0);
             tc_fence_after();
-            const uint32_t pa = sb + L::off_p, va = sb + L::off_v + buf * L::V;
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                const uint64_t ad = ((uint64_t)desc_hi_noswz(2048) << 32) | desc_lo(pa + ks * 256, 128);
-                const uint64_t bd = ((uint64_t)desc_hi_noswz(2048) << 32) | desc_lo(va + ks * 256, 128);
-                tc_mma(tO, ad, bd, idesc_o, ks > 0);
+            issue_s(0, 0);
+            issue_s(1, 0);
+            for (int j = 0; j < nkt; ++j) {
+                const int stn = (j + 1) % kAttnStages;
+                const bool more = j + 1 < nkt;
+                if (more) {
+                    mbar_wait_spin_addr(kv_full + 8 * stn, ((j + 1) / kAttnStages) & 1);
+                    tc_fence_after();
+                }
+                for (int tt = 0; tt < 2; ++tt) {
+                    mbar_wait_spin_addr(p_full + 8 * tt, j & 1);   // P_t(j) written, S_t(j) released
+                    tc_fence_after();
+                    issue_pv(tt, j);
+                    if (more) issue_s(tt, j + 1);
+                }
+                tc_commit_addr(kv_empty + 8 * (j % kAttnStages));
             }
-            tc_commit(&bars[1]);
         }
-        mbar_wait(&bars[1], ph_o);
-        ph_o ^= 1;
-        tc_fence_after();
+    } else {
+        // ===================== softmax groups =====================
+        const int tt = warp >> 2, q4 = warp & 3;
+        const int row = q4 * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+        const uint32_t tS = tmem + lane_off + tt * 128;
+        const uint32_t p_row = sb + L::off_p + tt * L::P + (row >> 3) * 128 + (row & 7) * 16;
+        float o[D];
 #pragma unroll
-        for (int c = 0; c < D / 16; ++c) {
-            uint32_t r[16];
-            tmem_ld16(tO + lane_off + c * 16, r);
+        for (int i = 0; i < D; ++i) o[i] = 0.f;
+        float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+        auto accumulate = [&](int j) {   // O <- O * alpha_prev + PV(j)
+            mbar_wait_addr(o_full + 8 * (2 * tt + (j & 1)), (j >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tO = tmem + lane_off + 256 + tt * 128 + (j & 1) * 64;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[c * 16 + i] = fmaf(o[c * 16 + i], alpha, __uint_as_float(r[i]));
+            for (int c = 0; c < D / 16; ++c) {
+                uint32_t r[16];
+                tmem_ld16(tO + c * 16, r);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[c * 16 + i] = fmaf(o[c * 16 + i], alpha_prev, __uint_as_float(r[i]));
+            }
+        };
+        for (int j = 0; j < nkt; ++j) {
+            mbar_wait_addr(s_full + 8 * tt, j & 1);
+            tc_fence_after();
+            const int kvalid = N - j * 128;
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 8; c += 2) {
+                uint32_t r[16], r2[16];
+                tmem_ld16_nowait(tS + c * 16, r);
+                tmem_ld16_nowait(tS + c * 16 + 16, r2);
+                tmem_wait16(r);
+                tmem_wait16(r2);
+                if (kvalid >= 128) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) mx = fmaxf(mx, fmaxf(__uint_as_float(r[i]), __uint_as_float(r2[i])));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        if (c * 16 + i < kvalid) mx = fmaxf(mx, __uint_as_float(r[i]));
+                        if (c * 16 + 16 + i < kvalid) mx = fmaxf(mx, __uint_as_float(r2[i]));
+                    }
+                }
+            }
+            const float m_new = fmaxf(m, mx * scale_log2);
+            const float alpha = ex2f(m - m_new);
+            if (j > 0) accumulate(j - 1);   // PV(j-1) done: P_t is free, O catches up
+            float rs = 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                uint32_t r[16];
+                tmem_ld16(tS + c * 16, r);
+                float p[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float e = ex2f(fmaf(__uint_as_float(r[i]), scale_log2, -m_new));
+                    p[i] = (kvalid >= 128 || c * 16 + i < kvalid) ? e : 0.f;
+                    rs += p[i];
+                }
+                st_shared_v4(p_row + (2 * c) * 2048, pack2<T>(p[0], p[1]), pack2<T>(p[2], p[3]),
+                             pack2<T>(p[4], p[5]), pack2<T>(p[6], p[7]));
+                st_shared_v4(p_row + (2 * c + 1) * 2048, pack2<T>(p[8], p[9]), pack2<T>(p[10], p[11]),
+                             pack2<T>(p[12], p[13]), pack2<T>(p[14], p[15]));
+            }
+            fence_proxy_async();   // P (generic-proxy stores) visible to the tensor core
+            tc_fence_before();     // S reads ordered before the release
+            __syncwarp();
+            if (lane == 0) mbar_arrive(p_full + 8 * tt);
+            l = l * alpha + rs;
+            m = m_new;
+            alpha_prev = alpha;
         }
-        tc_fence_before();
-    }
-    // ---- epilogue: O / l, 16-bit store of this row's D channels
-    const int n = q0 + row;
-    if (n < N) {
-        const float inv = 1.f / l;
-        T *y = out + ((size_t)t * N + n) * C + h * D;
+        accumulate(nkt - 1);
+        const int n = q0 + tt * 128 + row;
+        if (n < N) {
+            const float inv = 1.f / l;
+            T *y = out + ((size_t)t * N + n) * C + h * D;
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
-            float f[8];
+            for (int c = 0; c < D / 8; ++c) {
+                float f[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) f[i] = o[c * 8 + i] * inv;
-            store8(y + c * 8, f);
+                for (int i = 0; i < 8; ++i) f[i] = o[c * 8 + i] * inv;
+                store8(y + c * 8, f);
+            }
         }
     }
     griddep_launch();
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<1>(tmem, 256);
+    if (warp == 8) tmem_dealloc<1>(tmem, 512);
 }
 
 // ----------------------------------------------------------------- host side
@@ -400,18 +453,43 @@ static int grid_for(long work, int threads) {
     return (int)(b < 148L * 16 ? (b > 0 ? b : 1) : 148L * 16);
 }
 
+PFN_encodeTiled_t get_encode_fn();
+
+// 3D view {8 elements, rows, 16-byte chunks} of a row-major [rows][cols] 16-bit matrix: a box
+// {8, box_rows, box_chunks} lands chunk-major, i.e. as no-swizzle UMMA core matrices
+static dvc_status make_chunk_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows,
+                                 int box_chunks) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && cols % 8 == 0, DVC_ERR_ARG, "attention: operand alignment");
+    cuuint64_t gdim[3] = {8, (cuuint64_t)rows, (cuuint64_t)(cols / 8)};
+    cuuint64_t gstride[2] = {(cuuint64_t)cols * 2, 16};
+    cuuint32_t box[3] = {8, (cuuint32_t)box_rows, (cuuint32_t)box_chunks};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                     const_cast<void *>(ptr), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (attention) failed (%d)", (int)r);
+    return DVC_OK;
+}
+
 template <typename T, int D>
 static dvc_status attn_tc_launch(const void *qkv, const void *vt, void *out, int T_, int N, int Npad, int C,
                                  cudaStream_t stream) {
     using L = AttnSmem<D>;
+    const dvc_dtype dt = std::is_same<T, __nv_bfloat16>::value ? DVC_BF16 : DVC_F16;
+    AttnMaps maps;
+    dvc_status st = make_chunk_map(&maps.q, qkv, dt, (long)T_ * N, 3L * C, 128, D / 8);
+    if (st != DVC_OK) return st;
+    maps.k = maps.q;
+    if ((st = make_chunk_map(&maps.v, vt, dt, (long)T_ * C, Npad, D, 16)) != DVC_OK) return st;
     const void *kern = reinterpret_cast<const void *>(attn_tc_kernel<T, D>);
     if (!smem_attr_ok(kern, L::bytes))
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes));
-    const int bf = std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
+    const int bf = dt == DVC_BF16 ? 1 : 0;
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-    DVC_CUDA(launch_pdl(attn_tc_kernel<T, D>, dim3((N + 127) / 128, C / D, T_), dim3(kAttnThreads), (size_t)L::bytes,
-                        stream, 1, reinterpret_cast<const T *>(qkv), reinterpret_cast<const T *>(vt),
-                        reinterpret_cast<T *>(out), N, Npad, C, scale_log2, make_idesc(bf, 128, 128),
+    DVC_CUDA(launch_pdl(attn_tc_kernel<T, D>, dim3((N + 255) / 256, C / D, T_), dim3(kAttnThreads), (size_t)L::bytes,
+                        stream, 1, maps, reinterpret_cast<T *>(out), N, C, scale_log2, make_idesc(bf, 128, 128),
                         make_idesc(bf, 128, D)));
     ++g_launches;
     return DVC_OK;
@@ -435,7 +513,9 @@ static dvc_status attention_t(const void *qkv, int T_, int N, int C, int D, void
         case 48: st = attn_tc_launch<T, 48>(qkv, vt, out, T_, N, Npad, C, s); break;
         default: st = attn_tc_launch<T, 64>(qkv, vt, out, T_, N, Npad, C, s); break;
     }
-    prof_end_aux(slot, s, "attn_tc");
+    char lab[96];
+    snprintf(lab, sizeof(lab), "attn_tc T=%d N=%d C=%d d=%d", T_, N, C, D);
+    prof_end_aux(slot, s, lab, 4.0 * T_ * (double)N * N * C);   // QK^T + PV: 2*N*N*C each
     return st;
 }
 

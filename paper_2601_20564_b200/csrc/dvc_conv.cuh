@@ -91,7 +91,8 @@ struct ProfSlot {
 ProfSlot prof_begin(cudaStream_t stream);
 struct ConvDesc;
 void prof_end(ProfSlot s, cudaStream_t stream, double flops, const char *engine, const ConvDesc &d);
-void prof_end_aux(ProfSlot s, cudaStream_t stream, const char *label);   // non-conv kernel (not summed)
+// non-conv kernel (not summed into the conv totals); flops: its algorithmic FLOPs, if any (attention)
+void prof_end_aux(ProfSlot s, cudaStream_t stream, const char *label, double flops = 0.0);
 double conv_flops(const ConvDesc &d);
 
 // Validates the descriptor for the given engine; returns DVC_OK or an error.

@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][2][4][32] box-statistics staging
-    float *sbias = red + 512;   // [2][cout] bias0, bias1 in fp32 (16-byte aligned: even barrier count)
+    float *sbias = red + 512;   // [1 or 2][cout] bias0 (, bias1) in fp32 (16-byte aligned: even barrier count)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
     if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), ncols);
     for (int i = tid; i < p.cout; i += kWsThreads) {
         sbias[i] = p.bias0 ? Elem<T>::to_f(reinterpret_cast<const T *>(p.bias0)[i]) : 0.f;
-        sbias[p.cout + i] = p.bias1 ? Elem<T>::to_f(reinterpret_cast<const T *>(p.bias1)[i]) : 0.f;
+        if (p.bias1) sbias[p.cout + i] = Elem<T>::to_f(reinterpret_cast<const T *>(p.bias1)[i]);
     }
     tc_fence_before();
     __syncthreads();
@@ -366,7 +366,7 @@ static int g_num_sms = 0;
 template <typename T, int CG, int STAGES>
 static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
     const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16 + 2048 +
-                        (size_t)2 * p.cout * 4;
+                        (size_t)(p.bias1 ? 2 : 1) * p.cout * 4;   // bias1 staged only when present
     auto kern = conv_ws_kernel<T, CG, STAGES>;
     if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
