@@ -6,7 +6,7 @@
 //   h0 = proj_in(a)                 1x1 tensor-core conv (conv_run)
 //   l1 = LN1(h0)                    layernorm_kernel  (one warp per pixel)
 //   qkv = l1 W_qkv^T                1x1 conv, no bias, [T][N][3C]
-//   Vt = transpose(v)               vt_kernel: [T][C][Npad] so V is a K-major UMMA operand
+//   Qp|Kp|Vp = pack(qkv)            qkv_pack_kernel: per-(frame, head, tile) UMMA images (V transposed)
 //   o  = attention(q, k, v)         attn_tc_kernel (tcgen05, S and PV in TMEM)
 //   h1 = out(o) + h0                1x1 conv with residual
 //   l2 = LN2(h1)
@@ -27,6 +27,7 @@
 // matrices adjacent in K 128 B apart (LBO), 8-row groups SBO apart.
 #include <cuda.h>
 #include <cstdio>
+#include <cstdlib>
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
 #include "dvc_ptx.cuh"
@@ -132,25 +133,42 @@ __global__ void __launch_bounds__(256) geglu_kernel(const T *__restrict__ f, T *
     griddep_launch();
 }
 
-// V part of qkv [T][N][3C] -> Vt [T][C][Npad] (zero for n >= N): 32x32 tiles through smem.
-template <typename T>
-__global__ void __launch_bounds__(256) vt_kernel(const T *__restrict__ qkv, T *__restrict__ vt, int N, int Npad,
-                                                 int C) {
+// qkv [T][N][3C] -> three pre-tiled operand arrays, one contiguous 128*D block per (frame, head,
+// 128-token tile) in exactly the shared-memory image the attention kernel's UMMA descriptors
+// read (no-swizzle core matrices), so each tile moves with ONE 1D bulk copy:
+//   Qp, Kp [T][heads][ntiles]: element (r, d) of the tile at (d/8)*1024 + r*8 + d%8   (chunk-major)
+//   Vp     [T][heads][ntiles]: element (r, d) (key r)  at (r/8)*D*8  + d*8 + r%8    (V^T, K = keys)
+// Tokens n >= N of the last tile are zero.  One CTA per (tile, head, frame).
+template <typename T, int D>
+__global__ void __launch_bounds__(256) qkv_pack_kernel(const T *__restrict__ qkv, T *__restrict__ qp,
+                                                       T *__restrict__ kp, T *__restrict__ vp, int N, int C) {
     griddep_wait();
-    __shared__ T tile[32][33];
-    const int t = blockIdx.z;
-    const int n0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int r = ty; r < 32; r += 8) {
-        const int n = n0 + r, c = c0 + tx;
-        T v = Elem<T>::from_f(0.f);
-        if (n < N && c < C) v = qkv[((size_t)t * N + n) * 3 * C + 2 * C + c];
-        tile[r][tx] = v;
+    __shared__ __align__(16) T sv[128 * D];
+    const int jt = blockIdx.x, h = blockIdx.y, t = blockIdx.z;
+    const int heads = gridDim.y, ntiles = gridDim.x;
+    const size_t tile = (((size_t)t * heads + h) * ntiles + jt) * (128 * D);
+    constexpr int DC = D / 8;
+    for (int i = threadIdx.x; i < 128 * DC; i += 256) {
+        const int r = i / DC, kc = i - r * DC;
+        const int n = jt * 128 + r;
+        uint4 q = make_uint4(0, 0, 0, 0), k = q, v = q;
+        if (n < N) {
+            const T *src = qkv + ((size_t)t * N + n) * 3 * C + h * D + kc * 8;
+            q = __ldg(reinterpret_cast<const uint4 *>(src));
+            k = __ldg(reinterpret_cast<const uint4 *>(src + C));
+            v = __ldg(reinterpret_cast<const uint4 *>(src + 2 * C));
+        }
+        *reinterpret_cast<uint4 *>(qp + tile + kc * 1024 + r * 8) = q;
+        *reinterpret_cast<uint4 *>(kp + tile + kc * 1024 + r * 8) = k;
+        *reinterpret_cast<uint4 *>(sv + r * D + kc * 8) = v;
     }
     __syncthreads();
-    for (int r = ty; r < 32; r += 8) {
-        const int c = c0 + r, n = n0 + tx;
-        if (c < C && n < Npad) vt[((size_t)t * C + c) * Npad + n] = tile[tx][r];
+    for (int i = threadIdx.x; i < 16 * D; i += 256) {   // (key chunk, d): 8 consecutive keys of column d
+        const int kc = i / D, d = i - kc * D;
+        Vec8<T> u;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) u.v[e] = sv[(kc * 8 + e) * D + d];
+        *reinterpret_cast<Vec8<T> *>(vp + tile + kc * D * 8 + d * 8) = u;
     }
     griddep_launch();
 }
@@ -197,33 +215,35 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const float *__restrict_
 //   warps 4-7  softmax group 1 (tile 1)
 //   warp 8     MMA issuer (one elected lane): S_t = Q_t K_j^T, PV_t = P_t V_j
 //   warp 9     TMA producer: Q tiles once, then a 3-stage ring of (K_j, V_j^T) tiles
-// TMEM (512 columns): S_0 [0,128), S_1 [128,256), PV_0 [256 + 64 b), PV_1 [384 + 64 b), b = j & 1.
-// The MMA warp issues PV_t(j) then S_t(j+1) as soon as group t has released S_t(j) and
-// written P_t(j), so the two groups drift half an iteration apart and the exp2 units (the
-// bound for head_dim 48: 192 FLOP per exp) stay busy while the other group waits.
-// All tiles are TMA'd with 3D views whose first dim is one 16-byte core-matrix row, which lands
-// them directly in the canonical no-swizzle K-major UMMA layout:
-//   Q/K [rows][D]:  box {8, 128, D/8}   -> core (r8, kc) at kc*2048 + r8*128   (LBO 2048, SBO 128)
-//   V^T [D][keys]:  box {8, D, 16}      -> core (d8, kc) at kc*D*16 + d8*128   (LBO D*16, SBO 128)
-//   P   [128][128]: written by the softmax threads in the same kc*2048 + r8*128 form
+// TMEM (512 columns): S_0 [0,128), S_1 [128,256), O_0 [256,+D), O_1 [320,+D), P_0 [384,448),
+// P_1 [448,512) (P as packed 16-bit pairs: the PV MMA takes A from TMEM, so neither the P stores
+// nor the PV operand reads touch shared memory).
+// The MMA warp issues PV_t(j) (accumulating into O_t) then S_t(j+1) as soon as group t has
+// written P_t(j) (which also releases S_t(j)), so the two groups drift half an iteration apart.
+// TMEM reads are the scarce resource (64 B/clk/SM): each softmax thread reads its S row ONCE
+// (128 registers), and O stays in TMEM.  O uses a lazy maximum: a row's reference max m only
+// moves (with an in-TMEM rescale of its O row by 2^(m - m_new)) when the tile max exceeds it
+// by more than 8 (log2 units), so P <= 2^8 and the rescale is rare.  Because the MMA warp
+// issues PV_t(j-1) before S_t(j), the commit that signals S_t(j) also covers PV_t(j-1): when
+// group t holds S_t(j), O_t is quiescent and may be rescaled, and P_t may be overwritten.
+// Operand tiles arrive as single 1D bulk copies of the pre-tiled blocks qkv_pack_kernel writes
+// (a 3D TMA view of the packed qkv moved 16 B per request and capped the kernel at ~2 TB/s of
+// L2 reads); all are canonical no-swizzle K-major UMMA layouts:
+//   Q/K [rows][D]:  core (r8, kc) at kc*2048 + r8*128   (LBO 2048, SBO 128)
+//   V^T [D][keys]:  core (d8, kc) at kc*D*16 + d8*128   (LBO D*16, SBO 128)
+
 constexpr int kAttnThreads = 320;
-constexpr int kAttnStages = 3;
+constexpr int kAttnStages = 4;
 template <int D>
 struct AttnSmem {
     static constexpr int Q = 128 * D * 2;        // one query tile
     static constexpr int K = 128 * D * 2;        // one key tile
     static constexpr int V = D * 128 * 2;        // one transposed value tile
-    static constexpr int P = 128 * 128 * 2;      // one probability tile
     static constexpr int off_q = 0, off_k = 2 * Q, off_v = off_k + kAttnStages * K;
-    static constexpr int off_p = off_v + kAttnStages * V;
-    static constexpr int off_bar = off_p + 2 * P;
+    static constexpr int off_bar = off_v + kAttnStages * V;
     // barriers: q_full, kv_full[3], kv_empty[3], s_full[2], s_free[2], p_full[2], o_full[2][2]
     static constexpr int nbar = 1 + 2 * kAttnStages + 2 + 2 + 2 + 4;
     static constexpr int bytes = off_bar + nbar * 8 + 16 + 1024;   // + TMEM slot + alignment slack
-};
-
-struct AttnMaps {
-    CUtensorMap q, k, v;   // q and k: the same qkv view at different channel offsets
 };
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -233,6 +253,20 @@ __device__ __forceinline__ float ex2f(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+// 2^x on the FMA pipe (x <= 0 here): round-to-nearest split x = j + f, f in [-1/2, 1/2], a
+// degree-3 fit of 2^f (max relative error 7.5e-5, below the 16-bit rounding of P) and j added
+// to the exponent field.  Used for part of every 8-score group so the MUFU ex2 unit (the bound of
+// a head_dim-48 softmax: 192 MMA FLOP per exponential) shares the work with the FMA pipe.
+#ifndef DVC_ATTN_POLY
+#define DVC_ATTN_POLY 3   // scores per 8 computed by ex2_poly
+#endif
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -126.f);
+    const float r = x + 12582912.f;   // 1.5 * 2^23: the integer nearest x lands in the low mantissa bits
+    const float f = x - (r - 12582912.f);
+    const float p = fmaf(fmaf(fmaf(0.055172063f, f, 0.24261240f), f, 0.69326103f), f, 0.99992794f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t addr) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
@@ -248,10 +282,10 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     }
 }
 
-template <typename T, int D>
+template <typename T, int D, int NPOLY>
 __global__ void __launch_bounds__(kAttnThreads, 1)
-    attn_tc_kernel(const __grid_constant__ AttnMaps maps, T *__restrict__ out, int N, int C, float scale_log2,
-                   uint32_t idesc_s, uint32_t idesc_o) {
+    attn_tc_kernel(const T *__restrict__ qp, const T *__restrict__ kp, const T *__restrict__ vp, T *__restrict__ out,
+                   int N, int C, float scale_log2, uint32_t idesc_s, uint32_t idesc_o, int dbg) {
     using L = AttnSmem<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -278,11 +312,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int i = 0; i < 4; ++i) mbar_init(&b[sf + 6 + i], 1);   // o_full
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 9 && lane == 0) {
-        tma_prefetch(&maps.q);
-        tma_prefetch(&maps.k);
-        tma_prefetch(&maps.v);
-    }
     if (warp == 8) tmem_alloc<1>(smem_u32(tslot), 512);
     tc_fence_before();
     __syncthreads();
@@ -290,20 +319,25 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     const uint32_t tmem = *tslot;
     griddep_wait();
 
+    // The MMA warp and the softmax groups are one latency chain (S -> softmax -> P -> PV, S):
+    // they poll without a suspend hint (a suspended try_wait wakes late, measured ~1.6 us per
+    // iteration of pure barrier round trips); the TMA producer runs ahead and may sleep.
     if (warp == 9) {
         // ===================== TMA producer =====================
         if (elect_one()) {
-            const int row_q = t * N + q0, row_k = t * N;
-            mbar_arrive_expect_tx_addr(q_full, 2 * L::Q);
-            tma_load_3d(sb + L::off_q, &maps.q, q_full, 0, row_q, h * D / 8);
-            tma_load_3d(sb + L::off_q + L::Q, &maps.q, q_full, 0, row_q + 128, h * D / 8);
+            const int ntiles = (N + 127) / 128, heads = gridDim.y;
+            const size_t base = ((size_t)t * heads + h) * ntiles * (128 * D);   // this (frame, head)
+            const int qt = blockIdx.x * 2;
+            const uint32_t nq = qt + 1 < ntiles ? 2 : 1;
+            mbar_arrive_expect_tx_addr(q_full, nq * L::Q);
+            bulk_load(sb + L::off_q, qp + base + (size_t)qt * 128 * D, L::Q, q_full);
+            if (nq == 2) bulk_load(sb + L::off_q + L::Q, qp + base + (size_t)(qt + 1) * 128 * D, L::Q, q_full);
             for (int j = 0; j < nkt; ++j) {
                 const int st = j % kAttnStages;
-                if (j >= kAttnStages) mbar_wait_spin_addr(kv_empty + 8 * st, ((j / kAttnStages) - 1) & 1);
+                if (j >= kAttnStages) mbar_wait_addr(kv_empty + 8 * st, ((j / kAttnStages) - 1) & 1);
                 mbar_arrive_expect_tx_addr(kv_full + 8 * st, L::K + L::V);
-                tma_load_3d(sb + L::off_k + st * L::K, &maps.k, kv_full + 8 * st, 0, row_k + j * 128,
-                            (C + h * D) / 8);
-                tma_load_3d(sb + L::off_v + st * L::V, &maps.v, kv_full + 8 * st, 0, t * C + h * D, j * 16);
+                bulk_load(sb + L::off_k + st * L::K, kp + base + (size_t)j * 128 * D, L::K, kv_full + 8 * st);
+                bulk_load(sb + L::off_v + st * L::V, vp + base + (size_t)j * 128 * D, L::V, kv_full + 8 * st);
             }
         }
     } else if (warp == 8) {
@@ -316,22 +350,23 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 const uint32_t qa = sb + L::off_q + tt * L::Q, ka = sb + L::off_k + st * L::K;
 #pragma unroll
                 for (int ks = 0; ks < D / 16; ++ks) {
+                    if (dbg & 2) break;   // DVC_ATTN_DEBUG bit 1: no MMAs (pipeline-only timing)
                     const uint64_t ad = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(qa + ks * 4096, 2048);
                     const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(ka + ks * 4096, 2048);
                     tc_mma(tmem + tt * 128, ad, bd, idesc_s, ks > 0);
                 }
                 tc_commit_addr(s_full + 8 * tt);
             };
-            auto issue_pv = [&](int tt, int j) {
+            auto issue_pv = [&](int tt, int j) {   // A = P_t from TMEM (8 columns per K step)
                 const int st = j % kAttnStages;
-                const uint32_t pa = sb + L::off_p + tt * L::P, va = sb + L::off_v + st * L::V;
+                const uint32_t va = sb + L::off_v + st * L::V;
 #pragma unroll
                 for (int ks = 0; ks < 8; ++ks) {
-                    const uint64_t ad = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(pa + ks * 4096, 2048);
+                    if (dbg & 2) break;
                     const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(va + ks * 2 * D * 16, D * 16);
-                    tc_mma(tmem + 256 + tt * 128 + (j & 1) * 64, ad, bd, idesc_o, ks > 0);
+                    tc_mma_ts(tmem + 256 + tt * 64, tmem + 384 + tt * 64 + ks * 8, bd, idesc_o,
+                              (j > 0 || ks > 0) ? 1u : 0u);
                 }
-                tc_commit_addr(o_full + 8 * (2 * tt + (j & 1)));
             };
             mbar_wait_spin_addr(kv_full, 0);
             tc_fence_after();
@@ -352,6 +387,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 }
                 tc_commit_addr(kv_empty + 8 * (j % kAttnStages));
             }
+            tc_commit_addr(o_full);       // O_0 and O_1 final
+            tc_commit_addr(o_full + 8);
         }
     } else {
         // ===================== softmax groups =====================
@@ -359,85 +396,110 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int row = q4 * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
         const uint32_t tS = tmem + lane_off + tt * 128;
-        const uint32_t p_row = sb + L::off_p + tt * L::P + (row >> 3) * 128 + (row & 7) * 16;
-        float o[D];
-#pragma unroll
-        for (int i = 0; i < D; ++i) o[i] = 0.f;
-        float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-        auto accumulate = [&](int j) {   // O <- O * alpha_prev + PV(j)
-            mbar_wait_addr(o_full + 8 * (2 * tt + (j & 1)), (j >> 1) & 1);
-            tc_fence_after();
-            const uint32_t tO = tmem + lane_off + 256 + tt * 128 + (j & 1) * 64;
-#pragma unroll
-            for (int c = 0; c < D / 16; ++c) {
-                uint32_t r[16];
-                tmem_ld16(tO + c * 16, r);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) o[c * 16 + i] = fmaf(o[c * 16 + i], alpha_prev, __uint_as_float(r[i]));
-            }
-        };
+        const uint32_t tO = tmem + lane_off + 256 + tt * 64;
+        const uint32_t tP = tmem + lane_off + 384 + tt * 64;
+        float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nkt; ++j) {
-            mbar_wait_addr(s_full + 8 * tt, j & 1);
+            mbar_wait_spin_addr(s_full + 8 * tt, j & 1);
             tc_fence_after();
-            const int kvalid = N - j * 128;
-            float mx = -INFINITY;
+            if (dbg & 1) {   // DVC_ATTN_DEBUG bit 0: no softmax (MMA/TMA pipeline timing)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full + 8 * tt);
+                continue;
+            }
+            // each thread reads its S row ONCE (128 registers); max and exp2 from registers
+            const int kvalid = N - j * 128;   // keys >= kvalid of this tile are padding
+            uint32_t sr[128];
 #pragma unroll
-            for (int c = 0; c < 8; c += 2) {
-                uint32_t r[16], r2[16];
-                tmem_ld16_nowait(tS + c * 16, r);
-                tmem_ld16_nowait(tS + c * 16 + 16, r2);
-                tmem_wait16(r);
-                tmem_wait16(r2);
-                if (kvalid >= 128) {
+            for (int c = 0; c < 4; ++c)
+                tmem_ld32_nowait(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) mx = fmaxf(mx, fmaxf(__uint_as_float(r[i]), __uint_as_float(r2[i])));
-                } else {
+            for (int c = 0; c < 4; ++c) tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+            if (dbg & 4) {   // DVC_ATTN_DEBUG bit 2: S loads only (TMEM read bandwidth probe)
+                if (sr[0] == 0x7fffffffu && sr[127] == 0x7fffffffu) l += 1.f;
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full + 8 * tt);
+                continue;
+            }
+            if (kvalid < 128) {
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        if (c * 16 + i < kvalid) mx = fmaxf(mx, __uint_as_float(r[i]));
-                        if (c * 16 + 16 + i < kvalid) mx = fmaxf(mx, __uint_as_float(r2[i]));
+                for (int i = 0; i < 128; ++i)
+                    if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
+            }
+            // independent partial maxima / sums: with two softmax warps per SM sub-partition a
+            // single 128-long dependency chain would leave the pipes idle
+            float mxp[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mxp[i] = fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[8 + i]));
+#pragma unroll
+            for (int i = 16; i < 128; i += 16)
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    mxp[k] = fmaxf(mxp[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
+            const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                                   fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+            const float mt = mx * scale_log2;
+            if (j == 0) {
+                m = mt;
+            } else {
+                const bool move = mt > m + 8.f;   // lazy maximum: P stays <= 2^8
+                if (__any_sync(0xffffffffu, move)) {
+                    const float alpha = move ? ex2f(m - mt) : 1.f;
+#pragma unroll
+                    for (int c = 0; c < D / 16; ++c) {
+                        uint32_t r[16];
+                        tmem_ld16(tO + c * 16, r);
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                        tmem_st16(tO + c * 16, r);
                     }
+                    tmem_wait_st();
+                    l *= alpha;
+                    if (move) m = mt;
                 }
             }
-            const float m_new = fmaxf(m, mx * scale_log2);
-            const float alpha = ex2f(m - m_new);
-            if (j > 0) accumulate(j - 1);   // PV(j-1) done: P_t is free, O catches up
-            float rs = 0.f;
+            float rsp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint32_t r[16];
-                tmem_ld16(tS + c * 16, r);
-                float p[16];
+            for (int c = 0; c < 4; ++c) {   // 32 keys -> 16 packed columns of P_t in TMEM
+                uint32_t pk[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float e = ex2f(fmaf(__uint_as_float(r[i]), scale_log2, -m_new));
-                    p[i] = (kvalid >= 128 || c * 16 + i < kvalid) ? e : 0.f;
-                    rs += p[i];
+                for (int q = 0; q < 4; ++q) {
+                    float p[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float x = fmaf(__uint_as_float(sr[c * 32 + q * 8 + i]), scale_log2, -m);
+                        p[i] = i < NPOLY ? ex2_poly(x) : ex2f(x);   // padding: x = -inf -> ~0
+                        rsp[i] += p[i];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) pk[q * 4 + i] = pack2<T>(p[2 * i], p[2 * i + 1]);
                 }
-                st_shared_v4(p_row + (2 * c) * 2048, pack2<T>(p[0], p[1]), pack2<T>(p[2], p[3]),
-                             pack2<T>(p[4], p[5]), pack2<T>(p[6], p[7]));
-                st_shared_v4(p_row + (2 * c + 1) * 2048, pack2<T>(p[8], p[9]), pack2<T>(p[10], p[11]),
-                             pack2<T>(p[12], p[13]), pack2<T>(p[14], p[15]));
+                tmem_st16(tP + c * 16, pk);
             }
-            fence_proxy_async();   // P (generic-proxy stores) visible to the tensor core
-            tc_fence_before();     // S reads ordered before the release
+            tmem_wait_st();
+            l += ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
+            tc_fence_before();     // S reads, P stores, O rescale ordered before the release
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full + 8 * tt);
-            l = l * alpha + rs;
-            m = m_new;
-            alpha_prev = alpha;
         }
-        accumulate(nkt - 1);
+        mbar_wait_spin_addr(o_full + 8 * tt, 0);
+        tc_fence_after();
         const int n = q0 + tt * 128 + row;
-        if (n < N) {
-            const float inv = 1.f / l;
-            T *y = out + ((size_t)t * N + n) * C + h * D;
+        const float inv = 1.f / l;
 #pragma unroll
-            for (int c = 0; c < D / 8; ++c) {
+        for (int c = 0; c < D / 16; ++c) {
+            uint32_t r[16];
+            tmem_ld16(tO + c * 16, r);
+            if (n < N) {
+                T *y = out + ((size_t)t * N + n) * C + h * D + c * 16;
                 float f[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) f[i] = o[c * 8 + i] * inv;
-                store8(y + c * 8, f);
+                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]) * inv;
+                store8(y, f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[8 + i]) * inv;
+                store8(y + 8, f);
             }
         }
     }
@@ -455,68 +517,59 @@ static int grid_for(long work, int threads) {
 
 PFN_encodeTiled_t get_encode_fn();
 
-// 3D view {8 elements, rows, 16-byte chunks} of a row-major [rows][cols] 16-bit matrix: a box
-// {8, box_rows, box_chunks} lands chunk-major, i.e. as no-swizzle UMMA core matrices
-static dvc_status make_chunk_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows,
-                                 int box_chunks) {
-    PFN_encodeTiled_t enc = get_encode_fn();
-    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && cols % 8 == 0, DVC_ERR_ARG, "attention: operand alignment");
-    cuuint64_t gdim[3] = {8, (cuuint64_t)rows, (cuuint64_t)(cols / 8)};
-    cuuint64_t gstride[2] = {(cuuint64_t)cols * 2, 16};
-    cuuint32_t box[3] = {8, (cuuint32_t)box_rows, (cuuint32_t)box_chunks};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
-                     const_cast<void *>(ptr), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (attention) failed (%d)", (int)r);
-    return DVC_OK;
+static int attn_debug() {   // DVC_ATTN_DEBUG (experiments only): 1 = skip softmax, 2 = skip MMAs
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("DVC_ATTN_DEBUG");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
 }
 
 template <typename T, int D>
-static dvc_status attn_tc_launch(const void *qkv, const void *vt, void *out, int T_, int N, int Npad, int C,
-                                 cudaStream_t stream) {
+static dvc_status attn_tc_launch(const void *qkv, void *ws, void *out, int T_, int N, int C, cudaStream_t stream) {
     using L = AttnSmem<D>;
-    const dvc_dtype dt = std::is_same<T, __nv_bfloat16>::value ? DVC_BF16 : DVC_F16;
-    AttnMaps maps;
-    dvc_status st = make_chunk_map(&maps.q, qkv, dt, (long)T_ * N, 3L * C, 128, D / 8);
-    if (st != DVC_OK) return st;
-    maps.k = maps.q;
-    if ((st = make_chunk_map(&maps.v, vt, dt, (long)T_ * C, Npad, D, 16)) != DVC_OK) return st;
-    const void *kern = reinterpret_cast<const void *>(attn_tc_kernel<T, D>);
+    const int ntiles = (N + 127) / 128;
+    const size_t plane = (size_t)T_ * C * ntiles * 128;   // elements of one packed operand
+    T *qp = reinterpret_cast<T *>(ws), *kp = qp + plane, *vp = kp + plane;
+    DVC_CUDA(launch_pdl(qkv_pack_kernel<T, D>, dim3(ntiles, C / D, T_), dim3(256), 0, stream, 1,
+                        reinterpret_cast<const T *>(qkv), qp, kp, vp, N, C));
+    ++g_launches;
+    ProfSlot slot = prof_begin(stream);
+    static int npoly = -1;   // scores per 8 on the FMA pipe (DVC_ATTN_POLY: 0, 3 (default), 8)
+    if (npoly < 0) {
+        const char *e = getenv("DVC_ATTN_POLY");
+        npoly = e ? atoi(e) : DVC_ATTN_POLY;
+    }
+    auto kfn = npoly == 0 ? attn_tc_kernel<T, D, 0> : npoly == 8 ? attn_tc_kernel<T, D, 8>
+             : npoly == 5 ? attn_tc_kernel<T, D, 5> : attn_tc_kernel<T, D, 3>;
+    const void *kern = reinterpret_cast<const void *>(kfn);
     if (!smem_attr_ok(kern, L::bytes))
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes));
-    const int bf = dt == DVC_BF16 ? 1 : 0;
+    const int bf = std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-    DVC_CUDA(launch_pdl(attn_tc_kernel<T, D>, dim3((N + 255) / 256, C / D, T_), dim3(kAttnThreads), (size_t)L::bytes,
-                        stream, 1, maps, reinterpret_cast<T *>(out), N, C, scale_log2, make_idesc(bf, 128, 128),
-                        make_idesc(bf, 128, D)));
+    DVC_CUDA(launch_pdl(kfn, dim3((N + 255) / 256, C / D, T_), dim3(kAttnThreads), (size_t)L::bytes,
+                        stream, 1, (const T *)qp, (const T *)kp, (const T *)vp, reinterpret_cast<T *>(out), N, C,
+                        scale_log2, make_idesc(bf, 128, 128), make_idesc(bf, 128, D), attn_debug()));
     ++g_launches;
+    char lab[96];
+    snprintf(lab, sizeof(lab), "attn_tc T=%d N=%d C=%d d=%d", T_, N, C, D);
+    prof_end_aux(slot, stream, lab, 4.0 * T_ * (double)N * N * C);   // QK^T + PV: 2*N*N*C each
     return DVC_OK;
 }
 
-size_t attn_vt_bytes(int T, int N, int C, dvc_dtype dt) {
-    return align256((size_t)T * C * (size_t)((N + 127) / 128 * 128) * dt_size(dt));
+size_t attn_ws_bytes(int T, int N, int C, dvc_dtype dt) {   // packed Q, K, V^T tiles
+    return align256(3 * (size_t)T * C * (size_t)((N + 127) / 128 * 128) * dt_size(dt));
 }
 
 template <typename T>
-static dvc_status attention_t(const void *qkv, int T_, int N, int C, int D, void *vt, void *out, cudaStream_t s) {
-    const int Npad = (N + 127) / 128 * 128;
-    DVC_CUDA(launch_pdl(vt_kernel<T>, dim3(Npad / 32, (C + 31) / 32, T_), dim3(256), 0, s, 1,
-                        reinterpret_cast<const T *>(qkv), reinterpret_cast<T *>(vt), N, Npad, C));
-    ++g_launches;
-    ProfSlot slot = prof_begin(s);
-    dvc_status st;
+static dvc_status attention_t(const void *qkv, int T_, int N, int C, int D, void *ws, void *out, cudaStream_t s) {
     switch (D) {
-        case 16: st = attn_tc_launch<T, 16>(qkv, vt, out, T_, N, Npad, C, s); break;
-        case 32: st = attn_tc_launch<T, 32>(qkv, vt, out, T_, N, Npad, C, s); break;
-        case 48: st = attn_tc_launch<T, 48>(qkv, vt, out, T_, N, Npad, C, s); break;
-        default: st = attn_tc_launch<T, 64>(qkv, vt, out, T_, N, Npad, C, s); break;
+        case 16: return attn_tc_launch<T, 16>(qkv, ws, out, T_, N, C, s);
+        case 32: return attn_tc_launch<T, 32>(qkv, ws, out, T_, N, C, s);
+        case 48: return attn_tc_launch<T, 48>(qkv, ws, out, T_, N, C, s);
+        default: return attn_tc_launch<T, 64>(qkv, ws, out, T_, N, C, s);
     }
-    char lab[96];
-    snprintf(lab, sizeof(lab), "attn_tc T=%d N=%d C=%d d=%d", T_, N, C, D);
-    prof_end_aux(slot, s, lab, 4.0 * T_ * (double)N * N * C);   // QK^T + PV: 2*N*N*C each
-    return st;
 }
 
 dvc_status attention_run(const void *qkv, int T_, int N, int C, int D, dvc_dtype dt, void *vt, void *out,
@@ -550,7 +603,7 @@ size_t transformer_ws_bytes(int C, int T, int H, int W, dvc_dtype dt) {
     const size_t px = (size_t)T * H * W, es = dt_size(dt);
     // A, B, E: [px][C]; big: [px][8C] (qkv, then ff1); F: [px][4C]; Vt; coef; box statistics of X
     return 3 * align256(px * C * es) + align256(px * 8 * C * es) + align256(px * 4 * C * es) +
-           attn_vt_bytes(T, H * W, C, dt) + align256((size_t)T * C * 8) + box_stats_bytes(T, H, W, C);
+           attn_ws_bytes(T, H * W, C, dt) + align256((size_t)T * C * 8) + box_stats_bytes(T, H, W, C);
 }
 
 dvc_status transformer_validate(const TF &b, int T, int H, int W) {
@@ -616,7 +669,7 @@ dvc_status transformer_launch(const TF &b, const void *x, int T, int H, int W, v
     };
     void *A = take(px * C * es), *B = take(px * C * es), *E = take(px * C * es);
     void *big = take(px * 8 * C * es), *Fb = take(px * 4 * C * es);
-    void *vt = take(attn_vt_bytes(T, H * W, C, b.dt));
+    void *vt = take(attn_ws_bytes(T, H * W, C, b.dt));
     float2 *coef = reinterpret_cast<float2 *>(take((size_t)T * C * 8));
     void *bst = take(box_stats_bytes(T, H, W, C));
     dvc_status st;
@@ -692,7 +745,7 @@ dvc_status dvc_transformer_forward(const dvc_transformer *b, const void *x, int 
 
 dvc_status dvc_attention_workspace_size(int T, int N, int C, dvc_dtype dt, size_t *bytes) {
     DVC_CHECK_ARG(bytes && T >= 1 && N >= 1 && C >= 1 && dt_valid(dt), DVC_ERR_ARG, "bad arguments");
-    *bytes = dt == DVC_F32 ? 0 : attn_vt_bytes(T, N, C, dt);
+    *bytes = dt == DVC_F32 ? 0 : attn_ws_bytes(T, N, C, dt);
     return DVC_OK;
 }
 
@@ -701,7 +754,7 @@ dvc_status dvc_attention_forward(const void *qkv, int T, int N, int C, int head_
     DVC_CHECK_ARG(qkv && out && dt_valid(dt), DVC_ERR_ARG, "null argument / bad dtype");
     DVC_CHECK_ARG(C % 8 == 0, DVC_ERR_UNSUPPORTED, "attention: C must be a multiple of 8");
     if (dt != DVC_F32) {
-        DVC_CHECK_ARG(workspace && ws_bytes >= attn_vt_bytes(T, N, C, dt), DVC_ERR_WORKSPACE, "workspace too small");
+        DVC_CHECK_ARG(workspace && ws_bytes >= attn_ws_bytes(T, N, C, dt), DVC_ERR_WORKSPACE, "workspace too small");
         DVC_CHECK_ARG(((uintptr_t)workspace & 255) == 0 && ((uintptr_t)qkv & 15) == 0 && ((uintptr_t)out & 15) == 0,
                       DVC_ERR_ARG, "workspace 256-byte, qkv/out 16-byte aligned");
     }

@@ -18,8 +18,8 @@ dvc_status transformer_validate(const TF &b, int T, int H, int W);
 // y may alias x.  stats_x: box statistics of x (null = computed here); stats_y: box statistics of y or null.
 dvc_status transformer_launch(const TF &b, const void *x, int T, int H, int W, void *y, void *ws, cudaStream_t s,
                               const void *stats_x = nullptr, void *stats_y = nullptr);
-// multi-head self-attention over a packed qkv [T][N][3C] -> out [T][N][C]; vt: attn_vt_bytes scratch
-size_t attn_vt_bytes(int T, int N, int C, dvc_dtype dt);
+// multi-head self-attention over a packed qkv [T][N][3C] -> out [T][N][C]; ws: attn_ws_bytes scratch (packed operand tiles)
+size_t attn_ws_bytes(int T, int N, int C, dvc_dtype dt);
 dvc_status attention_run(const void *qkv, int T, int N, int C, int D, dvc_dtype dt, void *vt, void *out,
                          cudaStream_t s);
 
