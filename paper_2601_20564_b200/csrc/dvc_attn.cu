@@ -210,11 +210,11 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const float *__restrict_
 }
 
 // ----------------------------------------------------------------- attention, tcgen05
-// One CTA = two 128-query tiles (256 queries) of one (frame, head), 10 warps:
-//   warps 0-3  softmax group 0 (tile 0; thread r owns query row r = TMEM lane r)
-//   warps 4-7  softmax group 1 (tile 1)
-//   warp 8     MMA issuer (one elected lane): S_t = Q_t K_j^T, PV_t = P_t V_j
-//   warp 9     TMA producer: Q tiles once, then a 3-stage ring of (K_j, V_j^T) tiles
+// One CTA = two 128-query tiles (256 queries) of one (frame, head), 18 warps:
+//   warps 0-15 softmax: tile (bit 2), TMEM lane quarter (bits 0-1), key half (bit 3); the two
+//              threads of a query row each handle 64 of the tile's 128 keys
+//   warp 16    MMA issuer (one elected lane): S_t = Q_t K_j^T, PV_t = P_t V_j
+//   warp 17    producer: Q tiles once, then a 4-stage ring of (K_j, V_j^T) tiles
 // TMEM (512 columns): S_0 [0,128), S_1 [128,256), O_0 [256,+D), O_1 [320,+D), P_0 [384,448),
 // P_1 [448,512) (P as packed 16-bit pairs: the PV MMA takes A from TMEM, so neither the P stores
 // nor the PV operand reads touch shared memory).
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const float *__restrict_
 //   Q/K [rows][D]:  core (r8, kc) at kc*2048 + r8*128   (LBO 2048, SBO 128)
 //   V^T [D][keys]:  core (d8, kc) at kc*D*16 + d8*128   (LBO D*16, SBO 128)
 
-constexpr int kAttnThreads = 320;
+constexpr int kAttnThreads = 576;   // 16 softmax warps + MMA warp + TMA warp
 constexpr int kAttnStages = 4;
 template <int D>
 struct AttnSmem {
@@ -243,7 +243,8 @@ struct AttnSmem {
     static constexpr int off_bar = off_v + kAttnStages * V;
     // barriers: q_full, kv_full[3], kv_empty[3], s_full[2], s_free[2], p_full[2], o_full[2][2]
     static constexpr int nbar = 1 + 2 * kAttnStages + 2 + 2 + 2 + 4;
-    static constexpr int bytes = off_bar + nbar * 8 + 16 + 1024;   // + TMEM slot + alignment slack
+    static constexpr int off_red = off_bar + nbar * 8 + 16;     // [2 tiles][2 halves][128 rows] float exchange
+    static constexpr int bytes = off_red + 2 * 2 * 128 * 4 + 1024;   // + alignment slack
 };
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -308,11 +309,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const int sf = 1 + 2 * kAttnStages;
         mbar_init(&b[sf], 1), mbar_init(&b[sf + 1], 1);          // s_full (tcgen05.commit)
         mbar_init(&b[sf + 2], 4), mbar_init(&b[sf + 3], 4);      // s_free (one arrive per softmax warp)
-        mbar_init(&b[sf + 4], 4), mbar_init(&b[sf + 5], 4);      // p_full
+        mbar_init(&b[sf + 4], 8), mbar_init(&b[sf + 5], 8);      // p_full (8 softmax warps per tile)
         for (int i = 0; i < 4; ++i) mbar_init(&b[sf + 6 + i], 1);   // o_full
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) tmem_alloc<1>(smem_u32(tslot), 512);
+    if (warp == 16) tmem_alloc<1>(smem_u32(tslot), 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // The MMA warp and the softmax groups are one latency chain (S -> softmax -> P -> PV, S):
     // they poll without a suspend hint (a suspended try_wait wakes late, measured ~1.6 us per
     // iteration of pure barrier round trips); the TMA producer runs ahead and may sleep.
-    if (warp == 9) {
+    if (warp == 17) {
         // ===================== TMA producer =====================
         if (elect_one()) {
             const int ntiles = (N + 127) / 128, heads = gridDim.y;
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 bulk_load(sb + L::off_v + st * L::V, vp + base + (size_t)j * 128 * D, L::V, kv_full + 8 * st);
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == 16) {
         // ===================== MMA issuer =====================
         if (elect_one()) {
             mbar_wait_spin_addr(q_full, 0);
@@ -392,12 +393,19 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
     } else {
         // ===================== softmax groups =====================
-        const int tt = warp >> 2, q4 = warp & 3;
+        // tile tt = bit 2 of the warp, lane quarter q4 = bits 0-1, column half = bit 3: each S row is
+        // split over two threads (64 keys each) in two warps of the same lane quarter, four softmax
+        // warps per SM sub-partition; the row max / sum halves meet through shared memory behind a
+        // 64-thread named barrier per warp pair
+        const int tt = (warp >> 2) & 1, q4 = warp & 3, half = warp >> 3;
         const int row = q4 * 32 + lane;
+        const uint32_t bar_id = 1 + tt * 4 + q4;
+        float *red = reinterpret_cast<float *>(smem + L::off_red) + tt * 256;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-        const uint32_t tS = tmem + lane_off + tt * 128;
+        const uint32_t tS = tmem + lane_off + tt * 128 + half * 64;
         const uint32_t tO = tmem + lane_off + 256 + tt * 64;
-        const uint32_t tP = tmem + lane_off + 384 + tt * 64;
+        const uint32_t tP = tmem + lane_off + 384 + tt * 64 + half * 32;
+        auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nkt; ++j) {
             mbar_wait_spin_addr(s_full + 8 * tt, j & 1);
@@ -407,47 +415,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 if (lane == 0) mbar_arrive(p_full + 8 * tt);
                 continue;
             }
-            // each thread reads its S row ONCE (128 registers); max and exp2 from registers
-            const int kvalid = N - j * 128;   // keys >= kvalid of this tile are padding
-            uint32_t sr[128];
+            const int kvalid = N - j * 128 - half * 64;   // keys >= kvalid of this half are padding
+            uint32_t sr[64];
+            tmem_ld32_nowait(tS, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+            tmem_ld32_nowait(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+            tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+            tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+            if (kvalid < 64) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                tmem_ld32_nowait(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-            if (dbg & 4) {   // DVC_ATTN_DEBUG bit 2: S loads only (TMEM read bandwidth probe)
-                if (sr[0] == 0x7fffffffu && sr[127] == 0x7fffffffu) l += 1.f;
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(p_full + 8 * tt);
-                continue;
-            }
-            if (kvalid < 128) {
-#pragma unroll
-                for (int i = 0; i < 128; ++i)
+                for (int i = 0; i < 64; ++i)
                     if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
             }
-            // independent partial maxima / sums: with two softmax warps per SM sub-partition a
-            // single 128-long dependency chain would leave the pipes idle
             float mxp[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) mxp[i] = fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[8 + i]));
 #pragma unroll
-            for (int i = 16; i < 128; i += 16)
+            for (int i = 16; i < 64; i += 16)
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     mxp[k] = fmaxf(mxp[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
-            const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                                   fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+            float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+            red[half * 128 + row] = mx;
+            pair_sync();
+            mx = fmaxf(mx, red[(half ^ 1) * 128 + row]);
             const float mt = mx * scale_log2;
             if (j == 0) {
                 m = mt;
             } else {
-                const bool move = mt > m + 8.f;   // lazy maximum: P stays <= 2^8
+                const bool move = mt > m + 8.f;   // lazy maximum: P stays <= 2^8 (same decision in both halves)
                 if (__any_sync(0xffffffffu, move)) {
                     const float alpha = move ? ex2f(m - mt) : 1.f;
 #pragma unroll
                     for (int c = 0; c < D / 16; ++c) {
+                        if ((c & 1) != half) continue;   // O column chunks split between the halves
                         uint32_t r[16];
                         tmem_ld16(tO + c * 16, r);
 #pragma unroll
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             }
             float rsp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {   // 32 keys -> 16 packed columns of P_t in TMEM
+            for (int c = 0; c < 2; ++c) {   // 32 keys -> 16 packed columns of P_t in TMEM
                 uint32_t pk[16];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -483,12 +484,18 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full + 8 * tt);
         }
+        // row sum = both halves' partial sums (same reference max m)
+        pair_sync();   // the partner has finished reading red[] of the last iteration
+        red[half * 128 + row] = l;
+        pair_sync();
+        l += red[(half ^ 1) * 128 + row];
         mbar_wait_spin_addr(o_full + 8 * tt, 0);
         tc_fence_after();
         const int n = q0 + tt * 128 + row;
         const float inv = 1.f / l;
 #pragma unroll
         for (int c = 0; c < D / 16; ++c) {
+            if ((c & 1) != half) continue;
             uint32_t r[16];
             tmem_ld16(tO + c * 16, r);
             if (n < N) {
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     griddep_launch();
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) tmem_dealloc<1>(tmem, 512);
+    if (warp == 16) tmem_dealloc<1>(tmem, 512);
 }
 
 // ----------------------------------------------------------------- host side
