@@ -228,6 +228,39 @@ DVC_API dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *
                                int T_local, const void *carry_in, void *carry_out, void *out,
                                void *workspace, size_t ws_bytes, void *stream);
 
+/* The configuration a handle was created with (NULL for a NULL handle). */
+DVC_API const dvc_unet_config *dvc_unet_get_config(const dvc_unet *n);
+
+/* ------------------------------------------------------------------------
+ * f3.  Asynchronous and Parallel Decoding Pipeline (Fig. APDP).
+ * The in-loop Latent Compressor produces (Lbar_t, C^m_t) frame by frame on
+ * the caller's stream; the out-of-loop Frame Reconstructor (the U-Net) runs
+ * on the pipeline's own stream over batches of N frames taken from a FIFO of
+ * `fifo_batches` slots, with the Batch-dimension OTSM carry passed from batch
+ * to batch (Inter-batch Shift).  Latency is N-1 frames.
+ *   push(lat_t, ctx_t): device pointers [h,w,c_lat] / [h,w,c_ctx] in the
+ *     net's dtype, valid on `stream`; copied into the FIFO (stream-ordered,
+ *     no host sync).  When N frames are buffered their decode is enqueued on
+ *     the pipeline stream (after an event on `stream`).  DVC_ERR_ARG if all
+ *     slots hold decoded batches nobody popped (pop first).
+ *   pop(out, stream, &frames, &first): if the oldest batch is complete on the
+ *     host's bookkeeping, enqueue (on `stream`, after the decode's event) the
+ *     copy of its `frames` reconstructed latents into out [frames,h,w,c_lat]
+ *     and return the index of its first frame; frames = 0 if none is ready.
+ *   flush(): enqueue the decode of a partial last batch (T < N, R18).
+ *   reset(): the next push starts a new chain (zero carry, R8/R9); flushes
+ *     a partial batch first.
+ * Frames t of one chain come out bit-identical to one dvc_unet_decode_gop
+ * call over the whole chain (batch == online, P9).
+ * ------------------------------------------------------------------------ */
+typedef struct dvc_pipeline dvc_pipeline;
+DVC_API dvc_status dvc_pipeline_create(dvc_unet *net, int batch_n, int fifo_batches, dvc_pipeline **out);
+DVC_API dvc_status dvc_pipeline_destroy(dvc_pipeline *p);
+DVC_API dvc_status dvc_pipeline_push(dvc_pipeline *p, const void *lat, const void *ctx, void *stream);
+DVC_API dvc_status dvc_pipeline_pop(dvc_pipeline *p, void *out, void *stream, int *frames, long long *first_frame);
+DVC_API dvc_status dvc_pipeline_flush(dvc_pipeline *p);
+DVC_API dvc_status dvc_pipeline_reset(dvc_pipeline *p);
+
 /* Multi-GPU halo communicator (NCCL, loaded at run time from the process's
  * libnccl.so.2).  id128: 128-byte ncclUniqueId, created on rank 0 and
  * broadcast by the caller (e.g. torch.distributed). */

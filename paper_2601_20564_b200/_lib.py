@@ -77,6 +77,14 @@ _SIGS = {
     "dvc_attention_workspace_size": ([c_int, c_int, c_int, c_int, ctypes.POINTER(c_size_t)], c_int),
     "dvc_attention_forward": ([c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_size_t,
                                c_void_p], c_int),
+    "dvc_unet_get_config": ([c_void_p], ctypes.POINTER(dvc_unet_config)),
+    "dvc_pipeline_create": ([c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)], c_int),
+    "dvc_pipeline_destroy": ([c_void_p], c_int),
+    "dvc_pipeline_push": ([c_void_p, c_void_p, c_void_p, c_void_p], c_int),
+    "dvc_pipeline_pop": ([c_void_p, c_void_p, c_void_p, ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_longlong)],
+                         c_int),
+    "dvc_pipeline_flush": ([c_void_p], c_int),
+    "dvc_pipeline_reset": ([c_void_p], c_int),
     "dvc_set_conv_engine": ([c_int], c_int),
     "dvc_profile_begin": ([c_int], c_int),
     "dvc_profile_end": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),

@@ -468,6 +468,8 @@ dvc_status dvc_unet_destroy(dvc_unet *n) {
     return DVC_OK;
 }
 
+const dvc_unet_config *dvc_unet_get_config(const dvc_unet *n) { return n ? &n->cfg : nullptr; }
+
 dvc_status dvc_unet_carry_size(const dvc_unet *n, size_t *elems) {
     DVC_CHECK_ARG(n && elems, DVC_ERR_ARG, "null argument");
     *elems = n->carry_total;

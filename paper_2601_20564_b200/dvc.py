@@ -270,6 +270,49 @@ def dvc_unet_decode_gop(net: UNet, lat, ctx, comm: Comm | None = None, carry_in=
     return out
 
 
+class Pipeline:
+    """f3 Asynchronous and Parallel Decoding Pipeline (dvc_pipeline_*): push one frame's
+    (Lbar_t, C^m_t) at a time from the in-loop producer's stream; the U-Net decodes batches of N
+    frames on the pipeline's own stream; pop() hands back decoded batches in order (latency N-1)."""
+
+    def __init__(self, net: UNet, batch_n: int, fifo_batches: int = 2):
+        self.net = net
+        cfg = net.cfg
+        self.dtype = {0: torch.bfloat16, 1: torch.float16, 2: torch.float32}[cfg.dt]
+        self.shape = (cfg.h, cfg.w, cfg.c_lat)
+        self.N = batch_n
+        self.handle = ctypes.c_void_p()
+        check(lib().dvc_pipeline_create(net.handle, batch_n, fifo_batches, ctypes.byref(self.handle)))
+
+    def push(self, lat, ctx, stream=None):
+        check(lib().dvc_pipeline_push(self.handle, _ptr(lat), _ptr(ctx), _stream(stream)))
+
+    def pop(self, out=None, stream=None):
+        """-> (first frame index, decoded latents [frames,h,w,c_lat]) or None if nothing is ready."""
+        if out is None:
+            out = torch.empty((self.N,) + self.shape, dtype=self.dtype, device="cuda")
+        n, first = ctypes.c_int(), ctypes.c_longlong()
+        check(lib().dvc_pipeline_pop(self.handle, _ptr(out), _stream(stream), ctypes.byref(n), ctypes.byref(first)))
+        return None if n.value == 0 else (first.value, out[:n.value])
+
+    def flush(self):
+        check(lib().dvc_pipeline_flush(self.handle))
+
+    def reset(self):
+        check(lib().dvc_pipeline_reset(self.handle))
+
+    def close(self):
+        if self.handle:
+            lib().dvc_pipeline_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class StreamingDecoder:
     """f4 online streaming: one frame per step (latency N-1 = 0), the 22 block carries in a ring of
     two buffers, every step one CUDA-graph replay of dvc_unet_decode_gop(T=1).
