@@ -128,7 +128,7 @@ DVC_API dvc_status dvc_debug_shift_gather(const void *x_a, const void *x_b, int 
 /* ------------------------------------------------------------------------
  * f1.  One self-attention Transformer2D block of the full U-Net (the
  * U-Net of SD-2.1 via AdcSR; 444.78 M parameters with these blocks;
- * readings R21-R24 in DESIGN.md): SD-2.1's Transformer2DModel with the text
+ * readings R24-R27 in DESIGN.md): SD-2.1's Transformer2DModel with the text
  * cross-attention removed, frames independent (no temporal shift):
  *   a  = GN(x)             groups, eps_gn (1e-6), per frame, no SiLU
  *   h0 = a proj_in_w^T + proj_in_b                  ([C][C])
@@ -178,7 +178,7 @@ DVC_API dvc_status dvc_attention_forward(const void *qkv, int T, int N, int C, i
  * (identity; the ResBlock skeleton of SURVEY 8a).  head_dim > 0 (f1, the full
  * U-Net): a Transformer2D block (dvc_transformer, groups/eps_gn 1e-6/eps_ln
  * 1e-5) follows every ResBlock of down levels 0-2, mid.r0 and every ResBlock
- * of up levels 2-0 (R23); its 17 tensors (gn_w, gn_b, proj_in_w, proj_in_b,
+ * of up levels 2-0 (R26); its 17 tensors (gn_w, gn_b, proj_in_w, proj_in_b,
  * ln1_w, ln1_b, qkv_w, out_w, out_b, ln2_w, ln2_b, ff1_w, ff1_b, ff2_w, ff2_b,
  * proj_out_w, proj_out_b) follow that ResBlock's in the blob.
  *
@@ -200,7 +200,7 @@ typedef struct {
     dvc_dtype dt;
     int h, w;          /* latent size, e.g. 90x160 (720p), 135x240 (1080p) */
     int max_T;         /* largest T_local per call; sizes the workspace */
-    int head_dim;      /* 0 = skeleton (attention elided); 16/32/48/64 = full U-Net (48: R22) */
+    int head_dim;      /* 0 = skeleton (attention elided); 16/32/48/64 = full U-Net (48: R25) */
 } dvc_unet_config;
 
 typedef struct dvc_unet dvc_unet;

@@ -255,12 +255,12 @@ def resblock(X, carry, w: dict, G: int, P: int, eps: float = 1e-5, mode=None,
 
 # --------------------------------------------------------------------------
 # f1. Self-attention Transformer2D blocks ("U-Net"; P:525 parameter count;
-# readings R21-R24 in DESIGN.md section 3).  SD-2.1's Transformer2DModel with
+# readings R24-R27 in DESIGN.md section 3).  SD-2.1's Transformer2DModel with
 # the text cross-attention removed: GN -> proj_in -> [LN -> self-attention ->
 # +res] -> [LN -> GEGLU FF -> +res] -> proj_out -> + block input.
 # --------------------------------------------------------------------------
 def layernorm(X, gamma, beta, eps: float = 1e-5):
-    """LayerNorm over the channels of every pixel, biased two-pass variance (R21)."""
+    """LayerNorm over the channels of every pixel, biased two-pass variance (R24)."""
     X = _f64(X)
     mu = X.mean(axis=-1, keepdims=True)
     var = ((X - mu) ** 2).mean(axis=-1, keepdims=True)
@@ -268,14 +268,14 @@ def layernorm(X, gamma, beta, eps: float = 1e-5):
 
 
 def gelu(X):
-    """Exact GELU x * Phi(x) = x/2 * (1 + erf(x / sqrt 2)) (GEGLU gate, R21)."""
+    """Exact GELU x * Phi(x) = x/2 * (1 + erf(x / sqrt 2)) (GEGLU gate, R24)."""
     from scipy.special import erf
     X = _f64(X)
     return 0.5 * X * (1.0 + erf(X / np.sqrt(2.0)))
 
 
 def attention(Q, K, V, head_dim: int, rows=None):
-    """Multi-head self-attention of every frame over its own h*w tokens (R22):
+    """Multi-head self-attention of every frame over its own h*w tokens (R25):
     for each frame t and head j (channels [j*d, (j+1)*d)),
         O_j = softmax(Q_j K_j^T / sqrt(d)) V_j   (row softmax).
     Q, K, V [T,N,C]; rows: optional query indices (sampled check at large N).
@@ -313,7 +313,7 @@ def tf_shapes(C: int) -> dict:
 
 def transformer(X, w: dict, G: int, head_dim: int, eps_gn: float = 1e-6, eps_ln: float = 1e-5,
                 mode=None):
-    """One Transformer2D block over X [T,h,w,C] (R21-R24), frames independent:
+    """One Transformer2D block over X [T,h,w,C] (R24-R27), frames independent:
         a  = GN(X)                          (G groups, eps 1e-6, no SiLU)
         h0 = proj_in(a)                     (1x1, C -> C, bias)
         q,k,v = split(LN1(h0) W_qkv^T)      (no bias)
@@ -321,7 +321,7 @@ def transformer(X, w: dict, G: int, head_dim: int, eps_gn: float = 1e-6, eps_ln:
         f  = ff1(LN2(h1))                   (C -> 8C, bias); g = f[:4C] * gelu(f[4C:])
         h2 = ff2(g) + h1                    (4C -> C, bias)
         Y  = proj_out(h2) + X               (1x1 + bias)
-    mode rounds every stored tensor to 16-bit (R24)."""
+    mode rounds every stored tensor to 16-bit (R27)."""
     X = _f64(X)
     T, H, W, C = X.shape
     N = H * W
@@ -427,7 +427,7 @@ def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int 
                                   if u < 3: nearest to the next skip's size, conv3x3
         out = conv_out(silu(gn_out(h)))
     attention=False: the 16 self-attention Transformer2D blocks are elided (identity).
-    attention=True (f1, full U-Net, R23): a Transformer2D block follows every ResBlock of
+    attention=True (f1, full U-Net, R26): a Transformer2D block follows every ResBlock of
     down levels 0-2, mid.r0, and every ResBlock of up levels 2-0; its weights follow that
     ResBlock's in the blob (TF_ORDER).
     weights: iterable of (name, array) in the blob order of include/dvc.h.

@@ -1,5 +1,5 @@
 // dvc_attn.cu -- f1: the self-attention Transformer2D blocks of the full pruned U-Net
-// ("U-Net" of SD-2.1 via AdcSR, P:525 parameter count; readings R21-R24).
+// ("U-Net" of SD-2.1 via AdcSR, P:525 parameter count; readings R24-R27).
 //
 // One block over X [T][H][W][C] (frames independent, no temporal shift):
 //   a  = GN(X)                      gn_affine_kernel  (coefficients from box statistics)
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(256) gn_affine_kernel(const T *__restrict__ x,
     griddep_launch();
 }
 
-// LayerNorm over the C channels of each pixel (R21): one warp per pixel, fp32 two-pass
+// LayerNorm over the C channels of each pixel (R24): one warp per pixel, fp32 two-pass
 // from registers (C <= 32 * 8 * 4 = 1024).
 template <typename T>
 __global__ void __launch_bounds__(256) layernorm_kernel(const T *__restrict__ x, const T *__restrict__ gamma,
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const T *__restrict__ x,
     griddep_launch();
 }
 
-// GEGLU (R21): g[m][j] = f[m][j] * gelu(f[m][C4 + j]), exact erf GELU.
+// GEGLU (R24): g[m][j] = f[m][j] * gelu(f[m][C4 + j]), exact erf GELU.
 template <typename T>
 __global__ void __launch_bounds__(256) geglu_kernel(const T *__restrict__ f, T *__restrict__ g, int C4, long total8) {
     griddep_wait();

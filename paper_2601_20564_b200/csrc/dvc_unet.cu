@@ -147,7 +147,7 @@ void walk(dvc_unet &n, Take take) {
         n.tf_of[bi] = -1;
         ++bi;
     };
-    // f1 (R23): a Transformer2D block after the ResBlock just walked; tensors follow its weights
+    // f1 (R26): a Transformer2D block after the ResBlock just walked; tensors follow its weights
     n.ntf = 0;
     auto tfb = [&](int C) {
         if (c.head_dim <= 0) return;

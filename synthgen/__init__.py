@@ -83,7 +83,7 @@ TF_ORDER = ("gn_w", "gn_b", "proj_in_w", "proj_in_b", "ln1_w", "ln1_b", "qkv_w",
 
 
 def transformer_weights(C: int, seed: int = SEED_WEIGHTS, g=None, qkv_scale: float = 1.0) -> dict:
-    """One Transformer2D block's parameters (reading R21; blob order TF_ORDER):
+    """One Transformer2D block's parameters (reading R24; blob order TF_ORDER):
     Linear layers PyTorch-default U(+-1/sqrt(fan_in)); norms gamma ~ U(0.5,1.5),
     beta ~ U(-0.5,0.5).  qkv_scale > 1 sharpens the attention (test-only knob)."""
     g = rng(seed) if g is None else g

@@ -17,7 +17,7 @@ def _rng(s=0):
     return np.random.default_rng(s)
 
 
-# ---------------------------------------------------------------- GELU (R21)
+# ---------------------------------------------------------------- GELU (R24)
 def test_gelu_closed_forms(orc):
     assert orc.gelu(np.array([0.0]))[0] == 0.0
     # x * Phi(x) at 1: Phi(1) = 0.8413447460685429 (standard normal CDF table value)
@@ -28,7 +28,7 @@ def test_gelu_closed_forms(orc):
     assert np.allclose(orc.gelu(x), F.gelu(torch.from_numpy(x)).numpy(), rtol=1e-13, atol=1e-15)
 
 
-# ---------------------------------------------------------------- LayerNorm (R21)
+# ---------------------------------------------------------------- LayerNorm (R24)
 def test_layernorm_moments_and_library(orc):
     X = _rng(1).standard_normal((2, 3, 4, 48)) * 2 + 0.7
     one, zero = np.ones(48), np.zeros(48)
@@ -43,7 +43,7 @@ def test_layernorm_moments_and_library(orc):
     assert np.array_equal(orc.layernorm(np.full((1, 1, 1, 48), 3.25), g, b)[0, 0, 0], b)
 
 
-# ---------------------------------------------------------------- attention (R22)
+# ---------------------------------------------------------------- attention (R25)
 def test_attention_uniform_and_single_key(orc):
     T, N, C, d = 2, 7, 32, 16
     V = _rng(4).standard_normal((T, N, C))
@@ -87,7 +87,7 @@ def test_attention_matches_library_and_permutations(orc):
     assert np.array_equal(orc.attention(Q, K, V, d, rows=rows), O[:, rows])
 
 
-# ---------------------------------------------------------------- Transformer2D block (R21-R24)
+# ---------------------------------------------------------------- Transformer2D block (R24-R27)
 def _tf(C, seed=0, **kw):
     return {k: v.astype(np.float64) for k, v in synthgen.transformer_weights(C, seed=seed, **kw).items()}
 
@@ -134,7 +134,7 @@ def test_transformer_pixel_permutation_equivariant_and_frame_local(orc):
     assert np.array_equal(Y2[0], Y[0]) and not np.allclose(Y2[1], Y[1])
 
 
-# ---------------------------------------------------------------- full U-Net (R1 + R23)
+# ---------------------------------------------------------------- full U-Net (R1 + R26)
 def test_full_unet_blob_matches_table8(orc):      # 444.78 M parameters
     wts = synthgen.unet_weights(attention=True)
     n = sum(a.size for _, a in wts)

@@ -5,7 +5,7 @@
   ATTN  the tcgen05 attention kernel alone at the 720p U-Net shapes (T=32 frames: level 0
         N=14400 C=240, level 1 N=3600 C=480, level 2 N=920 C=960, head_dim 48): ms, algorithmic
         TFLOP/s (4*N^2*C per frame) and the fraction of the measured bf16 peaks
-  F1    full pruned U-Net (22 ResBlocks + 16 Transformer2D blocks, R21-R23) decode at 720p,
+  F1    full pruned U-Net (22 ResBlocks + 16 Transformer2D blocks, R24-R26) decode at 720p,
         T=32, bf16: frames/s, and the per-kernel-family split of one profiled step
 The headline metric (bench.py) stays the ResBlock-skeleton decode the north star names.
 """
