@@ -510,6 +510,105 @@ def skeleton(lat, ctx, weights, width=(240, 480, 960, 960), G: int = 24, P: int 
     return out, k_out
 
 
+# --------------------------------------------------------------------------
+# f2. Pruned VAE Decoder ("Pruned VAE Decoder reduces intermediate channels by
+# 50%", P:108 latent interface expanded to 256 channels; Table 8; readings R29-R31).
+# SD-2.1's AutoencoderKL decoder with block widths x0.5 = (64, 128, 256, 256), no temporal
+# shift (frames independent).
+# --------------------------------------------------------------------------
+def vae_resblock(X, w: dict, G: int, eps: float, mode=None):
+    """SD VAE ResnetBlock2D: Out = S(X) + conv2(silu(gn2(conv1(silu(gn1(X)))))) (no shift)."""
+    X = _f64(X)
+    H1 = rnd(silu(groupnorm(X, G, w["gn1_w"], w["gn1_b"], eps)), mode)
+    Y1 = rnd(conv2d(H1, w["conv1_w"], w["conv1_b"]), mode)
+    H2 = rnd(silu(groupnorm(Y1, G, w["gn2_w"], w["gn2_b"], eps)), mode)
+    Y2 = conv2d(H2, w["conv2_w"], w["conv2_b"])
+    S = X if w.get("sc_w") is None else conv1x1(X, w["sc_w"], w["sc_b"])
+    return rnd(S + Y2, mode)
+
+
+def vae_attention(X, w: dict, G: int, eps: float, mode=None):
+    """SD VAE mid-block attention: single head over the h*w tokens of each frame,
+    Y = X + out(softmax(q k^T / sqrt C) v), q/k/v/out linear with bias on GN(X)."""
+    X = _f64(X)
+    T, H, W, C = X.shape
+    a = rnd(groupnorm(X, G, w["gn_w"], w["gn_b"], eps), mode)
+    q = rnd(conv1x1(a, w["q_w"], w["q_b"]), mode).reshape(T, H * W, C)
+    k = rnd(conv1x1(a, w["k_w"], w["k_b"]), mode).reshape(T, H * W, C)
+    v = rnd(conv1x1(a, w["v_w"], w["v_b"]), mode).reshape(T, H * W, C)
+    o = rnd(attention(q, k, v, C), mode).reshape(T, H, W, C)
+    return rnd(conv1x1(o, w["out_w"], w["out_b"]) + X, mode)
+
+
+def vae_blocks(width=(64, 128, 256, 256)):
+    """Reading R29: [(name, level, cin, cout)] of the decoder's ResBlocks in execution order;
+    level 0 = latent resolution, 3 = full resolution."""
+    top = width[-1]
+    blocks = [("mid.r0", 0, top, top), ("mid.r1", 0, top, top)]
+    cur = top
+    for i, c in enumerate(reversed(width)):
+        for r in range(3):
+            blocks.append((f"up{i}.r{r}", i, cur, c))
+            cur = c
+    return blocks
+
+
+def vae_param_count(width=(64, 128, 256, 256), c_lat=256, out_ch=3, mid_attn=True):
+    """Closed form of reading R29 (compare Table 8: 12.38 M)."""
+    top = width[-1]
+    n = 9 * c_lat * top + top
+    for _, _, ci, co in vae_blocks(width):
+        n += 2 * ci + 9 * ci * co + co + 2 * co + 9 * co * co + co + (ci * co + co if ci != co else 0)
+    if mid_attn:
+        n += 2 * top + 4 * (top * top + top)
+    for c in list(reversed(width))[:3]:
+        n += 9 * c * c + c
+    return n + 2 * width[0] + 9 * width[0] * out_ch + out_ch
+
+
+def vae_decode(L, weights, width=(64, 128, 256, 256), G: int = 32, eps: float = 1e-6, out_ch: int = 3,
+               mid_attn: bool = True, mode=None):
+    """L [T,h,w,c_lat] (the U-Net's Lhat) -> frames [T,8h,8w,out_ch] (NHWC), R29-R31:
+        x = conv_in(L); mid: ResBlock, [attention], ResBlock
+        for i = 0..3 (widths reversed): 3 ResBlocks; if i < 3: nearest 2x, conv3x3
+        out = conv_out(silu(gn_out(x)))
+    weights: iterable of (name, array) in the blob order of include/dvc.h (dvc_vae_create)."""
+    it = iter(weights)
+    L = _f64(L)
+    top = width[-1]
+    x = rnd(conv2d(L, _take(it, (top, 3, 3, L.shape[-1]), "conv_in_w"), _take(it, (top,), "conv_in_b")), mode)
+    blocks = vae_blocks(width)
+    bi = 0
+
+    def rb(x):
+        nonlocal bi
+        _, _, ci, co = blocks[bi]
+        bi += 1
+        return vae_resblock(x, _rb_weights(it, ci, co), G, eps, mode)
+
+    x = rb(x)
+    if mid_attn:
+        sh = {"gn_w": (top,), "gn_b": (top,), "q_w": (top, top), "q_b": (top,), "k_w": (top, top), "k_b": (top,),
+              "v_w": (top, top), "v_b": (top,), "out_w": (top, top), "out_b": (top,)}
+        x = vae_attention(x, {k: _take(it, sh[k], k) for k in sh}, G, eps, mode)
+    x = rb(x)
+    for i, c in enumerate(reversed(width)):
+        for _ in range(3):
+            x = rb(x)
+        if i < 3:
+            T, H, W, _ = x.shape
+            x = rnd(conv2d(nearest_to(x, 2 * H, 2 * W), _take(it, (c, 3, 3, c), "up_w"), _take(it, (c,), "up_b")),
+                    mode)
+    C = x.shape[-1]
+    g, b = _take(it, (C,), "gn_out_w"), _take(it, (C,), "gn_out_b")
+    hn = rnd(silu(groupnorm(x, G, g, b, eps)), mode)
+    out = rnd(conv2d(hn, _take(it, (out_ch, 3, 3, C), "conv_out_w"), _take(it, (out_ch,), "conv_out_b")), mode)
+    rest = list(it)
+    if rest:
+        raise ValueError(f"{len(rest)} unused weight tensors")
+    return out
+
+
 def rel_l2(a, ref) -> float:
     """||a - ref||_2 / ||ref||_2 (R16)."""
     a, ref = _f64(a), _f64(ref)

@@ -168,3 +168,49 @@ def unet_weights(width=(240, 480, 960, 960), c_lat: int = 256, c_ctx: int = 256,
     out.append(("gn_out.b", gb))
     conv("conv_out", c_lat, cur)
     return out
+
+
+def vae_weights(width=(64, 128, 256, 256), c_lat: int = 256, out_ch: int = 3, mid_attn: bool = True,
+                seed: int = SEED_WEIGHTS, attn_scale: float = 1.0):
+    """Pruned VAE decoder tensors (f2, reading R29) in the blob order of include/dvc.h's
+    dvc_vae_create: conv_in{w,b}; mid.r0; [mid attention {gn_w, gn_b, q_w, q_b, k_w, k_b, v_w, v_b,
+    out_w, out_b}]; mid.r1; for each up level i (widths reversed) 3 ResBlocks then (i < 3) the
+    post-upsample conv{w,b}; gn_out{w,b}; conv_out{w,b}.  ResBlocks as in resblock_weights."""
+    g = rng(seed)
+    out = []
+
+    def conv(name, cout, cin, k=3):
+        w, b = _conv(g, cout, k, cin)
+        out.append((name + ".w", w))
+        out.append((name + ".b", b))
+
+    def block(name, cin, cout):
+        d = resblock_weights(cin, cout, g=g)
+        for k in RB_ORDER:
+            if d[k] is not None:
+                out.append((f"{name}.{k}", d[k]))
+
+    top = width[-1]
+    conv("conv_in", top, c_lat)
+    block("mid.r0", top, top)
+    if mid_attn:
+        gw, gb = _gn(g, top)
+        out += [("mid.attn.gn_w", gw), ("mid.attn.gn_b", gb)]
+        for nm in ("q", "k", "v", "out"):
+            w, b = _linear(g, top, top)
+            if nm in ("q", "k"):
+                w = (w * attn_scale).astype(np.float32)
+            out += [(f"mid.attn.{nm}_w", w), (f"mid.attn.{nm}_b", b)]
+    block("mid.r1", top, top)
+    cur = top
+    for i, c in enumerate(reversed(width)):
+        for r in range(3):
+            block(f"up{i}.r{r}", cur, c)
+            cur = c
+        if i < 3:
+            conv(f"up{i}.us", c, c)
+    gw, gb = _gn(g, cur)
+    out += [("gn_out.w", gw), ("gn_out.b", gb)]
+    conv("conv_out", out_ch, cur)
+    return out
+

@@ -163,3 +163,56 @@ def test_full_unet_batch_equals_online_and_causal(orc):
     lat2[2] += 1
     b, _ = orc.skeleton(lat2, ctx, wts, SMALL, **kw)
     assert np.array_equal(full[:2], b[:2]) and not np.array_equal(full[2], b[2])
+
+
+# ---------------------------------------------------------------- f2 pruned VAE decoder (R29-R31)
+def test_vae_topology_matches_table8(orc):       # P:525 Table 8: VAE Decoder 12.38 M parameters
+    # SD-2.1's decoder with widths x0.5 counts 12.387 M with the original 4-channel latent
+    # interface; variants of the reading are far off
+    assert abs(orc.vae_param_count(c_lat=4) / 1e6 - 12.38) < 0.01
+    assert abs(orc.vae_param_count(c_lat=4, mid_attn=False) / 1e6 - 12.38) > 0.2
+    assert abs(orc.vae_param_count(width=(96, 192, 384, 384), c_lat=4) / 1e6 - 12.38) > 5
+    # the 256-channel interface of P:108 (reading R29) adds 9*252*256 conv_in weights
+    assert orc.vae_param_count() - orc.vae_param_count(c_lat=4) == 9 * 252 * 256
+    wts = synthgen.vae_weights()
+    assert sum(a.size for _, a in wts) == orc.vae_param_count()
+
+
+VSMALL = (16, 32, 48, 48)
+
+
+def _vae_w(**kw):
+    return [(n, a.astype(np.float64)) for n, a in synthgen.vae_weights(VSMALL, 32, **kw)]
+
+
+def test_vae_shapes_and_frame_independence(orc):
+    T, h, w = 2, 3, 4
+    L = synthgen.normal((T, h, w, 32), 1)
+    out = orc.vae_decode(L, _vae_w(), VSMALL, G=8)
+    assert out.shape == (T, 8 * h, 8 * w, 3)
+    L2 = L.copy()
+    L2[1] += 1
+    out2 = orc.vae_decode(L2, _vae_w(), VSMALL, G=8)
+    assert np.array_equal(out[0], out2[0]) and not np.allclose(out[1], out2[1])
+
+
+def test_vae_attention_and_resblock_wiring(orc):
+    C = 32
+    d = dict(synthgen.vae_weights(VSMALL, 32))
+    w = {k.split(".")[-1]: d[k].astype(np.float64) for k in d if k.startswith("mid.attn.")}
+    X = _rng(12).standard_normal((2, 3, 5, 48))
+    w0 = dict(w, out_w=np.zeros_like(w["out_w"]), out_b=np.zeros_like(w["out_b"]))
+    assert np.array_equal(orc.vae_attention(X, w0, 8, 1e-6), X)          # residual wiring
+    # single-head attention over all tokens == the library routine on GN(X) projections
+    Xt = torch.from_numpy(X).permute(0, 3, 1, 2)
+    a = F.group_norm(Xt, 8, torch.from_numpy(w["gn_w"]), torch.from_numpy(w["gn_b"]), 1e-6)
+    a = a.permute(0, 2, 3, 1).reshape(2, 15, 48)
+    q, k, v = (a @ torch.from_numpy(w[f"{n}_w"]).T + torch.from_numpy(w[f"{n}_b"]) for n in "qkv")
+    o = F.scaled_dot_product_attention(q, k, v)
+    ref = (o @ torch.from_numpy(w["out_w"]).T + torch.from_numpy(w["out_b"])).reshape(2, 3, 5, 48).numpy() + X
+    assert np.allclose(orc.vae_attention(X, w, 8, 1e-6), ref, rtol=1e-12, atol=1e-12)
+    rb = synthgen.resblock_weights(48, 32)
+    rb = {k: (None if v is None else v.astype(np.float64)) for k, v in rb.items()}
+    rb["conv2_w"][:] = 0
+    rb["conv2_b"][:] = 0
+    assert np.allclose(orc.vae_resblock(X, rb, 8, 1e-6), orc.conv1x1(X, rb["sc_w"], rb["sc_b"]), rtol=0, atol=0)
