@@ -162,6 +162,7 @@ DVC_API dvc_status dvc_transformer_forward(const dvc_transformer *b, const void 
  * channels [j*d,(j+1)*d) of each) -> out [T,N,C], softmax(q k^T / sqrt d) v per
  * frame and head.  workspace >= dvc_attention_workspace_size (the transposed V). */
 DVC_API dvc_status dvc_attention_workspace_size(int T, int N, int C, dvc_dtype dt, size_t *bytes);
+/* head_dim in {16, 32, 48, 64, 256} (256: the VAE decoder's single-head attention). */
 DVC_API dvc_status dvc_attention_forward(const void *qkv, int T, int N, int C, int head_dim, dvc_dtype dt, void *out,
                                          void *workspace, size_t ws_bytes, void *stream);
 
@@ -260,6 +261,44 @@ DVC_API dvc_status dvc_pipeline_push(dvc_pipeline *p, const void *lat, const voi
 DVC_API dvc_status dvc_pipeline_pop(dvc_pipeline *p, void *out, void *stream, int *frames, long long *first_frame);
 DVC_API dvc_status dvc_pipeline_flush(dvc_pipeline *p);
 DVC_API dvc_status dvc_pipeline_reset(dvc_pipeline *p);
+
+/* ------------------------------------------------------------------------
+ * f2.  Pruned VAE Decoder ("Pruned VAE Decoder reduces intermediate
+ * channels by 50%"; P:108 256-channel latent interface; Table 8 P:525;
+ * readings R29-R31): SD-2.1's AutoencoderKL decoder with block widths x0.5.
+ *   x = conv_in(Lhat)                  3x3, c_lat -> width[3], latent resolution
+ *   mid: ResBlock, [single-head self-attention: x += out(softmax(q k^T/sqrt C) v),
+ *        q|k|v|out linear + bias on GN(x)], ResBlock
+ *   up level i = 0..3 (widths width[3], width[2], width[1], width[0]):
+ *        3 ResBlocks (first maps the incoming width); i < 3: nearest 2x, 3x3 conv
+ *   frames = conv_out(SiLU(GN_out(x)))  3x3, width[0] -> out_ch, 8x resolution
+ * ResBlocks as dvc_resblock without the temporal shift; GroupNorm `groups`, `eps`
+ * (SD: 32, 1e-6).  Frames independent.  Output NHWC [T, 8h, 8w, out_ch].
+ * Weight blob (dt elements, in this order): conv_in{w [W3][3][3][c_lat], b};
+ * mid.r0; [mid attention {gn_w, gn_b, q_w [W3][W3], q_b, k_w, k_b, v_w, v_b,
+ * out_w, out_b}]; mid.r1; per up level 3 ResBlocks then (i < 3) the
+ * post-upsample conv{w, b}; gn_out{w, b}; conv_out{w [out_ch][3][3][W0], b}.
+ * Requirements: widths multiples of 16, groups dividing them, out_ch <= 16,
+ * mid attention needs width[3] in {16,32,48,64,256}.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    int width[4];      /* 64, 128, 256, 256 (SD-2.1 decoder x 0.5) */
+    int c_lat;         /* 256 */
+    int out_ch;        /* 3 */
+    int groups;        /* 32 */
+    float eps;         /* 1e-6 */
+    int mid_attn;      /* 1: the mid-block self-attention; 0: elided */
+    dvc_dtype dt;
+    int h, w;          /* latent size; frames are 8h x 8w */
+    int max_T;
+} dvc_vae_config;
+typedef struct dvc_vae dvc_vae;
+DVC_API dvc_status dvc_vae_weight_count(const dvc_vae_config *cfg, size_t *elems);
+DVC_API dvc_status dvc_vae_create(const dvc_vae_config *cfg, const void *host_weights, size_t bytes, dvc_vae **out);
+DVC_API dvc_status dvc_vae_destroy(dvc_vae *v);
+DVC_API dvc_status dvc_vae_workspace_size(const dvc_vae *v, int T, size_t *bytes);
+DVC_API dvc_status dvc_vae_decode(dvc_vae *v, const void *lat, int T, void *frames, void *workspace, size_t ws_bytes,
+                                  void *stream);
 
 /* Multi-GPU halo communicator (NCCL, loaded at run time from the process's
  * libnccl.so.2).  id128: 128-byte ncclUniqueId, created on rank 0 and

@@ -49,6 +49,11 @@ class dvc_transformer(ctypes.Structure):
                 ("dt", c_int)] + [(f, c_void_p) for f in TF_FIELDS]
 
 
+class dvc_vae_config(ctypes.Structure):
+    _fields_ = [("width", c_int * 4), ("c_lat", c_int), ("out_ch", c_int), ("groups", c_int), ("eps", c_float),
+                ("mid_attn", c_int), ("dt", c_int), ("h", c_int), ("w", c_int), ("max_T", c_int)]
+
+
 _SIGS = {
     "dvc_status_string": ([c_int], ctypes.c_char_p),
     "dvc_last_error": ([], ctypes.c_char_p),
@@ -85,6 +90,11 @@ _SIGS = {
                          c_int),
     "dvc_pipeline_flush": ([c_void_p], c_int),
     "dvc_pipeline_reset": ([c_void_p], c_int),
+    "dvc_vae_weight_count": ([ctypes.POINTER(dvc_vae_config), ctypes.POINTER(c_size_t)], c_int),
+    "dvc_vae_create": ([ctypes.POINTER(dvc_vae_config), c_void_p, c_size_t, ctypes.POINTER(c_void_p)], c_int),
+    "dvc_vae_destroy": ([c_void_p], c_int),
+    "dvc_vae_workspace_size": ([c_void_p, c_int, ctypes.POINTER(c_size_t)], c_int),
+    "dvc_vae_decode": ([c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
     "dvc_set_conv_engine": ([c_int], c_int),
     "dvc_profile_begin": ([c_int], c_int),
     "dvc_profile_end": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),

@@ -147,7 +147,7 @@ static const void *identity_weights(int c, dvc_dtype dt) {
 
 // ----------------------------------------------------------------- ResBlock (a3-a8)
 static bool box_mode(const RB &b) {
-    const int cin = b.ca + b.cb, cs = cin / b.P, cg = cin / b.G;
+    const int cin = b.ca + b.cb, cs = b.P > 0 ? cin / b.P : 0, cg = cin / b.G;
     return cs % cg == 0;   // the shifted slice is whole GN groups: statistics from box partials
 }
 
@@ -164,10 +164,12 @@ dvc_status resblock_validate(const RB &b, int T, int H, int W) {
     DVC_CHECK_ARG(dt_valid(b.dt), DVC_ERR_ARG, "bad dtype");
     DVC_CHECK_ARG(T >= 1 && H >= 1 && W >= 1, DVC_ERR_ARG, "T, H, W must be >= 1");
     DVC_CHECK_ARG(b.ca > 0 && b.cb >= 0 && b.cout > 0, DVC_ERR_ARG, "bad channel counts");
-    DVC_CHECK_ARG(b.P >= 1 && cin % b.P == 0, DVC_ERR_DIVISIBILITY, "shift_p=%d must divide C_in=%d", b.P, cin);
+    // P = 0: no temporal shift (the VAE decoder's ResBlocks, f2)
+    DVC_CHECK_ARG(b.P == 0 || (b.P >= 1 && cin % b.P == 0), DVC_ERR_DIVISIBILITY, "shift_p=%d must divide C_in=%d", b.P,
+                  cin);
     DVC_CHECK_ARG(b.G >= 1 && cin % b.G == 0 && b.cout % b.G == 0, DVC_ERR_DIVISIBILITY,
                   "groups=%d must divide C_in=%d and C_out=%d", b.G, cin, b.cout);
-    DVC_CHECK_ARG(cin / b.P <= b.ca, DVC_ERR_UNSUPPORTED, "shift slice C_in/P must lie in x_a");
+    DVC_CHECK_ARG(b.P == 0 || cin / b.P <= b.ca, DVC_ERR_UNSUPPORTED, "shift slice C_in/P must lie in x_a");
     DVC_CHECK_ARG(b.gn1_w && b.gn1_b && b.conv1_w && b.conv1_b && b.gn2_w && b.gn2_b && b.conv2_w && b.conv2_b,
                   DVC_ERR_ARG, "null ResBlock parameter");
     DVC_CHECK_ARG((b.sc_w == nullptr) == (cin == b.cout), DVC_ERR_SHAPE,
@@ -189,7 +191,8 @@ dvc_status resblock_validate(const RB &b, int T, int H, int W) {
 dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, int H, int W, const void *carry_in,
                            void *carry_out, void *y, void *ws, cudaStream_t stream, const void *stats_a,
                            const void *stats_b, void *stats_y) {
-    const int HW = H * W, cin = b.ca + b.cb, cs = cin / b.P;
+    const int HW = H * W, cin = b.ca + b.cb, cs = b.P > 0 ? cin / b.P : 0;
+    if (cs == 0) carry_in = nullptr, carry_out = nullptr;   // no shift: no carries
     const size_t es = dt_size(b.dt);
     uint8_t *p = reinterpret_cast<uint8_t *>(ws);
     void *gnws = p;
@@ -247,11 +250,11 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
         FzDesc f1{};
         if (b.conv1_pk) {
             const int rows_a = 9 * ((b.ca + 63) / 64) * b.cout;
-            f1.seg[0] = FzDesc::Seg{xa, b.ca, 0, 9, 1, 1, b.conv1_pk, 64, 0, 0, 1};
+            f1.seg[0] = FzDesc::Seg{xa, b.ca, 0, 9, 1, cs > 0 ? 1 : 0, b.conv1_pk, 64, 0, 0, 1};
             f1.nseg = 1;
             if (b.cb > 0) f1.seg[f1.nseg++] = FzDesc::Seg{xb, b.cb, b.ca, 9, 1, 0, b.conv1_pk, 64, rows_a, 0, 1};
         } else {
-            f1.seg[0] = FzDesc::Seg{xa, b.ca, 0, 9, 1, 1, b.conv1_w, 9 * cin, 0, cin, 0};
+            f1.seg[0] = FzDesc::Seg{xa, b.ca, 0, 9, 1, cs > 0 ? 1 : 0, b.conv1_w, 9 * cin, 0, cin, 0};
             f1.nseg = 1;
             if (b.cb > 0) f1.seg[f1.nseg++] = FzDesc::Seg{xb, b.cb, b.ca, 9, 1, 0, b.conv1_w, 9 * cin, b.ca, cin, 0};
         }

@@ -143,32 +143,37 @@ template <typename T, int D>
 __global__ void __launch_bounds__(256) qkv_pack_kernel(const T *__restrict__ qkv, T *__restrict__ qp,
                                                        T *__restrict__ kp, T *__restrict__ vp, int N, int C) {
     griddep_wait();
-    __shared__ __align__(16) T sv[128 * D];
+    constexpr int DCH = D < 64 ? D : 64;   // channels per pass (V^T staged through shared memory)
+    __shared__ __align__(16) T sv[128 * DCH];
     const int jt = blockIdx.x, h = blockIdx.y, t = blockIdx.z;
     const int heads = gridDim.y, ntiles = gridDim.x;
     const size_t tile = (((size_t)t * heads + h) * ntiles + jt) * (128 * D);
-    constexpr int DC = D / 8;
-    for (int i = threadIdx.x; i < 128 * DC; i += 256) {
-        const int r = i / DC, kc = i - r * DC;
-        const int n = jt * 128 + r;
-        uint4 q = make_uint4(0, 0, 0, 0), k = q, v = q;
-        if (n < N) {
-            const T *src = qkv + ((size_t)t * N + n) * 3 * C + h * D + kc * 8;
-            q = __ldg(reinterpret_cast<const uint4 *>(src));
-            k = __ldg(reinterpret_cast<const uint4 *>(src + C));
-            v = __ldg(reinterpret_cast<const uint4 *>(src + 2 * C));
+    constexpr int DC = DCH / 8;
+#pragma unroll 1
+    for (int d0 = 0; d0 < D; d0 += DCH) {
+        for (int i = threadIdx.x; i < 128 * DC; i += 256) {
+            const int r = i / DC, kl = i - r * DC, kc = d0 / 8 + kl;
+            const int n = jt * 128 + r;
+            uint4 q = make_uint4(0, 0, 0, 0), k = q, v = q;
+            if (n < N) {
+                const T *src = qkv + ((size_t)t * N + n) * 3 * C + h * D + kc * 8;
+                q = __ldg(reinterpret_cast<const uint4 *>(src));
+                k = __ldg(reinterpret_cast<const uint4 *>(src + C));
+                v = __ldg(reinterpret_cast<const uint4 *>(src + 2 * C));
+            }
+            *reinterpret_cast<uint4 *>(qp + tile + kc * 1024 + r * 8) = q;
+            *reinterpret_cast<uint4 *>(kp + tile + kc * 1024 + r * 8) = k;
+            *reinterpret_cast<uint4 *>(sv + r * DCH + kl * 8) = v;
         }
-        *reinterpret_cast<uint4 *>(qp + tile + kc * 1024 + r * 8) = q;
-        *reinterpret_cast<uint4 *>(kp + tile + kc * 1024 + r * 8) = k;
-        *reinterpret_cast<uint4 *>(sv + r * D + kc * 8) = v;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 16 * D; i += 256) {   // (key chunk, d): 8 consecutive keys of column d
-        const int kc = i / D, d = i - kc * D;
-        Vec8<T> u;
+        __syncthreads();
+        for (int i = threadIdx.x; i < 16 * DCH; i += 256) {   // (key chunk, d): 8 consecutive keys of column d
+            const int kc = i / DCH, dl = i - kc * DCH;
+            Vec8<T> u;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) u.v[e] = sv[(kc * 8 + e) * D + d];
-        *reinterpret_cast<Vec8<T> *>(vp + tile + kc * D * 8 + d * 8) = u;
+            for (int e = 0; e < 8; ++e) u.v[e] = sv[(kc * 8 + e) * DCH + dl];
+            *reinterpret_cast<Vec8<T> *>(vp + tile + kc * D * 8 + (d0 + dl) * 8) = u;
+        }
+        __syncthreads();
     }
     griddep_launch();
 }
@@ -232,19 +237,25 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const float *__restrict_
 //   Q/K [rows][D]:  core (r8, kc) at kc*2048 + r8*128   (LBO 2048, SBO 128)
 //   V^T [D][keys]:  core (d8, kc) at kc*D*16 + d8*128   (LBO D*16, SBO 128)
 
-constexpr int kAttnThreads = 576;   // 16 softmax warps + MMA warp + TMA warp
-constexpr int kAttnStages = 4;
+// head_dim <= 64: two query tiles per CTA (TMEM S0 S1 | O0 O1 | P0 P1), 4-stage K/V ring;
+// head_dim 256 (the VAE decoder's single-head mid attention, f2): one tile (S | P | O = 256
+// columns), K/V single-buffered (192 KB of operand tiles).
 template <int D>
 struct AttnSmem {
+    static constexpr int NT = D <= 64 ? 2 : 1;            // query tiles per CTA
+    static constexpr int STAGES = D <= 64 ? 4 : 1;
+    static constexpr int THREADS = (8 * NT + 2) * 32;     // 8 softmax warps per tile + MMA + TMA
     static constexpr int Q = 128 * D * 2;        // one query tile
     static constexpr int K = 128 * D * 2;        // one key tile
     static constexpr int V = D * 128 * 2;        // one transposed value tile
-    static constexpr int off_q = 0, off_k = 2 * Q, off_v = off_k + kAttnStages * K;
-    static constexpr int off_bar = off_v + kAttnStages * V;
-    // barriers: q_full, kv_full[3], kv_empty[3], s_full[2], s_free[2], p_full[2], o_full[2][2]
-    static constexpr int nbar = 1 + 2 * kAttnStages + 2 + 2 + 2 + 4;
-    static constexpr int off_red = off_bar + nbar * 8 + 16;     // [2 tiles][2 halves][128 rows] float exchange
-    static constexpr int bytes = off_red + 2 * 2 * 128 * 4 + 1024;   // + alignment slack
+    static constexpr int off_q = 0, off_k = NT * Q, off_v = off_k + STAGES * K;
+    static constexpr int off_bar = off_v + STAGES * V;
+    // barriers: q_full, kv_full[S], kv_empty[S], s_full[2], s_free[2], p_full[2], o_full[2][2]
+    static constexpr int nbar = 1 + 2 * STAGES + 2 + 2 + 2 + 4;
+    static constexpr int off_red = off_bar + nbar * 8 + 16;     // [NT tiles][2 halves][128 rows] float exchange
+    static constexpr int bytes = off_red + NT * 2 * 128 * 4 + 1024;   // + alignment slack
+    // TMEM columns (512 allocated)
+    static constexpr int tm_o = 256, tm_o_step = NT == 2 ? 64 : 0, tm_p = NT == 2 ? 384 : 128, tm_p_step = 64;
 };
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -284,7 +295,7 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 }
 
 template <typename T, int D, int NPOLY>
-__global__ void __launch_bounds__(kAttnThreads, 1)
+__global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
     attn_tc_kernel(const T *__restrict__ qp, const T *__restrict__ kp, const T *__restrict__ vp, T *__restrict__ out,
                    int N, int C, float scale_log2, uint32_t idesc_s, uint32_t idesc_o, int dbg) {
     using L = AttnSmem<D>;
@@ -292,12 +303,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(smem);
     const uint32_t bar0 = sb + L::off_bar;
+    constexpr int kAttnStages = L::STAGES, NT = L::NT;
     const uint32_t q_full = bar0, kv_full = bar0 + 8, kv_empty = kv_full + 8 * kAttnStages;
     const uint32_t s_full = kv_empty + 8 * kAttnStages, s_free = s_full + 16, p_full = s_free + 16;
     const uint32_t o_full = p_full + 16;   // [t][b] at o_full + 8 * (2 t + b)
     uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + L::off_bar + L::nbar * 8);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int t = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * 256;
+    const int t = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * 128 * NT;
+    const int w_mma = 8 * NT, w_tma = 8 * NT + 1;
     const int nkt = (N + 127) / 128;
     if (tid == 0) {
         uint64_t *b = reinterpret_cast<uint64_t *>(smem + L::off_bar);
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         for (int i = 0; i < 4; ++i) mbar_init(&b[sf + 6 + i], 1);   // o_full
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 16) tmem_alloc<1>(smem_u32(tslot), 512);
+    if (warp == w_mma) tmem_alloc<1>(smem_u32(tslot), 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -323,13 +336,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     // The MMA warp and the softmax groups are one latency chain (S -> softmax -> P -> PV, S):
     // they poll without a suspend hint (a suspended try_wait wakes late, measured ~1.6 us per
     // iteration of pure barrier round trips); the TMA producer runs ahead and may sleep.
-    if (warp == 17) {
+    if (warp == w_tma) {
         // ===================== TMA producer =====================
         if (elect_one()) {
             const int ntiles = (N + 127) / 128, heads = gridDim.y;
             const size_t base = ((size_t)t * heads + h) * ntiles * (128 * D);   // this (frame, head)
-            const int qt = blockIdx.x * 2;
-            const uint32_t nq = qt + 1 < ntiles ? 2 : 1;
+            const int qt = blockIdx.x * NT;
+            const uint32_t nq = (NT == 2 && qt + 1 < ntiles) ? 2 : 1;
             mbar_arrive_expect_tx_addr(q_full, nq * L::Q);
             bulk_load(sb + L::off_q, qp + base + (size_t)qt * 128 * D, L::Q, q_full);
             if (nq == 2) bulk_load(sb + L::off_q + L::Q, qp + base + (size_t)(qt + 1) * 128 * D, L::Q, q_full);
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 bulk_load(sb + L::off_v + st * L::V, vp + base + (size_t)j * 128 * D, L::V, kv_full + 8 * st);
             }
         }
-    } else if (warp == 16) {
+    } else if (warp == w_mma) {
         // ===================== MMA issuer =====================
         if (elect_one()) {
             mbar_wait_spin_addr(q_full, 0);
@@ -365,31 +378,42 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
                 for (int ks = 0; ks < 8; ++ks) {
                     if (dbg & 2) break;
                     const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(va + ks * 2 * D * 16, D * 16);
-                    tc_mma_ts(tmem + 256 + tt * 64, tmem + 384 + tt * 64 + ks * 8, bd, idesc_o,
+                    tc_mma_ts(tmem + L::tm_o + tt * L::tm_o_step, tmem + L::tm_p + tt * L::tm_p_step + ks * 8, bd, idesc_o,
                               (j > 0 || ks > 0) ? 1u : 0u);
                 }
             };
             mbar_wait_spin_addr(kv_full, 0);
             tc_fence_after();
-            issue_s(0, 0);
-            issue_s(1, 0);
+            for (int tt = 0; tt < NT; ++tt) issue_s(tt, 0);
             for (int j = 0; j < nkt; ++j) {
                 const int stn = (j + 1) % kAttnStages;
                 const bool more = j + 1 < nkt;
-                if (more) {
-                    mbar_wait_spin_addr(kv_full + 8 * stn, ((j + 1) / kAttnStages) & 1);
+                if constexpr (kAttnStages == 1) {
+                    // single K/V buffer: PV(j) must retire before K/V(j+1) can land
+                    mbar_wait_spin_addr(p_full, j & 1);
                     tc_fence_after();
+                    issue_pv(0, j);
+                    tc_commit_addr(kv_empty);
+                    if (more) {
+                        mbar_wait_spin_addr(kv_full, (j + 1) & 1);
+                        tc_fence_after();
+                        issue_s(0, j + 1);
+                    }
+                } else {
+                    if (more) {
+                        mbar_wait_spin_addr(kv_full + 8 * stn, ((j + 1) / kAttnStages) & 1);
+                        tc_fence_after();
+                    }
+                    for (int tt = 0; tt < NT; ++tt) {
+                        mbar_wait_spin_addr(p_full + 8 * tt, j & 1);   // P_t(j) written, S_t(j) released
+                        tc_fence_after();
+                        issue_pv(tt, j);
+                        if (more) issue_s(tt, j + 1);
+                    }
+                    tc_commit_addr(kv_empty + 8 * (j % kAttnStages));
                 }
-                for (int tt = 0; tt < 2; ++tt) {
-                    mbar_wait_spin_addr(p_full + 8 * tt, j & 1);   // P_t(j) written, S_t(j) released
-                    tc_fence_after();
-                    issue_pv(tt, j);
-                    if (more) issue_s(tt, j + 1);
-                }
-                tc_commit_addr(kv_empty + 8 * (j % kAttnStages));
             }
-            tc_commit_addr(o_full);       // O_0 and O_1 final
-            tc_commit_addr(o_full + 8);
+            for (int tt = 0; tt < NT; ++tt) tc_commit_addr(o_full + 8 * tt);   // O_t final
         }
     } else {
         // ===================== softmax groups =====================
@@ -397,14 +421,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         // split over two threads (64 keys each) in two warps of the same lane quarter, four softmax
         // warps per SM sub-partition; the row max / sum halves meet through shared memory behind a
         // 64-thread named barrier per warp pair
-        const int tt = (warp >> 2) & 1, q4 = warp & 3, half = warp >> 3;
+        const int tt = (warp >> 2) % NT, q4 = warp & 3, half = warp / (4 * NT);
         const int row = q4 * 32 + lane;
         const uint32_t bar_id = 1 + tt * 4 + q4;
         float *red = reinterpret_cast<float *>(smem + L::off_red) + tt * 256;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
         const uint32_t tS = tmem + lane_off + tt * 128 + half * 64;
-        const uint32_t tO = tmem + lane_off + 256 + tt * 64;
-        const uint32_t tP = tmem + lane_off + 384 + tt * 64 + half * 32;
+        const uint32_t tO = tmem + lane_off + L::tm_o + tt * L::tm_o_step;
+        const uint32_t tP = tmem + lane_off + L::tm_p + tt * L::tm_p_step + half * 32;
         auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nkt; ++j) {
@@ -513,7 +537,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     griddep_launch();
     tc_fence_before();
     __syncthreads();
-    if (warp == 16) tmem_dealloc<1>(tmem, 512);
+    if (warp == w_mma) tmem_dealloc<1>(tmem, 512);
 }
 
 // ----------------------------------------------------------------- host side
@@ -555,7 +579,7 @@ static dvc_status attn_tc_launch(const void *qkv, void *ws, void *out, int T_, i
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes));
     const int bf = std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-    DVC_CUDA(launch_pdl(kfn, dim3((N + 255) / 256, C / D, T_), dim3(kAttnThreads), (size_t)L::bytes,
+    DVC_CUDA(launch_pdl(kfn, dim3((N + 128 * L::NT - 1) / (128 * L::NT), C / D, T_), dim3(L::THREADS), (size_t)L::bytes,
                         stream, 1, (const T *)qp, (const T *)kp, (const T *)vp, reinterpret_cast<T *>(out), N, C,
                         scale_log2, make_idesc(bf, 128, 128), make_idesc(bf, 128, D), attn_debug()));
     ++g_launches;
@@ -575,15 +599,16 @@ static dvc_status attention_t(const void *qkv, int T_, int N, int C, int D, void
         case 16: return attn_tc_launch<T, 16>(qkv, ws, out, T_, N, C, s);
         case 32: return attn_tc_launch<T, 32>(qkv, ws, out, T_, N, C, s);
         case 48: return attn_tc_launch<T, 48>(qkv, ws, out, T_, N, C, s);
-        default: return attn_tc_launch<T, 64>(qkv, ws, out, T_, N, C, s);
+        case 64: return attn_tc_launch<T, 64>(qkv, ws, out, T_, N, C, s);
+        default: return attn_tc_launch<T, 256>(qkv, ws, out, T_, N, C, s);
     }
 }
 
 dvc_status attention_run(const void *qkv, int T_, int N, int C, int D, dvc_dtype dt, void *vt, void *out,
                          cudaStream_t s) {
     DVC_CHECK_ARG(T_ >= 1 && T_ < 65536 && N >= 1 && C >= 1, DVC_ERR_ARG, "attention: empty shape");
-    DVC_CHECK_ARG(D == 16 || D == 32 || D == 48 || D == 64, DVC_ERR_UNSUPPORTED, "attention: head_dim %d not in {16,32,48,64}",
-                  D);
+    DVC_CHECK_ARG(D == 16 || D == 32 || D == 48 || D == 64 || D == 256, DVC_ERR_UNSUPPORTED,
+                  "attention: head_dim %d not in {16,32,48,64,256}", D);
     DVC_CHECK_ARG(C % D == 0, DVC_ERR_DIVISIBILITY, "attention: head_dim %d must divide C=%d", D, C);
     if (dt == DVC_F32) {
         const float scale = 1.f / sqrtf((float)D);
@@ -594,7 +619,8 @@ dvc_status attention_run(const void *qkv, int T_, int N, int C, int D, dvc_dtype
             case 16: attn_simt_kernel<16><<<g, 128, 0, s>>>(q, o, N, C, scale); break;
             case 32: attn_simt_kernel<32><<<g, 128, 0, s>>>(q, o, N, C, scale); break;
             case 48: attn_simt_kernel<48><<<g, 128, 0, s>>>(q, o, N, C, scale); break;
-            default: attn_simt_kernel<64><<<g, 128, 0, s>>>(q, o, N, C, scale); break;
+            case 64: attn_simt_kernel<64><<<g, 128, 0, s>>>(q, o, N, C, scale); break;
+            default: attn_simt_kernel<256><<<g, 128, 0, s>>>(q, o, N, C, scale); break;
         }
         ++g_launches;
         return check_launch("attn_simt_kernel");
@@ -662,6 +688,11 @@ static dvc_status ew(int which, dvc_dtype dt, const void *a, const void *b, cons
     }
     prof_end_aux(slot, s, which == 0 ? "tf_gn" : which == 1 ? "tf_ln" : "tf_geglu");
     return st;
+}
+
+dvc_status gn_affine_run(const void *x, const void *coef, int T, int HW, int C, dvc_dtype dt, void *y,
+                         cudaStream_t s) {
+    return ew(0, dt, x, coef, nullptr, y, (long)T * HW, C, 0.f, s, HW);
 }
 
 dvc_status transformer_launch(const TF &b, const void *x, int T, int H, int W, void *y, void *ws, cudaStream_t s,

@@ -23,4 +23,8 @@ size_t attn_ws_bytes(int T, int N, int C, dvc_dtype dt);
 dvc_status attention_run(const void *qkv, int T, int N, int C, int D, dvc_dtype dt, void *vt, void *out,
                          cudaStream_t s);
 
+// y = x * coef.x + coef.y per (frame, channel) (GroupNorm apply without SiLU)
+dvc_status gn_affine_run(const void *x, const void *coef, int T, int HW, int C, dvc_dtype dt, void *y,
+                         cudaStream_t s);
+
 }  // namespace dvc

@@ -313,6 +313,53 @@ class Pipeline:
             pass
 
 
+class VAE:
+    """Handle of the device-resident pruned VAE decoder (f2, dvc_vae_create)."""
+
+    def __init__(self, host_blob: torch.Tensor, width=(64, 128, 256, 256), c_lat=256, out_ch=3, groups=32,
+                 eps=1e-6, mid_attn=True, dtype=torch.bfloat16, h=90, w=160, max_T=8):
+        self.cfg = _lib.dvc_vae_config((ctypes.c_int * 4)(*width), c_lat, out_ch, groups, eps, int(mid_attn),
+                                       dtype_code(dtype), h, w, max_T)
+        blob = host_blob.contiguous()
+        self.dtype, self.out_ch = dtype, out_ch
+        self.handle = ctypes.c_void_p()
+        check(lib().dvc_vae_create(ctypes.byref(self.cfg), ctypes.c_void_p(blob.data_ptr()),
+                                   blob.numel() * blob.element_size(), ctypes.byref(self.handle)))
+
+    def weight_count(self) -> int:
+        n = ctypes.c_size_t()
+        check(lib().dvc_vae_weight_count(ctypes.byref(self.cfg), ctypes.byref(n)))
+        return n.value
+
+    def workspace_size(self, T: int) -> int:
+        n = ctypes.c_size_t()
+        check(lib().dvc_vae_workspace_size(self.handle, T, ctypes.byref(n)))
+        return n.value
+
+    def close(self):
+        if self.handle:
+            lib().dvc_vae_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dvc_vae_decode(vae: VAE, lat, out=None, workspace=None, stream=None):
+    """Lhat [T,h,w,c_lat] -> frames [T,8h,8w,out_ch] (NHWC)."""
+    T, h, w, _ = lat.shape
+    if out is None:
+        out = torch.empty((T, 8 * h, 8 * w, vae.out_ch), dtype=lat.dtype, device=lat.device)
+    if workspace is None:
+        workspace = _ws(vae.workspace_size(T), lat.device)
+    check(lib().dvc_vae_decode(vae.handle, _ptr(lat), T, _ptr(out), _ptr(workspace),
+                               workspace.numel() * workspace.element_size(), _stream(stream)))
+    return out
+
+
 class StreamingDecoder:
     """f4 online streaming: one frame per step (latency N-1 = 0), the 22 block carries in a ring of
     two buffers, every step one CUDA-graph replay of dvc_unet_decode_gop(T=1).

@@ -1,0 +1,82 @@
+"""GPU parity of f2, the pruned VAE decoder (dvc_vae_decode), against the fp64 oracle
+(oracle.vae_decode, readings R29-R31), plus the single-head head_dim-256 attention it uses and
+the shift-free ResBlock (shift_p = 0)."""
+import numpy as np
+import pytest
+import torch
+
+import synthgen
+from tests.gpu_helpers import MODE, TOL, dev, host64, rb_device, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+VSMALL = (16, 32, 48, 48)
+
+
+@pytest.fixture(scope="module")
+def dvc():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2601_20564_b200 as m
+    m.device_check(0)
+    return m
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32])
+@pytest.mark.parametrize("T,N", [(2, 300), (1, 129)])
+def test_attention_head_dim_256(dvc, orc, dtype, T, N):
+    C = 256
+    qkv, q64 = dev(synthgen.normal((T, N, 3 * C), 21, scale=0.5), dtype)
+    out = dvc.dvc_attention_forward(qkv, 256)
+    ref = orc.rnd(orc.attention(q64[..., :C], q64[..., C:2 * C], q64[..., 2 * C:], 256), MODE[dtype])
+    assert rel_l2(host64(out), ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("cin,cout,H,W", [(48, 48, 12, 20), (64, 32, 40, 48)])
+def test_resblock_without_shift(dvc, orc, dtype, cin, cout, H, W):
+    T = 2
+    w = synthgen.resblock_weights(cin, cout)
+    wd, wh = rb_device(w, dtype)
+    p = dvc.ResBlockParams(wd, cin, 0, 8, 0)          # shift_p = 0: no temporal shift
+    x, x64 = dev(synthgen.normal((T, H, W, cin), 3), dtype)
+    y = dvc.dvc_resblock_tsm_forward(p, x)
+    ref = orc.vae_resblock(x64, wh, 8, 1e-5, MODE[dtype])
+    assert rel_l2(host64(y), ref) <= TOL[dtype]
+
+
+def _vae(dvc, dtype, h, w, T, mid_attn=True, attn_scale=2.0):
+    named = synthgen.vae_weights(VSMALL, 32, mid_attn=mid_attn, attn_scale=attn_scale)
+    v = dvc.VAE(dvc.pack_weights(named, dtype), VSMALL, 32, 3, 8, 1e-6, mid_attn, dtype, h, w, T)
+    assert v.weight_count() == sum(a.size for _, a in named)
+    exact = [(n, torch.from_numpy(a).to(dtype).double().numpy()) for n, a in named]
+    return v, exact
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32])
+@pytest.mark.parametrize("h,w,T,mid", [(3, 4, 2, True), (6, 8, 2, True), (5, 7, 1, False)])
+def test_vae_decoder_parity(dvc, orc, dtype, h, w, T, mid):
+    v, wts = _vae(dvc, dtype, h, w, T, mid)
+    lat, lat64 = dev(synthgen.normal((T, h, w, 32), 1), dtype)
+    out = dvc.dvc_vae_decode(v, lat)
+    assert out.shape == (T, 8 * h, 8 * w, 3)
+    ref = orc.vae_decode(lat64, wts, VSMALL, G=8, eps=1e-6, mid_attn=mid, mode=MODE[dtype])
+    err = rel_l2(host64(out), ref)
+    tol = TOL[dtype]
+    if dtype == torch.bfloat16:
+        # R31: bf16 storage alone moves the decoder output by 1.4e-2..2.3e-2 (emulated oracle vs pure
+        # fp64), above the 1e-2 ResBlock gate, so end to end bf16 is gated at twice that intrinsic
+        # error; its ResBlocks are gated at 1e-2 one by one (test_resblock_without_shift)
+        pure = orc.vae_decode(lat64, wts, VSMALL, G=8, eps=1e-6, mid_attn=mid, mode=None)
+        tol = max(tol, 2 * rel_l2(ref, pure))
+    assert err <= tol, (err, tol)
+    assert torch.equal(out, dvc.dvc_vae_decode(v, lat))              # deterministic
+
+
+def test_vae_frames_independent(dvc):
+    h, w = 6, 8
+    v, _ = _vae(dvc, torch.bfloat16, h, w, 3)
+    lat, _ = dev(synthgen.normal((3, h, w, 32), 1), torch.bfloat16)
+    full = dvc.dvc_vae_decode(v, lat)
+    for t in range(3):
+        assert torch.equal(dvc.dvc_vae_decode(v, lat[t:t + 1].contiguous())[0], full[t])
