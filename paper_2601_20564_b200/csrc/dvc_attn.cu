@@ -271,7 +271,7 @@ __device__ __forceinline__ float ex2f(float x) {
 // to the exponent field.  Used for part of every 8-score group so the MUFU ex2 unit (the bound of
 // a head_dim-48 softmax: 192 MMA FLOP per exponential) shares the work with the FMA pipe.
 #ifndef DVC_ATTN_POLY
-#define DVC_ATTN_POLY 3   // scores per 8 computed by ex2_poly
+#define DVC_ATTN_POLY 2   // scores per 8 computed by ex2_poly (even: packed pairs)
 #endif
 __device__ __forceinline__ float ex2_poly(float x) {
     x = fmaxf(x, -126.f);
@@ -279,6 +279,20 @@ __device__ __forceinline__ float ex2_poly(float x) {
     const float f = x - (r - 12582912.f);
     const float p = fmaf(fmaf(fmaf(0.055172063f, f, 0.24261240f), f, 0.69326103f), f, 0.99992794f);
     return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
+}
+// two lanes of ex2_poly with packed fp32x2 adds / FMAs
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -126.f);
+    x.y = fmaxf(x.y, -126.f);
+    const float2 mg = make_float2(12582912.f, 12582912.f), nmg = make_float2(-12582912.f, -12582912.f);
+    const float2 r = __fadd2_rn(x, mg);
+    const float2 j = __fadd2_rn(r, nmg);
+    const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
+    float2 p = __ffma2_rn(make_float2(0.055172063f, 0.055172063f), f, make_float2(0.24261240f, 0.24261240f));
+    p = __ffma2_rn(p, f, make_float2(0.69326103f, 0.69326103f));
+    p = __ffma2_rn(p, f, make_float2(0.99992794f, 0.99992794f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t addr) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
@@ -484,26 +498,28 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
                     if (move) m = mt;
                 }
             }
-            float rsp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            // packed fp32x2 arithmetic (FFMA2 / FADD2): two scores per instruction
+            float2 rsp[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+            const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
 #pragma unroll
             for (int c = 0; c < 2; ++c) {   // 32 keys -> 16 packed columns of P_t in TMEM
                 uint32_t pk[16];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    float p[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const float x = fmaf(__uint_as_float(sr[c * 32 + q * 8 + i]), scale_log2, -m);
-                        p[i] = i < NPOLY ? ex2_poly(x) : ex2f(x);   // padding: x = -inf -> ~0
-                        rsp[i] += p[i];
+                    for (int i = 0; i < 4; ++i) {
+                        const int e = c * 32 + q * 8 + 2 * i;
+                        const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])),
+                                                    sc2, nm2);
+                        const float2 p = 2 * i < NPOLY ? ex2_poly2(x) : make_float2(ex2f(x.x), ex2f(x.y));
+                        rsp[i] = __fadd2_rn(rsp[i], p);   // padding: x = -inf -> ~0
+                        pk[q * 4 + i] = pack2<T>(p.x, p.y);
                     }
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) pk[q * 4 + i] = pack2<T>(p[2 * i], p[2 * i + 1]);
                 }
                 tmem_st16(tP + c * 16, pk);
             }
             tmem_wait_st();
-            l += ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
+            l += ((rsp[0].x + rsp[1].x) + (rsp[2].x + rsp[3].x)) + ((rsp[0].y + rsp[1].y) + (rsp[2].y + rsp[3].y));
             tc_fence_before();     // S reads, P stores, O rescale ordered before the release
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full + 8 * tt);
@@ -567,13 +583,13 @@ static dvc_status attn_tc_launch(const void *qkv, void *ws, void *out, int T_, i
                         reinterpret_cast<const T *>(qkv), qp, kp, vp, N, C));
     ++g_launches;
     ProfSlot slot = prof_begin(stream);
-    static int npoly = -1;   // scores per 8 on the FMA pipe (DVC_ATTN_POLY: 0, 3 (default), 8)
+    static int npoly = -1;   // scores per 8 on the FMA pipe (DVC_ATTN_POLY: 0, 2 (default), 4)
     if (npoly < 0) {
         const char *e = getenv("DVC_ATTN_POLY");
         npoly = e ? atoi(e) : DVC_ATTN_POLY;
     }
-    auto kfn = npoly == 0 ? attn_tc_kernel<T, D, 0> : npoly == 8 ? attn_tc_kernel<T, D, 8>
-             : npoly == 5 ? attn_tc_kernel<T, D, 5> : attn_tc_kernel<T, D, 3>;
+    auto kfn = npoly == 0 ? attn_tc_kernel<T, D, 0> : npoly == 4 ? attn_tc_kernel<T, D, 4>
+             : attn_tc_kernel<T, D, 2>;
     const void *kern = reinterpret_cast<const void *>(kfn);
     if (!smem_attr_ok(kern, L::bytes))
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes));
