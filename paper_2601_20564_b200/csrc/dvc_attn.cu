@@ -178,6 +178,22 @@ __global__ void __launch_bounds__(256) qkv_pack_kernel(const T *__restrict__ qkv
     griddep_launch();
 }
 
+// FF1 weight / bias rows [8C] -> blocks of 32 = 16 value rows (j) then the 16 gate rows (4C + j),
+// the order the GEGLU epilogue of the TMA engine consumes (one row of `cols` elements each)
+template <typename T>
+__global__ void __launch_bounds__(256) geglu_interleave_kernel(const T *__restrict__ src, T *__restrict__ dst, int C4,
+                                                               int cols) {
+    griddep_wait();
+    const long total = 2L * C4 * cols;
+    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cols), c = (int)(i - (long)r * cols);
+        const int blk = r >> 5, w = r & 31;
+        const int src_row = w < 16 ? blk * 16 + w : C4 + blk * 16 + (w - 16);
+        dst[i] = src[(size_t)src_row * cols + c];
+    }
+    griddep_launch();
+}
+
 // ----------------------------------------------------------------- attention, fp32 validation mode
 // One thread per (frame, head, query): online softmax over all keys (DVC_F32, R16's 1e-5 gate).
 template <int D>
@@ -652,7 +668,8 @@ size_t transformer_ws_bytes(int C, int T, int H, int W, dvc_dtype dt) {
     const size_t px = (size_t)T * H * W, es = dt_size(dt);
     // A, B, E: [px][C]; big: [px][8C] (qkv, then ff1); F: [px][4C]; Vt; coef; box statistics of X
     return 3 * align256(px * C * es) + align256(px * 8 * C * es) + align256(px * 4 * C * es) +
-           attn_ws_bytes(T, H * W, C, dt) + align256((size_t)T * C * 8) + box_stats_bytes(T, H, W, C);
+           attn_ws_bytes(T, H * W, C, dt) + align256((size_t)T * C * 8) + box_stats_bytes(T, H, W, C) +
+           align256((size_t)8 * C * C * es) + align256((size_t)8 * C * es);
 }
 
 dvc_status transformer_validate(const TF &b, int T, int H, int W) {
@@ -711,6 +728,25 @@ dvc_status gn_affine_run(const void *x, const void *coef, int T, int HW, int C, 
     return ew(0, dt, x, coef, nullptr, y, (long)T * HW, C, 0.f, s, HW);
 }
 
+static dvc_status interleave_ff1(const TF &b, void *wi, void *bi, cudaStream_t s) {
+    const int C4 = 4 * b.c;
+    auto one = [&](auto *tag, const void *src, void *dst, int cols) -> dvc_status {
+        using E = std::remove_pointer_t<decltype(tag)>;
+        const int blocks = (int)std::min<long>((2L * C4 * cols + 255) / 256, 148L * 8);
+        DVC_CUDA(launch_pdl(geglu_interleave_kernel<E>, dim3(blocks), dim3(256), 0, s, 1,
+                            reinterpret_cast<const E *>(src), reinterpret_cast<E *>(dst), C4, cols));
+        ++g_launches;
+        return DVC_OK;
+    };
+    dvc_status st;
+    if (b.dt == DVC_BF16) {
+        if ((st = one((__nv_bfloat16 *)nullptr, b.ff1_w, wi, b.c)) != DVC_OK) return st;
+        return one((__nv_bfloat16 *)nullptr, b.ff1_b, bi, 1);
+    }
+    if ((st = one((__half *)nullptr, b.ff1_w, wi, b.c)) != DVC_OK) return st;
+    return one((__half *)nullptr, b.ff1_b, bi, 1);
+}
+
 dvc_status transformer_launch(const TF &b, const void *x, int T, int H, int W, void *y, void *ws, cudaStream_t s,
                               const void *stats_x, void *stats_y) {
     const int C = b.c;
@@ -726,6 +762,7 @@ dvc_status transformer_launch(const TF &b, const void *x, int T, int H, int W, v
     void *vt = take(attn_ws_bytes(T, H * W, C, b.dt));
     float2 *coef = reinterpret_cast<float2 *>(take((size_t)T * C * 8));
     void *bst = take(box_stats_bytes(T, H, W, C));
+    void *ff1_wi = take((size_t)8 * C * C * es), *ff1_bi = take((size_t)8 * C * es);
     dvc_status st;
     // a = GN(X): coefficients from box statistics of X (the producer's, or computed here)
     if (!stats_x) {
@@ -757,8 +794,19 @@ dvc_status transformer_launch(const TF &b, const void *x, int T, int H, int W, v
     if ((st = attention_run(big, T, H * W, C, b.head_dim, b.dt, vt, A, s)) != DVC_OK) return st;          // o = A
     if ((st = lin(A, C, b.out_w, b.out_b, C, B, E, nullptr)) != DVC_OK) return st;                        // h1 = E
     if ((st = ew(1, b.dt, E, b.ln2_w, b.ln2_b, A, (long)px, C, b.eps_ln, s)) != DVC_OK) return st;        // l2 = A
-    if ((st = lin(A, C, b.ff1_w, b.ff1_b, 8 * C, nullptr, big, nullptr)) != DVC_OK) return st;            // f
-    if ((st = ew(2, b.dt, big, nullptr, nullptr, Fb, (long)px, 4 * C, 0.f, s)) != DVC_OK) return st;      // g
+    if (b.dt != DVC_F32 && g_ws_cg != 0) {
+        // g = f[:4C] * gelu(f[4C:]) in FF1's epilogue (rows interleaved in 16 + 16 blocks): the 8C-wide
+        // FF1 output never reaches HBM
+        if ((st = interleave_ff1(b, ff1_wi, ff1_bi, s)) != DVC_OK) return st;
+        ConvDesc d{};
+        d.seg[0] = ConvSeg{A, C, SEG_SAME, H, W, 1, ff1_wi, C, 0, C};
+        d.nseg = 1, d.T = T, d.ho = H, d.wo = W, d.cout = 8 * C, d.bias0 = ff1_bi, d.out = Fb, d.dt = b.dt;
+        d.geglu = 1;
+        if ((st = conv_run(d, s)) != DVC_OK) return st;                                                    // g
+    } else {
+        if ((st = lin(A, C, b.ff1_w, b.ff1_b, 8 * C, nullptr, big, nullptr)) != DVC_OK) return st;        // f
+        if ((st = ew(2, b.dt, big, nullptr, nullptr, Fb, (long)px, 4 * C, 0.f, s)) != DVC_OK) return st;  // g
+    }
     if ((st = lin(Fb, 4 * C, b.ff2_w, b.ff2_b, C, E, B, nullptr)) != DVC_OK) return st;                   // h2 = B
     return lin(B, C, b.proj_out_w, b.proj_out_b, C, x, y, stats_y);                                       // Y
 }

@@ -47,6 +47,10 @@ struct ConvDesc {
     void *out;                   // [M][cout]
     void *stats_out;             // per-channel box statistics of out (dvc_boxstats.cuh) or null
     dvc_dtype dt;
+    // GEGLU epilogue (f1 feed-forward, TMA engine only): the weight rows come in blocks of 32 =
+    // 16 "value" rows then the matching 16 "gate" rows; out is [M][cout/2] with
+    // out = value * gelu(gate) (exact erf GELU); no residual, no statistics
+    int geglu = 0;
     long M() const { return (long)T * ho * wo; }
 };
 

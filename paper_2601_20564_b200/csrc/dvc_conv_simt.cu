@@ -168,6 +168,7 @@ double conv_flops(const ConvDesc &d) {
 dvc_status conv_run(const ConvDesc &d, cudaStream_t stream) {
     ProfSlot slot = prof_begin(stream);
     const bool ws = d.dt != DVC_F32 && conv_ws_applicable(d);
+    DVC_CHECK_ARG(!d.geglu || ws, DVC_ERR_UNSUPPORTED, "GEGLU epilogue needs the TMA conv engine");
     dvc_status st = d.dt == DVC_F32 ? conv_simt_run(d, stream) : ws ? conv_ws_run(d, stream) : conv_tc_run(d, stream);
     prof_end(slot, stream, conv_flops(d), d.dt == DVC_F32 ? "simt" : ws ? "ws" : "tc", d);
     if (st == DVC_OK && d.stats_out != nullptr && !ws)   // engines without the fused epilogue statistics

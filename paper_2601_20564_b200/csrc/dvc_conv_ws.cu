@@ -39,6 +39,7 @@ struct WsParams {
     void *out;
     uint32_t idesc;
     float *stats;   // per-channel box statistics of the output (dvc_boxstats.cuh), or null
+    int geglu;      // ConvDesc::geglu: 32-column batches = 16 values + 16 gates -> 16 outputs
 };
 
 constexpr int kWsThreads = 256;
@@ -256,6 +257,40 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
             // combine split over warps 0 / 1 (canonical order, dvc_boxstats.cuh)
             const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
             int par = 0;
+            if (p.geglu) {   // f1 GEGLU epilogue: out[m][n/2 + i] = (v_i + b) * gelu(g_i + b')
+                const int half = p.cout / 2;
+#pragma unroll 1
+                for (int cc = 0; cc < BN; cc += 32) {
+                    uint32_t va[16], vb[16];
+                    tmem_ld16_nowait(taddr + (uint32_t)cc, va);
+                    tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
+                    tmem_wait16(va);
+                    tmem_wait16(vb);
+                    if (m >= 0) {
+                        const int n = nt * BN + cc;
+                        float f[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            float a = __uint_as_float(va[i]), g = __uint_as_float(vb[i]);
+                            if (sb0) a += sb0[n + i], g += sb0[n + 16 + i];
+                            f[i] = a * (0.5f * g * (1.f + erff(g * 0.70710678118654752f)));
+                        }
+                        Vec8<T> lo, hi;
+                        round_store16<T>(f, lo, hi);
+                        *reinterpret_cast<Vec8<T> *>(out + m * half + n / 2) = lo;
+                        *reinterpret_cast<Vec8<T> *>(out + m * half + n / 2 + 8) = hi;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (CG == 1) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                                                            smem_u32(&tempty[buf]))
+                                                        : "memory");
+                    else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int cc = 0; cc < BN; cc += 32, par ^= 1) {
                 const bool two = cc + 16 < BN;   // warp-uniform
@@ -408,16 +443,19 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
     memset(&p, 0, sizeof(p));
     const int CG = g_ws_cg == 1 ? 1 : 2;
     int bn = d.cout;
-    if (bn > 256) {
+    if (bn > 256 || (d.geglu && bn % 32)) {
         bn = 0;
-        for (int c = 256; c >= 16; c -= 16)
-            if (d.cout % c == 0 && (c / CG) % 8 == 0) {
+        for (int c = 256; c >= 16; c -= 16)   // GEGLU: whole 32-column value/gate blocks per tile
+            if (d.cout % c == 0 && (c / CG) % 8 == 0 && (!d.geglu || c % 32 == 0)) {
                 bn = c;
                 break;
             }
     }
     DVC_CHECK_ARG(bn >= 16 && (bn / CG) % 8 == 0, DVC_ERR_UNSUPPORTED, "no N tile for cout=%d", d.cout);
+    DVC_CHECK_ARG(!d.geglu || (bn % 32 == 0 && d.residual == nullptr && d.stats_out == nullptr && d.bias1 == nullptr),
+                  DVC_ERR_UNSUPPORTED, "GEGLU epilogue: 32-column tiles, no residual / statistics / second bias");
     p.bn = bn;
+    p.geglu = d.geglu;
     p.nseg = d.nseg;
     p.T = d.T;
     p.H = d.ho;
