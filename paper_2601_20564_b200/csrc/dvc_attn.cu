@@ -728,7 +728,7 @@ dvc_status gn_affine_run(const void *x, const void *coef, int T, int HW, int C, 
     return ew(0, dt, x, coef, nullptr, y, (long)T * HW, C, 0.f, s, HW);
 }
 
-static dvc_status interleave_ff1(const TF &b, void *wi, void *bi, cudaStream_t s) {
+dvc_status interleave_ff1(const TF &b, void *wi, void *bi, cudaStream_t s) {
     const int C4 = 4 * b.c;
     auto one = [&](auto *tag, const void *src, void *dst, int cols) -> dvc_status {
         using E = std::remove_pointer_t<decltype(tag)>;
@@ -797,10 +797,14 @@ dvc_status transformer_launch(const TF &b, const void *x, int T, int H, int W, v
     if (b.dt != DVC_F32 && g_ws_cg != 0) {
         // g = f[:4C] * gelu(f[4C:]) in FF1's epilogue (rows interleaved in 16 + 16 blocks): the 8C-wide
         // FF1 output never reaches HBM
-        if ((st = interleave_ff1(b, ff1_wi, ff1_bi, s)) != DVC_OK) return st;
+        const void *wi = b.ff1_wi, *bi = b.ff1_bi;
+        if (!wi || !bi) {
+            if ((st = interleave_ff1(b, ff1_wi, ff1_bi, s)) != DVC_OK) return st;
+            wi = ff1_wi, bi = ff1_bi;
+        }
         ConvDesc d{};
-        d.seg[0] = ConvSeg{A, C, SEG_SAME, H, W, 1, ff1_wi, C, 0, C};
-        d.nseg = 1, d.T = T, d.ho = H, d.wo = W, d.cout = 8 * C, d.bias0 = ff1_bi, d.out = Fb, d.dt = b.dt;
+        d.seg[0] = ConvSeg{A, C, SEG_SAME, H, W, 1, wi, C, 0, C};
+        d.nseg = 1, d.T = T, d.ho = H, d.wo = W, d.cout = 8 * C, d.bias0 = bi, d.out = Fb, d.dt = b.dt;
         d.geglu = 1;
         if ((st = conv_run(d, s)) != DVC_OK) return st;                                                    // g
     } else {

@@ -11,7 +11,12 @@ struct TF {
     dvc_dtype dt;
     const void *gn_w, *gn_b, *proj_in_w, *proj_in_b, *ln1_w, *ln1_b, *qkv_w, *out_w, *out_b, *ln2_w, *ln2_b, *ff1_w,
         *ff1_b, *ff2_w, *ff2_b, *proj_out_w, *proj_out_b;
+    // FF1 rows pre-interleaved for the GEGLU epilogue (16 value + 16 gate rows per block), or null
+    // (then interleaved into the workspace on every call)
+    const void *ff1_wi = nullptr, *ff1_bi = nullptr;
 };
+// interleave b.ff1_w / b.ff1_b into wi [8C][C] / bi [8C] (the GEGLU epilogue's row order)
+dvc_status interleave_ff1(const TF &b, void *wi, void *bi, cudaStream_t s);
 
 size_t transformer_ws_bytes(int C, int T, int H, int W, dvc_dtype dt);
 dvc_status transformer_validate(const TF &b, int T, int H, int W);

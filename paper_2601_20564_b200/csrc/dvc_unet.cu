@@ -92,6 +92,7 @@ struct dvc_unet {
     dvc_unet_config cfg;
     void *dweights = nullptr;
     void *dpacked = nullptr;   // packed weight images (16-bit configs)
+    void *dff1i = nullptr;     // f1: FF1 weights / biases interleaved for the GEGLU epilogue
     size_t welems = 0;
     ConvW conv_in, ds[3], us[3], conv_out;
     const void *gno_w = nullptr, *gno_b = nullptr;
@@ -444,6 +445,33 @@ dvc_status dvc_unet_create(const dvc_unet_config *cfg, const void *host_weights,
         n->carry_total += (size_t)n->lh[l] * n->lw[l] * ((r.ca + r.cb) / r.P);
     }
     n->welems = elems;
+    if (cfg->head_dim > 0 && cfg->dt != DVC_F32 && g_ws_cg != 0) {
+        // f1: FF1 rows interleaved once for the GEGLU epilogue (16 value + 16 gate rows per block)
+        size_t tot = 0;
+        for (int i = 0; i < n->ntf; ++i) tot += align256((size_t)8 * n->tf[i].c * n->tf[i].c * es) +
+                                               align256((size_t)8 * n->tf[i].c * es);
+        if (cudaMalloc(&n->dff1i, tot) != cudaSuccess) {
+            cudaFree(n->dweights);
+            delete n;
+            set_error("cudaMalloc of %zu interleaved FF1 bytes failed", tot);
+            return DVC_ERR_CUDA;
+        }
+        uint8_t *q = reinterpret_cast<uint8_t *>(n->dff1i);
+        for (int i = 0; i < n->ntf && st == DVC_OK; ++i) {
+            TF &t = n->tf[i];
+            void *wi = q, *bi = q + align256((size_t)8 * t.c * t.c * es);
+            q += align256((size_t)8 * t.c * t.c * es) + align256((size_t)8 * t.c * es);
+            st = interleave_ff1(t, wi, bi, 0);
+            t.ff1_wi = wi, t.ff1_bi = bi;
+        }
+        if (st == DVC_OK && cudaDeviceSynchronize() != cudaSuccess) st = DVC_ERR_CUDA;
+        if (st != DVC_OK) {
+            cudaFree(n->dweights);
+            cudaFree(n->dff1i);
+            delete n;
+            return st;
+        }
+    }
     // Packed weight images (contiguous weight tiles) measured slower than the OHWI rows on B200
     // (r1 profiles), so they are opt-in: DVC_PACK_WEIGHTS=1.
     const char *pe = getenv("DVC_PACK_WEIGHTS");
@@ -464,6 +492,7 @@ dvc_status dvc_unet_destroy(dvc_unet *n) {
     if (!n) return DVC_OK;
     cudaFree(n->dweights);
     cudaFree(n->dpacked);
+    cudaFree(n->dff1i);
     delete n;
     return DVC_OK;
 }
