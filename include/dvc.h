@@ -300,6 +300,20 @@ DVC_API dvc_status dvc_vae_workspace_size(const dvc_vae *v, int T, size_t *bytes
 DVC_API dvc_status dvc_vae_decode(dvc_vae *v, const void *lat, int T, void *frames, void *workspace, size_t ws_bytes,
                                   void *stream);
 
+/* ------------------------------------------------------------------------
+ * f4 variant: fp8 (E4M3) convolutions on the tensor cores (kind::f8f6f4).
+ *   dvc_quantize_e4m3: q[i] = E4M3(RNE(x[i] / scale)), saturating to +-448 (fp32
+ *     quotient); x in dt (n % 8 == 0, 16-byte aligned), q bytes.
+ *   dvc_conv_fp8: y = (sx * sw) * conv(x8, w8) + bias with fp32 accumulation;
+ *     x8 [T,H,W,cin] E4M3 NHWC, w8 [cout][taps][cin] E4M3 (OHWI, taps 9 = 3x3 pad 1,
+ *     1 = 1x1), bias [cout] in out_dt or NULL, y [T,H,W,cout] in out_dt (bf16/fp16).
+ *     cin % 32 == 0, cout % 16 == 0.  A variant of the decode's convolutions
+ *     (SURVEY 8f rank 4), not used by dvc_unet_decode_gop.
+ * ------------------------------------------------------------------------ */
+DVC_API dvc_status dvc_quantize_e4m3(const void *x, dvc_dtype dt, size_t n, float scale, void *q, void *stream);
+DVC_API dvc_status dvc_conv_fp8(const void *x8, float sx, const void *w8, float sw, const void *bias, int T, int H,
+                                int W, int cin, int cout, int taps, dvc_dtype out_dt, void *y, void *stream);
+
 /* Multi-GPU halo communicator (NCCL, loaded at run time from the process's
  * libnccl.so.2).  id128: 128-byte ncclUniqueId, created on rank 0 and
  * broadcast by the caller (e.g. torch.distributed). */

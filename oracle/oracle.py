@@ -609,6 +609,37 @@ def vae_decode(L, weights, width=(64, 128, 256, 256), G: int = 32, eps: float = 
     return out
 
 
+# --------------------------------------------------------------------------
+# f4 variant: fp8 E4M3 quantisation (OCP FP8 E4M3 "fn": bias 7, 3 mantissa bits, no
+# infinities, max 448, subnormal quantum 2^-9) and the dequantised convolution
+# --------------------------------------------------------------------------
+def e4m3_round(v):
+    """Round-to-nearest-even to E4M3, saturating to +-448 (the GPU's SATFINITE conversion).
+    v: fp64 array of the values to round (callers pass the fp32 quotient x / scale)."""
+    v = _f64(v)
+    a = np.abs(v)
+    fin = np.isfinite(a)
+    af = np.where(fin, a, 0.0)
+    e = np.floor(np.log2(np.where(af > 0, af, 1.0)))
+    e = np.maximum(e, -6.0)                        # below 2^-6: subnormal quantum 2^-9
+    q = np.exp2(e - 3.0)
+    r = np.round(af / q) * q                       # numpy rounds half to even; af / q is exact
+    r = np.where(fin, np.minimum(r, 448.0), 448.0)  # saturating: +-inf and overflow -> +-448
+    return np.where(np.isnan(v), np.nan, np.sign(v) * r)
+
+
+def quantize_e4m3(x, scale: float):
+    """q = E4M3(x / scale), the quotient taken in fp32 as the GPU does (R32)."""
+    quot = (np.asarray(x, np.float32) / np.float32(scale)).astype(np.float64)
+    return e4m3_round(quot)
+
+
+def conv_fp8(q_x, sx: float, q_w, sw: float, b=None):
+    """The fp8 convolution's exact value: conv(sx * q_x, sw * q_w) + b in fp64 (3x3 pad 1 or 1x1)."""
+    k = q_w.shape[1]
+    return conv2d(_f64(q_x) * sx, _f64(q_w) * sw, b, 1, k // 2)
+
+
 def rel_l2(a, ref) -> float:
     """||a - ref||_2 / ||ref||_2 (R16)."""
     a, ref = _f64(a), _f64(ref)

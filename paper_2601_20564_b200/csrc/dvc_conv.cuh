@@ -51,6 +51,11 @@ struct ConvDesc {
     // 16 "value" rows then the matching 16 "gate" rows; out is [M][cout/2] with
     // out = value * gelu(gate) (exact erf GELU); no residual, no statistics
     int geglu = 0;
+    // fp8 operands (f4, TMA engine only): every segment's source and weights are E4M3 bytes; the
+    // fp32 accumulator is multiplied by out_scale (the product of the two dequantisation scales)
+    // before bias and the 16-bit (dt) store
+    int fp8 = 0;
+    float out_scale = 1.f;
     long M() const { return (long)T * ho * wo; }
 };
 

@@ -40,6 +40,9 @@ struct WsParams {
     uint32_t idesc;
     float *stats;   // per-channel box statistics of the output (dvc_boxstats.cuh), or null
     int geglu;      // ConvDesc::geglu: 32-column batches = 16 values + 16 gates -> 16 outputs
+    int fp8;        // ConvDesc::fp8: E4M3 operands, 128 channels per 128-byte stage row, kind::f8f6f4
+    int chw;        // channels per stage: 64 (16-bit) or 128 (fp8)
+    float out_scale;
 };
 
 constexpr int kWsThreads = 256;
@@ -134,12 +137,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                     // weight tile origin: column block of this tap, or (packed) its row block
                     const int bc0 = packed ? 0 : p.seg_col0[s] + tap * p.seg_tapstride[s];
                     const int br0 = packed ? p.seg_col0[s] + tap * nch * p.cout + n0 : n0;
-                    const int bcs = packed ? 0 : 64, brs = packed ? p.cout : 0;
+                    const int bcs = packed ? 0 : p.chw, brs = packed ? p.cout : 0;
                     for (int ch = 0; ch < nch; ++ch) {
                         mbar_wait_spin_addr(empty0 + 8 * stage, phase ^ 1);
                         const uint32_t lb = CG == 2 ? lead_full0 + 8 * stage : full0 + 8 * stage;
                         mbar_expect_tx_if(expect, full0 + 8 * stage, tx);
-                        tma_load_4d_if<CG>(issue, sA0 + stage * A_STAGE, am, lb, ch * 64, sst * x0 + dx, sst * y0 + dy, t);
+                        tma_load_4d_if<CG>(issue, sA0 + stage * A_STAGE, am, lb, ch * p.chw, sst * x0 + dx, sst * y0 + dy, t);
                         tma_load_2d_if<CG>(issue, sB0 + stage * B_STAGE, bm, lb, bc0 + ch * bcs, br0 + ch * brs);
                         if (++stage == STAGES) {
                             stage = 0;
@@ -172,9 +175,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         for (int ch = 0; ch < nch; ++ch) {
                             mbar_wait_spin_addr(full0 + 8 * stage, phase);
                             tc_fence_after();
-                            mma_stage<CG>(d, a_lo0 + (uint32_t)stage * (A_STAGE >> 4), kDescHiSw128, 2u,
-                                          b_lo0 + (uint32_t)(stage * (B_STAGE >> 4)), kDescHiSw128, p.idesc,
-                                          ch == nch - 1 ? klast : 4u, acc, empty0 + 8 * stage);
+                            if (p.fp8)
+                                mma_stage_f8<CG>(d, a_lo0 + (uint32_t)stage * (A_STAGE >> 4), kDescHiSw128, 2u,
+                                                 b_lo0 + (uint32_t)(stage * (B_STAGE >> 4)), kDescHiSw128, p.idesc,
+                                                 ch == nch - 1 ? klast : 4u, acc, empty0 + 8 * stage);
+                            else
+                                mma_stage<CG>(d, a_lo0 + (uint32_t)stage * (A_STAGE >> 4), kDescHiSw128, 2u,
+                                              b_lo0 + (uint32_t)(stage * (B_STAGE >> 4)), kDescHiSw128, p.idesc,
+                                              ch == nch - 1 ? klast : 4u, acc, empty0 + 8 * stage);
                             acc = 1;
                             if (++stage == STAGES) {
                                 stage = 0;
@@ -224,7 +232,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         load8(res + m * p.cout + n + 8, *reinterpret_cast<float(*)[8]>(&rv[8]));
                     }
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
+                    for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) * p.out_scale;
                     if (sb0) {
 #pragma unroll
                         for (int i = 0; i < 16; i += 4) {
@@ -417,6 +425,37 @@ static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
     return check_launch("conv_ws_kernel");
 }
 
+// fp8 (E4M3 bytes) variants of the activation / weight tensor maps: 128 channels = 128 bytes per row
+static dvc_status make_amap8(CUtensorMap *map, const void *ptr, int T, int H, int W, int C, int BX, int BY,
+                             int stride) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && C % 16 == 0, DVC_ERR_ARG, "fp8 activation must be 16-byte aligned");
+    cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
+    cuuint64_t gstride[3] = {(cuuint64_t)C, (cuuint64_t)W * C, (cuuint64_t)H * W * C};
+    cuuint32_t box[4] = {128, (cuuint32_t)(BX * stride), (cuuint32_t)(BY * stride), 1};
+    cuuint32_t estr[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(ptr), gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (fp8 activation) failed (%d)", (int)r);
+    return DVC_OK;
+}
+static dvc_status make_bmap8(CUtensorMap *map, const void *ptr, long rows, long cols, int box_rows) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && cols % 16 == 0, DVC_ERR_ARG, "fp8 weights: 16-byte rows");
+    cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)cols};
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (fp8 weights) failed (%d)", (int)r);
+    return DVC_OK;
+}
+
 static int engine_from_env() {
     const char *e = getenv("DVC_CONV_ENGINE");
     if (e && (e[0] == '0' || e[0] == '1' || e[0] == '2') && e[1] == 0) return e[0] - '0';
@@ -456,6 +495,9 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
                   DVC_ERR_UNSUPPORTED, "GEGLU epilogue: 32-column tiles, no residual / statistics / second bias");
     p.bn = bn;
     p.geglu = d.geglu;
+    p.fp8 = d.fp8;
+    p.chw = d.fp8 ? 128 : 64;
+    p.out_scale = d.fp8 ? d.out_scale : 1.f;
     p.nseg = d.nseg;
     p.T = d.T;
     p.H = d.ho;
@@ -476,7 +518,8 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
     for (int s = 0; s < d.nseg; ++s) {
         const ConvSeg &g = d.seg[s];
         p.seg_stride[s] = g.mode == SEG_STRIDE2 ? 2 : 1;
-        st = make_amap(&p.amap[s], g.src, d.dt, d.T, g.hi, g.wi, g.c_src, p.BX, p.BY, p.seg_stride[s]);
+        st = d.fp8 ? make_amap8(&p.amap[s], g.src, d.T, g.hi, g.wi, g.c_src, p.BX, p.BY, p.seg_stride[s])
+                   : make_amap(&p.amap[s], g.src, d.dt, d.T, g.hi, g.wi, g.c_src, p.BX, p.BY, p.seg_stride[s]);
         if (st != DVC_OK) return st;
         int idx = -1;
         for (int k = 0; k < nb; ++k)
@@ -493,21 +536,28 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
                         if (r > rows) rows = r;
                     }
                 st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, rows, 64, bn / CG);
-            } else
+            } else if (d.fp8)
+                st = make_bmap8(&p.bmap[idx], g.w, d.cout, g.w_ld, bn / CG);
+            else
                 st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
             if (st != DVC_OK) return st;
         }
         p.bidx[s] = idx;
         p.seg_packed[s] = g.packed;
         p.seg_c[s] = g.c_src;
-        p.seg_nch[s] = (g.c_src + 63) / 64;
-        p.seg_klast[s] = (g.c_src - 64 * (p.seg_nch[s] - 1)) / 16;
+        p.seg_nch[s] = (g.c_src + p.chw - 1) / p.chw;
+        p.seg_klast[s] = (g.c_src - p.chw * (p.seg_nch[s] - 1)) / (d.fp8 ? 32 : 16);
         p.seg_taps[s] = g.taps;
         p.seg_col0[s] = g.w_col0;
         p.seg_tapstride[s] = g.w_tapstride;
     }
     const int bf = d.dt == DVC_BF16;
-    p.idesc = make_idesc(bf, 128 * CG, bn);
+    // kind::f8f6f4 with A/B format 0 = E4M3 (the same descriptor fields as kind::f16)
+    p.idesc = make_idesc(d.fp8 ? 0 : bf, 128 * CG, bn);
+    if (d.fp8)
+        for (int s = 0; s < d.nseg; ++s)
+            DVC_CHECK_ARG(d.seg[s].c_src % 32 == 0 && !d.seg[s].packed && d.seg[s].w_ld % 16 == 0, DVC_ERR_UNSUPPORTED,
+                          "fp8 conv: channels multiple of 32, unpacked 16-byte weight rows");
     p.stats = reinterpret_cast<float *>(d.stats_out);
     if (CG == 2) {
         if (bf) return launch_ws<__nv_bfloat16, 2, 6>(p, stream);

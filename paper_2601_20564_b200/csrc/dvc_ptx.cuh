@@ -320,26 +320,28 @@ __host__ __device__ constexpr uint32_t desc_hi_sw128(uint32_t sbo_bytes) {
     return ((sbo_bytes >> 4) & 0x3FFFu) | (1u << 14) | (2u << 29);
 }
 
-#define DVC_MMA_STAGE_ASM(CGS)                                                         \
+#define DVC_MMA_STAGE_ASM_K(CGS, KIND)                                                 \
     "{\n\t.reg .pred e, q, acc, one;\n\t.reg .b32 al, bl;\n\t.reg .b64 ad, bd;\n\t"    \
     "elect.sync _|e, 0xffffffff;\n\t"                                                  \
     "setp.ne.b32 acc, %8, 0;\n\t"                                                      \
     "setp.eq.u32 one, %7, %7;\n\t"                                                     \
     "mov.b64 ad, {%1, %2};\n\t"                                                        \
     "mov.b64 bd, {%4, %5};\n\t"                                                        \
-    "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ad, bd, %6, acc;\n\t"           \
+    "@e tcgen05.mma.cta_group::" CGS "." KIND " [%0], ad, bd, %6, acc;\n\t"           \
     "setp.gt.u32 q, %7, 1;\n\tand.pred q, q, e;\n\t"                                   \
     "add.u32 al, %1, %3;\n\tadd.u32 bl, %4, 2;\n\t"                                    \
     "mov.b64 ad, {al, %2};\n\tmov.b64 bd, {bl, %5};\n\t"                               \
-    "@q tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ad, bd, %6, one;\n\t"           \
+    "@q tcgen05.mma.cta_group::" CGS "." KIND " [%0], ad, bd, %6, one;\n\t"           \
     "setp.gt.u32 q, %7, 2;\n\tand.pred q, q, e;\n\t"                                   \
     "add.u32 al, al, %3;\n\tadd.u32 bl, bl, 2;\n\t"                                    \
     "mov.b64 ad, {al, %2};\n\tmov.b64 bd, {bl, %5};\n\t"                               \
-    "@q tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ad, bd, %6, one;\n\t"           \
+    "@q tcgen05.mma.cta_group::" CGS "." KIND " [%0], ad, bd, %6, one;\n\t"           \
     "setp.gt.u32 q, %7, 3;\n\tand.pred q, q, e;\n\t"                                   \
     "add.u32 al, al, %3;\n\tadd.u32 bl, bl, 2;\n\t"                                    \
     "mov.b64 ad, {al, %2};\n\tmov.b64 bd, {bl, %5};\n\t"                               \
-    "@q tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ad, bd, %6, one;\n\t"
+    "@q tcgen05.mma.cta_group::" CGS "." KIND " [%0], ad, bd, %6, one;\n\t"
+
+#define DVC_MMA_STAGE_ASM(CGS) DVC_MMA_STAGE_ASM_K(CGS, "kind::f16")
 
 // ks (1..4) K=16 MMAs over one 64-channel stage (first one overwrites D iff accum == 0),
 // then a commit arriving on `bar` (every CTA of the pair for CG = 2).
@@ -354,6 +356,27 @@ __device__ __forceinline__ void mma_stage(uint32_t d, uint32_t a_lo, uint32_t a_
                      : "memory");
     } else {
         asm volatile(DVC_MMA_STAGE_ASM("2")
+                     "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+                     "[%9], %10;\n\t}\n" ::"r"(d),
+                     "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(ks), "r"(accum),
+                     "r"(bar), "h"((uint16_t)3)
+                     : "memory");
+    }
+}
+// fp8 (E4M3) operands: one 128-byte row = 128 channels, K = 32 per instruction -- the same
+// descriptor walk (32 bytes per K step) with kind::f8f6f4
+template <int CG>
+__device__ __forceinline__ void mma_stage_f8(uint32_t d, uint32_t a_lo, uint32_t a_hi, uint32_t a_step, uint32_t b_lo,
+                                             uint32_t b_hi, uint32_t idesc, uint32_t ks, uint32_t accum,
+                                             uint32_t bar) {
+    if constexpr (CG == 1) {
+        asm volatile(DVC_MMA_STAGE_ASM_K("1", "kind::f8f6f4")
+                     "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}\n" ::"r"(d),
+                     "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(ks), "r"(accum),
+                     "r"(bar)
+                     : "memory");
+    } else {
+        asm volatile(DVC_MMA_STAGE_ASM_K("2", "kind::f8f6f4")
                      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
                      "[%9], %10;\n\t}\n" ::"r"(d),
                      "r"(a_lo), "r"(a_hi), "r"(a_step), "r"(b_lo), "r"(b_hi), "r"(idesc), "r"(ks), "r"(accum),

@@ -360,6 +360,25 @@ def dvc_vae_decode(vae: VAE, lat, out=None, workspace=None, stream=None):
     return out
 
 
+def dvc_quantize_e4m3(x, scale: float, out=None, stream=None):
+    """x (16/32-bit, numel % 8 == 0) -> E4M3 bytes (torch.uint8, same shape): sat(RNE(x / scale))."""
+    if out is None:
+        out = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    check(lib().dvc_quantize_e4m3(_ptr(x), dtype_code(x.dtype), x.numel(), scale, _ptr(out), _stream(stream)))
+    return out
+
+
+def dvc_conv_fp8(x8, sx: float, w8, sw: float, bias=None, out_dtype=torch.bfloat16, out=None, stream=None):
+    """x8 [T,H,W,cin] and w8 [cout,k,k,cin] E4M3 bytes -> y [T,H,W,cout] = sx*sw*conv + bias."""
+    T, H, W, cin = x8.shape
+    cout, k = w8.shape[0], w8.shape[1]
+    if out is None:
+        out = torch.empty((T, H, W, cout), dtype=out_dtype, device=x8.device)
+    check(lib().dvc_conv_fp8(_ptr(x8), sx, _ptr(w8), sw, _ptr(bias), T, H, W, cin, cout, k * k, dtype_code(out_dtype),
+                             _ptr(out), _stream(stream)))
+    return out
+
+
 class StreamingDecoder:
     """f4 online streaming: one frame per step (latency N-1 = 0), the 22 block carries in a ring of
     two buffers, every step one CUDA-graph replay of dvc_unet_decode_gop(T=1).

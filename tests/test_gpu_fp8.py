@@ -1,0 +1,50 @@
+"""GPU checks of the f4 fp8 variant: E4M3 quantisation bit-exact against the oracle's rounding
+(R32), and the fp8 tcgen05 convolution (kind::f8f6f4 on the TMA engine) against the exact
+dequantised convolution."""
+import numpy as np
+import pytest
+import torch
+
+import synthgen
+from tests.gpu_helpers import host64, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dvc():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2601_20564_b200 as m
+    m.device_check(0)
+    return m
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32])
+@pytest.mark.parametrize("scale", [1.0, 0.013, 0.25])
+def test_quantize_e4m3_bit_exact(dvc, orc, dtype, scale):
+    x = torch.from_numpy(synthgen.normal((4096,), 31, scale=3.0)).to(dtype)
+    x[:4] = torch.tensor([1e5, -1e5, 0.0, 448.0 * scale])
+    q = dvc.dvc_quantize_e4m3(x.cuda(), scale).cpu()
+    got = q.view(torch.float8_e4m3fn).float().double().numpy()
+    ref = orc.quantize_e4m3(x.float().numpy(), scale)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("T,H,W,cin,cout,k", [(2, 12, 20, 64, 64, 3), (1, 45, 80, 480, 480, 3), (2, 9, 14, 96, 48, 1),
+                                               (1, 23, 40, 960, 960, 3)])
+def test_conv_fp8_parity(dvc, orc, out_dtype, T, H, W, cin, cout, k):
+    x = torch.from_numpy(synthgen.normal((T, H, W, cin), 32)).cuda()
+    w = torch.from_numpy(synthgen.normal((cout, k, k, cin), 33, scale=1.0 / np.sqrt(k * k * cin))).cuda()
+    b = torch.from_numpy(synthgen.normal((cout,), 34, scale=0.1)).to(out_dtype)
+    sx = float(x.abs().max()) / 448.0
+    sw = float(w.abs().max()) / 448.0
+    x8, w8 = dvc.dvc_quantize_e4m3(x, sx), dvc.dvc_quantize_e4m3(w, sw)
+    y = dvc.dvc_conv_fp8(x8, sx, w8, sw, b.cuda(), out_dtype=out_dtype)
+    qx = x8.cpu().view(torch.float8_e4m3fn).double().numpy()
+    qw = w8.cpu().view(torch.float8_e4m3fn).double().numpy()
+    ref = orc.conv_fp8(qx, sx, qw, sw, b.double().numpy())
+    assert rel_l2(host64(y), ref) <= 1e-2                          # accumulation order + 16-bit output
+    exact = orc.conv2d(x.cpu().double().numpy(), w.cpu().double().numpy(), b.double().numpy(), 1, k // 2)
+    assert rel_l2(host64(y), exact) <= 8e-2                        # E4M3 quantisation error (3 mantissa bits)

@@ -216,3 +216,28 @@ def test_vae_attention_and_resblock_wiring(orc):
     rb["conv2_w"][:] = 0
     rb["conv2_b"][:] = 0
     assert np.allclose(orc.vae_resblock(X, rb, 8, 1e-6), orc.conv1x1(X, rb["sc_w"], rb["sc_b"]), rtol=0, atol=0)
+
+
+# ---------------------------------------------------------------- f4 fp8 E4M3 (R32)
+def test_e4m3_rounding_pins(orc):
+    # the E4M3 value set: 448 max, 2^-9 smallest subnormal, 2^-6 smallest normal, 3 mantissa bits
+    assert orc.e4m3_round(np.array([448.0, 500.0, -1e9, 2.0 ** -9, 2.0 ** -6, 1.0 + 1 / 8]))[0] == 448.0
+    r = orc.e4m3_round(np.array([448.0, 500.0, -1e9, 2.0 ** -9, 2.0 ** -6, 1.125, 1.0625, 1.1875, 0.0, np.inf]))
+    assert list(r) == [448.0, 448.0, -448.0, 2.0 ** -9, 2.0 ** -6, 1.125, 1.0, 1.25, 0.0, 448.0]  # ties to even
+    # every finite E4M3 value (from torch's float8_e4m3fn) is a fixed point, and rounding matches torch
+    allv = torch.arange(256, dtype=torch.uint8).view(torch.float8_e4m3fn).float().numpy().astype(np.float64)
+    fin = allv[np.isfinite(allv)]
+    assert np.array_equal(orc.e4m3_round(fin), fin)
+    x = _rng(13).standard_normal(20000) * 60
+    ref = torch.from_numpy(x.astype(np.float32)).to(torch.float8_e4m3fn).float().numpy()
+    assert np.array_equal(orc.e4m3_round(x.astype(np.float32)), ref.astype(np.float64))
+
+
+def test_conv_fp8_is_the_dequantised_conv(orc):
+    x = _rng(14).standard_normal((1, 4, 5, 32))
+    w = _rng(15).standard_normal((16, 3, 3, 32)) * 0.1
+    qx, qw = orc.quantize_e4m3(x, 0.05), orc.quantize_e4m3(w, 0.01)
+    y = orc.conv_fp8(qx, 0.05, qw, 0.01)
+    ref = F.conv2d(torch.from_numpy(qx * 0.05).permute(0, 3, 1, 2), torch.from_numpy(qw * 0.01).permute(0, 3, 1, 2),
+                   padding=1).permute(0, 2, 3, 1).numpy()
+    assert np.allclose(y, ref, rtol=1e-12, atol=1e-12)
