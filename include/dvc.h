@@ -310,6 +310,10 @@ DVC_API dvc_status dvc_vae_decode(dvc_vae *v, const void *lat, int T, void *fram
  *     cin % 32 == 0, cout % 16 == 0.  A variant of the decode's convolutions
  *     (SURVEY 8f rank 4), not used by dvc_unet_decode_gop.
  * ------------------------------------------------------------------------ */
+/* One plain convolution y = conv(x, w) + bias in dt (the engines the decode uses; a building
+ * block and the 16-bit reference point of dvc_conv_fp8): same layouts, dt in {bf16, fp16, f32}. */
+DVC_API dvc_status dvc_conv(const void *x, const void *w, const void *bias, int T, int H, int W, int cin, int cout,
+                            int taps, dvc_dtype dt, void *y, void *stream);
 DVC_API dvc_status dvc_quantize_e4m3(const void *x, dvc_dtype dt, size_t n, float scale, void *q, void *stream);
 DVC_API dvc_status dvc_conv_fp8(const void *x8, float sx, const void *w8, float sw, const void *bias, int T, int H,
                                 int W, int cin, int cout, int taps, dvc_dtype out_dt, void *y, void *stream);

@@ -95,6 +95,8 @@ _SIGS = {
     "dvc_vae_destroy": ([c_void_p], c_int),
     "dvc_vae_workspace_size": ([c_void_p, c_int, ctypes.POINTER(c_size_t)], c_int),
     "dvc_vae_decode": ([c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
+    "dvc_conv": ([c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p],
+                 c_int),
     "dvc_quantize_e4m3": ([c_void_p, c_int, c_size_t, c_float, c_void_p, c_void_p], c_int),
     "dvc_conv_fp8": ([c_void_p, c_float, c_void_p, c_float, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
                       c_int, c_void_p, c_void_p], c_int),

@@ -81,4 +81,22 @@ dvc_status dvc_conv_fp8(const void *x8, float sx, const void *w8, float sw, cons
     return st;
 }
 
+dvc_status dvc_conv(const void *x, const void *w, const void *bias, int T, int H, int W, int cin, int cout, int taps,
+                    dvc_dtype dt, void *y, void *stream) {
+    DVC_CHECK_ARG(x && w && y && (taps == 1 || taps == 9) && dt_valid(dt), DVC_ERR_ARG, "bad arguments");
+    dvc_status st = check_device();
+    if (st != DVC_OK) return st;
+    ConvDesc d{};
+    d.seg[0] = ConvSeg{x, cin, SEG_SAME, H, W, taps, w, taps * cin, 0, cin};
+    d.nseg = 1;
+    d.T = T;
+    d.ho = H;
+    d.wo = W;
+    d.cout = cout;
+    d.bias0 = bias;
+    d.out = y;
+    d.dt = dt;
+    return conv_run(d, reinterpret_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

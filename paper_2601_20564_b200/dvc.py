@@ -360,6 +360,17 @@ def dvc_vae_decode(vae: VAE, lat, out=None, workspace=None, stream=None):
     return out
 
 
+def dvc_conv(x, w, bias=None, out=None, stream=None):
+    """x [T,H,W,cin], w [cout,k,k,cin] (k = 1 or 3) in one dtype -> y [T,H,W,cout] = conv + bias."""
+    T, H, W, cin = x.shape
+    cout, k = w.shape[0], w.shape[1]
+    if out is None:
+        out = torch.empty((T, H, W, cout), dtype=x.dtype, device=x.device)
+    check(lib().dvc_conv(_ptr(x), _ptr(w), _ptr(bias), T, H, W, cin, cout, k * k, dtype_code(x.dtype), _ptr(out),
+                         _stream(stream)))
+    return out
+
+
 def dvc_quantize_e4m3(x, scale: float, out=None, stream=None):
     """x (16/32-bit, numel % 8 == 0) -> E4M3 bytes (torch.uint8, same shape): sat(RNE(x / scale))."""
     if out is None:

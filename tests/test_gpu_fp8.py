@@ -48,3 +48,13 @@ def test_conv_fp8_parity(dvc, orc, out_dtype, T, H, W, cin, cout, k):
     assert rel_l2(host64(y), ref) <= 1e-2                          # accumulation order + 16-bit output
     exact = orc.conv2d(x.cpu().double().numpy(), w.cpu().double().numpy(), b.double().numpy(), 1, k // 2)
     assert rel_l2(host64(y), exact) <= 8e-2                        # E4M3 quantisation error (3 mantissa bits)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_dvc_conv_parity(dvc, orc, dtype):
+    x = torch.from_numpy(synthgen.normal((2, 12, 20, 64), 35)).to(dtype)
+    w = torch.from_numpy(synthgen.normal((48, 3, 3, 64), 36, scale=1 / 24)).to(dtype)
+    b = torch.from_numpy(synthgen.normal((48,), 37, scale=0.1)).to(dtype)
+    y = dvc.dvc_conv(x.cuda(), w.cuda(), b.cuda())
+    ref = orc.conv2d(x.double().numpy(), w.double().numpy(), b.double().numpy())
+    assert rel_l2(host64(y), ref) <= (1e-2 if dtype != torch.float32 else 1e-5)
