@@ -80,3 +80,20 @@ def test_vae_frames_independent(dvc):
     full = dvc.dvc_vae_decode(v, lat)
     for t in range(3):
         assert torch.equal(dvc.dvc_vae_decode(v, lat[t:t + 1].contiguous())[0], full[t])
+
+
+def test_error_paths_return_before_launch(dvc):
+    # unsupported shapes fail loudly with a status, never a silent fallback (include/dvc.h)
+    qkv = torch.zeros((1, 10, 3 * 80), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(dvc.DvcError, match="UNSUPPORTED"):
+        dvc.dvc_attention_forward(qkv, 40)                       # head_dim 40 not in {16,32,48,64,256}
+    with pytest.raises(dvc.DvcError, match="DIVISIBILITY"):
+        dvc.dvc_attention_forward(torch.zeros((1, 10, 3 * 96), dtype=torch.bfloat16, device="cuda"), 64)
+    named = synthgen.vae_weights((16, 32, 48, 80), 32)
+    with pytest.raises(dvc.DvcError, match="UNSUPPORTED"):       # single-head attention of width 80
+        dvc.VAE(dvc.pack_weights(named, torch.bfloat16), (16, 32, 48, 80), 32, 3, 8, 1e-6, True, torch.bfloat16,
+                4, 4, 1)
+    x8 = torch.zeros((1, 4, 4, 48), dtype=torch.uint8, device="cuda")
+    w8 = torch.zeros((16, 3, 3, 48), dtype=torch.uint8, device="cuda")
+    with pytest.raises(dvc.DvcError, match="UNSUPPORTED"):       # fp8 conv needs C_in % 32
+        dvc.dvc_conv_fp8(x8, 1.0, w8, 1.0)
