@@ -247,6 +247,7 @@ DVC_API const dvc_unet_config *dvc_unet_get_config(const dvc_unet *n);
  *   pop(out, stream, &frames, &first): if the oldest batch is complete on the
  *     host's bookkeeping, enqueue (on `stream`, after the decode's event) the
  *     copy of its `frames` reconstructed latents into out [frames,h,w,c_lat]
+ *     (or, with a VAE, the decoded frames [frames,8h,8w,out_ch])
  *     and return the index of its first frame; frames = 0 if none is ready.
  *   flush(): enqueue the decode of a partial last batch (T < N, R18).
  *   reset(): the next push starts a new chain (zero carry, R8/R9); flushes
@@ -255,7 +256,11 @@ DVC_API const dvc_unet_config *dvc_unet_get_config(const dvc_unet *n);
  * call over the whole chain (batch == online, P9).
  * ------------------------------------------------------------------------ */
 typedef struct dvc_pipeline dvc_pipeline;
-DVC_API dvc_status dvc_pipeline_create(dvc_unet *net, int batch_n, int fifo_batches, dvc_pipeline **out);
+typedef struct dvc_vae dvc_vae;   /* f2, below */
+/* vae: NULL = the pipeline outputs Lhat; else the VAE decoder (same h, w, c_lat, dt; max_T >= N)
+ * runs after the U-Net on the pipeline stream and pop() returns frames [n, 8h, 8w, out_ch]. */
+DVC_API dvc_status dvc_pipeline_create(dvc_unet *net, dvc_vae *vae, int batch_n, int fifo_batches,
+                                       dvc_pipeline **out);
 DVC_API dvc_status dvc_pipeline_destroy(dvc_pipeline *p);
 DVC_API dvc_status dvc_pipeline_push(dvc_pipeline *p, const void *lat, const void *ctx, void *stream);
 DVC_API dvc_status dvc_pipeline_pop(dvc_pipeline *p, void *out, void *stream, int *frames, long long *first_frame);
@@ -292,10 +297,10 @@ typedef struct {
     int h, w;          /* latent size; frames are 8h x 8w */
     int max_T;
 } dvc_vae_config;
-typedef struct dvc_vae dvc_vae;
 DVC_API dvc_status dvc_vae_weight_count(const dvc_vae_config *cfg, size_t *elems);
 DVC_API dvc_status dvc_vae_create(const dvc_vae_config *cfg, const void *host_weights, size_t bytes, dvc_vae **out);
 DVC_API dvc_status dvc_vae_destroy(dvc_vae *v);
+DVC_API const dvc_vae_config *dvc_vae_get_config(const dvc_vae *v);
 DVC_API dvc_status dvc_vae_workspace_size(const dvc_vae *v, int T, size_t *bytes);
 DVC_API dvc_status dvc_vae_decode(dvc_vae *v, const void *lat, int T, void *frames, void *workspace, size_t ws_bytes,
                                   void *stream);

@@ -83,7 +83,7 @@ _SIGS = {
     "dvc_attention_forward": ([c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_size_t,
                                c_void_p], c_int),
     "dvc_unet_get_config": ([c_void_p], ctypes.POINTER(dvc_unet_config)),
-    "dvc_pipeline_create": ([c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)], c_int),
+    "dvc_pipeline_create": ([c_void_p, c_void_p, c_int, c_int, ctypes.POINTER(c_void_p)], c_int),
     "dvc_pipeline_destroy": ([c_void_p], c_int),
     "dvc_pipeline_push": ([c_void_p, c_void_p, c_void_p, c_void_p], c_int),
     "dvc_pipeline_pop": ([c_void_p, c_void_p, c_void_p, ctypes.POINTER(c_int), ctypes.POINTER(ctypes.c_longlong)],
@@ -93,6 +93,7 @@ _SIGS = {
     "dvc_vae_weight_count": ([ctypes.POINTER(dvc_vae_config), ctypes.POINTER(c_size_t)], c_int),
     "dvc_vae_create": ([ctypes.POINTER(dvc_vae_config), c_void_p, c_size_t, ctypes.POINTER(c_void_p)], c_int),
     "dvc_vae_destroy": ([c_void_p], c_int),
+    "dvc_vae_get_config": ([c_void_p], ctypes.POINTER(dvc_vae_config)),
     "dvc_vae_workspace_size": ([c_void_p, c_int, ctypes.POINTER(c_size_t)], c_int),
     "dvc_vae_decode": ([c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p], c_int),
     "dvc_conv": ([c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p],

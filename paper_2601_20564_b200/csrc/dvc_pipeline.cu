@@ -1,7 +1,8 @@
 // dvc_pipeline.cu -- f3: the Asynchronous and Parallel Decoding Pipeline.
 //
 // The paper's decoder has two branches: the Latent Compressor runs in the prediction loop
-// (frame t needs Lbar_{t-1}) and the Frame Reconstructor (U-Net) runs out of the loop.  They
+// (frame t needs Lbar_{t-1}) and the Frame Reconstructor (U-Net, then optionally the VAE
+// decoder -> frames) runs out of the loop.  They
 // are decoupled through buffers and the reconstructor takes N frames at a time on the batch
 // dimension, the Batch-dimension OTSM carrying the shifted slices from batch to batch.
 //
@@ -19,11 +20,14 @@
 
 struct dvc_pipeline {
     dvc_unet *net = nullptr;
+    dvc_vae *vae = nullptr;      // optional: the Frame Reconstructor's VAE decoder (frames out)
+    void *vws = nullptr;
+    size_t vws_bytes = 0, out_elems = 0;   // per frame: h*w*c_lat latents or 8h*8w*out_ch pixels
     dvc_unet_config cfg{};
     int N = 0, K = 0;
     size_t lat_elems = 0, ctx_elems = 0, es = 0;   // per frame
     struct Slot {
-        void *lat = nullptr, *ctx = nullptr, *out = nullptr;
+        void *lat = nullptr, *ctx = nullptr, *out = nullptr, *pix = nullptr;   // pix: VAE frames
         int frames = 0;
         long long first = 0;
         bool launched = false;   // decode enqueued, not yet popped
@@ -51,6 +55,7 @@ static void pipeline_free(dvc_pipeline *p) {
         cudaFree(s.lat);
         cudaFree(s.ctx);
         cudaFree(s.out);
+        cudaFree(s.pix);
         if (s.filled) cudaEventDestroy(s.filled);
         if (s.decoded) cudaEventDestroy(s.decoded);
         if (s.freed) cudaEventDestroy(s.freed);
@@ -58,6 +63,7 @@ static void pipeline_free(dvc_pipeline *p) {
     cudaFree(p->carry[0]);
     cudaFree(p->carry[1]);
     cudaFree(p->ws);
+    cudaFree(p->vws);
     if (p->fr) cudaStreamDestroy(p->fr);
     delete p;
 }
@@ -71,6 +77,10 @@ static dvc_status launch_slot(dvc_pipeline *p, cudaStream_t producer) {
     dvc_status st = dvc_unet_decode_gop(p->net, nullptr, s.lat, s.ctx, s.frames, cin, cout, s.out, p->ws, p->ws_bytes,
                                         p->fr);
     if (st != DVC_OK) return st;
+    if (p->vae) {   // Lhat -> frames through the VAE decoder on the same stream
+        st = dvc_vae_decode(p->vae, s.out, s.frames, s.pix, p->vws, p->vws_bytes, p->fr);
+        if (st != DVC_OK) return st;
+    }
     DVC_CUDA(cudaEventRecord(s.decoded, p->fr));
     p->cur ^= 1;
     p->chain_start = false;
@@ -82,7 +92,7 @@ static dvc_status launch_slot(dvc_pipeline *p, cudaStream_t producer) {
 
 extern "C" {
 
-dvc_status dvc_pipeline_create(dvc_unet *net, int batch_n, int fifo_batches, dvc_pipeline **out) {
+dvc_status dvc_pipeline_create(dvc_unet *net, dvc_vae *vae, int batch_n, int fifo_batches, dvc_pipeline **out) {
     DVC_CHECK_ARG(net && out, DVC_ERR_ARG, "null argument");
     const dvc_unet_config *c = dvc_unet_get_config(net);
     DVC_CHECK_ARG(batch_n >= 1 && batch_n <= c->max_T, DVC_ERR_ARG, "batch_n=%d outside [1, max_T=%d]", batch_n,
@@ -98,18 +108,32 @@ dvc_status dvc_pipeline_create(dvc_unet *net, int batch_n, int fifo_batches, dvc
     p->es = dt_size(c->dt);
     p->lat_elems = (size_t)c->h * c->w * c->c_lat;
     p->ctx_elems = (size_t)c->h * c->w * c->c_ctx;
+    p->out_elems = p->lat_elems;
+    if (vae) {
+        const dvc_vae_config *vc = dvc_vae_get_config(vae);
+        if (vc->h != c->h || vc->w != c->w || vc->c_lat != c->c_lat || vc->dt != c->dt || vc->max_T < batch_n) {
+            delete p;
+            set_error("pipeline: VAE config does not match the U-Net (h, w, c_lat, dtype, max_T >= N)");
+            return DVC_ERR_SHAPE;
+        }
+        p->vae = vae;
+        p->out_elems = (size_t)64 * c->h * c->w * vc->out_ch;
+        dvc_vae_workspace_size(vae, batch_n, &p->vws_bytes);
+    }
     size_t carry = 0;
     dvc_unet_carry_size(net, &carry);
     dvc_unet_workspace_size(net, batch_n, &p->ws_bytes);
     bool ok = cudaStreamCreateWithFlags(&p->fr, cudaStreamNonBlocking) == cudaSuccess &&
               cudaMalloc(&p->ws, p->ws_bytes) == cudaSuccess &&
               cudaMalloc(&p->carry[0], carry * p->es + 16) == cudaSuccess &&
-              cudaMalloc(&p->carry[1], carry * p->es + 16) == cudaSuccess;
+              cudaMalloc(&p->carry[1], carry * p->es + 16) == cudaSuccess &&
+              (!vae || cudaMalloc(&p->vws, p->vws_bytes) == cudaSuccess);
     p->slots.resize(fifo_batches);
     for (auto &s : p->slots) {
         ok = ok && cudaMalloc(&s.lat, p->lat_elems * p->es * batch_n) == cudaSuccess &&
              cudaMalloc(&s.ctx, p->ctx_elems * p->es * batch_n) == cudaSuccess &&
              cudaMalloc(&s.out, p->lat_elems * p->es * batch_n) == cudaSuccess &&
+             (!vae || cudaMalloc(&s.pix, p->out_elems * p->es * batch_n) == cudaSuccess) &&
              cudaEventCreateWithFlags(&s.filled, cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&s.decoded, cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&s.freed, cudaEventDisableTiming) == cudaSuccess;
@@ -154,7 +178,8 @@ dvc_status dvc_pipeline_pop(dvc_pipeline *p, void *out, void *stream, int *frame
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     dvc_pipeline::Slot &sl = p->slots[p->oldest];
     DVC_CUDA(cudaStreamWaitEvent(s, sl.decoded, 0));
-    DVC_CUDA(cudaMemcpyAsync(out, sl.out, (size_t)sl.frames * p->lat_elems * p->es, cudaMemcpyDeviceToDevice, s));
+    DVC_CUDA(cudaMemcpyAsync(out, p->vae ? sl.pix : sl.out, (size_t)sl.frames * p->out_elems * p->es,
+                             cudaMemcpyDeviceToDevice, s));
     DVC_CUDA(cudaEventRecord(sl.freed, s));
     sl.freed_valid = true;
     *frames = sl.frames;

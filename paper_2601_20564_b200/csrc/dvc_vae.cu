@@ -292,6 +292,8 @@ dvc_status dvc_vae_create(const dvc_vae_config *cfg, const void *host_weights, s
     return DVC_OK;
 }
 
+const dvc_vae_config *dvc_vae_get_config(const dvc_vae *v) { return v ? &v->cfg : nullptr; }
+
 dvc_status dvc_vae_destroy(dvc_vae *v) {
     if (!v) return DVC_OK;
     cudaFree(v->dweights);

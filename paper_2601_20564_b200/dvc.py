@@ -275,14 +275,15 @@ class Pipeline:
     (Lbar_t, C^m_t) at a time from the in-loop producer's stream; the U-Net decodes batches of N
     frames on the pipeline's own stream; pop() hands back decoded batches in order (latency N-1)."""
 
-    def __init__(self, net: UNet, batch_n: int, fifo_batches: int = 2):
-        self.net = net
+    def __init__(self, net: UNet, batch_n: int, fifo_batches: int = 2, vae=None):
+        self.net, self.vae = net, vae
         cfg = net.cfg
         self.dtype = {0: torch.bfloat16, 1: torch.float16, 2: torch.float32}[cfg.dt]
-        self.shape = (cfg.h, cfg.w, cfg.c_lat)
+        self.shape = (cfg.h, cfg.w, cfg.c_lat) if vae is None else (8 * cfg.h, 8 * cfg.w, vae.out_ch)
         self.N = batch_n
         self.handle = ctypes.c_void_p()
-        check(lib().dvc_pipeline_create(net.handle, batch_n, fifo_batches, ctypes.byref(self.handle)))
+        check(lib().dvc_pipeline_create(net.handle, None if vae is None else vae.handle, batch_n, fifo_batches,
+                                        ctypes.byref(self.handle)))
 
     def push(self, lat, ctx, stream=None):
         check(lib().dvc_pipeline_push(self.handle, _ptr(lat), _ptr(ctx), _stream(stream)))

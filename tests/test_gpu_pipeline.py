@@ -95,3 +95,32 @@ def test_pipeline_full_fifo_is_an_error(dvc):
         pipe.push(lat[4], lat[4])
     assert pipe.pop() is not None
     pipe.push(lat[4], lat[4])
+
+
+def test_pipeline_with_vae_decoder_outputs_frames(dvc):
+    # the whole Frame Reconstructor in the pipeline: U-Net then the VAE decoder ("pass them
+    # through the U-Net and VAE Decoder in parallel"); equal to the two calls made directly
+    h, w, N, T = 8, 10, 2, 5
+    net = _net(dvc, h, w, T)
+    VS = (16, 32, 48, 48)
+    vae = dvc.VAE(dvc.pack_weights(synthgen.vae_weights(VS, 32), torch.bfloat16), VS, 32, 3, 8, 1e-6, True,
+                  torch.bfloat16, h, w, T)
+    lat, _ = dev(synthgen.normal((T, h, w, 32), 1), torch.bfloat16)
+    ctx, _ = dev(synthgen.normal((T, h, w, 32), 5), torch.bfloat16)
+    ref = dvc.dvc_vae_decode(vae, dvc.dvc_unet_decode_gop(net, lat, ctx))
+    pipe = dvc.Pipeline(net, N, 3, vae=vae)
+    got = {}
+    for t in range(T):
+        pipe.push(lat[t], ctx[t])
+        while (r := pipe.pop()) is not None:
+            for i in range(r[1].shape[0]):
+                got[r[0] + i] = r[1][i].clone()
+    pipe.flush()
+    while (r := pipe.pop()) is not None:
+        for i in range(r[1].shape[0]):
+            got[r[0] + i] = r[1][i].clone()
+    torch.cuda.synchronize()
+    out = torch.stack([got[t] for t in range(T)])
+    assert out.shape == (T, 8 * h, 8 * w, 3)
+    assert torch.equal(out, ref)
+

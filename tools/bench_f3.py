@@ -89,6 +89,41 @@ def main():
         print(json.dumps({"config": f"F3 pipeline N={N} FIFO 3, 720p bf16, {F} frames",
                           "frames_per_s": F / (ms / 1e3), "latency_frames": N - 1}), flush=True)
         pipe.close()
+    # the whole Frame Reconstructor (U-Net + VAE decoder -> 720p frames) behind the same pipeline
+    vae = dvc.VAE(dvc.pack_weights(synthgen.vae_weights(), dt), dtype=dt, h=h, w=w, max_T=8)
+    vws1 = torch.empty(vae.workspace_size(1), dtype=torch.uint8, device="cuda")
+    px1 = torch.empty((1, 8 * h, 8 * w, 3), dtype=dt, device="cuda")
+
+    def sequential_fr():
+        cin = None
+        for t in range(F):
+            produce(t)
+            dvc.dvc_unet_decode_gop(net, lat[t:t + 1], ctx[t % 8:t % 8 + 1], carry_in=cin, carry_out=carries[t % 2],
+                                    out=out1, workspace=ws1)
+            dvc.dvc_vae_decode(vae, out1, out=px1, workspace=vws1)
+            cin = carries[t % 2]
+    ms = timed(sequential_fr)
+    print(json.dumps({"config": f"F3 sequential Frame Reconstructor (U-Net + VAE, T=1 per frame), 720p bf16, {F} frames",
+                      "frames_per_s": F / (ms / 1e3), "latency_frames": 0}), flush=True)
+    for N in (4, 8):
+        pipe = dvc.Pipeline(net, N, 3, vae=vae)
+        prod = torch.cuda.Stream()
+        outp = torch.empty((N, 8 * h, 8 * w, 3), dtype=dt, device="cuda")
+
+        def pipelined_fr():
+            pipe.reset()
+            for t in range(F):
+                with torch.cuda.stream(prod):
+                    produce(t, stream=prod)
+                    pipe.push(lat[t], ctx[t % 8], stream=prod)
+                pipe.pop(outp)
+            pipe.flush()
+            while pipe.pop(outp) is not None:
+                pass
+        ms = timed(pipelined_fr)
+        print(json.dumps({"config": f"F3 pipeline Frame Reconstructor (U-Net + VAE) N={N} FIFO 3, 720p bf16, {F} frames",
+                          "frames_per_s": F / (ms / 1e3), "latency_frames": N - 1}), flush=True)
+        pipe.close()
 
 
 if __name__ == "__main__":
