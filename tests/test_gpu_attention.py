@@ -70,7 +70,7 @@ def _tf_dev(C, dtype, seed=0, qkv_scale=3.0):
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32])
 @pytest.mark.parametrize("T,H,W,C,G,d", [(2, 6, 10, 96, 8, 48), (1, 12, 20, 240, 24, 48), (3, 9, 14, 64, 8, 16),
-                                         (2, 23, 40, 128, 8, 64)])
+                                         (2, 23, 40, 128, 8, 64), (1, 9, 12, 480, 24, 48), (1, 6, 8, 960, 24, 48)])
 def test_transformer_block_parity(dvc, orc, dtype, T, H, W, C, G, d):
     wd, wh = _tf_dev(C, dtype)
     p = dvc.TransformerParams(wd, G, d)
@@ -137,3 +137,24 @@ def test_full_unet_batch_equals_online(dvc):
         parts.append(dvc.dvc_unet_decode_gop(net, lat[t:t + 1], ctx[t:t + 1], carry_in=carry, carry_out=co))
         carry = co
     assert torch.equal(torch.cat(parts), full)
+
+
+@pytest.mark.slow
+def test_full_unet_720p_batch_equals_online_and_deterministic(dvc):
+    # the bench's real widths and 720p latent (90x160) with the 16 Transformer2D blocks: batch == online
+    # (T=2 vs 2 x T=1 with the carry) and run-to-run bit-exact
+    W = (240, 480, 960, 960)
+    T, h, w = 2, 90, 160
+    named = synthgen.unet_weights(W, 256, 256, attention=True)
+    cfg = dvc.unet_config(W, 256, 256, 24, 8, 1e-5, torch.bfloat16, h, w, T, head_dim=48)
+    net = dvc.UNet(cfg, dvc.pack_weights(named, torch.bfloat16))
+    lat, _ = dev(synthgen.normal((T, h, w, 256), 1), torch.bfloat16)
+    ctx, _ = dev(synthgen.normal((T, h, w, 256), 5), torch.bfloat16)
+    full = dvc.dvc_unet_decode_gop(net, lat, ctx)
+    assert torch.equal(full, dvc.dvc_unet_decode_gop(net, lat, ctx))
+    assert torch.isfinite(full.float()).all()
+    co = torch.empty(net.carry_elems, dtype=torch.bfloat16, device="cuda")
+    a = dvc.dvc_unet_decode_gop(net, lat[:1], ctx[:1], carry_out=co)
+    b = dvc.dvc_unet_decode_gop(net, lat[1:], ctx[1:], carry_in=co)
+    assert torch.equal(torch.cat([a, b]), full)
+

@@ -97,3 +97,15 @@ def test_error_paths_return_before_launch(dvc):
     w8 = torch.zeros((16, 3, 3, 48), dtype=torch.uint8, device="cuda")
     with pytest.raises(dvc.DvcError, match="UNSUPPORTED"):       # fp8 conv needs C_in % 32
         dvc.dvc_conv_fp8(x8, 1.0, w8, 1.0)
+
+
+@pytest.mark.slow
+def test_vae_720p_frames_independent_and_deterministic(dvc):
+    # the bench's real decoder at 720p (90x160 latent -> 720x1280): per-frame == batched, bit-exact
+    v = dvc.VAE(dvc.pack_weights(synthgen.vae_weights(), torch.bfloat16), dtype=torch.bfloat16, h=90, w=160, max_T=2)
+    lat, _ = dev(synthgen.normal((2, 90, 160, 256), 1), torch.bfloat16)
+    full = dvc.dvc_vae_decode(v, lat)
+    assert full.shape == (2, 720, 1280, 3) and torch.isfinite(full.float()).all()
+    assert torch.equal(full, dvc.dvc_vae_decode(v, lat))
+    assert torch.equal(dvc.dvc_vae_decode(v, lat[1:].contiguous())[0], full[1])
+
