@@ -10,10 +10,13 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline /
 ``--impl reference`` legs may use this module.  It never imports the product.
 
 Parity status: every function below is pinned by a
-``-m "not gpu"`` test in tests/test_oracle_pins.py except agreement with the
-paper's trained model, which is unpinnable (no weights are published):
-the readings R2-R4, R8, R11, R13 are "parity unpinned" against the paper's
-numbers and pinned only structurally.
+``-m "not gpu"`` test in tests/test_oracle_pins.py (the a-rows) or
+tests/test_oracle_attention.py (f1 Transformer2D / attention / GELU / LayerNorm,
+f2 VAE decoder, f4 E4M3 rounding) except agreement with the paper's trained
+model, which is unpinnable (no weights are published): the readings R2-R4, R8,
+R11, R13, R24-R25, R29's 256-channel interface and R30 are "parity unpinned"
+against the paper's numbers and pinned only structurally (the topologies are
+pinned by Table 8's parameter counts).
 """
 from __future__ import annotations
 

@@ -266,7 +266,7 @@ struct AttnSmem {
     static constexpr int V = D * 128 * 2;        // one transposed value tile
     static constexpr int off_q = 0, off_k = NT * Q, off_v = off_k + STAGES * K;
     static constexpr int off_bar = off_v + STAGES * V;
-    // barriers: q_full, kv_full[S], kv_empty[S], s_full[2], s_free[2], p_full[2], o_full[2][2]
+    // barriers: q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_full[2], 6 spare
     static constexpr int nbar = 1 + 2 * STAGES + 2 + 2 + 2 + 4;
     static constexpr int off_red = off_bar + nbar * 8 + 16;     // [NT tiles][2 halves][128 rows] float exchange
     static constexpr int bytes = off_red + NT * 2 * 128 * 4 + 1024;   // + alignment slack
@@ -335,8 +335,8 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
     const uint32_t bar0 = sb + L::off_bar;
     constexpr int kAttnStages = L::STAGES, NT = L::NT;
     const uint32_t q_full = bar0, kv_full = bar0 + 8, kv_empty = kv_full + 8 * kAttnStages;
-    const uint32_t s_full = kv_empty + 8 * kAttnStages, s_free = s_full + 16, p_full = s_free + 16;
-    const uint32_t o_full = p_full + 16;   // [t][b] at o_full + 8 * (2 t + b)
+    const uint32_t s_full = kv_empty + 8 * kAttnStages, p_full = s_full + 16;   // p_full also releases S
+    const uint32_t o_full = p_full + 16;   // [t] at o_full + 8 t: O_t final
     uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + L::off_bar + L::nbar * 8);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * 128 * NT;
@@ -351,9 +351,8 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
         }
         const int sf = 1 + 2 * kAttnStages;
         mbar_init(&b[sf], 1), mbar_init(&b[sf + 1], 1);          // s_full (tcgen05.commit)
-        mbar_init(&b[sf + 2], 4), mbar_init(&b[sf + 3], 4);      // s_free (one arrive per softmax warp)
-        mbar_init(&b[sf + 4], 8), mbar_init(&b[sf + 5], 8);      // p_full (8 softmax warps per tile)
-        for (int i = 0; i < 4; ++i) mbar_init(&b[sf + 6 + i], 1);   // o_full
+        mbar_init(&b[sf + 2], 8), mbar_init(&b[sf + 3], 8);      // p_full (8 softmax warps per tile)
+        for (int i = 0; i < 2; ++i) mbar_init(&b[sf + 4 + i], 1);   // o_full
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == w_mma) tmem_alloc<1>(smem_u32(tslot), 512);
