@@ -684,7 +684,14 @@ extern int g_ws_cg;
 
 dvc_status make_box_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX, int BY);
 
-bool conv_fz_applicable(int H, int W, dvc_dtype dt) { return g_ws_cg == 2 && dt != DVC_F32 && H >= 32 && W >= 8; }
+static int fz_off_from_env() {   // DVC_NO_FZ=1: never use the fused engine (A/B experiments)
+    const char *e = getenv("DVC_NO_FZ");
+    return e && e[0] == '1';
+}
+static const int g_fz_off = fz_off_from_env();
+bool conv_fz_applicable(int H, int W, dvc_dtype dt) {
+    return !g_fz_off && g_ws_cg == 2 && dt != DVC_F32 && H >= 32 && W >= 8;
+}
 
 static int g_fz_sms = 0;
 
