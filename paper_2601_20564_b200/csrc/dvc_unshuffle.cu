@@ -13,25 +13,34 @@
 
 namespace dvc {
 
-constexpr int kUxb = 16;   // output pixels per block (fast path)
+constexpr int kUxb = 16;   // output pixels per block pass (fast path)
+constexpr int kUpass = 4;  // passes per block: 4 independent 16-byte loads in flight per thread
 
 __global__ void __launch_bounds__(384) unshuffle8_16bit_kernel(const uint4 *__restrict__ F, uint4 *__restrict__ L,
                                                                int T, int H, int W) {
-    __shared__ uint4 tile[24][kUxb];
+    __shared__ uint4 tile[kUpass][24][kUxb];
     const int h = H / 8, w = W / 8;
     const int xb = blockIdx.x, y = blockIdx.y, t = blockIdx.z;
-    const int x0 = xb * kUxb;
     const int k = threadIdx.x;
-    {   // read: k -> (gi = c*8 + i, px): consecutive threads walk along one input row
+    {   // read: k -> (gi = c*8 + i, px): consecutive threads walk along one input row; all passes'
+        // loads are issued before any is consumed (memory-level parallelism for the HBM stream)
         const int gi = k / kUxb, px = k % kUxb;
         const int c = gi >> 3, i = gi & 7;
-        if (x0 + px < w)
-            tile[gi][px] = __ldg(F + ((((size_t)t * 3 + c) * H + 8 * y + i) * W) / 8 + (x0 + px));
+        const uint4 *row = F + ((((size_t)t * 3 + c) * H + 8 * y + i) * W) / 8;
+#pragma unroll
+        for (int q = 0; q < kUpass; ++q) {
+            const int x = (xb * kUpass + q) * kUxb + px;
+            if (x < w) tile[q][gi][px] = __ldg(row + x);
+        }
     }
     __syncthreads();
     {   // write: k -> (px, gi): consecutive threads fill consecutive 16-byte granules of the output
         const int px = k / 24, gi = k % 24;
-        if (x0 + px < w) L[(((size_t)t * h + y) * w + x0 + px) * 24 + gi] = tile[gi][px];
+#pragma unroll
+        for (int q = 0; q < kUpass; ++q) {
+            const int x = (xb * kUpass + q) * kUxb + px;
+            if (x < w) L[(((size_t)t * h + y) * w + x) * 24 + gi] = tile[q][gi][px];
+        }
     }
 }
 
@@ -53,7 +62,7 @@ __global__ void unshuffle_generic_kernel(const T *__restrict__ F, T *__restrict_
 dvc_status unshuffle_run(const void *frames, dvc_dtype dt, int T, int H, int W, int s, void *latent,
                          cudaStream_t stream) {
     if (s == 8 && dt != DVC_F32 && ((uintptr_t)frames & 15) == 0 && ((uintptr_t)latent & 15) == 0) {
-        dim3 grid(ceil_div(W / 8, kUxb), H / 8, T);
+        dim3 grid(ceil_div(W / 8, kUxb * kUpass), H / 8, T);
         unshuffle8_16bit_kernel<<<grid, 384, 0, stream>>>(reinterpret_cast<const uint4 *>(frames),
                                                           reinterpret_cast<uint4 *>(latent), T, H, W);
         ++g_launches;
