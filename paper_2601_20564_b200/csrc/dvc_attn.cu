@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) geglu_kernel(const T *__restrict__ f, T *
 //   Qp, Kp [T][heads][ntiles]: element (r, d) of the tile at (d/8)*1024 + r*8 + d%8   (chunk-major)
 //   Vp     [T][heads][ntiles]: element (r, d) (key r)  at (r/8)*D*8  + d*8 + r%8    (V^T, K = keys)
 // Tokens n >= N of the last tile are zero.  One CTA per (tile, head, frame).
-template <typename T, int D>
+template <typename T, int D, int KT>
 __global__ void __launch_bounds__(256) qkv_pack_kernel(const T *__restrict__ qkv, T *__restrict__ qp,
                                                        T *__restrict__ kp, T *__restrict__ vp, int N, int C) {
     griddep_wait();
@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(256) qkv_pack_kernel(const T *__restrict__ qkv
                 v = __ldg(reinterpret_cast<const uint4 *>(src + 2 * C));
             }
             *reinterpret_cast<uint4 *>(qp + tile + kc * 1024 + r * 8) = q;
-            *reinterpret_cast<uint4 *>(kp + tile + kc * 1024 + r * 8) = k;
+            // K in KT-row sub-tiles of the 128-token block (chunk-major inside each)
+            *reinterpret_cast<uint4 *>(kp + tile + (r / KT) * (KT * D) + kc * (KT * 8) + (r % KT) * 8) = k;
             *reinterpret_cast<uint4 *>(sv + r * DCH + kl * 8) = v;
         }
         __syncthreads();
@@ -171,7 +172,8 @@ __global__ void __launch_bounds__(256) qkv_pack_kernel(const T *__restrict__ qkv
             Vec8<T> u;
 #pragma unroll
             for (int e = 0; e < 8; ++e) u.v[e] = sv[(kc * 8 + e) * DCH + dl];
-            *reinterpret_cast<Vec8<T> *>(vp + tile + kc * D * 8 + (d0 + dl) * 8) = u;
+            const int r0 = kc * 8;   // V^T in KT-key sub-tiles
+            *reinterpret_cast<Vec8<T> *>(vp + tile + (r0 / KT) * (KT * D) + ((r0 % KT) / 8) * D * 8 + (d0 + dl) * 8) = u;
         }
         __syncthreads();
     }
@@ -256,22 +258,27 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const float *__restrict_
 // head_dim <= 64: two query tiles per CTA (TMEM S0 S1 | O0 O1 | P0 P1), 4-stage K/V ring;
 // head_dim 256 (the VAE decoder's single-head mid attention, f2): one tile (S | P | O = 256
 // columns), K/V single-buffered (192 KB of operand tiles).
-template <int D>
+template <int D, int KT = 128>
 struct AttnSmem {
-    static constexpr int NT = D <= 64 ? 2 : 1;            // query tiles per CTA
-    static constexpr int STAGES = D <= 64 ? 4 : 1;
+    // KT = keys per S tile: 128 (two query tiles per CTA); 64 gives three query tiles per CTA (six
+    // softmax warps per SM sub-partition) -- measured slower at 720p level 0 (609 vs 650 TFLOP/s:
+    // the per-iteration handshakes double), so only KT = 128 is instantiated
+    static constexpr int NT = D <= 64 ? (KT == 64 ? 3 : 2) : 1;   // query tiles per CTA
+    static constexpr int STAGES = D <= 64 ? (KT == 64 ? 6 : 4) : 1;
     static constexpr int THREADS = (8 * NT + 2) * 32;     // 8 softmax warps per tile + MMA + TMA
     static constexpr int Q = 128 * D * 2;        // one query tile
-    static constexpr int K = 128 * D * 2;        // one key tile
-    static constexpr int V = D * 128 * 2;        // one transposed value tile
+    static constexpr int K = KT * D * 2;         // one key tile
+    static constexpr int V = D * KT * 2;         // one transposed value tile
     static constexpr int off_q = 0, off_k = NT * Q, off_v = off_k + STAGES * K;
     static constexpr int off_bar = off_v + STAGES * V;
     // barriers: q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_full[2], 6 spare
-    static constexpr int nbar = 1 + 2 * STAGES + 2 + 2 + 2 + 4;
+    static constexpr int nbar = 1 + 2 * STAGES + 3 * 4;   // + s_full[4], p_full[4], o_full[4] (NT <= 3)
     static constexpr int off_red = off_bar + nbar * 8 + 16;     // [NT tiles][2 halves][128 rows] float exchange
     static constexpr int bytes = off_red + NT * 2 * 128 * 4 + 1024;   // + alignment slack
     // TMEM columns (512 allocated)
-    static constexpr int tm_o = 256, tm_o_step = NT == 2 ? 64 : 0, tm_p = NT == 2 ? 384 : 128, tm_p_step = 64;
+    // S_t at t*KT, P_t (KT/2 packed columns) at tm_p + t*KT/2, O_t at tm_o + t*64
+    static constexpr int tm_o = NT == 3 ? 320 : 256, tm_o_step = NT == 1 ? 0 : 64;
+    static constexpr int tm_p = NT == 3 ? 192 : NT == 2 ? 384 : 128, tm_p_step = KT / 2;
 };
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -324,24 +331,24 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     }
 }
 
-template <typename T, int D, int NPOLY>
-__global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
+template <typename T, int D, int NPOLY, int KT>
+__global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
     attn_tc_kernel(const T *__restrict__ qp, const T *__restrict__ kp, const T *__restrict__ vp, T *__restrict__ out,
                    int N, int C, float scale_log2, uint32_t idesc_s, uint32_t idesc_o, int dbg) {
-    using L = AttnSmem<D>;
+    using L = AttnSmem<D, KT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(smem);
     const uint32_t bar0 = sb + L::off_bar;
     constexpr int kAttnStages = L::STAGES, NT = L::NT;
     const uint32_t q_full = bar0, kv_full = bar0 + 8, kv_empty = kv_full + 8 * kAttnStages;
-    const uint32_t s_full = kv_empty + 8 * kAttnStages, p_full = s_full + 16;   // p_full also releases S
-    const uint32_t o_full = p_full + 16;   // [t] at o_full + 8 t: O_t final
+    const uint32_t s_full = kv_empty + 8 * kAttnStages, p_full = s_full + 32;   // p_full also releases S
+    const uint32_t o_full = p_full + 32;   // [t] at o_full + 8 t: O_t final
     uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + L::off_bar + L::nbar * 8);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int t = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * 128 * NT;
     const int w_mma = 8 * NT, w_tma = 8 * NT + 1;
-    const int nkt = (N + 127) / 128;
+    const int nkt = (N + KT - 1) / KT;
     if (tid == 0) {
         uint64_t *b = reinterpret_cast<uint64_t *>(smem + L::off_bar);
         mbar_init(&b[0], 1);
@@ -350,9 +357,11 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
             mbar_init(&b[1 + kAttnStages + i], 1);
         }
         const int sf = 1 + 2 * kAttnStages;
-        mbar_init(&b[sf], 1), mbar_init(&b[sf + 1], 1);          // s_full (tcgen05.commit)
-        mbar_init(&b[sf + 2], 8), mbar_init(&b[sf + 3], 8);      // p_full (8 softmax warps per tile)
-        for (int i = 0; i < 2; ++i) mbar_init(&b[sf + 4 + i], 1);   // o_full
+        for (int i = 0; i < NT; ++i) {
+            mbar_init(&b[sf + i], 1);       // s_full[t] (tcgen05.commit)
+            mbar_init(&b[sf + 4 + i], 8);   // p_full[t] (8 softmax warps per tile)
+            mbar_init(&b[sf + 8 + i], 1);   // o_full[t]
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == w_mma) tmem_alloc<1>(smem_u32(tslot), 512);
@@ -371,16 +380,16 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
             const int ntiles = (N + 127) / 128, heads = gridDim.y;
             const size_t base = ((size_t)t * heads + h) * ntiles * (128 * D);   // this (frame, head)
             const int qt = blockIdx.x * NT;
-            const uint32_t nq = (NT == 2 && qt + 1 < ntiles) ? 2 : 1;
+            const uint32_t nq = (uint32_t)min(NT, ntiles - qt);
             mbar_arrive_expect_tx_addr(q_full, nq * L::Q);
-            bulk_load(sb + L::off_q, qp + base + (size_t)qt * 128 * D, L::Q, q_full);
-            if (nq == 2) bulk_load(sb + L::off_q + L::Q, qp + base + (size_t)(qt + 1) * 128 * D, L::Q, q_full);
+            for (uint32_t i = 0; i < nq; ++i)
+                bulk_load(sb + L::off_q + i * L::Q, qp + base + (size_t)(qt + i) * 128 * D, L::Q, q_full);
             for (int j = 0; j < nkt; ++j) {
                 const int st = j % kAttnStages;
                 if (j >= kAttnStages) mbar_wait_addr(kv_empty + 8 * st, ((j / kAttnStages) - 1) & 1);
                 mbar_arrive_expect_tx_addr(kv_full + 8 * st, L::K + L::V);
-                bulk_load(sb + L::off_k + st * L::K, kp + base + (size_t)j * 128 * D, L::K, kv_full + 8 * st);
-                bulk_load(sb + L::off_v + st * L::V, vp + base + (size_t)j * 128 * D, L::V, kv_full + 8 * st);
+                bulk_load(sb + L::off_k + st * L::K, kp + base + (size_t)j * KT * D, L::K, kv_full + 8 * st);
+                bulk_load(sb + L::off_v + st * L::V, vp + base + (size_t)j * KT * D, L::V, kv_full + 8 * st);
             }
         }
     } else if (warp == w_mma) {
@@ -395,8 +404,8 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
                 for (int ks = 0; ks < D / 16; ++ks) {
                     if (dbg & 2) break;   // DVC_ATTN_DEBUG bit 1: no MMAs (pipeline-only timing)
                     const uint64_t ad = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(qa + ks * 4096, 2048);
-                    const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(ka + ks * 4096, 2048);
-                    tc_mma(tmem + tt * 128, ad, bd, idesc_s, ks > 0);
+                    const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(ka + ks * 2 * KT * 16, KT * 16);
+                    tc_mma(tmem + tt * KT, ad, bd, idesc_s, ks > 0);
                 }
                 tc_commit_addr(s_full + 8 * tt);
             };
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
                 const int st = j % kAttnStages;
                 const uint32_t va = sb + L::off_v + st * L::V;
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
+                for (int ks = 0; ks < KT / 16; ++ks) {
                     if (dbg & 2) break;
                     const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(va + ks * 2 * D * 16, D * 16);
                     tc_mma_ts(tmem + L::tm_o + tt * L::tm_o_step, tmem + L::tm_p + tt * L::tm_p_step + ks * 8, bd, idesc_o,
@@ -455,9 +464,9 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
         const uint32_t bar_id = 1 + tt * 4 + q4;
         float *red = reinterpret_cast<float *>(smem + L::off_red) + tt * 256;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-        const uint32_t tS = tmem + lane_off + tt * 128 + half * 64;
+        const uint32_t tS = tmem + lane_off + tt * KT + half * (KT / 2);
         const uint32_t tO = tmem + lane_off + L::tm_o + tt * L::tm_o_step;
-        const uint32_t tP = tmem + lane_off + L::tm_p + tt * L::tm_p_step + half * 32;
+        const uint32_t tP = tmem + lane_off + L::tm_p + tt * L::tm_p_step + half * (KT / 4);
         auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nkt; ++j) {
@@ -468,22 +477,24 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
                 if (lane == 0) mbar_arrive(p_full + 8 * tt);
                 continue;
             }
-            const int kvalid = N - j * 128 - half * 64;   // keys >= kvalid of this half are padding
-            uint32_t sr[64];
-            tmem_ld32_nowait(tS, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-            tmem_ld32_nowait(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-            tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-            tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-            if (kvalid < 64) {
+            constexpr int HK = KT / 2;   // keys of this thread's half row
+            const int kvalid = N - j * KT - half * HK;   // keys >= kvalid of this half are padding
+            uint32_t sr[HK];
 #pragma unroll
-                for (int i = 0; i < 64; ++i)
+            for (int c = 0; c < HK / 32; ++c)
+                tmem_ld32_nowait(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+#pragma unroll
+            for (int c = 0; c < HK / 32; ++c) tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+            if (kvalid < HK) {
+#pragma unroll
+                for (int i = 0; i < HK; ++i)
                     if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
             }
             float mxp[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) mxp[i] = fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[8 + i]));
 #pragma unroll
-            for (int i = 16; i < 64; i += 16)
+            for (int i = 16; i < HK; i += 16)
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     mxp[k] = fmaxf(mxp[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
@@ -517,7 +528,7 @@ __global__ void __launch_bounds__(AttnSmem<D>::THREADS, 1)
             float2 rsp[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
             const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {   // 32 keys -> 16 packed columns of P_t in TMEM
+            for (int c = 0; c < HK / 32; ++c) {   // 32 keys -> 16 packed columns of P_t in TMEM
                 uint32_t pk[16];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -588,13 +599,13 @@ static int attn_debug() {   // DVC_ATTN_DEBUG (experiments only): 1 = skip softm
     return v;
 }
 
-template <typename T, int D>
+template <typename T, int D, int KT = 128>
 static dvc_status attn_tc_launch(const void *qkv, void *ws, void *out, int T_, int N, int C, cudaStream_t stream) {
-    using L = AttnSmem<D>;
+    using L = AttnSmem<D, KT>;
     const int ntiles = (N + 127) / 128;
     const size_t plane = (size_t)T_ * C * ntiles * 128;   // elements of one packed operand
     T *qp = reinterpret_cast<T *>(ws), *kp = qp + plane, *vp = kp + plane;
-    DVC_CUDA(launch_pdl(qkv_pack_kernel<T, D>, dim3(ntiles, C / D, T_), dim3(256), 0, stream, 1,
+    DVC_CUDA(launch_pdl(qkv_pack_kernel<T, D, KT>, dim3(ntiles, C / D, T_), dim3(256), 0, stream, 1,
                         reinterpret_cast<const T *>(qkv), qp, kp, vp, N, C));
     ++g_launches;
     ProfSlot slot = prof_begin(stream);
@@ -603,8 +614,8 @@ static dvc_status attn_tc_launch(const void *qkv, void *ws, void *out, int T_, i
         const char *e = getenv("DVC_ATTN_POLY");
         npoly = e ? atoi(e) : DVC_ATTN_POLY;
     }
-    auto kfn = npoly == 0 ? attn_tc_kernel<T, D, 0> : npoly == 4 ? attn_tc_kernel<T, D, 4>
-             : attn_tc_kernel<T, D, 2>;
+    auto kfn = npoly == 0 ? attn_tc_kernel<T, D, 0, KT> : npoly == 4 ? attn_tc_kernel<T, D, 4, KT>
+             : attn_tc_kernel<T, D, 2, KT>;
     const void *kern = reinterpret_cast<const void *>(kfn);
     if (!smem_attr_ok(kern, L::bytes))
         DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes));
@@ -612,7 +623,7 @@ static dvc_status attn_tc_launch(const void *qkv, void *ws, void *out, int T_, i
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
     DVC_CUDA(launch_pdl(kfn, dim3((N + 128 * L::NT - 1) / (128 * L::NT), C / D, T_), dim3(L::THREADS), (size_t)L::bytes,
                         stream, 1, (const T *)qp, (const T *)kp, (const T *)vp, reinterpret_cast<T *>(out), N, C,
-                        scale_log2, make_idesc(bf, 128, 128), make_idesc(bf, 128, D), attn_debug()));
+                        scale_log2, make_idesc(bf, 128, KT), make_idesc(bf, 128, D), attn_debug()));
     ++g_launches;
     char lab[96];
     snprintf(lab, sizeof(lab), "attn_tc T=%d N=%d C=%d d=%d", T_, N, C, D);
