@@ -109,3 +109,25 @@ def test_vae_720p_frames_independent_and_deterministic(dvc):
     assert torch.equal(full, dvc.dvc_vae_decode(v, lat))
     assert torch.equal(dvc.dvc_vae_decode(v, lat[1:].contiguous())[0], full[1])
 
+
+
+@pytest.mark.slow
+def test_1080p_sizes_no_index_overflow(dvc):
+    # 1080p latents (135x240): level-3 VAE tensors of 8 frames exceed 2^31 bytes; batched == per-frame /
+    # chunked bit for bit for the VAE decoder and the full U-Net (32-bit index overflow would break it)
+    dt, h, w = torch.bfloat16, 135, 240
+    vae = dvc.VAE(dvc.pack_weights(synthgen.vae_weights(), dt), dtype=dt, h=h, w=w, max_T=8)
+    lat, _ = dev(synthgen.normal((8, h, w, 256), 7), dt)
+    fr = dvc.dvc_vae_decode(vae, lat)
+    assert torch.isfinite(fr.float()).all()
+    assert torch.equal(dvc.dvc_vae_decode(vae, lat[7:].contiguous())[0], fr[7])
+    del fr
+    W = (240, 480, 960, 960)
+    net = dvc.UNet(dvc.unet_config(W, 256, 256, 24, 8, 1e-5, dt, h, w, 4, head_dim=48),
+                   dvc.pack_weights(synthgen.unet_weights(W, attention=True), dt))
+    ctx, _ = dev(synthgen.normal((4, h, w, 256), 5), dt)
+    full = dvc.dvc_unet_decode_gop(net, lat[:4].contiguous(), ctx)
+    co = torch.empty(net.carry_elems, dtype=dt, device="cuda")
+    a = dvc.dvc_unet_decode_gop(net, lat[:3].contiguous(), ctx[:3].contiguous(), carry_out=co)
+    b = dvc.dvc_unet_decode_gop(net, lat[3:4].contiguous(), ctx[3:].contiguous(), carry_in=co)
+    assert torch.isfinite(full.float()).all() and torch.equal(torch.cat([a, b]), full)
