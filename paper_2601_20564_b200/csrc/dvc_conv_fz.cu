@@ -689,8 +689,13 @@ static int fz_off_from_env() {   // DVC_NO_FZ=1: never use the fused engine (A/B
     return e && e[0] == '1';
 }
 static const int g_fz_off = fz_off_from_env();
+static int fz_min_h_from_env() {   // DVC_FZ_MIN_H: smallest frame height on the fused engine (A/B experiments)
+    const char *e = getenv("DVC_FZ_MIN_H");
+    return e ? atoi(e) : 32;
+}
+static const int g_fz_min_h = fz_min_h_from_env();
 bool conv_fz_applicable(int H, int W, dvc_dtype dt) {
-    return !g_fz_off && g_ws_cg == 2 && dt != DVC_F32 && H >= 32 && W >= 8;
+    return !g_fz_off && g_ws_cg == 2 && dt != DVC_F32 && H >= g_fz_min_h && W >= 8;
 }
 
 static int g_fz_sms = 0;
