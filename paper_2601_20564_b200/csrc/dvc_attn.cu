@@ -281,29 +281,19 @@ struct AttnSmem {
     static constexpr int tm_p = NT == 3 ? 192 : NT == 2 ? 384 : 128, tm_p_step = KT / 2;
 };
 
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
 __device__ __forceinline__ float ex2f(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// 2^x on the FMA pipe (x <= 0 here): round-to-nearest split x = j + f, f in [-1/2, 1/2], a
+// 2^x on the FMA pipe (x <= 8 here, lazy maximum): round-to-nearest split x = j + f, f in [-1/2, 1/2], a
 // degree-3 fit of 2^f (max relative error 7.5e-5, below the 16-bit rounding of P) and j added
 // to the exponent field.  Used for part of every 8-score group so the MUFU ex2 unit (the bound of
 // a head_dim-48 softmax: 192 MMA FLOP per exponential) shares the work with the FMA pipe.
 #ifndef DVC_ATTN_POLY
-#define DVC_ATTN_POLY 2   // scores per 8 computed by ex2_poly (even: packed pairs)
+#define DVC_ATTN_POLY 2   // scores per 8 computed by ex2_poly2 (even: packed pairs)
 #endif
-__device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -126.f);
-    const float r = x + 12582912.f;   // 1.5 * 2^23: the integer nearest x lands in the low mantissa bits
-    const float f = x - (r - 12582912.f);
-    const float p = fmaf(fmaf(fmaf(0.055172063f, f, 0.24261240f), f, 0.69326103f), f, 0.99992794f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
-}
-// two lanes of ex2_poly with packed fp32x2 adds / FMAs
+// two lanes at a time with packed fp32x2 adds / FMAs (FADD2 / FFMA2)
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
     x.x = fmaxf(x.x, -126.f);
     x.y = fmaxf(x.y, -126.f);
