@@ -99,6 +99,18 @@ __device__ __forceinline__ float fz_ex2(float u) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(u));
     return e;
 }
+// SiLU(z) = z * sigmoid(z) = hz + hz * tanh(hz) with hz = z / 2: ONE MUFU op (tanh.approx,
+// max rel. error 2^-11) and two FMAs per element, from an affine pre-scaled by 1/2.  The MUFU
+// count is what bounds the in-place transform when a convolution has few output channels (the VAE
+// decoder's 64-channel full-resolution convs: 2 MUFU ops per input element outran the MMAs).
+#ifndef FZ_SILU_TANH
+#define FZ_SILU_TANH 1
+#endif
+__device__ __forceinline__ float fz_tanh(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float fz_rcp(float d) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
@@ -386,8 +398,10 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                             for (int i = 0; i < 8; ++i) sc[i] = 1.f, sh[i] = 0.f;
                         }
 #pragma unroll
-                        for (int i = 0; i < 8; ++i)
+                        for (int i = 0; i < 8; ++i) {
+                            if constexpr (FZ_SILU_TANH) sc[i] *= 0.5f, sh[i] *= 0.5f;   // hz = z / 2
                             sc2[i] = sc[i] * -1.4426950408889634f, sh2[i] = sh[i] * -1.4426950408889634f;
+                        }
                         // a group straddling C_in/P: its first nprev channels come from the side buffer.
                         // C_in/P is even (C_in % 16 == 0): merge per 32-bit word.
                         const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
@@ -431,7 +445,10 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                                     Pk<T>::unpack(wv[k0 + k][j], v0, v1);
                                     z[k][2 * j] = fmaf(v0, sc[2 * j], sh[2 * j]);
                                     z[k][2 * j + 1] = fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]);
-                                    if constexpr (FZ_TFW == 16) {   // register budget: u = -z log2(e) from z
+                                    if constexpr (FZ_SILU_TANH) {   // z holds hz = z / 2; e = tanh(hz)
+                                        e[k][2 * j] = fz_tanh(z[k][2 * j]);
+                                        e[k][2 * j + 1] = fz_tanh(z[k][2 * j + 1]);
+                                    } else if constexpr (FZ_TFW == 16) {   // register budget: u = -z log2(e) from z
                                         e[k][2 * j] = fz_ex2(z[k][2 * j] * -1.4426950408889634f);
                                         e[k][2 * j + 1] = fz_ex2(z[k][2 * j + 1] * -1.4426950408889634f);
                                     } else {
@@ -450,8 +467,14 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                                 uint32_t o[4];
 #pragma unroll
                                 for (int j = 0; j < 4; ++j) {
-                                    const float h0 = z[k][2 * j] * fz_rcp(1.0f + e[k][2 * j]);
-                                    const float h1 = z[k][2 * j + 1] * fz_rcp(1.0f + e[k][2 * j + 1]);
+                                    float h0, h1;
+                                    if constexpr (FZ_SILU_TANH) {
+                                        h0 = fmaf(z[k][2 * j], e[k][2 * j], z[k][2 * j]);
+                                        h1 = fmaf(z[k][2 * j + 1], e[k][2 * j + 1], z[k][2 * j + 1]);
+                                    } else {
+                                        h0 = z[k][2 * j] * fz_rcp(1.0f + e[k][2 * j]);
+                                        h1 = z[k][2 * j + 1] * fz_rcp(1.0f + e[k][2 * j + 1]);
+                                    }
                                     o[j] = live ? Pk<T>::pack(h0, h1) : 0u;
                                 }
                                 *reinterpret_cast<uint4 *>(slot + roff(r)) = make_uint4(o[0], o[1], o[2], o[3]);
