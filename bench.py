@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--attention", action="store_true",
+                    help="f1: the full U-Net (22 ResBlocks + 16 Transformer2D blocks, head_dim 48) instead of the "
+                         "ResBlock skeleton the north star names (not the headline workload)")
     return ap.parse_args()
 
 
@@ -250,8 +253,8 @@ def run_ours(args):
     h, w = H // S, W // S
 
     # weights (replicated), inputs of this rank's chunk
-    named = synthgen.unet_weights(WIDTH, C_LAT, C_CTX)
-    cfg = dvc.unet_config(WIDTH, C_LAT, C_CTX, G, P, 1e-5, dtype, h, w, T)
+    named = synthgen.unet_weights(WIDTH, C_LAT, C_CTX, attention=args.attention)
+    cfg = dvc.unet_config(WIDTH, C_LAT, C_CTX, G, P, 1e-5, dtype, h, w, T, head_dim=48 if args.attention else 0)
     net = dvc.UNet(cfg, dvc.pack_weights(named, dtype))
     we, be = synthgen.expansion_weights()
     w_exp = torch.from_numpy(we).to(dtype).cuda()
@@ -289,7 +292,7 @@ def run_ours(args):
 
     # ---- device-resident timed region
     launches0 = dvc.launch_count()
-    dvc.profile_begin(200 * args.steps + 64)
+    dvc.profile_begin((800 if args.attention else 200) * args.steps + 64)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -299,9 +302,16 @@ def run_ours(args):
         ev1.record(stream)
         barrier()
     conv_ms, conv_flops, conv_n = dvc.profile_end()
+    attn_ms = attn_flops = 0.0
+    if args.attention:   # the attention launches (aux records with their algorithmic FLOPs)
+        for lab, kms, fl in dvc.profile_records():
+            if lab.startswith("attn_tc"):
+                attn_ms += kms
+                attn_flops += fl
     launches = dvc.launch_count() - launches0
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     conv_ms = max_over_ranks(conv_ms)
+    attn_ms = max_over_ranks(attn_ms)
     total_frames = T * world * args.steps
     value = total_frames / (ms / 1e3)
 
@@ -367,8 +377,10 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded frames / N(0,1) context, R19 init weights)",
-        "config": {"workload": f"720p GOP decode: encode (unshuffle+expansion) + pruned U-Net ResBlock skeleton, "
-                               f"{T} frames per GPU on the batch dim" + (f", chain of {T * world} frames in "
+        "config": {"workload": f"720p GOP decode: encode (unshuffle+expansion) + "
+                               + ("full pruned U-Net (22 ResBlocks + 16 Transformer2D), " if args.attention
+                                  else "pruned U-Net ResBlock skeleton, ")
+                               + f"{T} frames per GPU on the batch dim" + (f", chain of {T * world} frames in "
                                                                          f"{world} contiguous chunks + NCCL halo"
                                                                          if world > 1 else ""),
                    "latent": f"{h}x{w}", "frames_per_gpu": T, "widths": list(WIDTH), "groups": G, "shift_p": P,
@@ -382,6 +394,14 @@ def run_ours(args):
                      "conv_share_of_step": conv_ms / ms, "peak_source": peak_src},
         "clocks": clk.summary(),
     }
+    if args.attention:   # the dominant kernel of the full U-Net is the attention
+        aach = max(attn_ms, 1e-9)
+        line["roofline_conv"] = dict(line["roofline"], traffic=None)   # traffic.json is the skeleton's
+        line["roofline"] = {"bound": "tensor", "achieved": attn_flops / (aach / 1e3) / 1e12, "peak": peak,
+                            "unit": "TFLOP/s", "frac": attn_flops / (aach / 1e3) / 1e12 / peak, "traffic": None,
+                            "kernel": "attn_tc_kernel (all attention launches of the step, summed; 4*N^2*C per frame)",
+                            "attn_ms_per_step": aach / args.steps, "attn_share_of_step": aach / ms,
+                            "peak_source": peak_src}
     if e2e:
         line["e2e"] = e2e
     if not args.no_cpu_baseline:
