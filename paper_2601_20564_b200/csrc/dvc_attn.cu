@@ -41,19 +41,30 @@ __global__ void __launch_bounds__(256) gn_affine_kernel(const T *__restrict__ x,
                                                         T *__restrict__ y, int HW, int C, long total8) {
     griddep_wait();
     const int c8 = C / 8;
-    for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total8; i += (long)gridDim.x * blockDim.x) {
-        const long pix = i / c8;
-        const int c = (int)(i - pix * c8) * 8;
-        const int t = (int)(pix / HW);
-        float f[8];
-        load8(x + pix * C + c, f);
-        const float2 *cf = coef + (size_t)t * C + c;
+    const long stride = (long)gridDim.x * blockDim.x;
+    // four independent 16-byte loads in flight per thread per round (the pass is HBM-bound)
+    for (long i0 = blockIdx.x * (long)blockDim.x + threadIdx.x; i0 < total8; i0 += 4 * stride) {
+        float f[4][8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float2 s = cf[k];
-            f[k] = fmaf(f[k], s.x, s.y);
+        for (int u = 0; u < 4; ++u) {
+            const long i = i0 + u * stride;
+            if (i < total8) load8(x + (i / c8) * C + (int)(i % c8) * 8, f[u]);
         }
-        store8(y + pix * C + c, f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long i = i0 + u * stride;
+            if (i >= total8) break;
+            const long pix = i / c8;
+            const int c = (int)(i - pix * c8) * 8;
+            const float4 *cf = reinterpret_cast<const float4 *>(coef + (size_t)(pix / HW) * C + c);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float4 s = __ldg(cf + k);   // (scale, shift) of channels c+2k, c+2k+1
+                f[u][2 * k] = fmaf(f[u][2 * k], s.x, s.y);
+                f[u][2 * k + 1] = fmaf(f[u][2 * k + 1], s.z, s.w);
+            }
+            store8(y + pix * C + c, f[u]);
+        }
     }
     griddep_launch();
 }
