@@ -2,21 +2,26 @@
 """Benchmark of the DiffVC-RT decode hot path on B200 (metric of BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scaling strong|weak] [--transport p2p|nccl] [--attention]
 
-Workload: 720p, frames of one chain packed on the batch
-dimension, `--frames` (default 32 = the paper's intra period) frames per
-GPU.  One step = the whole hot path over one batch:
+Workload: 720p, one GOP of `--frames` (default 32 = the paper's intra
+period) frames packed on the batch dimension.  One step = the whole hot path:
   a1+a2  dvc_encode_pixelunshuffle: frames [T,3,720,1280] -> Lbar [T,90,160,256]
-         (PixelUnshuffle + Latent Channel Expansion; the encoded latent stands in
-         for the compressor's reconstruction Lbar, which is out of scope)
+         (PixelUnshuffle + Latent Channel Expansion; the encoded latent stands in for the
+         compressor's reconstruction Lbar, which is out of scope)
   a3-a10 dvc_unet_decode_gop: concat(Lbar, C^m) -> 22 OTSM ResBlocks + glue -> Lhat
-With N GPUs (torchrun) the chain has N*T frames in contiguous chunks, one per
-rank, and every ResBlock's shifted slice moves rank r -> r+1 over NCCL (weak
-scaling: per-GPU work fixed).  Synthetic seeded inputs and random-init weights
-of the paper's shapes (synthgen).  Inputs per step (472 MB) exceed the 126 MB L2.
+         (the 16 Transformer2D blocks are elided -- the north star's ResBlock skeleton; the full
+         U-Net is `--attention`; the VAE decoder (f2) is not part of this metric)
+Multi-GPU (row e): `--scaling strong` (default) splits the ONE 32-frame GOP into N
+contiguous chunks (32/16/8/4 frames per rank) and every ResBlock's shifted slice moves rank r ->
+r+1 (P2P copy-engine halo, or NCCL with --transport nccl); `--scaling weak` runs one independent
+GOP per GPU (replicas, no exchange).  With --gpus N > 1 and no torchrun environment, bench.py
+re-launches itself under torch.distributed.run with N ranks (127.0.0.1).
+Synthetic seeded inputs and random-init weights of the paper's shapes (synthgen).  Inputs per
+step (472 MB at N=1) exceed the 126 MB L2.
 
---impl reference times the fp64 CPU oracle (this tier's reference arm) on a
-bounded sample of the same workload; see DESIGN.md section 7.
+--impl reference times the fp64 CPU oracle (this tier's reference arm) on a bounded sample of
+the same workload; see DESIGN.md section 6.
 """
 from __future__ import annotations
 
@@ -50,6 +55,11 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: one GOP split over the ranks (halo per ResBlock); weak: one GOP per GPU")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"], help="halo transport (strong, N>1)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch/rendezvous check only: every rank joins a gloo group, rank 0 prints the ranks")
     ap.add_argument("--attention", action="store_true",
                     help="f1: the full U-Net (22 ResBlocks + 16 Transformer2D blocks, head_dim 48) instead of the "
                          "ResBlock skeleton the north star names (not the headline workload)")
@@ -65,44 +75,52 @@ def dist_env():
 
 # ------------------------------------------------------------------ clocks during the timed region
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+    """SM clock and clock-event reasons of this rank's GPU, polled every ~10 ms by NVML in a thread
+    while the timed region runs (nvidia-smi at 200 ms saw one sample of a 0.5 s region)."""
+    REASONS = (("sw_power_cap", 0x4), ("hw_slowdown", 0x8), ("sw_thermal_slowdown", 0x20),
+               ("hw_thermal_slowdown", 0x40), ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+    def __init__(self, local: int):
+        self.local, self.rows, self.stop, self.h, self.max_mhz = local, [], threading.Event(), None, None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            try:
+                self.h = nv.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(self.local).uuid))
+            except Exception:
+                self.h = nv.nvmlDeviceGetHandleByIndex(self.local)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.nv = nv
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:
+            self.h = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _poll(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                  nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                pass
+            time.sleep(0.01)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.h is not None:
+            self.t.join(timeout=2)
 
     def summary(self):
-        rows = [r for r in self.rows if len(r) == 6 and r[0].isdigit()]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [int(r[0]) for r in rows]
-        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
-                "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        reasons = sorted({n for _, m in self.rows for n, bit in self.REASONS if m & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 10 ms polling"}
 
 
 # ------------------------------------------------------------------ algorithmic work
@@ -194,6 +212,20 @@ def oracle_inputs():
     return frames, ctx, wts, (we.astype(np.float64), be.astype(np.float64))
 
 
+def host_cpu():
+    """CPU model and the cores this process may run on (the oracle's OpenMP threads use them)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "affinity_cores": len(os.sched_getaffinity(0)), "os_cpu_count": os.cpu_count()}
+
+
 def cpu_baseline():
     import oracle
     frames, ctx, wts, wexp = oracle_inputs()
@@ -203,13 +235,15 @@ def cpu_baseline():
     return {"value": fps, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
             "sample": (f"fp64 C oracle (OpenMP) on 1 frame of the workload: encode + conv_in + down0.r0 + "
                        f"down0.r1 = {fl / 1e9:.1f} GFLOP in {secs:.1f} s; frames/s extrapolated by the "
-                       f"skeleton's {per_frame / 1e9:.1f} GFLOP/frame")}
+                       f"skeleton's {per_frame / 1e9:.1f} GFLOP/frame"), **host_cpu()}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    # torchrun exports OMP_NUM_THREADS=1; the oracle uses every core this process may run on
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     import oracle
     oracle.build()
     frames, ctx, wts, wexp = oracle_inputs()
@@ -224,20 +258,48 @@ def run_reference(args):
     fps = (fl / per_frame) * args.steps / tot
     line = {"metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "720p GOP decode (bounded oracle sample per step)", "latent": "90x160",
-                       "frames_per_gpu": args.frames},
+            "config": dict(workload_config(args, world),
+                           sample="bounded oracle sample per step (1 frame: encode + conv_in + 2 ResBlocks)"),
             "cpu_baseline": {"value": fps, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                              "sample": "per step: 1 frame, encode + conv_in + down0.r0 + down0.r1 "
-                                       f"({fl / 1e9:.1f} GFLOP), extrapolated by GFLOP/frame"},
+                                       f"({fl / 1e9:.1f} GFLOP), extrapolated by GFLOP/frame", **host_cpu()},
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
+def frames_of_rank(args, world, rank):
+    """(t0, t1) of this rank's frames in the step's chain: strong = one GOP of args.frames split in
+    contiguous chunks (remainder to the last ranks, R18); weak = a whole GOP per rank."""
+    if args.scaling == "weak":
+        return 0, args.frames
+    base, rem = divmod(args.frames, world)
+    sizes = [base + (1 if r >= world - rem else 0) for r in range(world)]
+    return sum(sizes[:rank]), sum(sizes[:rank + 1])
+
+
+def workload_config(args, world):
+    T_local = frames_of_rank(args, world, 0)[1] - frames_of_rank(args, world, 0)[0]
+    body = ("full pruned U-Net (22 ResBlocks + 16 Transformer2D)" if args.attention else
+            "pruned U-Net ResBlock skeleton (16 Transformer2D blocks elided; no VAE decoder)")
+    if args.scaling == "strong":
+        split = (f"one {args.frames}-frame GOP split into {world} contiguous chunks "
+                 f"({'/'.join(str(b - a) for a, b in (frames_of_rank(args, world, r) for r in range(world)))} "
+                 f"frames per rank) with a per-ResBlock {args.transport.upper()} halo" if world > 1
+                 else f"one {args.frames}-frame GOP on the batch dim")
+    else:
+        split = f"one independent {args.frames}-frame GOP per GPU ({world} replicas, no exchange)"
+    return {"workload": f"720p GOP decode: encode (unshuffle+expansion) + {body}; {split}",
+            "latent": "90x160", "gop_frames": args.frames, "frames_per_gpu": T_local, "widths": list(WIDTH),
+            "groups": G, "shift_p": P,
+            "parallelism": (f"frame-chunk x{world}" + (f" + {args.transport} halo" if world > 1 and
+                                                        args.scaling == "strong" else "")),
+            "l2": "inputs larger than L2 (472 MB frames+context per 32-frame GOP)"}
+
+
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -249,25 +311,29 @@ def run_ours(args):
     import paper_2601_20564_b200 as dvc
     dvc.device_check(local)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float16
-    T = args.frames
+    t0, t1 = frames_of_rank(args, world, rank)
+    T = t1 - t0
+    T_max = frames_of_rank(args, world, world - 1)[1] - frames_of_rank(args, world, world - 1)[0]
     h, w = H // S, W // S
 
-    # weights (replicated), inputs of this rank's chunk
+    # weights (replicated), inputs of this rank's frames (strong: slices of one GOP; weak: own GOP)
     named = synthgen.unet_weights(WIDTH, C_LAT, C_CTX, attention=args.attention)
-    cfg = dvc.unet_config(WIDTH, C_LAT, C_CTX, G, P, 1e-5, dtype, h, w, T, head_dim=48 if args.attention else 0)
+    cfg = dvc.unet_config(WIDTH, C_LAT, C_CTX, G, P, 1e-5, dtype, h, w, T_max, head_dim=48 if args.attention else 0)
     net = dvc.UNet(cfg, dvc.pack_weights(named, dtype))
     we, be = synthgen.expansion_weights()
     w_exp = torch.from_numpy(we).to(dtype).cuda()
     b_exp = torch.from_numpy(be).to(dtype).cuda()
-    seed = 100 + rank
-    frames_h = torch.from_numpy(synthgen.frames(T, H, W, seed=seed)).to(dtype).pin_memory()
-    ctx_h = torch.from_numpy(synthgen.normal((T, h, w, C_CTX), seed=seed + 1000)).to(dtype).pin_memory()
+    gop = 0 if args.scaling == "strong" else rank
+    frames_h = torch.from_numpy(synthgen.frames(args.frames, H, W, seed=100 + gop)[t0:t1]).to(dtype).pin_memory()
+    ctx_h = torch.from_numpy(synthgen.normal((args.frames, h, w, C_CTX), seed=1100 + gop)[t0:t1]).to(dtype).pin_memory()
     frames = frames_h.cuda()
     ctx = ctx_h.cuda()
     lat = torch.empty((T, h, w, C_LAT), dtype=dtype, device="cuda")
     out = torch.empty((T, h, w, C_LAT), dtype=dtype, device="cuda")
     ws = torch.empty(net.workspace_size(T), dtype=torch.uint8, device="cuda")
-    comm = dvc.Comm(rank, world) if world > 1 else None
+    comm = None
+    if world > 1 and args.scaling == "strong":
+        comm = dvc.Comm(rank, world, net, transport=args.transport)
     stream = torch.cuda.current_stream()
 
     def step(frames_d, ctx_d, out_d):
@@ -290,9 +356,8 @@ def run_ours(args):
         step(frames, ctx, out)
     barrier()
 
-    # ---- device-resident timed region
+    # ---- device-resident timed region (no instrumentation inside it)
     launches0 = dvc.launch_count()
-    dvc.profile_begin((800 if args.attention else 200) * args.steps + 64)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -301,6 +366,18 @@ def run_ours(args):
             step(frames, ctx, out)
         ev1.record(stream)
         barrier()
+    launches = dvc.launch_count() - launches0
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    total_frames = (args.frames if args.scaling == "strong" else args.frames * world) * args.steps
+    value = total_frames / (ms / 1e3)
+
+    # ---- profile pass (separate, same K steps): every conv / attention launch bracketed by events on
+    # its own stream (dvc_profile_begin/end) -> the roofline's achieved rate
+    barrier()
+    dvc.profile_begin((800 if args.attention else 200) * args.steps + 64)
+    for _ in range(args.steps):
+        step(frames, ctx, out)
+    barrier()
     conv_ms, conv_flops, conv_n = dvc.profile_end()
     attn_ms = attn_flops = 0.0
     if args.attention:   # the attention launches (aux records with their algorithmic FLOPs)
@@ -308,12 +385,8 @@ def run_ours(args):
             if lab.startswith("attn_tc"):
                 attn_ms += kms
                 attn_flops += fl
-    launches = dvc.launch_count() - launches0
-    ms = max_over_ranks(ev0.elapsed_time(ev1))
     conv_ms = max_over_ranks(conv_ms)
     attn_ms = max_over_ranks(attn_ms)
-    total_frames = T * world * args.steps
-    value = total_frames / (ms / 1e3)
 
     # ---- end to end through the public API with host buffers (H2D inputs, D2H result).
     # Every step copies its frames + context H2D from pinned memory and its result L-hat
@@ -362,34 +435,30 @@ def run_ours(args):
         e2e_ms = max_over_ranks(e0.elapsed_time(e1))
         assert torch.isfinite(out_h[0].float()).all()
         e2e = {"value": total_frames / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": frames_h.numel() * frames_h.element_size() + ctx_h.numel() * ctx_h.element_size(),
-               "d2h_bytes_per_step": out_h[0].numel() * out_h[0].element_size(),
+               "h2d_bytes_per_step": world * (frames_h.numel() * frames_h.element_size()
+                                              + ctx_h.numel() * ctx_h.element_size()),
+               "d2h_bytes_per_step": world * out_h[0].numel() * out_h[0].element_size(),
                "overlap": "H2D of step i+1 and D2H of step i-1 overlap step i (2 copy streams, double buffers)"}
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        if comm is not None:
+            comm.close()
+        dist.destroy_process_group()
         return
     peak, peak_src = load_peaks()
     achieved = conv_flops / (conv_ms / 1e3) / 1e12
     traffic = load_traffic()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded frames / N(0,1) context, R19 init weights)",
-        "config": {"workload": f"720p GOP decode: encode (unshuffle+expansion) + "
-                               + ("full pruned U-Net (22 ResBlocks + 16 Transformer2D), " if args.attention
-                                  else "pruned U-Net ResBlock skeleton, ")
-                               + f"{T} frames per GPU on the batch dim" + (f", chain of {T * world} frames in "
-                                                                         f"{world} contiguous chunks + NCCL halo"
-                                                                         if world > 1 else ""),
-                   "latent": f"{h}x{w}", "frames_per_gpu": T, "widths": list(WIDTH), "groups": G, "shift_p": P,
-                   "parallelism": f"frame-chunk x{world}" + (" + NCCL halo" if world > 1 else ""),
-                   "l2": "inputs larger than L2 (472 MB frames+context per step)"},
+        "config": workload_config(args, world),
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None if traffic is None else traffic.get("bytes_per_step"),
-                     "kernel": "conv_fz_kernel + conv_ws_kernel + conv_tc_kernel (all convolution launches of the step, summed)",
+                     "frac": achieved / peak,
+                     "traffic": None if (traffic is None or world > 1) else traffic.get("bytes_per_step"),
+                     "kernel": "conv_fz_kernel + conv_ws_kernel + conv_tc_kernel (all convolution launches of the "
+                               "step, summed; rank 0; measured in a separate instrumented pass)",
                      "conv_ms_per_step": conv_ms / args.steps, "conv_launches_per_step": conv_n / args.steps,
                      "conv_share_of_step": conv_ms / ms, "peak_source": peak_src},
         "clocks": clk.summary(),
@@ -404,16 +473,58 @@ def run_ours(args):
                             "peak_source": peak_src}
     if e2e:
         line["e2e"] = e2e
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
 
+def dry_run(args):
+    """--dry-run: the multi-rank launch and rendezvous only (gloo, CPU): every rank joins, rank 0
+    prints which ranks exist and the frame chunks they would decode."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    dist.init_process_group("gloo")
+    t = torch.tensor([rank], dtype=torch.int64)
+    gathered = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(gathered, t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": [int(g.item()) for g in gathered],
+                          "chunks": [list(frames_of_rank(args, world, r)) for r in range(world)],
+                          "scaling": args.scaling}), flush=True)
+    dist.destroy_process_group()
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: re-exec this script under torch.distributed.run with N ranks."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    if not args.dry_run:   # NCCL's init lines (rank / transport evidence) go to stderr, the JSON to stdout
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    knobs = sorted(k for k in os.environ if k.startswith("DVC_"))
+    if knobs:   # experiment knobs / alternative libraries never reach a bench number
+        sys.exit(f"bench.py refuses to run with {', '.join(knobs)} set (experiment builds only)")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if args.dry_run:
+        dry_run(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

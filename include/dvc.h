@@ -99,7 +99,9 @@ DVC_API dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype dt, i
  * G | C_out; c_a, c_b, C_out multiples of 16 on the tensor-core path (16-bit)
  * and of 8 in F32; T >= 1.
  * carry_in: [H,W,C_in/P] or NULL (= zeros: chain start, R8).
- * carry_out: [H,W,C_in/P] or NULL.  y: [T,H,W,C_out]; must not alias inputs.
+ * carry_out: [H,W,C_in/P] or NULL; may equal carry_in (in-place carry update: it is
+ *            written after every read of carry_in), must not overlap it otherwise.
+ * y: [T,H,W,C_out]; must not alias inputs.
  * workspace: device scratch of at least dvc_resblock_workspace_size() bytes,
  * 256-byte aligned.
  * ------------------------------------------------------------------------ */
@@ -223,8 +225,9 @@ DVC_API dvc_status dvc_unet_workspace_size(const dvc_unet *n, int T_local, size_
  *             With comm and rank > 0 the carry comes from rank-1 instead.
  *   carry_out packed carry of the last frame, or NULL.  With comm, only the
  *             last rank writes it.
- *   comm      NULL = single GPU; else the halo of every ResBlock moves over
- *             NCCL from rank r to rank r+1 (contiguous frame chunks). */
+ *   comm      NULL = single GPU; else the halo of every ResBlock moves from
+ *             rank r to rank r+1 (contiguous frame chunks) over the
+ *             communicator's transport (P2P peer copies or NCCL, see below). */
 DVC_API dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, const void *ctx,
                                int T_local, const void *carry_in, void *carry_out, void *out,
                                void *workspace, size_t ws_bytes, void *stream);
@@ -323,9 +326,33 @@ DVC_API dvc_status dvc_quantize_e4m3(const void *x, dvc_dtype dt, size_t n, floa
 DVC_API dvc_status dvc_conv_fp8(const void *x8, float sx, const void *w8, float sw, const void *bias, int T, int H,
                                 int W, int cin, int cout, int taps, dvc_dtype out_dt, void *y, void *stream);
 
-/* Multi-GPU halo communicator (NCCL, loaded at run time from the process's
- * libnccl.so.2).  id128: 128-byte ncclUniqueId, created on rank 0 and
- * broadcast by the caller (e.g. torch.distributed). */
+/* Multi-GPU halo communicators (row e: SURVEY 8e; "passes the partial channels of the last
+ * sample ... to the subsequent batch").  Rank r of `world` decodes frames [t0_r, t0_r + T_local) of one
+ * chain (contiguous chunks); before ResBlock k it sends the C_in/P-channel slice of its last frame's
+ * block input to rank r+1 and receives rank r-1's slice as the carry of its first frame.  The send runs
+ * on the communicator's own (high-priority) stream and overlaps block k; only the receive is on the
+ * compute stream's critical path.  A communicator is bound to the device current at creation, is
+ * single-owner, and every rank must make the same sequence of dvc_unet_decode_gop calls.
+ *
+ * P2P transport (the default of the Python binding): each rank owns a receive region (two epoch slots
+ * of carry_bytes, arrival flags, acknowledgement words) allocated here.  The sender writes its slice
+ * directly into the successor's slot with a copy-engine peer copy (NVLink; no SM, no staging) and
+ * raises the successor's flag with a stream memory write; the receiver's stream waits on the flag
+ * (cuStreamWaitValue32: the stream front end blocks, no kernel spins).  carry_bytes = carry elements
+ * (dvc_unet_carry_size) x element size.  Connect every rank before its first decode:
+ *   - ranks in different processes: exchange the 64-byte dvc_comm_ipc_handle of every rank (e.g.
+ *     torch.distributed.all_gather_object) and call dvc_comm_connect_ipc(c, handle of rank+1 or NULL
+ *     on the last rank, handle of rank-1 or NULL on rank 0);
+ *   - ranks of one process (one GPU, the tests' loopback): dvc_comm_connect_local(c, next, prev).
+ * Errors: DVC_ERR_ARG (wrong neighbours, already connected), DVC_ERR_CUDA (IPC / allocation),
+ * DVC_ERR_UNSUPPORTED (no stream memory operations). */
+DVC_API dvc_status dvc_comm_create_p2p(int rank, int world, size_t carry_bytes, dvc_comm **out);
+DVC_API dvc_status dvc_comm_ipc_handle(const dvc_comm *c, void *handle64);
+DVC_API dvc_status dvc_comm_connect_ipc(dvc_comm *c, const void *next_handle64, const void *prev_handle64);
+DVC_API dvc_status dvc_comm_connect_local(dvc_comm *c, const dvc_comm *next, const dvc_comm *prev);
+/* NCCL transport (loaded at run time from the process's libnccl.so.2): the slice is staged in the
+ * decode workspace and moved by ncclSend/ncclRecv in one group on the comm stream.  id128: 128-byte
+ * ncclUniqueId, created on rank 0 and broadcast by the caller (e.g. torch.distributed). */
 DVC_API dvc_status dvc_comm_unique_id(void *id128);
 DVC_API dvc_status dvc_comm_create(int rank, int world, const void *id128, dvc_comm **out);
 DVC_API dvc_status dvc_comm_destroy(dvc_comm *c);

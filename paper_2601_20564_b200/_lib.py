@@ -111,6 +111,10 @@ _SIGS = {
     "dvc_comm_unique_id": ([c_void_p], c_int),
     "dvc_comm_create": ([c_int, c_int, c_void_p, ctypes.POINTER(c_void_p)], c_int),
     "dvc_comm_destroy": ([c_void_p], c_int),
+    "dvc_comm_create_p2p": ([c_int, c_int, c_size_t, ctypes.POINTER(c_void_p)], c_int),
+    "dvc_comm_ipc_handle": ([c_void_p, c_void_p], c_int),
+    "dvc_comm_connect_ipc": ([c_void_p, c_void_p, c_void_p], c_int),
+    "dvc_comm_connect_local": ([c_void_p, c_void_p, c_void_p], c_int),
 }
 
 EXPORTS = tuple(_SIGS)

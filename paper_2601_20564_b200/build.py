@@ -1,6 +1,10 @@
 """Build libdvc.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
     python -m paper_2601_20564_b200.build [--force]
+    python -m paper_2601_20564_b200.build --experiments OUT.so   # A/B build: honours DVC_* knobs
+
+The product library ignores every DVC_* environment variable; only an --experiments build
+(-DDVC_EXPERIMENTS, written elsewhere than libdvc.so) reads the timing/debug knobs.
 """
 from __future__ import annotations
 
@@ -35,25 +39,29 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, jobs: int = 8, experiments: str | None = None) -> str:
+    so = SO
+    extra = []
+    if experiments:
+        so, extra = os.path.abspath(experiments), ["-DDVC_EXPERIMENTS"]
+    elif not force and not _stale():
         return SO
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_exp" if experiments else "build")
     os.makedirs(objdir, exist_ok=True)
     objs, procs = [], []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
-        cmd = [nvcc, *NVCC_FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-dc" if False else "-c", src, "-o", obj]
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-Xptxas", "-v" if verbose else "-O3", "-dc" if False else "-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         if len(procs) >= jobs:
             _drain(procs, verbose)
     _drain(procs, verbose)
-    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", SO + ".tmp", *objs, "-ldl"]
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", so + ".tmp", *objs, "-ldl"]
     subprocess.check_call(link)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 def _drain(procs, verbose):
@@ -68,4 +76,5 @@ def _drain(procs, verbose):
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    exp = sys.argv[sys.argv.index("--experiments") + 1] if "--experiments" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, experiments=exp))

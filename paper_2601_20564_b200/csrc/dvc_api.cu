@@ -26,7 +26,9 @@ void set_error(const char *fmt, ...) {
     va_end(ap);
 }
 
-bool smem_attr_ok(const void *kern, int smem) {
+// Raise a kernel's dynamic shared memory limit once per (kernel, device, size): the cache records a
+// size only after cudaFuncSetAttribute succeeded, so a failed call is retried (and reported) next time.
+dvc_status ensure_smem(const void *kern, int smem) {
     static std::mutex mu;
     std::lock_guard<std::mutex> lock(mu);
     static const void *keys[64];
@@ -35,21 +37,17 @@ bool smem_attr_ok(const void *kern, int smem) {
     int dev = 0;
     cudaGetDevice(&dev);
     const void *key = reinterpret_cast<const char *>(kern) + dev;   // per device
-    for (int i = 0; i < n; ++i)
-        if (keys[i] == key) {
-            if (vals[i] >= smem) return true;
-            vals[i] = smem;
-            return false;
-        }
-    if (n < 64) {
-        keys[n] = key;
-        vals[n++] = smem;
-    }
-    return false;
+    int i = 0;
+    while (i < n && keys[i] != key) ++i;
+    if (i < n && vals[i] >= smem) return DVC_OK;
+    DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (i < n) vals[i] = smem;
+    else if (n < 64) keys[n] = key, vals[n++] = smem;
+    return DVC_OK;
 }
 
 bool pdl_enabled() {
-    static const bool on = !(getenv("DVC_PDL") && atoi(getenv("DVC_PDL")) == 0);
+    static const bool on = !(dvc_knob("DVC_PDL") && atoi(dvc_knob("DVC_PDL")) == 0);
     return on;
 }
 
@@ -188,11 +186,11 @@ dvc_status resblock_validate(const RB &b, int T, int H, int W) {
 // [T][HW][C_out] and the box statistics.  stats_a / stats_b: box statistics of x_a /
 // x_b if the caller has them (produced by the previous conv's epilogue), else they
 // are computed here; stats_y: where to put the box statistics of y (or null).
-dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, int H, int W, const void *carry_in,
-                           void *carry_out, void *y, void *ws, cudaStream_t stream, const void *stats_a,
-                           const void *stats_b, void *stats_y) {
+static dvc_status resblock_body(const RB &b, const void *xa, const void *xb, int T, int H, int W,
+                                const void *carry_in, void *y, void *ws, cudaStream_t stream, const void *stats_a,
+                                const void *stats_b, void *stats_y) {
     const int HW = H * W, cin = b.ca + b.cb, cs = b.P > 0 ? cin / b.P : 0;
-    if (cs == 0) carry_in = nullptr, carry_out = nullptr;   // no shift: no carries
+    if (cs == 0) carry_in = nullptr;   // no shift: no carry
     const size_t es = dt_size(b.dt);
     uint8_t *p = reinterpret_cast<uint8_t *>(ws);
     void *gnws = p;
@@ -211,12 +209,6 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
     p += box_stats_bytes(1, H, W, cin);
     void *st_y1 = p;
     dvc_status st;
-    // carry_out = X[T-1][..., 0:C_in/P] (raw input, before this block overwrites nothing; y never aliases x)
-    if (carry_out) {
-        DVC_CUDA(cudaMemcpy2DAsync(carry_out, cs * es, reinterpret_cast<const uint8_t *>(xa) +
-                                                           (size_t)(T - 1) * HW * b.ca * es,
-                                   b.ca * es, cs * es, HW, cudaMemcpyDeviceToDevice, stream));
-    }
     const bool boxed = box_mode(b);
     if (boxed && conv_fz_applicable(H, W, b.dt)) {
         // ---- fused path: GN statistics from box partials, GN-apply + SiLU + shift inside the convs
@@ -397,6 +389,21 @@ dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, i
     return conv_run(c2, stream);
 }
 
+dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, int H, int W, const void *carry_in,
+                           void *carry_out, void *y, void *ws, cudaStream_t stream, const void *stats_a,
+                           const void *stats_b, void *stats_y) {
+    const int cs = b.P > 0 ? (b.ca + b.cb) / b.P : 0;
+    dvc_status st = resblock_body(b, xa, xb, T, H, W, carry_in, y, ws, stream, stats_a, stats_b, stats_y);
+    if (st != DVC_OK || !carry_out || cs == 0) return st;
+    // carry_out = X[T-1][..., 0:C_in/P] (the raw block input; y never aliases x), enqueued after every
+    // reader of carry_in, so an in-place carry update (carry_out == carry_in) is well defined
+    const size_t es = dt_size(b.dt);
+    DVC_CUDA(cudaMemcpy2DAsync(carry_out, cs * es,
+                               reinterpret_cast<const uint8_t *>(xa) + (size_t)(T - 1) * H * W * b.ca * es,
+                               b.ca * es, cs * es, (size_t)H * W, cudaMemcpyDeviceToDevice, stream));
+    return DVC_OK;
+}
+
 static RB rb_from_abi(const dvc_resblock *b) {
     RB r;
     r.ca = b->c_a;
@@ -525,7 +532,7 @@ dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype dt, int T, in
     }
     DVC_CHECK_ARG(s == 8, DVC_ERR_UNSUPPORTED, "fused expansion needs s == 8");
     DVC_CHECK_ARG(c_lat >= 16 && c_lat % 16 == 0, DVC_ERR_UNSUPPORTED, "c_lat must be a multiple of 16");
-    if (encode_tma_applicable(dt, H, W, s, c_lat) && !getenv("DVC_ENCODE_GATHER"))
+    if (encode_tma_applicable(dt, H, W, s, c_lat) && !dvc_knob("DVC_ENCODE_GATHER"))
         return encode_tma_run(frames, dt, T, H, W, w_exp, b_exp, c_lat, latent, strm);
     ConvDesc d{};
     d.seg[0] = ConvSeg{frames, 192, SEG_UNSHUFFLE8, H, W, 1, w_exp, 192, 0, 0};
@@ -560,6 +567,12 @@ dvc_status dvc_resblock_tsm_forward(const dvc_resblock *b, const void *x_a, cons
     DVC_CHECK_ARG(ws_bytes >= resblock_ws_bytes(r.ca, r.cb, r.cout, r.G, T, H, W, r.dt), DVC_ERR_WORKSPACE,
                   "workspace too small");
     DVC_CHECK_ARG(((uintptr_t)workspace & 255) == 0, DVC_ERR_ARG, "workspace must be 256-byte aligned");
+    if (carry_in && carry_out && r.P > 0) {
+        const size_t cb = (size_t)H * W * ((r.ca + r.cb) / r.P) * dt_size(r.dt);
+        const uintptr_t a = (uintptr_t)carry_in, o = (uintptr_t)carry_out;
+        DVC_CHECK_ARG(a == o || a + cb <= o || o + cb <= a, DVC_ERR_ARG,
+                      "carry_out must equal carry_in or not overlap it");
+    }
     if ((st = check_device()) != DVC_OK) return st;
     return resblock_launch(r, x_a, r.cb ? x_b : nullptr, T, H, W, carry_in, carry_out, y, workspace,
                            reinterpret_cast<cudaStream_t>(stream));

@@ -594,7 +594,7 @@ PFN_encodeTiled_t get_encode_fn();
 static int attn_debug() {   // DVC_ATTN_DEBUG (experiments only): 1 = skip softmax, 2 = skip MMAs
     static int v = -1;
     if (v < 0) {
-        const char *e = getenv("DVC_ATTN_DEBUG");
+        const char *e = dvc_knob("DVC_ATTN_DEBUG");
         v = e ? atoi(e) : 0;
     }
     return v;
@@ -612,14 +612,16 @@ static dvc_status attn_tc_launch(const void *qkv, void *ws, void *out, int T_, i
     ProfSlot slot = prof_begin(stream);
     static int npoly = -1;   // scores per 8 on the FMA pipe (DVC_ATTN_POLY: 0, 2 (default), 4)
     if (npoly < 0) {
-        const char *e = getenv("DVC_ATTN_POLY");
+        const char *e = dvc_knob("DVC_ATTN_POLY");
         npoly = e ? atoi(e) : DVC_ATTN_POLY;
     }
     auto kfn = npoly == 0 ? attn_tc_kernel<T, D, 0, KT> : npoly == 4 ? attn_tc_kernel<T, D, 4, KT>
              : attn_tc_kernel<T, D, 2, KT>;
     const void *kern = reinterpret_cast<const void *>(kfn);
-    if (!smem_attr_ok(kern, L::bytes))
-        DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::bytes));
+    {
+        dvc_status ss_ = ensure_smem((const void *)kern, (int)(L::bytes));
+        if (ss_ != DVC_OK) return ss_;
+    }
     const int bf = std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
     DVC_CUDA(launch_pdl(kfn, dim3((N + 128 * L::NT - 1) / (128 * L::NT), C / D, T_), dim3(L::THREADS), (size_t)L::bytes,

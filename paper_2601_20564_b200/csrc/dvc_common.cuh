@@ -7,9 +7,22 @@
 #include <cstddef>
 #include <utility>
 #include <type_traits>
+#include <cstdlib>
 #include "../../include/dvc.h"
 
 namespace dvc {
+
+// Experiment knobs (A/B timing, work-skipping debug switches) are read from the environment only
+// in builds compiled with -DDVC_EXPERIMENTS (tools/ab.sh); the product library ignores every DVC_*
+// variable, so no environment can make it skip work or change its arithmetic.
+inline const char *dvc_knob(const char *name) {
+#ifdef DVC_EXPERIMENTS
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 
 // ----------------------------------------------------------------- errors
 void set_error(const char *fmt, ...);
@@ -134,7 +147,7 @@ __device__ __forceinline__ float silu_fast(float z) {
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 
 // true if `kern` already allows >= smem bytes of dynamic shared memory (records the new size otherwise)
-bool smem_attr_ok(const void *kern, int smem);
+dvc_status ensure_smem(const void *kern, int smem);   // cudaFuncSetAttribute, cached
 
 // Programmatic dependent launch (PDL): kernels of the decode chain are launched with
 // programmatic stream serialisation, so a kernel's CTAs may start (prologue: barriers, TMEM,

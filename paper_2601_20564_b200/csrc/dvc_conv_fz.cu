@@ -708,12 +708,12 @@ extern int g_ws_cg;
 dvc_status make_box_map(CUtensorMap *map, const void *ptr, dvc_dtype dt, int T, int H, int W, int C, int BX, int BY);
 
 static int fz_off_from_env() {   // DVC_NO_FZ=1: never use the fused engine (A/B experiments)
-    const char *e = getenv("DVC_NO_FZ");
+    const char *e = dvc_knob("DVC_NO_FZ");
     return e && e[0] == '1';
 }
 static const int g_fz_off = fz_off_from_env();
 static int fz_min_h_from_env() {   // DVC_FZ_MIN_H: smallest frame height on the fused engine (A/B experiments)
-    const char *e = getenv("DVC_FZ_MIN_H");
+    const char *e = dvc_knob("DVC_FZ_MIN_H");
     return e ? atoi(e) : 32;
 }
 static const int g_fz_min_h = fz_min_h_from_env();
@@ -773,7 +773,7 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     p.bias1 = d.bias1;
     p.out = d.out;
     p.stats = reinterpret_cast<float *>(d.stats_out);
-    if (getenv("DVC_FZ_XNOSTATS")) p.stats = nullptr;   // timing experiment only: results are wrong
+    if (dvc_knob("DVC_FZ_XNOSTATS")) p.stats = nullptr;   // timing experiment only: results are wrong
     p.coef = reinterpret_cast<const float2 *>(d.coef);
     DVC_CHECK_ARG(((uintptr_t)d.coef & 15) == 0 && d.cop % 2 == 0, DVC_ERR_ARG, "fused conv: coefficient alignment");
     p.cop = d.cop;
@@ -827,12 +827,12 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     }
     p.idesc = make_idesc(d.dt == DVC_BF16, 128 * CG, bn);
     {
-        static const int sw_env = getenv("DVC_FZ_SW") ? atoi(getenv("DVC_FZ_SW")) : 1;
+        static const int sw_env = dvc_knob("DVC_FZ_SW") ? atoi(dvc_knob("DVC_FZ_SW")) : 1;
         p.sw_mode = sw_env;
     }
     // shared memory: tile slots, weight stages, residual tile; fill the 227 KB budget with weight stages
     {
-        const char *e = getenv("DVC_FZ_NTF");
+        const char *e = dvc_knob("DVC_FZ_NTF");
         p.ntf = e ? atoi(e) : 4;
         if (p.ntf < 2 || p.ntf > FZ_MAX_NTF) p.ntf = 4;
     }
@@ -845,14 +845,14 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     const size_t bstage = (size_t)(bn / CG) * 128;
     int nbst = (int)((227 * 1024 - fixed) / bstage);
     {
-        const char *e = getenv("DVC_FZ_NB");
+        const char *e = dvc_knob("DVC_FZ_NB");
         if (e && atoi(e) >= 2 && atoi(e) < nbst) nbst = atoi(e);
     }
     if (nbst > FZ_MAX_BSTAGES) nbst = FZ_MAX_BSTAGES;
     DVC_CHECK_ARG(nbst >= 2, DVC_ERR_UNSUPPORTED, "fused conv: shared memory too small");
     p.nb = nbst;
     const size_t smem = fixed - 1024 + (size_t)nbst * bstage;
-    static const bool prof = getenv("DVC_FZ_PROF") != nullptr && atoi(getenv("DVC_FZ_PROF")) != 0;
+    static const bool prof = dvc_knob("DVC_FZ_PROF") != nullptr && atoi(dvc_knob("DVC_FZ_PROF")) != 0;
     static unsigned long long *prof_buf = nullptr;
     if (prof) {
         if (!prof_buf) DVC_CUDA(cudaMalloc(&prof_buf, 24 * sizeof(unsigned long long)));
@@ -861,8 +861,10 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     }
     auto kern = d.dt == DVC_BF16 ? (prof ? conv_fz_kernel<__nv_bfloat16, 2, true> : conv_fz_kernel<__nv_bfloat16, 2, false>)
                                  : (prof ? conv_fz_kernel<__half, 2, true> : conv_fz_kernel<__half, 2, false>);
-    if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
-        DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {   // host cost: the attribute is set once per kernel / size
+        dvc_status ss_ = ensure_smem((const void *)kern, (int)smem);
+        if (ss_ != DVC_OK) return ss_;
+    }
     if (g_fz_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);

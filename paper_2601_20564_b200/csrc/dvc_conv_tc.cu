@@ -335,8 +335,10 @@ template <typename T, int NACC, int STAGES>
 static dvc_status launch_tc(const TcParams &p, int grid_m, int grid_n, cudaStream_t stream) {
     size_t smem = 1024 + (size_t)STAGES * (NACC * 16384 + p.bn * 128) + 8 * (2 * STAGES + 1) + 16 + NACC * 128 * 4;
     auto kern = conv_tc_kernel<T, NACC, STAGES>;
-    if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
-        DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {   // host cost: the attribute is set once per kernel / size
+        dvc_status ss_ = ensure_smem((const void *)kern, (int)smem);
+        if (ss_ != DVC_OK) return ss_;
+    }
     DVC_CUDA(launch_pdl(kern, dim3(grid_m, grid_n), dim3(kThreads), smem, stream, 1, p));
     ++g_launches;
     return check_launch("conv_tc_kernel");

@@ -411,8 +411,10 @@ static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
     const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16 + 2048 +
                         (size_t)(p.bias1 ? 2 : 1) * p.cout * 4;   // bias1 staged only when present
     auto kern = conv_ws_kernel<T, CG, STAGES>;
-    if (!smem_attr_ok((const void *)kern, (int)smem))   // host cost: set the attribute once per kernel / size
-        DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {   // host cost: the attribute is set once per kernel / size
+        dvc_status ss_ = ensure_smem((const void *)kern, (int)smem);
+        if (ss_ != DVC_OK) return ss_;
+    }
     if (g_num_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -457,7 +459,7 @@ static dvc_status make_bmap8(CUtensorMap *map, const void *ptr, long rows, long 
 }
 
 static int engine_from_env() {
-    const char *e = getenv("DVC_CONV_ENGINE");
+    const char *e = dvc_knob("DVC_CONV_ENGINE");
     if (e && (e[0] == '0' || e[0] == '1' || e[0] == '2') && e[1] == 0) return e[0] - '0';
     return 2;
 }

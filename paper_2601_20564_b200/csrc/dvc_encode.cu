@@ -237,8 +237,10 @@ dvc_status encode_tma_run(const void *frames, dvc_dtype dt, int T, int H, int W,
     p.idesc = make_idesc(dt == DVC_BF16, 128, c_lat);
     const size_t smem = 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 8 * 10 + 16 + (size_t)c_lat * 4;
     auto kern = dt == DVC_BF16 ? encode_kernel<__nv_bfloat16> : encode_kernel<__half>;
-    if (!smem_attr_ok((const void *)kern, (int)smem))
-        DVC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    {   // host cost: the attribute is set once per kernel / size
+        dvc_status ss_ = ensure_smem((const void *)kern, (int)smem);
+        if (ss_ != DVC_OK) return ss_;
+    }
     if (g_enc_sms == 0) {
         int dev = 0;
         cudaGetDevice(&dev);

@@ -155,6 +155,12 @@ dvc_status dvc_pipeline_destroy(dvc_pipeline *p) {
 dvc_status dvc_pipeline_push(dvc_pipeline *p, const void *lat, const void *ctx, void *stream) {
     DVC_CHECK_ARG(p && lat && ctx, DVC_ERR_ARG, "null argument");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (!p->slots[p->fill].launched && p->slots[p->fill].frames >= p->N) {
+        // a full slot whose launch failed earlier (e.g. a pending CUDA error): launch it first, never
+        // copy past the slot's N-frame allocation
+        dvc_status st = launch_slot(p, p->last_stream);
+        if (st != DVC_OK) return st;
+    }
     dvc_pipeline::Slot &sl = p->slots[p->fill];
     DVC_CHECK_ARG(!sl.launched, DVC_ERR_ARG, "pipeline FIFO full: %d decoded batches not popped", p->in_flight);
     if (sl.frames == 0) {

@@ -11,10 +11,9 @@
 //   out = conv_out(SiLU(GN_out(h)))
 // Multi-GPU: a chain's frames are split into contiguous chunks, one
 // per rank; before ResBlock k, rank r sends the C_in/P-channel slice of its
-// last frame's block input to rank r+1 and receives rank r-1's (NCCL P2P on
-// the compute stream).  Weights are replicated.
-#include <dlfcn.h>
-#include <nccl.h>
+// last frame's block input to rank r+1 and receives rank r-1's (dvc_halo.cu:
+// copy-engine peer copies + stream memory flags, or NCCL, on a comm stream).
+// Weights are replicated.
 #include <cstring>
 #include <cstdlib>
 #include <vector>
@@ -22,65 +21,9 @@
 #include "dvc_norm.cuh"
 #include "dvc_resblock.cuh"
 #include "dvc_attn.cuh"
+#include "dvc_halo.cuh"
 
 using namespace dvc;
-
-// ----------------------------------------------------------------- NCCL (dlopen'd)
-namespace {
-struct NcclApi {
-    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*GroupStart)() = nullptr;
-    ncclResult_t (*GroupEnd)() = nullptr;
-    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
-    const char *(*GetErrorString)(ncclResult_t) = nullptr;
-    bool ok = false;
-};
-
-NcclApi &nccl() {
-    static NcclApi api;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        // prefer the copy already loaded in the process (torch's), then the system one
-        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-        if (h) {
-            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
-            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
-            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
-            api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
-            api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
-            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
-            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
-            api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
-            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-            api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
-                     api.GroupStart && api.GroupEnd;
-        }
-    }
-    return api;
-}
-
-#define DVC_NCCL(call)                                                                                   \
-    do {                                                                                                 \
-        ncclResult_t r_ = (call);                                                                        \
-        if (r_ != ncclSuccess) {                                                                         \
-            set_error("%s: NCCL error %d (%s)", #call, (int)r_,                                         \
-                      nccl().GetErrorString ? nccl().GetErrorString(r_) : "?");                          \
-            return DVC_ERR_NCCL;                                                                         \
-        }                                                                                                \
-    } while (0)
-}  // namespace
-
-struct dvc_comm {
-    ncclComm_t comm;
-    int rank, world;
-};
 
 // ----------------------------------------------------------------- the network
 struct ConvW {
@@ -334,38 +277,6 @@ dvc_status pack_all(dvc_unet &n) {
 
 extern "C" {
 
-dvc_status dvc_comm_unique_id(void *id128) {
-    DVC_CHECK_ARG(id128, DVC_ERR_ARG, "null id");
-    DVC_CHECK_ARG(nccl().ok, DVC_ERR_NCCL, "libnccl.so.2 not found");
-    ncclUniqueId id;
-    DVC_NCCL(nccl().GetUniqueId(&id));
-    memcpy(id128, &id, sizeof(id));
-    return DVC_OK;
-}
-
-dvc_status dvc_comm_create(int rank, int world, const void *id128, dvc_comm **out) {
-    DVC_CHECK_ARG(out && id128 && world >= 1 && rank >= 0 && rank < world, DVC_ERR_ARG, "bad comm arguments");
-    DVC_CHECK_ARG(nccl().ok, DVC_ERR_NCCL, "libnccl.so.2 not found");
-    ncclUniqueId id;
-    memcpy(&id, id128, sizeof(id));
-    dvc_comm *c = new dvc_comm{nullptr, rank, world};
-    ncclResult_t r = nccl().CommInitRank(&c->comm, world, id, rank);
-    if (r != ncclSuccess) {
-        delete c;
-        set_error("ncclCommInitRank failed: %d", (int)r);
-        return DVC_ERR_NCCL;
-    }
-    *out = c;
-    return DVC_OK;
-}
-
-dvc_status dvc_comm_destroy(dvc_comm *c) {
-    if (!c) return DVC_OK;
-    if (c->comm) nccl().CommDestroy(c->comm);
-    delete c;
-    return DVC_OK;
-}
-
 dvc_status dvc_unet_weight_count(const dvc_unet_config *cfg, size_t *elems) {
     dvc_status st = validate_cfg(cfg);
     if (st != DVC_OK) return st;
@@ -474,7 +385,7 @@ dvc_status dvc_unet_create(const dvc_unet_config *cfg, const void *host_weights,
     }
     // Packed weight images (contiguous weight tiles) measured slower than the OHWI rows on B200
     // (r1 profiles), so they are opt-in: DVC_PACK_WEIGHTS=1.
-    const char *pe = getenv("DVC_PACK_WEIGHTS");
+    const char *pe = dvc_knob("DVC_PACK_WEIGHTS");
     if (cfg->dt != DVC_F32 && pe && pe[0] == '1') {
         st = pack_all(*n);
         if (st != DVC_OK) {
@@ -521,8 +432,7 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     size_t offs[kRegions];
     const size_t need = plan_workspace(*n, T, offs);
     DVC_CHECK_ARG(ws_bytes >= need, DVC_ERR_WORKSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
-    const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
-    if (world > 1) DVC_CHECK_ARG(nccl().ok, DVC_ERR_NCCL, "NCCL unavailable");
+    const int world = comm_world(comm), rank = comm_rank(comm);
     dvc_status st = check_device();
     if (st != DVC_OK) return st;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -539,9 +449,8 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     void *hb[2] = {ws + offs[12], ws + offs[13]};
     void *hbst[2] = {ws + offs[28], ws + offs[29]};
     void *rbws = ws + offs[14];
-    uint8_t *halo = ws + offs[15];
-    uint8_t *recv = halo;                                    // packed received carries
-    uint8_t *sendb = halo + align256(n->carry_total * es);   // one slice staging buffer
+    if (world > 1 && (st = halo_call_begin(comm, n->carry_total * es, ws + offs[15], s)) != DVC_OK) return st;
+    (void)rank;
     auto hw = [&](int l) { return n->lh[l] * n->lw[l]; };
 
     int bi = 0;
@@ -554,25 +463,19 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         const int cs = (r.ca + r.cb) / r.P;
         const size_t off = n->carry_off[bi] * es;
         const void *cin_ptr = carry_in ? reinterpret_cast<const uint8_t *>(carry_in) + off : nullptr;
-        if (world > 1) {
-            NcclApi &api = nccl();
-            if (rank < world - 1)
-                DVC_CUDA(cudaMemcpy2DAsync(sendb, cs * es,
-                                           reinterpret_cast<const uint8_t *>(xa) + (size_t)(T - 1) * H * Wd * r.ca * es,
-                                           r.ca * es, cs * es, (size_t)H * Wd, cudaMemcpyDeviceToDevice, s));
-            DVC_NCCL(api.GroupStart());
-            const ncclDataType_t ty = dt == DVC_F32 ? ncclFloat32 : dt == DVC_F16 ? ncclFloat16 : ncclBfloat16;
-            if (rank < world - 1) DVC_NCCL(api.Send(sendb, (size_t)H * Wd * cs, ty, rank + 1, comm->comm, s));
-            if (rank > 0) DVC_NCCL(api.Recv(recv + off, (size_t)H * Wd * cs, ty, rank - 1, comm->comm, s));
-            DVC_NCCL(api.GroupEnd());
-            if (rank > 0) cin_ptr = recv + off;
+        if (world > 1) {   // rank > 0: the carry is rank-1's slice; rank < world-1: send mine onward
+            const HaloSlice sl{reinterpret_cast<const uint8_t *>(xa) + (size_t)(T - 1) * H * Wd * r.ca * es,
+                               (size_t)r.ca * es, (size_t)cs * es, (size_t)H * Wd, off};
+            dvc_status e = halo_exchange(comm, bi, sl, s, &cin_ptr);
+            if (e != DVC_OK) return e;
         }
         void *cout_ptr = nullptr;
-        if (carry_out && (world == 1 || rank == world - 1)) cout_ptr = reinterpret_cast<uint8_t *>(carry_out) + off;
+        if (carry_out && rank == world - 1) cout_ptr = reinterpret_cast<uint8_t *>(carry_out) + off;
         dvc_status e = resblock_launch(r, xa, xb, T, H, Wd, cin_ptr, cout_ptr, y, rbws, s, sa, sb, sy);
         // f1: the Transformer2D block after this ResBlock, in place on y (its statistics refreshed)
         if (e == DVC_OK && n->tf_of[bi] >= 0)
             e = transformer_launch(n->tf[n->tf_of[bi]], y, T, H, Wd, y, rbws, s, sy, sy);
+        if (e == DVC_OK && world > 1) e = halo_block_done(comm, bi, s);
         ++bi;
         return e;
     };
@@ -708,11 +611,7 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
                         nullptr)) != DVC_OK)
             return st;
     }
-    if (world > 1 && nccl().CommGetAsyncError) {
-        ncclResult_t ar = ncclSuccess;
-        nccl().CommGetAsyncError(comm->comm, &ar);
-        DVC_CHECK_ARG(ar == ncclSuccess || ar == ncclInProgress, DVC_ERR_NCCL, "NCCL async error %d", (int)ar);
-    }
+    if (world > 1 && (st = halo_call_end(comm, s)) != DVC_OK) return st;
     return DVC_OK;
 }
 

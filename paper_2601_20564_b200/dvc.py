@@ -194,24 +194,77 @@ def unet_weight_count(cfg) -> int:
     return n.value
 
 
-class Comm:
-    """NCCL halo communicator; the 128-byte unique id travels over torch.distributed."""
+def chunk_bounds(T: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous frame chunks [t0, t1) of a T-frame chain over `world` ranks: rank r
+    holds T // world frames, +1 for the last T % world ranks.  Pure host logic (tested on CPU)."""
+    if world < 1 or T < world:
+        raise ValueError(f"cannot split {T} frames over {world} ranks")
+    base, rem = divmod(T, world)
+    sizes = [base + (1 if r >= world - rem else 0) for r in range(world)]
+    out, t0 = [], 0
+    for n in sizes:
+        out.append((t0, t0 + n))
+        t0 += n
+    return out
 
-    def __init__(self, rank: int, world: int, group=None):
-        import torch.distributed as dist
-        idt = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            buf = (ctypes.c_uint8 * 128)()
-            check(lib().dvc_comm_unique_id(buf))
-            idt = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
-        if dist.is_initialized() and world > 1:
-            dev = idt.cuda() if dist.get_backend(group) == "nccl" else idt
-            dist.broadcast(dev, 0, group=group)
-            idt = dev.cpu()
-        raw = (ctypes.c_uint8 * 128)(*idt.tolist())
+
+def halo_neighbours(handles: list, rank: int):
+    """(next, prev) entries of a gathered per-rank list for rank `rank` (None at the chain ends)."""
+    world = len(handles)
+    return (handles[rank + 1] if rank < world - 1 else None), (handles[rank - 1] if rank > 0 else None)
+
+
+class Comm:
+    """Halo communicator of dvc_unet_decode_gop (include/dvc.h, row e).
+
+    transport="p2p" (default): library-owned receive slots, copy-engine peer copies and stream
+    memory flags; the 64-byte CUDA IPC handles travel over torch.distributed (all_gather_object).
+    transport="nccl": NCCL send/recv; the 128-byte unique id travels over torch.distributed.
+    Comm.local_group(world, net) builds `world` connected ranks inside ONE process (one GPU: the
+    loopback the tests use)."""
+
+    def __init__(self, rank: int, world: int, net: "UNet | None" = None, transport: str = "p2p", group=None,
+                 _connect: bool = True):
+        self.rank, self.world, self.transport = rank, world, transport
         self.handle = ctypes.c_void_p()
-        check(lib().dvc_comm_create(rank, world, raw, ctypes.byref(self.handle)))
-        self.rank, self.world = rank, world
+        if transport == "nccl":
+            import torch.distributed as dist
+            idt = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                buf = (ctypes.c_uint8 * 128)()
+                check(lib().dvc_comm_unique_id(buf))
+                idt = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+            if dist.is_initialized() and world > 1:
+                dev = idt.cuda() if dist.get_backend(group) == "nccl" else idt
+                dist.broadcast(dev, 0, group=group)
+                idt = dev.cpu()
+            raw = (ctypes.c_uint8 * 128)(*idt.tolist())
+            check(lib().dvc_comm_create(rank, world, raw, ctypes.byref(self.handle)))
+            return
+        if transport != "p2p":
+            raise ValueError(f"unknown transport {transport!r}")
+        if net is None:
+            raise ValueError("the P2P transport sizes its receive slots from the network (net=...)")
+        es = 4 if net.cfg.dt == DVC_F32 else 2
+        check(lib().dvc_comm_create_p2p(rank, world, net.carry_elems * es, ctypes.byref(self.handle)))
+        if _connect and world > 1:
+            import torch.distributed as dist
+            buf = (ctypes.c_uint8 * 64)()
+            check(lib().dvc_comm_ipc_handle(self.handle, buf))
+            gathered = [None] * world
+            dist.all_gather_object(gathered, bytes(buf), group=group)
+            nxt, prv = halo_neighbours(gathered, rank)
+            raw = lambda b: None if b is None else (ctypes.c_uint8 * 64)(*b)  # noqa: E731
+            check(lib().dvc_comm_connect_ipc(self.handle, raw(nxt), raw(prv)))
+
+    @classmethod
+    def local_group(cls, world: int, net: "UNet") -> list:
+        comms = [cls(r, world, net, _connect=False) for r in range(world)]
+        for r, c in enumerate(comms):
+            nxt, prv = halo_neighbours(comms, r)
+            check(lib().dvc_comm_connect_local(c.handle, None if nxt is None else nxt.handle,
+                                               None if prv is None else prv.handle))
+        return comms
 
     def close(self):
         if self.handle:

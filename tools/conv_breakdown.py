@@ -16,6 +16,7 @@ import synthgen  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=32)
+ap.add_argument("--json", default=None, help="also write the per-launch conv records [label, ms, flops] in order")
 a = ap.parse_args()
 T, h, w = a.frames, 90, 160
 WIDTH = (240, 480, 960, 960)
@@ -35,6 +36,9 @@ dvc.profile_begin(4096)
 dvc.dvc_unet_decode_gop(net, lat, ctx, out=out, workspace=ws)
 ms, fl, n = dvc.profile_end()
 rec = dvc.profile_records()
+if a.json:
+    with open(a.json, "w") as f:
+        json.dump([r for r in rec if r[2]], f)
 g = collections.OrderedDict()
 for lab, t, f in rec:
     e = g.setdefault(lab, [0, 0.0, 0.0])
