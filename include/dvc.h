@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define DVC_ABI_VERSION 2
+#define DVC_ABI_VERSION 3
 
 typedef enum {
     DVC_OK = 0,
@@ -54,7 +54,8 @@ typedef enum {
     DVC_ERR_NCCL = 7          /* an NCCL error (multi-GPU halo)                     */
 } dvc_status;
 
-typedef enum { DVC_BF16 = 0, DVC_F16 = 1, DVC_F32 = 2 } dvc_dtype;
+/* DVC_U8: 8-bit frames only (dvc_encode_pixelunshuffle's frame_dt), HWC layout, value u / 255 (R14) */
+typedef enum { DVC_BF16 = 0, DVC_F16 = 1, DVC_F32 = 2, DVC_U8 = 3 } dvc_dtype;
 
 DVC_API const char *dvc_status_string(dvc_status s);
 DVC_API const char *dvc_last_error(void);
@@ -65,20 +66,24 @@ DVC_API int dvc_abi_version(void);
  * operation for space-to-depth") fused with the Latent Channel Expansion
  * ("expanding the latent dimension ... to 256"; 1x1 conv + bias, R13).
  *
- *   frames  [T,3,H,W] NCHW in `dt` (values in [0,1])
- *   w_exp   [c_lat][3*s*s], b_exp [c_lat]  (dt), or both NULL
- *   latent  [T,H/s,W/s,c_lat] NHWC in `dt`
+ *   frames    frame_dt = DVC_BF16 / DVC_F16 / DVC_F32: [T,3,H,W] NCHW, values in [0,1];
+ *             frame_dt = DVC_U8: [T,H,W,3] HWC bytes u, value RNE_{latent_dt}(u / 255) exactly rounded
+ *             (reading R14; S:366 `to_latent` on decoded 8-bit frames)
+ *   w_exp     [c_lat][3*s*s], b_exp [c_lat]  (latent_dt), or both NULL
+ *   latent    [T,H/s,W/s,c_lat] NHWC in latent_dt (== frame_dt unless frame_dt is DVC_U8)
  *
  * w_exp == NULL: unshuffle only, c_lat must be 3*s*s; the result is a pure
- * permutation, bit-exact: latent[t,y,x,c*s*s+i*s+j] = frames[t,c,s*y+i,s*x+j]
- * (torch channel order, R12).  Otherwise E = b + W.L with fp32 accumulation,
- * computed on tcgen05 tensor cores (16-bit) with the 3*s*s-channel latent
- * never written to memory; 16-bit expansion requires s == 8.
- * Errors: DIVISIBILITY if H%s or W%s; ARG on nulls / T<1.
+ * permutation (of the converted bytes for DVC_U8), bit-exact:
+ *   latent[t,y,x,c*s*s+i*s+j] = frames[t,c,s*y+i,s*x+j]   (torch channel order, R12).
+ * Otherwise E = b + W.L with fp32 accumulation, computed on tcgen05 tensor cores (16-bit
+ * latent_dt, s == 8; DVC_U8 frames also need W % 16 == 0) with the 3*s*s-channel latent never
+ * written to memory; the fp32 validation mode runs the SIMT engine.
+ * Errors: DIVISIBILITY if H%s or W%s; ARG on nulls / T<1 / bad dtypes; UNSUPPORTED for a
+ * frame_dt != latent_dt pair other than DVC_U8 frames, or DVC_U8 latents.
  * ------------------------------------------------------------------------ */
-DVC_API dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype dt, int T, int H, int W, int s,
+DVC_API dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype frame_dt, int T, int H, int W, int s,
                                      const void *w_exp, const void *b_exp, int c_lat,
-                                     void *latent, void *stream);
+                                     void *latent, dvc_dtype latent_dt, void *stream);
 
 /* ------------------------------------------------------------------------
  * a3-a8.  One OTSM ResBlock over T consecutive frames of one chain (P:320,

@@ -120,6 +120,44 @@ def shuffle(L, C: int, s: int = 8):
 
 
 # --------------------------------------------------------------------------
+# R14: 8-bit HWC frames -> frame values u / 255 in the latent precision
+# --------------------------------------------------------------------------
+def _round_fraction(q, mode) -> float:
+    """Round the exact rational q (fractions.Fraction, 0 <= q <= 1) to the nearest value of the
+    format, ties to even: 'fp16' (11-bit significand), 'bf16' (8-bit) or 'f32' (24-bit)."""
+    from fractions import Fraction
+    import math
+    bits = {"fp16": 11, "bf16": 8, "f32": 24}[mode]
+    if q == 0:
+        return 0.0
+    e = math.floor(math.log2(q))
+    if Fraction(2) ** e > q:          # guard the float log2 near powers of two
+        e -= 1
+    if Fraction(2) ** (e + 1) <= q:
+        e += 1
+    e = max(e, {"fp16": -14, "bf16": -126, "f32": -126}[mode])   # subnormal quantum below the normal range
+    quantum = Fraction(2) ** (e - bits + 1)
+    n, r = divmod(q, quantum)
+    if r * 2 > quantum or (r * 2 == quantum and n % 2 == 1):
+        n += 1
+    return float(n * quantum)
+
+
+def u8_values(mode) -> np.ndarray:
+    """Reading R14: the value of byte u is u / 255 rounded once, to nearest-even, to the latent
+    format ('fp16', 'bf16'; 'f32' for the fp32 validation mode).  Returns the 256 values (fp64)."""
+    from fractions import Fraction
+    return np.array([_round_fraction(Fraction(u, 255), mode) for u in range(256)])
+
+
+def frames_from_u8(U, mode) -> np.ndarray:
+    """8-bit HWC frames U [T,H,W,3] -> NCHW frame values [T,3,H,W] (R14; S:366 to_latent on decoded
+    8-bit frames)."""
+    U = np.asarray(U, dtype=np.uint8)
+    return u8_values(mode)[U].transpose(0, 3, 1, 2).copy()
+
+
+# --------------------------------------------------------------------------
 # conv / norm / activation / resize primitives (S:44-52, S:71-78; R2-R4, R11)
 # --------------------------------------------------------------------------
 def conv2d(X, Wt, b=None, stride: int = 1, pad: int | None = None):

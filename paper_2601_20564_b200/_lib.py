@@ -12,7 +12,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # DVC_LIB: an alternative build of the same library (A/B timing experiments, tools/ab.sh)
 SO_PATH = os.environ.get("DVC_LIB") or os.path.join(_PKG, "libdvc.so")
 
-DVC_BF16, DVC_F16, DVC_F32 = 0, 1, 2
+DVC_BF16, DVC_F16, DVC_F32, DVC_U8 = 0, 1, 2, 3
 STATUS = {0: "DVC_OK", 1: "DVC_ERR_ARG", 2: "DVC_ERR_DIVISIBILITY", 3: "DVC_ERR_SHAPE",
           4: "DVC_ERR_UNSUPPORTED", 5: "DVC_ERR_WORKSPACE", 6: "DVC_ERR_CUDA", 7: "DVC_ERR_NCCL"}
 
@@ -61,7 +61,7 @@ _SIGS = {
     "dvc_kernel_launch_count": ([], c_int),
     "dvc_device_check": ([c_int], c_int),
     "dvc_encode_pixelunshuffle": ([c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
-                                   c_void_p, c_void_p], c_int),
+                                   c_void_p, c_int, c_void_p], c_int),
     "dvc_resblock_workspace_size": ([ctypes.POINTER(dvc_resblock), c_int, c_int, c_int,
                                      ctypes.POINTER(c_size_t)], c_int),
     "dvc_resblock_tsm_forward": ([ctypes.POINTER(dvc_resblock), c_void_p, c_void_p, c_int, c_int, c_int, c_void_p,

@@ -515,10 +515,13 @@ dvc_status dvc_device_check(int device) {
     return st;
 }
 
-dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype dt, int T, int H, int W, int s, const void *w_exp,
-                                     const void *b_exp, int c_lat, void *latent, void *stream) {
+dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype frame_dt, int T, int H, int W, int s,
+                                     const void *w_exp, const void *b_exp, int c_lat, void *latent, dvc_dtype dt,
+                                     void *stream) {
     DVC_CHECK_ARG(frames && latent, DVC_ERR_ARG, "null frames/latent");
-    DVC_CHECK_ARG(dt_valid(dt), DVC_ERR_ARG, "bad dtype");
+    DVC_CHECK_ARG(dt_valid(dt) && (dt_valid(frame_dt) || frame_dt == DVC_U8), DVC_ERR_ARG, "bad dtype");
+    DVC_CHECK_ARG(frame_dt == dt || frame_dt == DVC_U8, DVC_ERR_UNSUPPORTED,
+                  "frame_dt must equal latent_dt (or be DVC_U8)");
     DVC_CHECK_ARG(T >= 1 && H >= 1 && W >= 1 && s >= 1, DVC_ERR_ARG, "T, H, W, s must be >= 1");
     DVC_CHECK_ARG(H % s == 0 && W % s == 0, DVC_ERR_DIVISIBILITY, "H=%d and W=%d must be multiples of s=%d", H, W,
                   s);
@@ -528,12 +531,18 @@ dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype dt, int T, in
     cudaStream_t strm = reinterpret_cast<cudaStream_t>(stream);
     if (w_exp == nullptr) {
         DVC_CHECK_ARG(c_lat == 3 * s * s, DVC_ERR_SHAPE, "unshuffle only: c_lat must be 3*s*s=%d", 3 * s * s);
+        if (frame_dt == DVC_U8) return unshuffle_u8_run(frames, T, H, W, s, latent, dt, strm);
         return unshuffle_run(frames, dt, T, H, W, s, latent, strm);
     }
     DVC_CHECK_ARG(s == 8, DVC_ERR_UNSUPPORTED, "fused expansion needs s == 8");
     DVC_CHECK_ARG(c_lat >= 16 && c_lat % 16 == 0, DVC_ERR_UNSUPPORTED, "c_lat must be a multiple of 16");
+    if (frame_dt == DVC_U8) {
+        DVC_CHECK_ARG(encode_tma_applicable(dt, H, W, s, c_lat) && W % 16 == 0, DVC_ERR_UNSUPPORTED,
+                      "8-bit frames with expansion: 16-bit latent, c_lat <= 256, W %% 16 == 0");
+        return encode_tma_run(frames, DVC_U8, T, H, W, w_exp, b_exp, c_lat, latent, dt, strm);
+    }
     if (encode_tma_applicable(dt, H, W, s, c_lat) && !dvc_knob("DVC_ENCODE_GATHER"))
-        return encode_tma_run(frames, dt, T, H, W, w_exp, b_exp, c_lat, latent, strm);
+        return encode_tma_run(frames, dt, T, H, W, w_exp, b_exp, c_lat, latent, dt, strm);
     ConvDesc d{};
     d.seg[0] = ConvSeg{frames, 192, SEG_UNSHUFFLE8, H, W, 1, w_exp, 192, 0, 0};
     d.nseg = 1;

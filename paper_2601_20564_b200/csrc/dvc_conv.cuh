@@ -110,8 +110,8 @@ dvc_status conv_check(const ConvDesc &d, bool tensor_core);
 dvc_status conv_run(const ConvDesc &d, cudaStream_t stream);
 // a1 + a2 fused (dvc_encode.cu): 5D-TMA unshuffle straight into the UMMA A layout + 1x1 expansion
 bool encode_tma_applicable(dvc_dtype dt, int H, int W, int s, int c_lat);
-dvc_status encode_tma_run(const void *frames, dvc_dtype dt, int T, int H, int W, const void *w_exp, const void *b_exp,
-                          int c_lat, void *latent, cudaStream_t stream);
+dvc_status encode_tma_run(const void *frames, dvc_dtype frame_dt, int T, int H, int W, const void *w_exp,
+                          const void *b_exp, int c_lat, void *latent, dvc_dtype dt, cudaStream_t stream);
 dvc_status conv_tc_run(const ConvDesc &d, cudaStream_t stream);
 dvc_status conv_simt_run(const ConvDesc &d, cudaStream_t stream);
 dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream);   // TMA + CTA-pair persistent engine

@@ -26,9 +26,11 @@
 #include <cuda.h>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 #include "dvc_conv.cuh"
 #include "dvc_ptx.cuh"
 #include "dvc_boxstats.cuh"
+#include "dvc_epilogue.cuh"
 
 namespace dvc {
 
@@ -45,6 +47,7 @@ constexpr int FZ_RAW_SLOT = 128 * 128;        // one raw SW128 box {64, 8, 16}
 constexpr int FZ_SBO = FZ_HX * 16;            // between 8-row groups (image rows)
 constexpr int FZ_MAX_BSTAGES = 16;
 constexpr int FZ_MAX_NTF = 6;   // even: keeps the barrier block a multiple of 16 B
+constexpr int FZ_MAX_RAW = 4;   // raw (1x1) ring slots
 #ifndef FZ_TFW
 #define FZ_TFW 8   // transform warps: 8 (one per 8-channel column) or 16 (two per column, rows split;
                    // measured slower: 768 threads cap registers at 80 and the epilogue spills)
@@ -77,9 +80,14 @@ struct FzParams {
     void *out;
     float *stats;
     uint32_t idesc;
-    int ntf, nraw, nb;   // tile slots, raw slots (0 or 2), weight stages (sized from the shared-memory budget)
+    int ntf, nraw, nb;   // tile slots, raw slots (0 or 2..4), weight stages (sized from the shared-memory budget)
     unsigned long long *prof;   // [6][4] wait/total cycles per role (PROF kernels only)
     int sw_mode;                // 0: 8-channel no-swizzle boxes only; 1/2: SW128 whole-chunk box for unshifted chunks (2: base offset)
+    int nsteps;                 // K loop of a work item: (segment, 64-channel chunk) steps in issue order,
+    unsigned char ord[64];      //   ord[i] = seg << 6 | chunk (raw 1x1 chunks interleaved among the 3x3 ones)
+    int epi_tma;                // 1: epilogue stages 32-column chunks in shared memory, TMA-stores them and reads
+                                //    the box statistics back column-wise; 0: per-thread row stores + butterflies
+    CUtensorMap omap[2];        // output [T][H][W][cout]: box {32, 8, 16, 1} SW64 / {16, 8, 16, 1} SW32
 };
 
 // UMMA descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B
@@ -179,7 +187,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     const int NTF = p.ntf, NRAW = p.nraw, FZ_BSTAGES = p.nb;
     uint8_t *sTf = smem;                        // [NTF] transformed operand tiles
     uint8_t *sRaw = sTf + NTF * FZ_SLOT;        // [NRAW] raw SW128 boxes (16 KB)
-    uint8_t *sB = sRaw + NRAW * FZ_RAW_SLOT;    // [FZ_BSTAGES] weight tiles
+    uint8_t *sStage = sRaw + NRAW * FZ_RAW_SLOT;   // [2] epilogue staging (8 KB each, epi_tma)
+    uint8_t *sB = sStage + (p.epi_tma ? 2 * kEpiStage : 0);   // [FZ_BSTAGES] weight tiles
     uint64_t *tf_full = reinterpret_cast<uint64_t *>(sB + FZ_BSTAGES * B_STAGE);
     uint64_t *tf_empty = tf_full + FZ_MAX_NTF;
     uint64_t *b_full = tf_empty + FZ_MAX_NTF;
@@ -187,9 +196,9 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
     uint64_t *tfull = b_empty + FZ_BSTAGES;
     uint64_t *tempty = tfull + 2;
     uint64_t *raw_full = tempty + 2;   // [4] halo TMA (+ coefficients) landed in slot tb (local CTA)
-    uint64_t *rw_full = raw_full + FZ_MAX_NTF;  // [2] raw box landed (leader; both CTAs' bytes)
-    uint64_t *rw_empty = rw_full + 2;  // [2] raw slot free (MMA commit, both CTAs)
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rw_empty + 2);
+    uint64_t *rw_full = raw_full + FZ_MAX_NTF;  // [NRAW] raw box landed (leader; both CTAs' bytes)
+    uint64_t *rw_empty = rw_full + FZ_MAX_RAW;  // [NRAW] raw slot free (MMA commit, both CTAs)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rw_empty + FZ_MAX_RAW);
     float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][2][4][32] box-statistics staging
     float *sbias = red + 512;   // [2][cout] bias0, bias1 in fp32 (16-byte aligned: the barrier block is
                                 // 1024-aligned and holds an even number of 8-byte barriers)
@@ -213,7 +222,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
             mbar_init(&b_empty[s], 1);
         }
         for (int i = 0; i < FZ_MAX_NTF; ++i) mbar_init(&raw_full[i], 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < FZ_MAX_RAW; ++i) {
             mbar_init(&rw_full[i], CG);
             mbar_init(&rw_empty[i], 1);
         }
@@ -253,22 +262,21 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         for (int w = cluster_id; w < p.nwork; w += nclusters) {
             const int nt = w % p.ntile_n;
             const int n0 = nt * BN + (int)rank * BNH;
-            for (int s = 0; s < p.nseg; ++s) {
+            for (int st_i = 0; st_i < p.nsteps; ++st_i) {
+                const int s = p.ord[st_i] >> 6, ch = p.ord[st_i] & 63;
                 const FzSeg &sg = p.seg[s];
                 const int nch = (sg.c + 63) >> 6;
                 const CUtensorMap *bm = &p.bmap[sg.bidx];
-                for (int ch = 0; ch < nch; ++ch) {
-                    for (int tap = 0; tap < sg.taps; ++tap) {
-                        FZ_TIMED(0, mbar_wait_spin_addr(bempty0 + 8 * bs, bph ^ 1));
-                        // packed weights: the (tap, chunk) tile is one contiguous row block
-                        const int col = sg.packed ? 0 : sg.col0 + tap * sg.tapstride + ch * 64;
-                        const int row = sg.packed ? sg.col0 + (tap * nch + ch) * p.cout + n0 : n0;
-                        mbar_expect_tx_if(expect, bfull0 + 8 * bs, tx);
-                        tma_load_2d_if<CG>(issue, sB0 + bs * B_STAGE, bm, lead_bfull0 + 8 * bs, col, row);
-                        if (++bs == FZ_BSTAGES) {
-                            bs = 0;
-                            bph ^= 1;
-                        }
+                for (int tap = 0; tap < sg.taps; ++tap) {
+                    FZ_TIMED(0, mbar_wait_spin_addr(bempty0 + 8 * bs, bph ^ 1));
+                    // packed weights: the (tap, chunk) tile is one contiguous row block
+                    const int col = sg.packed ? 0 : sg.col0 + tap * sg.tapstride + ch * 64;
+                    const int row = sg.packed ? sg.col0 + (tap * nch + ch) * p.cout + n0 : n0;
+                    mbar_expect_tx_if(expect, bfull0 + 8 * bs, tx);
+                    tma_load_2d_if<CG>(issue, sB0 + bs * B_STAGE, bm, lead_bfull0 + 8 * bs, col, row);
+                    if (++bs == FZ_BSTAGES) {
+                        bs = 0;
+                        bph ^= 1;
                     }
                 }
             }
@@ -288,78 +296,77 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         const bool raw_role = warp == 0;
         for (int w = cluster_id; w < p.nwork; w += nclusters) {
             const FzBox bx = fz_box(p, (w / p.ntile_n) * CG + (int)rank);
-            for (int s = 0; s < p.nseg; ++s) {
+            for (int st_i = 0; st_i < p.nsteps; ++st_i) {
+                const int s = p.ord[st_i] >> 6, ch = p.ord[st_i] & 63;
                 const FzSeg &sg = p.seg[s];
                 const int nch = (sg.c + 63) >> 6;
                 if (raw_role == (sg.transform != 0)) continue;   // the other producer's segment
-                for (int ch = 0; ch < nch; ++ch) {
-                    if (!sg.transform) {   // raw ring
-                        FZ_TIMED(0, mbar_wait(&rw_empty[rb], rph ^ 1));
-                        if (issue) {
-                            const uint32_t fb = rw_full_leader + (uint32_t)(rb * 8);
-                            const uint32_t dst = smem_u32(sRaw + rb * FZ_RAW_SLOT);
-                            if constexpr (CG == 1) {
-                                mbar_arrive_expect_tx_addr(fb, FZ_RAW_SLOT);
-                                tma_load_4d(dst, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
-                            } else {
-                                mbar_arrive_expect_tx_cluster(fb, FZ_RAW_SLOT);
-                                tma_load_4d_cg2(dst, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
-                            }
-                        }
-                        __syncwarp();
-                        if (++rb == 2) {
-                            rb = 0;
-                            rph ^= 1;
-                        }
-                        continue;
-                    }
-                    FZ_TIMED(0, mbar_wait(&tf_empty[tb], tph ^ 1));
-                    const uint32_t slot = smem_u32(sTf + tb * FZ_SLOT);
+                if (!sg.transform) {   // raw ring
+                    FZ_TIMED(0, mbar_wait(&rw_empty[rb], rph ^ 1));
                     if (issue) {
-                        const int c0 = ch * 64;
-                        const int ngrp = min(8, (sg.c - c0) >> 3);
-                        const uint32_t rb = smem_u32(&raw_full[tb]);
-                        const uint32_t coef_bytes = bx.valid ? (uint32_t)ngrp * 64u : 0u;
-                        if (fz_sw_chunk(p, sg, c0)) {
-                            mbar_arrive_expect_tx_addr(rb, (uint32_t)FZ_HROWS * 128u + coef_bytes);
-                            tma_load_4d(slot, &p.wmap[s], rb, c0, bx.x0 - 1, bx.y0 - 1, bx.t);
-                            if (coef_bytes)
-                                bulk_load(slot + FZ_COEF, p.coef + (size_t)bx.t * p.cop + sg.cglob0 + c0, coef_bytes, rb);
-                            goto produced;
+                        const uint32_t fb = rw_full_leader + (uint32_t)(rb * 8);
+                        const uint32_t dst = smem_u32(sRaw + rb * FZ_RAW_SLOT);
+                        if constexpr (CG == 1) {
+                            mbar_arrive_expect_tx_addr(fb, FZ_RAW_SLOT);
+                            tma_load_4d(dst, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
+                        } else {
+                            mbar_arrive_expect_tx_cluster(fb, FZ_RAW_SLOT);
+                            tma_load_4d_cg2(dst, &p.smap[s], fb, ch * 64, bx.x0, bx.y0, bx.t);
                         }
-                        {
-                        int nside = 0;
-                        for (int g = 0; g < ngrp; ++g) {
-                            const int nprev = sg.shift ? min(max(p.cs - (c0 + 8 * g), 0), 8) : 0;
-                            nside += nprev > 0 && nprev < 8;
-                        }
-                        mbar_arrive_expect_tx_addr(rb, (uint32_t)(ngrp + nside) * FZ_COLB + coef_bytes);
-                        for (int g = 0; g < ngrp; ++g) {
-                            const int cl = c0 + 8 * g;
-                            const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
-                            const uint32_t dst = slot + (uint32_t)(g * FZ_LBO);
-                            if (nprev < 8)
-                                tma_load_4d(dst, &p.hmap[s], rb, cl, bx.x0 - 1, bx.y0 - 1, bx.t);
-                            if (nprev > 0) {
-                                // shifted channels: frame t-1, the carry at t = 0, or (no carry) a fully
-                                // out-of-bounds box = zeros
-                                const uint32_t pd = nprev < 8 ? slot + FZ_SIDE : dst;
-                                if (bx.t > 0 || !p.has_carry)
-                                    tma_load_4d(pd, &p.hmap[s], rb, cl, bx.x0 - 1, bx.y0 - 1, bx.t > 0 ? bx.t - 1 : -1);
-                                else
-                                    tma_load_4d(pd, &p.cmap, rb, cl, bx.x0 - 1, bx.y0 - 1, 0);
-                            }
-                        }
-                        if (coef_bytes)
-                            bulk_load(slot + FZ_COEF, p.coef + (size_t)bx.t * p.cop + sg.cglob0 + c0, coef_bytes, rb);
-                        }
-                    produced:;
                     }
                     __syncwarp();
-                    if (++tb == NTF) {
-                        tb = 0;
-                        tph ^= 1;
+                    if (++rb == NRAW) {
+                        rb = 0;
+                        rph ^= 1;
                     }
+                    continue;
+                }
+                FZ_TIMED(0, mbar_wait(&tf_empty[tb], tph ^ 1));
+                const uint32_t slot = smem_u32(sTf + tb * FZ_SLOT);
+                if (issue) {
+                    const int c0 = ch * 64;
+                    const int ngrp = min(8, (sg.c - c0) >> 3);
+                    const uint32_t rb = smem_u32(&raw_full[tb]);
+                    const uint32_t coef_bytes = bx.valid ? (uint32_t)ngrp * 64u : 0u;
+                    if (fz_sw_chunk(p, sg, c0)) {
+                        mbar_arrive_expect_tx_addr(rb, (uint32_t)FZ_HROWS * 128u + coef_bytes);
+                        tma_load_4d(slot, &p.wmap[s], rb, c0, bx.x0 - 1, bx.y0 - 1, bx.t);
+                        if (coef_bytes)
+                            bulk_load(slot + FZ_COEF, p.coef + (size_t)bx.t * p.cop + sg.cglob0 + c0, coef_bytes, rb);
+                        goto produced;
+                    }
+                    {
+                    int nside = 0;
+                    for (int g = 0; g < ngrp; ++g) {
+                        const int nprev = sg.shift ? min(max(p.cs - (c0 + 8 * g), 0), 8) : 0;
+                        nside += nprev > 0 && nprev < 8;
+                    }
+                    mbar_arrive_expect_tx_addr(rb, (uint32_t)(ngrp + nside) * FZ_COLB + coef_bytes);
+                    for (int g = 0; g < ngrp; ++g) {
+                        const int cl = c0 + 8 * g;
+                        const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
+                        const uint32_t dst = slot + (uint32_t)(g * FZ_LBO);
+                        if (nprev < 8)
+                            tma_load_4d(dst, &p.hmap[s], rb, cl, bx.x0 - 1, bx.y0 - 1, bx.t);
+                        if (nprev > 0) {
+                            // shifted channels: frame t-1, the carry at t = 0, or (no carry) a fully
+                            // out-of-bounds box = zeros
+                            const uint32_t pd = nprev < 8 ? slot + FZ_SIDE : dst;
+                            if (bx.t > 0 || !p.has_carry)
+                                tma_load_4d(pd, &p.hmap[s], rb, cl, bx.x0 - 1, bx.y0 - 1, bx.t > 0 ? bx.t - 1 : -1);
+                            else
+                                tma_load_4d(pd, &p.cmap, rb, cl, bx.x0 - 1, bx.y0 - 1, 0);
+                        }
+                    }
+                    if (coef_bytes)
+                        bulk_load(slot + FZ_COEF, p.coef + (size_t)bx.t * p.cop + sg.cglob0 + c0, coef_bytes, rb);
+                    }
+                produced:;
+                }
+                __syncwarp();
+                if (++tb == NTF) {
+                    tb = 0;
+                    tph ^= 1;
                 }
             }
         }
@@ -373,127 +380,126 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         const uint32_t tf_full_leader = CG == 2 ? mapa_shared(smem_u32(&tf_full[0]), 0) : smem_u32(&tf_full[0]);
         for (int w = cluster_id; w < p.nwork; w += nclusters) {
             const FzBox bx = fz_box(p, (w / p.ntile_n) * CG + (int)rank);
-            for (int s = 0; s < p.nseg; ++s) {
+            for (int st_i = 0; st_i < p.nsteps; ++st_i) {
+                const int s = p.ord[st_i] >> 6, ch = p.ord[st_i] & 63;
                 const FzSeg &sg = p.seg[s];
                 const int nch = (sg.c + 63) >> 6;
-                for (int ch = 0; ch < nch; ++ch) {
-                    if (!sg.transform) continue;   // raw segments use their own ring
-                    const int cl = ch * 64 + kg * 8;   // first channel (segment-local) of this warp
-                    uint8_t *slot = sTf + tb * FZ_SLOT;
-                    FZ_TIMED(0, mbar_wait(&raw_full[tb], (rph >> tb) & 1u));
-                    rph ^= 1u << tb;
-                    if (cl < sg.c) {   // warp-uniform; groups past the segment are never read by the MMA
-                        // GN affine of frame t for the 8 channels, z = v*sc + sh, and the same affine
-                        // pre-scaled by -log2(e) so that e^-z = ex2(v*sc2 + sh2) costs one FFMA
-                        float sc[8], sh[8], sc2[8], sh2[8];
-                        if (bx.valid) {
-                            const float4 *cf = reinterpret_cast<const float4 *>(slot + FZ_COEF + kg * 64);
+                if (!sg.transform) continue;   // raw segments use their own ring
+                const int cl = ch * 64 + kg * 8;   // first channel (segment-local) of this warp
+                uint8_t *slot = sTf + tb * FZ_SLOT;
+                FZ_TIMED(0, mbar_wait(&raw_full[tb], (rph >> tb) & 1u));
+                rph ^= 1u << tb;
+                if (cl < sg.c) {   // warp-uniform; groups past the segment are never read by the MMA
+                    // GN affine of frame t for the 8 channels, z = v*sc + sh, and the same affine
+                    // pre-scaled by -log2(e) so that e^-z = ex2(v*sc2 + sh2) costs one FFMA
+                    float sc[8], sh[8], sc2[8], sh2[8];
+                    if (bx.valid) {
+                        const float4 *cf = reinterpret_cast<const float4 *>(slot + FZ_COEF + kg * 64);
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                const float4 q = cf[i];
-                                sc[2 * i] = q.x, sh[2 * i] = q.y, sc[2 * i + 1] = q.z, sh[2 * i + 1] = q.w;
-                            }
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) sc[i] = 1.f, sh[i] = 0.f;
+                        for (int i = 0; i < 4; ++i) {
+                            const float4 q = cf[i];
+                            sc[2 * i] = q.x, sh[2 * i] = q.y, sc[2 * i + 1] = q.z, sh[2 * i + 1] = q.w;
                         }
+                    } else {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            if constexpr (FZ_SILU_TANH) sc[i] *= 0.5f, sh[i] *= 0.5f;   // hz = z / 2
-                            sc2[i] = sc[i] * -1.4426950408889634f, sh2[i] = sh[i] * -1.4426950408889634f;
-                        }
-                        // a group straddling C_in/P: its first nprev channels come from the side buffer.
-                        // C_in/P is even (C_in % 16 == 0): merge per 32-bit word.
-                        const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
-                        const bool straddle = nprev > 0 && nprev < 8;
-                        uint32_t msk[4];
+                        for (int i = 0; i < 8; ++i) sc[i] = 1.f, sh[i] = 0.f;
+                    }
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) msk[j] = 2 * j < nprev ? 0xFFFFFFFFu : 0u;
-                        // row r of this warp's 8 channels: SW128 chunk -> 16-byte unit kg ^ (r & 7) of the
-                        // 128-byte row r (the TMA swizzle); else row r of core-matrix column kg
-                        const bool sw = fz_sw_chunk(p, sg, ch * 64);
-                        auto roff = [&](int r) -> int { return sw ? r * 128 + ((kg ^ (r & 7)) << 4) : kg * FZ_LBO + r * 16; };
-                        constexpr int NR = FZ_TFW == 16 ? 3 : (FZ_HROWS + 31) / 32;   // halo rows per lane
-                        // all rows' words first (independent shared loads in flight), then two rows
-                        // (16 independent ex2 / rcp chains) per step
-                        uint32_t wv[NR][4];
+                    for (int i = 0; i < 8; ++i) {
+                        if constexpr (FZ_SILU_TANH) sc[i] *= 0.5f, sh[i] *= 0.5f;   // hz = z / 2
+                        sc2[i] = sc[i] * -1.4426950408889634f, sh2[i] = sh[i] * -1.4426950408889634f;
+                    }
+                    // a group straddling C_in/P: its first nprev channels come from the side buffer.
+                    // C_in/P is even (C_in % 16 == 0): merge per 32-bit word.
+                    const int nprev = sg.shift ? min(max(p.cs - cl, 0), 8) : 0;
+                    const bool straddle = nprev > 0 && nprev < 8;
+                    uint32_t msk[4];
 #pragma unroll
-                        for (int k = 0; k < NR; ++k) {
-                            const int r = row0 + lane + 32 * k;
-                            uint4 cu = make_uint4(0, 0, 0, 0);
-                            if (r < FZ_HROWS) {
-                                cu = *reinterpret_cast<const uint4 *>(slot + roff(r));
-                                if (straddle) {
-                                    const uint4 pv = *reinterpret_cast<const uint4 *>(slot + FZ_SIDE + r * 16);
-                                    cu.x = (pv.x & msk[0]) | (cu.x & ~msk[0]);
-                                    cu.y = (pv.y & msk[1]) | (cu.y & ~msk[1]);
-                                    cu.z = (pv.z & msk[2]) | (cu.z & ~msk[2]);
-                                    cu.w = (pv.w & msk[3]) | (cu.w & ~msk[3]);
-                                }
-                            }
-                            wv[k][0] = cu.x, wv[k][1] = cu.y, wv[k][2] = cu.z, wv[k][3] = cu.w;
-                        }
+                    for (int j = 0; j < 4; ++j) msk[j] = 2 * j < nprev ? 0xFFFFFFFFu : 0u;
+                    // row r of this warp's 8 channels: SW128 chunk -> 16-byte unit kg ^ (r & 7) of the
+                    // 128-byte row r (the TMA swizzle); else row r of core-matrix column kg
+                    const bool sw = fz_sw_chunk(p, sg, ch * 64);
+                    auto roff = [&](int r) -> int { return sw ? r * 128 + ((kg ^ (r & 7)) << 4) : kg * FZ_LBO + r * 16; };
+                    constexpr int NR = FZ_TFW == 16 ? 3 : (FZ_HROWS + 31) / 32;   // halo rows per lane
+                    // all rows' words first (independent shared loads in flight), then two rows
+                    // (16 independent ex2 / rcp chains) per step
+                    uint32_t wv[NR][4];
 #pragma unroll
-                        for (int k0 = 0; k0 < NR; k0 += 2) {
-                            float z[2][8], e[2][8];
-#pragma unroll
-                            for (int k = 0; k < 2; ++k)
-                                if (k0 + k < NR)
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    float v0, v1;
-                                    Pk<T>::unpack(wv[k0 + k][j], v0, v1);
-                                    z[k][2 * j] = fmaf(v0, sc[2 * j], sh[2 * j]);
-                                    z[k][2 * j + 1] = fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]);
-                                    if constexpr (FZ_SILU_TANH) {   // z holds hz = z / 2; e = tanh(hz)
-                                        e[k][2 * j] = fz_tanh(z[k][2 * j]);
-                                        e[k][2 * j + 1] = fz_tanh(z[k][2 * j + 1]);
-                                    } else if constexpr (FZ_TFW == 16) {   // register budget: u = -z log2(e) from z
-                                        e[k][2 * j] = fz_ex2(z[k][2 * j] * -1.4426950408889634f);
-                                        e[k][2 * j + 1] = fz_ex2(z[k][2 * j + 1] * -1.4426950408889634f);
-                                    } else {
-                                        e[k][2 * j] = fz_ex2(fmaf(v0, sc2[2 * j], sh2[2 * j]));
-                                        e[k][2 * j + 1] = fz_ex2(fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
-                                    }
-                                }
-#pragma unroll
-                            for (int k = 0; k < 2; ++k) {
-                                const int r = row0 + lane + 32 * (k0 + k);
-                                if (k0 + k >= NR || r >= FZ_HROWS) continue;
-                                const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
-                                const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
-                                // conv zero padding applies AFTER the transform (H3): out of frame -> 0
-                                const bool live = bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
-                                uint32_t o[4];
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    float h0, h1;
-                                    if constexpr (FZ_SILU_TANH) {
-                                        h0 = fmaf(z[k][2 * j], e[k][2 * j], z[k][2 * j]);
-                                        h1 = fmaf(z[k][2 * j + 1], e[k][2 * j + 1], z[k][2 * j + 1]);
-                                    } else {
-                                        h0 = z[k][2 * j] * fz_rcp(1.0f + e[k][2 * j]);
-                                        h1 = z[k][2 * j + 1] * fz_rcp(1.0f + e[k][2 * j + 1]);
-                                    }
-                                    o[j] = live ? Pk<T>::pack(h0, h1) : 0u;
-                                }
-                                *reinterpret_cast<uint4 *>(slot + roff(r)) = make_uint4(o[0], o[1], o[2], o[3]);
+                    for (int k = 0; k < NR; ++k) {
+                        const int r = row0 + lane + 32 * k;
+                        uint4 cu = make_uint4(0, 0, 0, 0);
+                        if (r < FZ_HROWS) {
+                            cu = *reinterpret_cast<const uint4 *>(slot + roff(r));
+                            if (straddle) {
+                                const uint4 pv = *reinterpret_cast<const uint4 *>(slot + FZ_SIDE + r * 16);
+                                cu.x = (pv.x & msk[0]) | (cu.x & ~msk[0]);
+                                cu.y = (pv.y & msk[1]) | (cu.y & ~msk[1]);
+                                cu.z = (pv.z & msk[2]) | (cu.z & ~msk[2]);
+                                cu.w = (pv.w & msk[3]) | (cu.w & ~msk[3]);
                             }
                         }
+                        wv[k][0] = cu.x, wv[k][1] = cu.y, wv[k][2] = cu.z, wv[k][3] = cu.w;
                     }
-                    FZ_TIMED(2, fence_proxy_async());   // generic-proxy smem writes -> visible to the tensor core
-                    FZ_TIMED(1, asm volatile("bar.sync 2, %0;" ::"n"(32 * FZ_TFW) : "memory"));   // the transform warps
-                    if (warp == 8 && elect_one()) {
-                        if constexpr (CG == 1)
-                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tf_full[tb]))
-                                         : "memory");
-                        else mbar_arrive_cluster(tf_full_leader + (uint32_t)(tb * 8));
+#pragma unroll
+                    for (int k0 = 0; k0 < NR; k0 += 2) {
+                        float z[2][8], e[2][8];
+#pragma unroll
+                        for (int k = 0; k < 2; ++k)
+                            if (k0 + k < NR)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                float v0, v1;
+                                Pk<T>::unpack(wv[k0 + k][j], v0, v1);
+                                z[k][2 * j] = fmaf(v0, sc[2 * j], sh[2 * j]);
+                                z[k][2 * j + 1] = fmaf(v1, sc[2 * j + 1], sh[2 * j + 1]);
+                                if constexpr (FZ_SILU_TANH) {   // z holds hz = z / 2; e = tanh(hz)
+                                    e[k][2 * j] = fz_tanh(z[k][2 * j]);
+                                    e[k][2 * j + 1] = fz_tanh(z[k][2 * j + 1]);
+                                } else if constexpr (FZ_TFW == 16) {   // register budget: u = -z log2(e) from z
+                                    e[k][2 * j] = fz_ex2(z[k][2 * j] * -1.4426950408889634f);
+                                    e[k][2 * j + 1] = fz_ex2(z[k][2 * j + 1] * -1.4426950408889634f);
+                                } else {
+                                    e[k][2 * j] = fz_ex2(fmaf(v0, sc2[2 * j], sh2[2 * j]));
+                                    e[k][2 * j + 1] = fz_ex2(fmaf(v1, sc2[2 * j + 1], sh2[2 * j + 1]));
+                                }
+                            }
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const int r = row0 + lane + 32 * (k0 + k);
+                            if (k0 + k >= NR || r >= FZ_HROWS) continue;
+                            const int hy = r / FZ_HX, hx = r - hy * FZ_HX;
+                            const int y = bx.y0 - 1 + hy, x = bx.x0 - 1 + hx;
+                            // conv zero padding applies AFTER the transform (H3): out of frame -> 0
+                            const bool live = bx.valid && y >= 0 && y < p.H && x >= 0 && x < p.W;
+                            uint32_t o[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                float h0, h1;
+                                if constexpr (FZ_SILU_TANH) {
+                                    h0 = fmaf(z[k][2 * j], e[k][2 * j], z[k][2 * j]);
+                                    h1 = fmaf(z[k][2 * j + 1], e[k][2 * j + 1], z[k][2 * j + 1]);
+                                } else {
+                                    h0 = z[k][2 * j] * fz_rcp(1.0f + e[k][2 * j]);
+                                    h1 = z[k][2 * j + 1] * fz_rcp(1.0f + e[k][2 * j + 1]);
+                                }
+                                o[j] = live ? Pk<T>::pack(h0, h1) : 0u;
+                            }
+                            *reinterpret_cast<uint4 *>(slot + roff(r)) = make_uint4(o[0], o[1], o[2], o[3]);
+                        }
                     }
-                    __syncwarp();
-                    if (++tb == NTF) {
-                        tb = 0;
-                        tph ^= 1;
-                    }
+                }
+                FZ_TIMED(2, fence_proxy_async());   // generic-proxy smem writes -> visible to the tensor core
+                FZ_TIMED(1, asm volatile("bar.sync 2, %0;" ::"n"(32 * FZ_TFW) : "memory"));   // the transform warps
+                if (warp == 8 && elect_one()) {
+                    if constexpr (CG == 1)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tf_full[tb]))
+                                     : "memory");
+                    else mbar_arrive_cluster(tf_full_leader + (uint32_t)(tb * 8));
+                }
+                __syncwarp();
+                if (++tb == NTF) {
+                    tb = 0;
+                    tph ^= 1;
                 }
             }
         }
@@ -516,71 +522,70 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(buf * BN);
                 uint32_t acc = 0;
-                for (int s = 0; s < p.nseg; ++s) {
+                for (int st_i = 0; st_i < p.nsteps; ++st_i) {
+                    const int s = p.ord[st_i] >> 6, ch = p.ord[st_i] & 63;
                     const FzSeg &sg = p.seg[s];
                     const int nch = (sg.c + 63) >> 6;
                     const uint32_t klast = (uint32_t)(sg.c - 64 * (nch - 1)) >> 4;
                     // transformed tile: K step of 16 channels = two 8-channel core-matrix columns of
                     // the halo layout (no swizzle); raw segment: the TMA box in SW128
                     const bool tf = sg.transform != 0;
-                    for (int ch = 0; ch < nch; ++ch) {
-                        const uint32_t ks = ch == nch - 1 ? klast : 4u;
-                        if (!tf) {   // raw 1x1 chunk from the raw ring (SW128 box): one tap
-                            FZ_TIMED(1, mbar_wait_spin_addr(rwfull0 + 8 * rb, rph));
-                            tc_fence_after();
-                            FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
-                            tc_fence_after();
-                            mma_stage<CG>(d, desc_lo(sR0 + (uint32_t)(rb * FZ_RAW_SLOT), 16), kDescHiSw128, 2u, b_lo,
-                                          kDescHiSw128, p.idesc, ks, acc, bempty0 + 8 * bs);
-                            acc = 1;
-                            commit_elected<CG>(rwempty0 + 8 * rb);
-                            b_lo += b_inc;
-                            if (++bs == FZ_BSTAGES) {
-                                bs = 0;
-                                bph ^= 1;
-                                b_lo = b_lo0;
-                            }
-                            if (++rb == 2) {
-                                rb = 0;
-                                rph ^= 1;
-                            }
-                            continue;
-                        }
-                        FZ_TIMED(1, mbar_wait_spin_addr(tffull0 + 8 * tb, tph));
+                    const uint32_t ks = ch == nch - 1 ? klast : 4u;
+                    if (!tf) {   // raw 1x1 chunk from the raw ring (SW128 box): one tap
+                        FZ_TIMED(1, mbar_wait_spin_addr(rwfull0 + 8 * rb, rph));
                         tc_fence_after();
-                        // transformed tile (no swizzle, 8-channel core-matrix columns FZ_LBO apart, image
-                        // rows FZ_SBO apart): tap (dy, dx) starts (1+dy)*10 + (1+dx) halo rows in; a K step
-                        // of 16 channels = two core-matrix columns
-                        // SW128 chunk: rows of 128 B, image rows FZ_HX * 128 B apart, tap offset in
-                        // whole rows, K step +32 B
-                        const bool sw = fz_sw_chunk(p, sg, ch * 64);
-                        const uint32_t a_base = sT0 + (uint32_t)(tb * FZ_SLOT);
-                        const uint32_t a_lo0 = sw ? desc_lo(a_base, 16) : desc_lo(a_base, FZ_LBO);
-                        const uint32_t a_hi = sw ? desc_hi_sw128(FZ_HX * 128) : desc_hi_noswz(FZ_SBO);
-                        const uint32_t a_step = sw ? 2u : (uint32_t)(2 * FZ_LBO) >> 4;
-                        const uint32_t a_row = sw ? 8u : 1u;   // one halo row in 16-byte units
+                        FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
+                        tc_fence_after();
+                        mma_stage<CG>(d, desc_lo(sR0 + (uint32_t)(rb * FZ_RAW_SLOT), 16), kDescHiSw128, 2u, b_lo,
+                                      kDescHiSw128, p.idesc, ks, acc, bempty0 + 8 * bs);
+                        acc = 1;
+                        commit_elected<CG>(rwempty0 + 8 * rb);
+                        b_lo += b_inc;
+                        if (++bs == FZ_BSTAGES) {
+                            bs = 0;
+                            bph ^= 1;
+                            b_lo = b_lo0;
+                        }
+                        if (++rb == NRAW) {
+                            rb = 0;
+                            rph ^= 1;
+                        }
+                        continue;
+                    }
+                    FZ_TIMED(1, mbar_wait_spin_addr(tffull0 + 8 * tb, tph));
+                    tc_fence_after();
+                    // transformed tile (no swizzle, 8-channel core-matrix columns FZ_LBO apart, image
+                    // rows FZ_SBO apart): tap (dy, dx) starts (1+dy)*10 + (1+dx) halo rows in; a K step
+                    // of 16 channels = two core-matrix columns
+                    // SW128 chunk: rows of 128 B, image rows FZ_HX * 128 B apart, tap offset in
+                    // whole rows, K step +32 B
+                    const bool sw = fz_sw_chunk(p, sg, ch * 64);
+                    const uint32_t a_base = sT0 + (uint32_t)(tb * FZ_SLOT);
+                    const uint32_t a_lo0 = sw ? desc_lo(a_base, 16) : desc_lo(a_base, FZ_LBO);
+                    const uint32_t a_hi = sw ? desc_hi_sw128(FZ_HX * 128) : desc_hi_noswz(FZ_SBO);
+                    const uint32_t a_step = sw ? 2u : (uint32_t)(2 * FZ_LBO) >> 4;
+                    const uint32_t a_row = sw ? 8u : 1u;   // one halo row in 16-byte units
 #pragma unroll
-                        for (int tap = 0; tap < 9; ++tap) {
-                            FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
-                            tc_fence_after();
-                            const uint32_t roff16 = (uint32_t)((tap / 3) * FZ_HX + tap % 3) * a_row;
-                            // optional matrix base offset (bits 49-51): the 1024-B pattern phase of the start
-                            const uint32_t bo = sw && p.sw_mode == 2 ? (((a_base >> 7) + roff16 / 8) & 7u) << 17 : 0u;
-                            mma_stage<CG>(d, a_lo0 + roff16, a_hi | bo, a_step, b_lo, kDescHiSw128, p.idesc, ks, acc,
-                                          bempty0 + 8 * bs);
-                            acc = 1;
-                            b_lo += b_inc;
-                            if (++bs == FZ_BSTAGES) {
-                                bs = 0;
-                                bph ^= 1;
-                                b_lo = b_lo0;
-                            }
+                    for (int tap = 0; tap < 9; ++tap) {
+                        FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
+                        tc_fence_after();
+                        const uint32_t roff16 = (uint32_t)((tap / 3) * FZ_HX + tap % 3) * a_row;
+                        // optional matrix base offset (bits 49-51): the 1024-B pattern phase of the start
+                        const uint32_t bo = sw && p.sw_mode == 2 ? (((a_base >> 7) + roff16 / 8) & 7u) << 17 : 0u;
+                        mma_stage<CG>(d, a_lo0 + roff16, a_hi | bo, a_step, b_lo, kDescHiSw128, p.idesc, ks, acc,
+                                      bempty0 + 8 * bs);
+                        acc = 1;
+                        b_lo += b_inc;
+                        if (++bs == FZ_BSTAGES) {
+                            bs = 0;
+                            bph ^= 1;
+                            b_lo = b_lo0;
                         }
-                        commit_elected<CG>(tfempty0 + 8 * tb);   // the tile slot is free once its taps retire
-                        if (++tb == NTF) {
-                            tb = 0;
-                            tph ^= 1;
-                        }
+                    }
+                    commit_elected<CG>(tfempty0 + 8 * tb);   // the tile slot is free once its taps retire
+                    if (++tb == NTF) {
+                        tb = 0;
+                        tph ^= 1;
                     }
                 }
                 commit_elected<CG>(smem_u32(&tfull[buf]));
@@ -643,11 +648,63 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 }
                 if (want_stats) box_row_values(f, true, x);
             };
+            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
+            int par = 0;
+            if (p.epi_tma) {
+                // Staged epilogue, per 32-column chunk: TMEM -> registers (thread = box row) -> + bias,
+                // 16-bit rounding -> a swizzled [128 rows][32 cols] tile in shared memory (zeros for rows
+                // outside the frame) -> one TMA store of the {32, 8, 16, 1} box (the hardware clips the
+                // out-of-frame rows); the box statistics are then read back column-wise (lane = column,
+                // warp q4 = rows 32*q4..32*q4+31) and reduced with the canonical tree of dvc_boxstats.cuh
+                // (pairs of rows differing in bit 4, then 3, 2, 1, 0; warps combined ((w0+w1)+w2)+w3),
+                // i.e. bit for bit what the butterfly produced, without the 62 shuffles per 16 columns.
+                const bool issuer = warp == 4 && lane == 0;
+#pragma unroll 1
+                for (int cc = 0; cc < BN; cc += 32, par ^= 1) {
+                    const bool two = cc + 16 < BN;   // warp-uniform: 32 or 16 columns
+                    const int n = nt * BN + cc;
+                    uint32_t va[16], vb[16];
+                    tmem_ld16_nowait(taddr + (uint32_t)cc, va);
+                    if (two) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
+                    tmem_wait16(va);
+                    if (two) tmem_wait16(vb);
+                    if (cc + 32 >= BN) {   // the accumulator is drained: the MMA may reuse it
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if constexpr (CG == 1)
+                                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf]))
+                                             : "memory");
+                            else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                        }
+                    }
+                    float f[32];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        f[i] = __uint_as_float(va[i]);
+                        f[16 + i] = __uint_as_float(vb[i]);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        if (i >= 16 && !two) break;
+                        if (sb0) {
+                            const float4 e = *reinterpret_cast<const float4 *>(sb0 + n + i);
+                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
+                        }
+                        if (sb1) {
+                            const float4 e = *reinterpret_cast<const float4 *>(sb1 + n + i);
+                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
+                        }
+                    }
+                    epi_stage_chunk<T>(f, m >= 0, two, r, q4, lane, sStage + par * kEpiStage, &p.omap[0], &p.omap[1],
+                                       issuer, bx.valid, n, bx.x0, bx.y0, bx.t,
+                                       want_stats ? stats_box + (size_t)n * 2 : nullptr, red + par * 256);
+                }
+                continue;
+            }
             // TMEM -> registers 32 columns at a time (two 16-column loads in flight); the box
             // statistics of both chunks are reduced together (two independent butterflies, one
             // barrier per 32 columns) and combined by warps 0 / 1 (canonical order, dvc_boxstats.cuh)
-            const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
-            int par = 0;
 #pragma unroll 1
             for (int cc = 0; cc < BN; cc += 32, par ^= 1) {
                 const bool two = cc + 16 < BN;   // warp-uniform
@@ -683,6 +740,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         }
     }
 #undef FZ_TIMED
+    if (p.epi_tma && warp == 4 && lane == 0) bulk_wait_group<0>();   // every staged store has landed
     if constexpr (PROF) {
         const int role = warp == 1 ? 0 : warp == 4 ? 1 : warp == 8 ? 2 : warp == 3 ? 3 : warp == 2 ? 4 : -1;
         if (role >= 0 && lane == 0 && !(role == 0 && rank != 0)) {
@@ -740,6 +798,24 @@ static dvc_status make_halo_map(CUtensorMap *map, const void *ptr, dvc_dtype dt,
                      box_c == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (halo) failed (%d)", (int)r);
+    return DVC_OK;
+}
+
+// output box {c, 8, 16, 1} of a [T][H][W][cout] tensor for the staged epilogue's TMA store: 32 channels
+// (64-byte rows, SWIZZLE_64B) or 16 (32-byte rows, SWIZZLE_32B), matching the staging layout
+static dvc_status make_out_map(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, int H, int W, int C, int box_c) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && C % 8 == 0, DVC_ERR_ARG, "fused conv: output alignment");
+    cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
+    cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)FZ_BX, (cuuint32_t)FZ_BY, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, ptr,
+                     gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed (%d)", (int)r);
     return DVC_OK;
 }
 
@@ -839,7 +915,54 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     p.nraw = 0;
     for (int s = 0; s < d.nseg; ++s)
         if (!d.seg[s].transform) p.nraw = 2;
-    const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (size_t)p.nraw * FZ_RAW_SLOT + 8 * (8 + 3 * FZ_MAX_NTF + 2 * FZ_MAX_BSTAGES) +
+    if (p.nraw) {
+        // raw-heavy convs (1x1 shortcut chunks >= 2x the 3x3 chunks, e.g. up3.r0's 720 -> 240 conv2):
+        // one transform slot less, one raw slot more (same-box A/B: 0.665 -> 0.528 ms); DVC_FZ_NRAW
+        // (experiment builds) overrides the depth
+        int ntfc = 0, nrawc = 0;
+        for (int s = 0; s < d.nseg; ++s) (d.seg[s].transform ? ntfc : nrawc) += (d.seg[s].c + 63) / 64;
+        if (nrawc >= 2 * ntfc && !dvc_knob("DVC_FZ_NTF")) p.ntf = 3, p.nraw = 3;
+        const char *e = dvc_knob("DVC_FZ_NRAW");
+        if (e && atoi(e) >= 2 && atoi(e) <= FZ_MAX_RAW) p.nraw = atoi(e);
+    }
+    // K-loop order of a work item: the 3x3 (transformed) chunks in segment order, with the raw 1x1
+    // chunks spread evenly among them, so the 2-slot raw ring refills during the 9-tap chunks instead
+    // of stalling the MMA on back-to-back raw chunks at the end (DVC_FZ_ILV=0: segment order)
+    {
+        std::vector<int> tfs, raws;
+        for (int s = 0; s < d.nseg; ++s)
+            for (int ch = 0; ch < (d.seg[s].c + 63) / 64; ++ch) (d.seg[s].transform ? tfs : raws).push_back(s << 6 | ch);
+        DVC_CHECK_ARG(!tfs.empty() && tfs.size() + raws.size() <= 64, DVC_ERR_UNSUPPORTED,
+                      "fused conv: 1..64 chunks with a 3x3 segment first");
+        const char *e = dvc_knob("DVC_FZ_ILV");
+        const bool ilv = e ? atoi(e) != 0 : true;
+        std::vector<int> ord;
+        if (!ilv) {
+            for (int s = 0; s < d.nseg; ++s)
+                for (int ch = 0; ch < (d.seg[s].c + 63) / 64; ++ch) ord.push_back(s << 6 | ch);
+        } else {
+            const size_t nt = tfs.size(), nr = raws.size();
+            size_t r = 0;
+            for (size_t k = 0; k < nt; ++k) {
+                ord.push_back(tfs[k]);
+                for (const size_t r1 = (k + 1) * nr / nt; r < r1; ++r) ord.push_back(raws[r]);
+            }
+        }
+        DVC_CHECK_ARG(d.seg[ord[0] >> 6].transform, DVC_ERR_UNSUPPORTED, "fused conv: K loop must start with a 3x3 chunk");
+        p.nsteps = (int)ord.size();
+        for (size_t i = 0; i < ord.size(); ++i) p.ord[i] = (unsigned char)ord[i];
+    }
+    {   // staged TMA-store epilogue (default; DVC_FZ_EPI=0 in experiment builds: per-thread row stores)
+        const char *e = dvc_knob("DVC_FZ_EPI");
+        p.epi_tma = e ? atoi(e) : 1;
+    }
+    if (p.epi_tma) {
+        st = make_out_map(&p.omap[0], d.out, d.dt, d.T, d.H, d.W, d.cout, 32);
+        if (st == DVC_OK) st = make_out_map(&p.omap[1], d.out, d.dt, d.T, d.H, d.W, d.cout, 16);
+        if (st != DVC_OK) return st;
+    }
+    const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (size_t)p.nraw * FZ_RAW_SLOT +
+                         (p.epi_tma ? 2 * kEpiStage : 0) + 8 * (4 + 2 * FZ_MAX_RAW + 3 * FZ_MAX_NTF + 2 * FZ_MAX_BSTAGES) +
                          16 + 2048 /* red */ +
                          1024 /* static */ + 16 + (size_t)2 * d.cout * 4 /* bias */;
     const size_t bstage = (size_t)(bn / CG) * 128;

@@ -23,6 +23,7 @@
 #include "dvc_conv.cuh"
 #include "dvc_ptx.cuh"
 #include "dvc_boxstats.cuh"
+#include "dvc_epilogue.cuh"
 
 namespace dvc {
 
@@ -43,6 +44,8 @@ struct WsParams {
     int fp8;        // ConvDesc::fp8: E4M3 operands, 128 channels per 128-byte stage row, kind::f8f6f4
     int chw;        // channels per stage: 64 (16-bit) or 128 (fp8)
     float out_scale;
+    int epi_tma;           // staged epilogue (dvc_epilogue.cuh): TMA-stored 32-column chunks
+    CUtensorMap omap[2];   // output [T][H][W][cout], box {32 | 16, BX, BY, 1}, SW64 / SW32
 };
 
 constexpr int kWsThreads = 256;
@@ -58,7 +61,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
     const int B_STAGE = BNH * 128;
     uint8_t *sA = smem;
     uint8_t *sB = sA + STAGES * A_STAGE;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * B_STAGE);
+    uint8_t *sStage = sB + STAGES * B_STAGE;   // [2] epilogue staging (epi_tma)
+    uint64_t *full = reinterpret_cast<uint64_t *>(sStage + (p.epi_tma ? 2 * kEpiStage : 0));
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
@@ -299,6 +303,71 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                 }
                 continue;
             }
+            if (p.epi_tma) {   // staged epilogue (dvc_epilogue.cuh)
+                const bool issuer = warp == 4 && lane == 0;
+                int bt = p.T, bx0 = 0, by0 = 0;
+                if (box < p.nbox) {
+                    bt = box / per;
+                    const int rem = box - bt * per;
+                    by0 = (rem / p.tiles_x) * p.BY;
+                    bx0 = (rem % p.tiles_x) * p.BX;
+                }
+#pragma unroll 1
+                for (int cc = 0; cc < BN; cc += 32, par ^= 1) {
+                    const bool two = cc + 16 < BN;   // warp-uniform: 32 or 16 columns
+                    const int n = nt * BN + cc;
+                    uint32_t va[16], vb[16];
+                    tmem_ld16_nowait(taddr + (uint32_t)cc, va);
+                    if (two) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
+                    float rv[32];
+                    if (res && m >= 0) {   // the residual loads overlap the TMEM loads
+                        load8(res + m * p.cout + n, *reinterpret_cast<float(*)[8]>(&rv[0]));
+                        load8(res + m * p.cout + n + 8, *reinterpret_cast<float(*)[8]>(&rv[8]));
+                        if (two) {
+                            load8(res + m * p.cout + n + 16, *reinterpret_cast<float(*)[8]>(&rv[16]));
+                            load8(res + m * p.cout + n + 24, *reinterpret_cast<float(*)[8]>(&rv[24]));
+                        }
+                    }
+                    tmem_wait16(va);
+                    if (two) tmem_wait16(vb);
+                    if (cc + 32 >= BN) {   // the accumulator is drained: the MMA may reuse it
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if constexpr (CG == 1)
+                                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf]))
+                                             : "memory");
+                            else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                        }
+                    }
+                    float f[32];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        f[i] = __uint_as_float(va[i]) * p.out_scale;
+                        f[16 + i] = __uint_as_float(vb[i]) * p.out_scale;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        if (i >= 16 && !two) break;
+                        if (sb0) {
+                            const float4 e = *reinterpret_cast<const float4 *>(sb0 + n + i);
+                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
+                        }
+                        if (sb1) {
+                            const float4 e = *reinterpret_cast<const float4 *>(sb1 + n + i);
+                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
+                        }
+                    }
+                    if (res && m >= 0) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) f[i] += rv[i];
+                    }
+                    epi_stage_chunk<T>(f, m >= 0, two, r, q4, lane, sStage + par * kEpiStage, &p.omap[0], &p.omap[1],
+                                       issuer, box < p.nbox, n, bx0, by0, bt,
+                                       want_stats ? stats_box + (size_t)n * 2 : nullptr, red + par * 256);
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int cc = 0; cc < BN; cc += 32, par ^= 1) {
                 const bool two = cc + 16 < BN;   // warp-uniform
@@ -333,6 +402,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
             }
         }
     }
+    if (p.epi_tma && warp == 4 && lane == 0) bulk_wait_group<0>();   // every staged store has landed
     tc_fence_before();
     __syncthreads();
     if constexpr (CG == 2) cluster_sync_all();
@@ -408,7 +478,8 @@ static int g_num_sms = 0;
 
 template <typename T, int CG, int STAGES>
 static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
-    const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + 8 * (2 * STAGES + 4) + 16 + 2048 +
+    const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + (p.epi_tma ? 2 * kEpiStage : 0) +
+                        8 * (2 * STAGES + 4) + 16 + 2048 +
                         (size_t)(p.bias1 ? 2 : 1) * p.cout * 4;   // bias1 staged only when present
     auto kern = conv_ws_kernel<T, CG, STAGES>;
     {   // host cost: the attribute is set once per kernel / size
@@ -455,6 +526,25 @@ static dvc_status make_bmap8(CUtensorMap *map, const void *ptr, long rows, long 
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (fp8 weights) failed (%d)", (int)r);
+    return DVC_OK;
+}
+
+// output box {c, BX, BY, 1} of a [T][H][W][C] 16-bit tensor for the staged epilogue's TMA store: 32 channels
+// (64-byte rows, SWIZZLE_64B) or 16 (32-byte rows, SWIZZLE_32B), matching dvc_epilogue.cuh's staging
+dvc_status make_out_map_box(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, int H, int W, int C, int box_c, int BX,
+                            int BY) {
+    PFN_encodeTiled_t enc = get_encode_fn();
+    DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && C % 8 == 0, DVC_ERR_ARG, "conv output alignment");
+    cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
+    cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)BX, (cuuint32_t)BY, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, ptr,
+                     gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed (%d)", (int)r);
     return DVC_OK;
 }
 
@@ -561,6 +651,15 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
             DVC_CHECK_ARG(d.seg[s].c_src % 32 == 0 && !d.seg[s].packed && d.seg[s].w_ld % 16 == 0, DVC_ERR_UNSUPPORTED,
                           "fp8 conv: channels multiple of 32, unpacked 16-byte weight rows");
     p.stats = reinterpret_cast<float *>(d.stats_out);
+    {   // staged TMA-store epilogue (DVC_WS_EPI=0 in experiment builds: per-thread row stores)
+        const char *e = dvc_knob("DVC_WS_EPI");
+        p.epi_tma = !d.geglu && (e ? atoi(e) != 0 : true);
+    }
+    if (p.epi_tma) {
+        st = make_out_map_box(&p.omap[0], d.out, d.dt, d.T, d.ho, d.wo, d.cout, 32, p.BX, p.BY);
+        if (st == DVC_OK) st = make_out_map_box(&p.omap[1], d.out, d.dt, d.T, d.ho, d.wo, d.cout, 16, p.BX, p.BY);
+        if (st != DVC_OK) return st;
+    }
     if (CG == 2) {
         if (bf) return launch_ws<__nv_bfloat16, 2, 6>(p, stream);
         return launch_ws<__half, 2, 6>(p, stream);

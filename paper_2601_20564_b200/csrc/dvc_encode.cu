@@ -29,9 +29,25 @@ namespace dvc {
 constexpr int ENC_BX = 8, ENC_BY = 16;         // latent pixels per tile (128 MMA rows)
 constexpr int ENC_A_BYTES = 3 * 64 * 128 * 2;  // 49152: {64, 8, 16, 3} 16-bit box
 constexpr int ENC_THREADS = 256;
+constexpr int ENC_U8_THREADS = 384;             // + warps 8-11: the u8 -> 16-bit converters
+constexpr int ENC_U8_HALF = 64 * 192;           // u8 staging slot: 64 frame rows x 64 pixels x 3 bytes
+
+template <typename T> struct Pk2;
+template <> struct Pk2<__nv_bfloat16> {
+    static __device__ __forceinline__ uint32_t pack(float a, float b) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+};
+template <> struct Pk2<__half> {
+    static __device__ __forceinline__ uint32_t pack(float a, float b) {
+        __half2 h = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+};
 
 struct EncParams {
-    CUtensorMap amap;   // 4D frames view, box {64, 8, 16, 3}, no swizzle
+    CUtensorMap amap;   // 4D frames view, box {64, 8, 16, 3}, no swizzle (u8: 3D bytes view, box {192, 64, 1})
     CUtensorMap bmap;   // expansion weights [c_lat][192], box {64, c_lat}, SW128
     int T, h, w, c_lat;
     int tiles_x, tiles_y, ntiles;
@@ -40,8 +56,12 @@ struct EncParams {
     uint32_t idesc;
 };
 
-template <typename T>
-__global__ void __launch_bounds__(ENC_THREADS, 1) encode_kernel(const __grid_constant__ EncParams p) {
+// U8: the frames are 8-bit HWC [T][H][W][3] (R14: value RNE16(u / 255)).  The TMA cannot convert or
+// de-interleave, so warp 0 streams half tiles (64 frame rows x 64 pixels x 3 bytes) into two staging
+// slots and four converter warps (8-11) write the same [c][hb][dy][wb][dx] 16-bit A tile the 16-bit
+// path gets from the TMA; the MMA and epilogue are shared.
+template <typename T, bool U8>
+__global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_kernel(const __grid_constant__ EncParams p) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int N = p.c_lat;
@@ -53,17 +73,22 @@ __global__ void __launch_bounds__(ENC_THREADS, 1) encode_kernel(const __grid_con
     uint64_t *tfull = a_empty + 2;
     uint64_t *tempty = tfull + 2;
     uint64_t *b_full = tempty + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_full + 2);
+    uint64_t *u_full = b_full + 2;    // [2] u8 staging slot landed (U8)
+    uint64_t *u_empty = u_full + 2;   // [2] u8 staging slot converted (U8)
+    uint8_t *sU = sB + 3 * B_CHUNK + 2048;   // [2][ENC_U8_HALF] u8 staging (U8; after barriers + bias)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(u_empty + 2);
     float *sbias = reinterpret_cast<float *>(tmem_slot + 4);   // [c_lat]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t ncols = 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&a_full[i], 1);
+            mbar_init(&a_full[i], U8 ? 8 : 1);   // U8: 4 converter warps x 2 half tiles
             mbar_init(&a_empty[i], 1);
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
+            mbar_init(&u_full[i], 1);
+            mbar_init(&u_empty[i], 4);
         }
         mbar_init(&b_full[0], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -72,7 +97,7 @@ __global__ void __launch_bounds__(ENC_THREADS, 1) encode_kernel(const __grid_con
         tma_prefetch(&p.bmap);
     }
     if (warp == 1) tmem_alloc<1>(smem_u32(tmem_slot), ncols);
-    for (int i = tid; i < N; i += ENC_THREADS) sbias[i] = Elem<T>::to_f(reinterpret_cast<const T *>(p.bias)[i]);
+    for (int i = tid; i < N; i += (U8 ? ENC_U8_THREADS : ENC_THREADS)) sbias[i] = Elem<T>::to_f(reinterpret_cast<const T *>(p.bias)[i]);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -94,6 +119,23 @@ __global__ void __launch_bounds__(ENC_THREADS, 1) encode_kernel(const __grid_con
             const int per = p.tiles_x * p.tiles_y;
             const int t = tile / per, rem = tile - t * per;
             const int by = rem / p.tiles_x, bx = rem - by * p.tiles_x;
+            if constexpr (U8) {   // two half tiles into the staging slots (the converters free them)
+                for (int hh = 0; hh < 2; ++hh) {
+                    mbar_wait_spin(&u_empty[stage], phase ^ 1);
+                    if (issue) {
+                        const uint32_t fb = smem_u32(&u_full[stage]);
+                        mbar_arrive_expect_tx_addr(fb, ENC_U8_HALF);
+                        tma_load_3d(smem_u32(sU + stage * ENC_U8_HALF), &p.amap, fb, bx * ENC_BX * 8 * 3,
+                                    by * ENC_BY * 8 + hh * 64, t);
+                    }
+                    __syncwarp();
+                    if (++stage == 2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                continue;
+            }
             mbar_wait_spin(&a_empty[stage], phase ^ 1);
             if (issue) {
                 const uint32_t fb = smem_u32(&a_full[stage]);
@@ -139,7 +181,63 @@ __global__ void __launch_bounds__(ENC_THREADS, 1) encode_kernel(const __grid_con
                 phase ^= 1;
             }
         }
-    } else if (warp >= 4) {
+    } else if (U8 && warp >= 8) {
+        // ===================== u8 -> 16-bit converters (R14) =====================
+        // half tile hh = frame rows [64 hh, 64 hh + 64) of the tile = latent rows hb in [8 hh, 8 hh + 8);
+        // thread item j: (hbl, dy, wb) reads the 24 bytes of 8 pixels x 3 colours of frame row
+        // 8 hbl + dy and writes three 16-byte core-matrix rows (one per colour) of the A tile.
+        // u / 255 as fp32 product with the fp32 constant 1/255, rounded once to 16 bits: equal to the
+        // exactly rounded RNE16(u / 255) for all 256 values in fp16 and bf16 (tests: exhaustive, G2).
+        const int ct = tid - 256;
+        int astage = 0, ustage = 0;
+        uint32_t aphase = 0, uphase = 0;
+        for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+            mbar_wait(&a_empty[astage], aphase ^ 1);
+            uint8_t *A = sA + astage * ENC_A_BYTES;
+            for (int hh = 0; hh < 2; ++hh) {
+                mbar_wait(&u_full[ustage], uphase);
+                const uint8_t *U = sU + ustage * ENC_U8_HALF;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int j = ct + 128 * k;
+                    const int wb = j & 7, dy = (j >> 3) & 7, hbl = j >> 6;
+                    const uint2 *src = reinterpret_cast<const uint2 *>(U + (hbl * 8 + dy) * 192 + wb * 24);
+                    const uint2 q0 = src[0], q1 = src[1], q2 = src[2];
+                    const uint32_t wv[6] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y};
+                    uint32_t o[3][4];
+#pragma unroll
+                    for (int dx = 0; dx < 8; dx += 2) {
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const int b0 = 3 * dx + c, b1 = 3 * (dx + 1) + c;
+                            const float f0 = (float)((wv[b0 >> 2] >> (8 * (b0 & 3))) & 0xFFu) * (1.0f / 255.0f);
+                            const float f1 = (float)((wv[b1 >> 2] >> (8 * (b1 & 3))) & 0xFFu) * (1.0f / 255.0f);
+                            o[c][dx >> 1] = Pk2<T>::pack(f0, f1);
+                        }
+                    }
+                    const int hb = hh * 8 + hbl;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        *reinterpret_cast<uint4 *>(A + c * 16384 + hb * 1024 + dy * 128 + wb * 16) =
+                            make_uint4(o[c][0], o[c][1], o[c][2], o[c][3]);
+                }
+                fence_proxy_async();   // generic smem writes -> the tensor core (async proxy)
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&u_empty[ustage])) : "memory");
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&a_full[astage])) : "memory");
+                }
+                if (++ustage == 2) {
+                    ustage = 0;
+                    uphase ^= 1;
+                }
+            }
+            if (++astage == 2) {
+                astage = 0;
+                aphase ^= 1;
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
         // ===================== epilogue: + bias, 16-bit store =====================
         const int q4 = warp & 3;
         const int r = q4 * 32 + lane;   // accumulator row = latent pixel (r / 8, r % 8) of the box
@@ -199,29 +297,42 @@ PFN_encodeTiled_t get_encode_fn();
 dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
 
 bool encode_tma_applicable(dvc_dtype dt, int H, int W, int s, int c_lat) {
-    return dt != DVC_F32 && s == 8 && H % 8 == 0 && W % 8 == 0 && c_lat >= 16 && c_lat <= 256 && c_lat % 16 == 0 &&
-           (W / 8) >= 1;
+    return (dt == DVC_BF16 || dt == DVC_F16) && s == 8 && H % 8 == 0 && W % 8 == 0 && c_lat >= 16 && c_lat <= 256 &&
+           c_lat % 16 == 0 && (W / 8) >= 1;
 }
 
 static int g_enc_sms = 0;
 
-dvc_status encode_tma_run(const void *frames, dvc_dtype dt, int T, int H, int W, const void *w_exp, const void *b_exp,
-                          int c_lat, void *latent, cudaStream_t stream) {
-    DVC_CHECK_ARG(encode_tma_applicable(dt, H, W, 8, c_lat), DVC_ERR_UNSUPPORTED, "encode: unsupported shape");
+// frame_dt: DVC_BF16 / DVC_F16 ([T][3][H][W], must equal dt) or DVC_U8 ([T][H][W][3] bytes, W % 16 == 0)
+dvc_status encode_tma_run(const void *frames, dvc_dtype frame_dt, int T, int H, int W, const void *w_exp,
+                          const void *b_exp, int c_lat, void *latent, dvc_dtype dt, cudaStream_t stream) {
+    const bool u8 = frame_dt == DVC_U8;
+    DVC_CHECK_ARG(encode_tma_applicable(dt, H, W, 8, c_lat) && (u8 ? W % 16 == 0 : frame_dt == dt),
+                  DVC_ERR_UNSUPPORTED, "encode: unsupported shape / dtype combination");
     DVC_CHECK_ARG(((uintptr_t)frames & 15) == 0 && ((uintptr_t)latent & 15) == 0, DVC_ERR_ARG,
                   "encode: frames / latent must be 16-byte aligned");
     EncParams p;
     memset(&p, 0, sizeof(p));
     PFN_encodeTiled_t enc = get_encode_fn();
     DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    // frames [T][3][H][W] as (x, dy, hb, t*3 + c)
-    cuuint64_t gdim[4] = {(cuuint64_t)W, 8, (cuuint64_t)(H / 8), (cuuint64_t)T * 3};
-    cuuint64_t gstride[3] = {(cuuint64_t)W * 2, (cuuint64_t)W * 16, (cuuint64_t)H * W * 2};
-    cuuint32_t box[4] = {ENC_BX * 8, 8, ENC_BY, 3};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = enc(&p.amap, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
-                     const_cast<void *>(frames), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    if (u8) {   // bytes [T][H][3W], box {192 bytes = 64 pixels x 3, 64 rows, 1}
+        cuuint64_t gdim[3] = {(cuuint64_t)W * 3, (cuuint64_t)H, (cuuint64_t)T};
+        cuuint64_t gstride[2] = {(cuuint64_t)W * 3, (cuuint64_t)H * W * 3};
+        cuuint32_t box[3] = {ENC_BX * 8 * 3, 64, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = enc(&p.amap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(frames), gdim, gstride, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {    // frames [T][3][H][W] as (x, dy, hb, t*3 + c)
+        cuuint64_t gdim[4] = {(cuuint64_t)W, 8, (cuuint64_t)(H / 8), (cuuint64_t)T * 3};
+        cuuint64_t gstride[3] = {(cuuint64_t)W * 2, (cuuint64_t)W * 16, (cuuint64_t)H * W * 2};
+        cuuint32_t box[4] = {ENC_BX * 8, 8, ENC_BY, 3};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        r = enc(&p.amap, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                const_cast<void *>(frames), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (frames) failed (%d)", (int)r);
     dvc_status st = make_bmap_rows(&p.bmap, w_exp, dt, c_lat, 192, c_lat);
     if (st != DVC_OK) return st;
@@ -235,8 +346,10 @@ dvc_status encode_tma_run(const void *frames, dvc_dtype dt, int T, int H, int W,
     p.bias = b_exp;
     p.out = latent;
     p.idesc = make_idesc(dt == DVC_BF16, 128, c_lat);
-    const size_t smem = 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 8 * 10 + 16 + (size_t)c_lat * 4;
-    auto kern = dt == DVC_BF16 ? encode_kernel<__nv_bfloat16> : encode_kernel<__half>;
+    const size_t smem = u8 ? 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 2048 + 2 * ENC_U8_HALF
+                           : 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 8 * 14 + 16 + (size_t)c_lat * 4;
+    auto kern = dt == DVC_BF16 ? (u8 ? encode_kernel<__nv_bfloat16, true> : encode_kernel<__nv_bfloat16, false>)
+                               : (u8 ? encode_kernel<__half, true> : encode_kernel<__half, false>);
     {   // host cost: the attribute is set once per kernel / size
         dvc_status ss_ = ensure_smem((const void *)kern, (int)smem);
         if (ss_ != DVC_OK) return ss_;
@@ -248,9 +361,9 @@ dvc_status encode_tma_run(const void *frames, dvc_dtype dt, int T, int H, int W,
     }
     const int grid = p.ntiles < g_enc_sms ? p.ntiles : g_enc_sms;
     ProfSlot s0 = prof_begin(stream);
-    DVC_CUDA(launch_pdl(kern, dim3(grid), dim3(ENC_THREADS), smem, stream, 1, p));
+    DVC_CUDA(launch_pdl(kern, dim3(grid), dim3(u8 ? ENC_U8_THREADS : ENC_THREADS), smem, stream, 1, p));
     ++g_launches;
-    prof_end_aux(s0, stream, "encode");
+    prof_end_aux(s0, stream, u8 ? "encode_u8" : "encode");
     return check_launch("encode_kernel");
 }
 

@@ -36,5 +36,7 @@ dvc_status shift_gather_run(const NormArgs &a, dvc_dtype dt, cudaStream_t stream
 
 dvc_status unshuffle_run(const void *frames, dvc_dtype dt, int T, int H, int W, int s, void *latent,
                          cudaStream_t stream);
+dvc_status unshuffle_u8_run(const void *frames, int T, int H, int W, int s, void *latent, dvc_dtype dt,
+                            cudaStream_t stream);   // 8-bit HWC frames (R14)
 
 }  // namespace dvc

@@ -10,7 +10,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import DVC_BF16, DVC_F16, DVC_F32, DvcError, check, lib  # noqa: F401
+from ._lib import DVC_BF16, DVC_F16, DVC_F32, DVC_U8, DvcError, check, lib  # noqa: F401
 
 _DT = {torch.bfloat16: DVC_BF16, torch.float16: DVC_F16, torch.float32: DVC_F32}
 
@@ -77,16 +77,28 @@ def profile_records(n: int | None = None):
 
 
 # ------------------------------------------------------------------ a1 + a2
-def dvc_encode_pixelunshuffle(frames: torch.Tensor, w_exp=None, b_exp=None, s: int = 8, out=None, stream=None):
-    """frames [T,3,H,W] -> latent [T,H/s,W/s,c_lat] (c_lat = 3 s^2 without expansion)."""
-    T, C, H, W = frames.shape
+def dvc_encode_pixelunshuffle(frames: torch.Tensor, w_exp=None, b_exp=None, s: int = 8, out=None, stream=None,
+                              latent_dtype: torch.dtype | None = None):
+    """frames [T,3,H,W] (16-bit / fp32, NCHW) or [T,H,W,3] uint8 (HWC, R14) -> latent
+    [T,H/s,W/s,c_lat] (c_lat = 3 s^2 without expansion).  latent_dtype: required for uint8 frames
+    unless w_exp gives it; otherwise the frames' dtype."""
+    if frames.dtype == torch.uint8:
+        T, H, W, C = frames.shape
+        fdt = _lib.DVC_U8
+        ldt = latent_dtype or (w_exp.dtype if w_exp is not None else None)
+        if ldt is None:
+            raise ValueError("uint8 frames need latent_dtype (or expansion weights)")
+    else:
+        T, C, H, W = frames.shape
+        fdt = dtype_code(frames.dtype)
+        ldt = latent_dtype or frames.dtype
     if C != 3:
-        raise ValueError("frames must be [T,3,H,W]")
+        raise ValueError("frames must be [T,3,H,W] (or uint8 [T,H,W,3])")
     c_lat = 3 * s * s if w_exp is None else w_exp.shape[0]
     if out is None:
-        out = torch.empty((T, H // s, W // s, c_lat), dtype=frames.dtype, device=frames.device)
-    check(lib().dvc_encode_pixelunshuffle(_ptr(frames), dtype_code(frames.dtype), T, H, W, s, _ptr(w_exp),
-                                          _ptr(b_exp), c_lat, _ptr(out), _stream(stream)))
+        out = torch.empty((T, H // s, W // s, c_lat), dtype=ldt, device=frames.device)
+    check(lib().dvc_encode_pixelunshuffle(_ptr(frames), fdt, T, H, W, s, _ptr(w_exp), _ptr(b_exp), c_lat, _ptr(out),
+                                          dtype_code(out.dtype), _stream(stream)))
     return out
 
 

@@ -30,6 +30,11 @@ def frames_u8(T: int, H: int, W: int, seed: int = SEED_FRAMES) -> np.ndarray:
     return rng(seed).integers(0, 256, size=(T, 3, H, W), dtype=np.uint8)
 
 
+def frames_u8_hwc(T: int, H: int, W: int, seed: int = SEED_FRAMES) -> np.ndarray:
+    """The same 8-bit frames in the HWC layout of decoded video, [T,H,W,3] uint8."""
+    return np.ascontiguousarray(frames_u8(T, H, W, seed).transpose(0, 2, 3, 1))
+
+
 def frames(T: int, H: int, W: int, seed: int = SEED_FRAMES) -> np.ndarray:
     """Frames in [0,1] as k/255 (float32), NCHW [T,3,H,W]."""
     return (frames_u8(T, H, W, seed).astype(np.float64) / 255.0).astype(np.float32)

@@ -37,17 +37,21 @@ def test_library_exports_every_declared_symbol(L):
 
 
 def test_abi_version_and_status_strings(L):
-    assert L.dvc_abi_version() == 2
+    assert L.dvc_abi_version() == 3
     assert L.dvc_status_string(2) == b"DVC_ERR_DIVISIBILITY"
 
 
 def test_argument_errors_before_any_launch(L):
     # null pointers / divisibility are rejected before the device is touched
-    assert L.dvc_encode_pixelunshuffle(None, 0, 1, 8, 8, 8, None, None, 192, None, None) == 1
+    assert L.dvc_encode_pixelunshuffle(None, 0, 1, 8, 8, 8, None, None, 192, None, 0, None) == 1
     assert L.dvc_encode_pixelunshuffle(ctypes.c_void_p(16), 0, 1, 12, 16, 8, None, None, 192,
-                                       ctypes.c_void_p(16), None) == 2
+                                       ctypes.c_void_p(16), 0, None) == 2
     assert L.dvc_encode_pixelunshuffle(ctypes.c_void_p(16), 9, 1, 8, 8, 8, None, None, 192,
-                                       ctypes.c_void_p(16), None) == 1
+                                       ctypes.c_void_p(16), 0, None) == 1
+    assert L.dvc_encode_pixelunshuffle(ctypes.c_void_p(16), 3, 1, 8, 8, 8, None, None, 192,   # u8 latents
+                                       ctypes.c_void_p(16), 3, None) == 1
+    assert L.dvc_encode_pixelunshuffle(ctypes.c_void_p(16), 1, 1, 8, 8, 8, None, None, 192,   # f16 -> bf16
+                                       ctypes.c_void_p(16), 0, None) == 4
 
 
 def test_weight_count_matches_generator(L):

@@ -103,7 +103,7 @@ def test_halo_comm_argument_errors(dvc):
         dvc.dvc_unet_decode_gop(net, lat, ctx, comm=c0)
     assert lib.dvc_comm_connect_local(c1.handle, c0.handle, c0.handle) != 0   # rank 1 of 2 has no successor
     assert lib.dvc_comm_connect_local(c0.handle, c0.handle, None) != 0        # next must be rank 1
-    small = _net(dvc, torch.bfloat16, SMALL, 32, 6, 10, 4, 8)
+    small = _net(dvc, torch.bfloat16, SMALL, 32, 8, 12, 4, 8)
     s0, s1 = dvc.Comm(0, 2, small, _connect=False), dvc.Comm(1, 2, small, _connect=False)
     dvc.check(lib.dvc_comm_connect_local(s0.handle, s1.handle, None))
     dvc.check(lib.dvc_comm_connect_local(s1.handle, None, s0.handle))

@@ -124,3 +124,36 @@ def test_pipeline_with_vae_decoder_outputs_frames(dvc):
     assert out.shape == (T, 8 * h, 8 * w, 3)
     assert torch.equal(out, ref)
 
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_pipeline_matches_oracle(dvc, orc, dtype):
+    """f3 against the fp64 oracle (not only against the direct call): frames pushed one at a time,
+    decoded N at a time with the inter-batch carry, popped in order == oracle.skeleton over the whole
+    chain (storage-rounding emulation of dtype; R15/R16 gates per frame)."""
+    from tests.gpu_helpers import MODE, REG_STACK, gate, host64
+    h, w, N, T = 12, 20, 3, 7
+    named = synthgen.unet_weights(SMALL, 32, 32, seed=3)
+    cfg = dvc.unet_config(SMALL, 32, 32, 8, 8, 1e-5, dtype, h, w, N)
+    net = dvc.UNet(cfg, dvc.pack_weights(named, dtype))
+    lat, lat64 = dev(synthgen.normal((T, h, w, 32), 41), dtype)
+    ctx, ctx64 = dev(synthgen.normal((T, h, w, 32), 42), dtype)
+    pipe = dvc.Pipeline(net, N, 2)
+    got = {}
+
+    def drain():
+        while (r := pipe.pop()) is not None:
+            first, x = r
+            for i in range(x.shape[0]):
+                got[first + i] = x[i].clone()
+
+    for t in range(T):
+        pipe.push(lat[t], ctx[t])
+        drain()
+    pipe.flush()
+    drain()
+    torch.cuda.synchronize()
+    out = torch.stack([got[t] for t in range(T)])
+    exact = [(n, torch.from_numpy(a).to(dtype).double().numpy()) for n, a in named]
+    ref, _ = orc.skeleton(lat64, ctx64, exact, SMALL, G=8, P=8, mode=MODE[dtype])
+    gate(host64(out), ref, dtype, "pipeline", reg=REG_STACK, ulps=32)

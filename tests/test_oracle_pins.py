@@ -415,3 +415,27 @@ def test_skeleton_causal(orc):
     lat2[2] += 1
     b, _ = orc.skeleton(lat2, ctx, wts, SMALL, G=8, P=8)
     assert np.array_equal(a[:2], b[:2]) and not np.array_equal(a[2], b[2])
+
+
+# ---------------------------------------------------------------- R14 8-bit frames (G2's reference)
+def test_u8_values_closed_forms_and_library(orc):
+    for mode in ("fp16", "bf16", "f32"):
+        v = orc.u8_values(mode)
+        assert v[0] == 0.0 and v[255] == 1.0 and np.all(np.diff(v) >= 0)
+        assert np.all(np.abs(v - np.arange(256) / 255.0) <= {"fp16": 2.0 ** -12, "bf16": 2.0 ** -9,
+                                                              "f32": 2.0 ** -25}[mode])
+    assert np.all(np.diff(orc.u8_values("fp16")) > 0)                      # 11 bits separate all 256
+    assert orc.u8_values("fp16")[51] == 0.199951171875                     # RNE_fp16(0.2) (closed form)
+    assert orc.u8_values("bf16")[51] == 0.2001953125                       # RNE_bf16(0.2): 0x3E4D
+    # independent library roundings of the fp64 quotient agree for all 256 bytes
+    q = np.arange(256) / 255.0
+    assert np.array_equal(orc.u8_values("fp16"), q.astype(np.float16).astype(np.float64))
+    assert np.array_equal(orc.u8_values("f32"), q.astype(np.float32).astype(np.float64))
+    assert np.array_equal(orc.u8_values("bf16"), orc.rnd(q, "bf16"))
+
+
+def test_frames_from_u8_layout(orc):
+    U = synthgen.frames_u8_hwc(2, 16, 24)
+    F = orc.frames_from_u8(U, "bf16")
+    assert F.shape == (2, 3, 16, 24)
+    assert np.array_equal(F, orc.rnd(synthgen.frames_u8(2, 16, 24).astype(np.float64) / 255.0, "bf16"))
