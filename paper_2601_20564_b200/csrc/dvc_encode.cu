@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include "dvc_conv.cuh"
 #include "dvc_ptx.cuh"
+#include "dvc_epilogue.cuh"
 
 namespace dvc {
 
@@ -53,6 +54,7 @@ struct EncParams {
     int tiles_x, tiles_y, ntiles;
     const void *bias;
     void *out;          // latent [T][h][w][c_lat]
+    CUtensorMap omap[2];   // latent, box {32 | 16, 8, 16, 1}, SW64 / SW32 (staged epilogue, 16-bit frames)
     uint32_t idesc;
 };
 
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
     uint8_t *sU = sB + 3 * B_CHUNK + 2048;   // [2][ENC_U8_HALF] u8 staging (U8; after barriers + bias)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(u_empty + 2);
     float *sbias = reinterpret_cast<float *>(tmem_slot + 4);   // [c_lat]
+    uint8_t *sStage = sB + 3 * B_CHUNK + 2048;   // [2] epilogue staging (16-bit frames; U8 uses it for sU)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t ncols = 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
@@ -254,6 +257,35 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
             mbar_wait(&tfull[buf], use);
             tc_fence_after();
             const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * N);
+            if constexpr (!U8) {   // staged epilogue (dvc_epilogue.cuh): one TMA store per 32 columns
+                const bool issuer = warp == 4 && lane == 0;
+                const int bx0 = (rem % p.tiles_x) * ENC_BX, by0 = (rem / p.tiles_x) * ENC_BY;
+                int par = 0;
+#pragma unroll 1
+                for (int cc = 0; cc < N; cc += 32, par ^= 1) {
+                    uint32_t va[16], vb[16];
+                    const bool two = cc + 16 < N;
+                    tmem_ld16_nowait(taddr + (uint32_t)cc, va);
+                    if (two) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
+                    tmem_wait16(va);
+                    if (two) tmem_wait16(vb);
+                    if (cc + 32 >= N) {   // accumulator drained
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0)
+                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+                    }
+                    float f[32];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        f[i] = __uint_as_float(va[i]) + sbias[cc + i];
+                        f[16 + i] = two ? __uint_as_float(vb[i]) + sbias[cc + 16 + i] : 0.f;
+                    }
+                    epi_stage_chunk<T>(f, live, two, r, q4, lane, sStage + par * kEpiStage, &p.omap[0], &p.omap[1],
+                                       issuer, true, cc, bx0, by0, t, nullptr, nullptr);
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int cc = 0; cc < N; cc += 32) {
                 uint32_t va[16], vb[16];
@@ -284,6 +316,7 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
         }
     }
+    if (!U8 && warp == 4 && lane == 0) bulk_wait_group<0>();   // every staged store has landed
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -295,6 +328,8 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
 // ----------------------------------------------------------------- host side
 PFN_encodeTiled_t get_encode_fn();
 dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
+dvc_status make_out_map_box(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, int H, int W, int C, int box_c, int BX,
+                            int BY);
 
 bool encode_tma_applicable(dvc_dtype dt, int H, int W, int s, int c_lat) {
     return (dt == DVC_BF16 || dt == DVC_F16) && s == 8 && H % 8 == 0 && W % 8 == 0 && c_lat >= 16 && c_lat <= 256 &&
@@ -347,7 +382,12 @@ dvc_status encode_tma_run(const void *frames, dvc_dtype frame_dt, int T, int H, 
     p.out = latent;
     p.idesc = make_idesc(dt == DVC_BF16, 128, c_lat);
     const size_t smem = u8 ? 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 2048 + 2 * ENC_U8_HALF
-                           : 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 8 * 14 + 16 + (size_t)c_lat * 4;
+                           : 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 2048 + 2 * kEpiStage;
+    if (!u8) {
+        st = make_out_map_box(&p.omap[0], latent, dt, T, H / 8, W / 8, c_lat, 32, ENC_BX, ENC_BY);
+        if (st == DVC_OK) st = make_out_map_box(&p.omap[1], latent, dt, T, H / 8, W / 8, c_lat, 16, ENC_BX, ENC_BY);
+        if (st != DVC_OK) return st;
+    }
     auto kern = dt == DVC_BF16 ? (u8 ? encode_kernel<__nv_bfloat16, true> : encode_kernel<__nv_bfloat16, false>)
                                : (u8 ? encode_kernel<__half, true> : encode_kernel<__half, false>);
     {   // host cost: the attribute is set once per kernel / size

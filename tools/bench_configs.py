@@ -65,11 +65,19 @@ def c2(steps):
     ms_u = timed(lambda: dvc.dvc_encode_pixelunshuffle(fr, out=lat192), steps)
     alg = fr.numel() * 2 + out.numel() * 2
     alg_u = fr.numel() * 2 * 2
+    # 8-bit HWC frames (R14): fused converter-warp encode, and the u8 unshuffle alone
+    fu8 = torch.from_numpy(synthgen.frames_u8_hwc(T, H, W)).cuda()
+    ms8 = timed(lambda: dvc.dvc_encode_pixelunshuffle(fu8, w, b, out=out), steps)
+    ms8u = timed(lambda: dvc.dvc_encode_pixelunshuffle(fu8, out=lat192), steps)
+    alg8, alg8u = fu8.numel() + out.numel() * 2, fu8.numel() + lat192.numel() * 2
     pk = peaks()
     return {"config": "C2 encode 720p x32 (bf16)", "ms": ms, "frames_per_s": T / (ms / 1e3),
             "hbm_gbs": alg / (ms / 1e3) / 1e9, "hbm_frac_of_measured": alg / (ms / 1e3) / 1e9 / pk,
             "unshuffle_only_ms": ms_u, "unshuffle_only_gbs": alg_u / (ms_u / 1e3) / 1e9,
-            "unshuffle_only_frac": alg_u / (ms_u / 1e3) / 1e9 / pk}
+            "unshuffle_only_frac": alg_u / (ms_u / 1e3) / 1e9 / pk,
+            "u8_hwc_ms": ms8, "u8_hwc_gbs": alg8 / (ms8 / 1e3) / 1e9, "u8_hwc_frac": alg8 / (ms8 / 1e3) / 1e9 / pk,
+            "u8_unshuffle_only_ms": ms8u, "u8_unshuffle_only_frac": alg8u / (ms8u / 1e3) / 1e9 / pk,
+            "peak_gbs": pk}
 
 
 def decode_fps(dtype, h, w, T, steps):
@@ -140,8 +148,15 @@ def f4_p_sweep(steps):   # f4: decode throughput vs the shift ratio P (Fig. 8a)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default=None, help="C2 | C3 | C4 | C5 | F4")
     args = ap.parse_args()
     steps = 3 if args.quick else 10
+    if args.only == "C2":
+        print(json.dumps(c2(steps)), flush=True)
+        return
+    if args.only == "C5":
+        print(json.dumps(c5([1, 2, 4, 8, 16, 32, 64], steps)), flush=True)
+        return
     print(json.dumps(c2(steps)), flush=True)
     for dt, name in ((torch.float16, "fp16"), (torch.bfloat16, "bf16")):
         ms, fps = decode_fps(dt, 90, 160, 16, steps)
