@@ -381,12 +381,15 @@ DVC_API dvc_status dvc_profile_record(int i, double *ms, double *flops, char *la
  * encoder; label "<kernel> ...", flops 0).  dvc_profile_end's sums cover convolutions only. */
 DVC_API int dvc_profile_record_count(void);
 
-/* Convolution engine selection (tuning / A-B testing; default 2, or the
- * DVC_CONV_ENGINE environment variable at load):
- *   2 = TMA-fed persistent tcgen05 engine with CTA pairs (cta_group::2, M=256)
- *   1 = the same engine with single-CTA MMAs (M=128)
+/* Convolution engine selection (tuning / A-B testing; default 2; experiment builds also read
+ * DVC_CONV_ENGINE at load):
+ *   2 = TMA-fed persistent tcgen05 engines with CTA pairs (cta_group::2, M=256): the fused
+ *       GN/SiLU/shift engine for frames with H >= 32, the TMA engine otherwise and for raw
+ *       operands -- including the stride-2 down-samplers (TMA boxes with element stride 2)
+ *   1 = the TMA engine with single-CTA MMAs (M=128), no fused engine
  *   0 = gather-fed tcgen05 engine only (cp.async producer warps)
- * Strided / resized / unshuffle convolutions always use the gather engine. */
+ * The gather engine also serves shapes the TMA engines do not take (the nearest-resize operand
+ * of engine 0, the 16-bit expansion when the fused encoder does not apply). */
 DVC_API dvc_status dvc_set_conv_engine(int engine);
 
 /* Device / build introspection (no compute). */

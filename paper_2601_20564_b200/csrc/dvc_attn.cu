@@ -15,16 +15,15 @@
 //   h2 = ff2(g) + h1                1x1 conv 4C -> C with residual
 //   Y  = proj_out(h2) + X           1x1 conv with residual (+ box statistics of Y for the next GN)
 //
-// attn_tc_kernel: one CTA = 128 queries of one (frame, head); 4 warps, thread r owns query
-// row r = TMEM lane r.  Per 128-key tile j:
-//   S = Q K_j^T          tcgen05.mma kind::f16 M=128 N=128 K=D (D/16 instructions), S in TMEM
-//   softmax              tcgen05.ld of the row, running max m / sum l (exp2 domain), P = 16-bit
-//                        probabilities written to shared memory in the UMMA K-major layout
-//   PV = P V_j           tcgen05.mma M=128 N=D K=128 into a second TMEM region
-//   O = O * alpha + PV   in registers (online softmax, no TMEM read-modify-write)
-// K/V tiles are double-buffered with cp.async (zero-filled past N; masked keys get p = 0).
-// All operands use the no-swizzle canonical layout: 8-row x 16-byte core matrices, core
-// matrices adjacent in K 128 B apart (LBO), 8-row groups SBO apart.
+// attn_tc_kernel: one CTA = 256 queries (two 128-row tiles) of one (frame,
+// head), warp-specialised: warp 17 streams (K_j, V_j^T) tiles through a 4-stage ring (1D bulk copies of
+// the pre-tiled images qkv_pack_kernel writes), warp 16 issues S_t = Q_t K_j^T (M=128, N=128, K=D) and
+// O_t += P_t V_j with P read from TMEM, 16 softmax warps (two threads per query row, 64 keys each)
+// read S once from TMEM, keep a lazy running maximum (moved only when the tile maximum exceeds it by
+// 8 in log2 units, with an in-TMEM rescale of that O row), exponentiate with ex2.approx for 6 of 8
+// scores and a degree-3 polynomial on the FMA pipe for 2 of 8 (packed fp32x2 arithmetic), and write P
+// as packed 16-bit pairs to TMEM.  TMEM: S0, S1, O0, O1, P0, P1 = 512 columns.  The head_dim-256
+// variant (VAE mid attention) keeps one query tile per CTA: S | P | O = 128 + 64 + 256 columns.
 #include <cuda.h>
 #include <cstdio>
 #include <cstdlib>

@@ -820,20 +820,14 @@ static dvc_status make_out_map(CUtensorMap *map, void *ptr, dvc_dtype dt, int T,
 }
 
 dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
+    // identity skips are X . I segments (an epilogue residual add measured slower: its per-row loads
+    // made the epilogue the bottleneck, fz2 0.97 -> 1.48 ms at 720p level 0)
     DVC_CHECK_ARG(d.nseg >= 1 && d.nseg <= 4 && d.T >= 1 && d.T < 256 && d.cout % 16 == 0 && d.residual == nullptr,
                   DVC_ERR_UNSUPPORTED, "fused conv: bad descriptor (identity skips are 1x1 segments, not residuals)");
     FzParams p;
     memset(&p, 0, sizeof(p));
     constexpr int CG = 2;
-    int bn = d.cout;
-    if (bn > 256) {
-        bn = 0;
-        for (int c = 256; c >= 16; c -= 16)
-            if (d.cout % c == 0 && (c / CG) % 8 == 0) {
-                bn = c;
-                break;
-            }
-    }
+    const int bn = choose_bn(d.cout, CG, 16);
     DVC_CHECK_ARG(bn >= 16 && (bn / CG) % 8 == 0, DVC_ERR_UNSUPPORTED, "no N tile for cout=%d", d.cout);
     p.bn = bn;
     p.T = d.T;

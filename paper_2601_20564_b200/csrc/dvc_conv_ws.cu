@@ -573,15 +573,7 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
     WsParams p;
     memset(&p, 0, sizeof(p));
     const int CG = g_ws_cg == 1 ? 1 : 2;
-    int bn = d.cout;
-    if (bn > 256 || (d.geglu && bn % 32)) {
-        bn = 0;
-        for (int c = 256; c >= 16; c -= 16)   // GEGLU: whole 32-column value/gate blocks per tile
-            if (d.cout % c == 0 && (c / CG) % 8 == 0 && (!d.geglu || c % 32 == 0)) {
-                bn = c;
-                break;
-            }
-    }
+    const int bn = choose_bn(d.cout, CG, d.geglu ? 32 : 16);   // GEGLU: whole 32-column value/gate blocks
     DVC_CHECK_ARG(bn >= 16 && (bn / CG) % 8 == 0, DVC_ERR_UNSUPPORTED, "no N tile for cout=%d", d.cout);
     DVC_CHECK_ARG(!d.geglu || (bn % 32 == 0 && d.residual == nullptr && d.stats_out == nullptr && d.bias1 == nullptr),
                   DVC_ERR_UNSUPPORTED, "GEGLU epilogue: 32-column tiles, no residual / statistics / second bias");

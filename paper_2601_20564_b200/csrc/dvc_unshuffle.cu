@@ -103,10 +103,13 @@ __global__ void __launch_bounds__(256) unshuffle8_u8_kernel(const uint8_t *__res
         const int i = (int)(e & 7);
         const long pix = e >> 3;
         const int x = (int)(pix % w), y = (int)((pix / w) % h), t = (int)(pix / ((long)w * h));
-        const uint8_t *src = F + (((long)t * H + 8 * y + i) * W + 8 * x) * 3;
-        uint8_t b[24];
+        // 24 bytes = three 8-byte words (8-byte aligned: W % 8 == 0)
+        const uint2 *src = reinterpret_cast<const uint2 *>(F + (((long)t * H + 8 * y + i) * W + 8 * x) * 3);
+        const uint2 q0 = __ldg(src), q1 = __ldg(src + 1), q2 = __ldg(src + 2);
+        const uint32_t wv[6] = {q0.x, q0.y, q1.x, q1.y, q2.x, q2.y};
+        uint32_t b[24];
 #pragma unroll
-        for (int q = 0; q < 24; ++q) b[q] = __ldg(src + q);
+        for (int q = 0; q < 24; ++q) b[q] = (wv[q >> 2] >> (8 * (q & 3))) & 0xFFu;
         O *dst = L + pix * 192 + i * 8;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -139,7 +142,7 @@ __global__ void unshuffle_u8_generic_kernel(const uint8_t *__restrict__ F, O *__
 
 template <typename O>
 static void unshuffle_u8_launch(const uint8_t *F, void *L, int T, int H, int W, int s, cudaStream_t stream) {
-    if (s == 8 && ((uintptr_t)L & 15) == 0) {
+    if (s == 8 && ((uintptr_t)L & 15) == 0 && ((uintptr_t)F & 7) == 0) {
         const long n = (long)T * (H / 8) * (W / 8) * 8;
         const int grid = (int)((n + 255) / 256 < 148L * 16 ? (n + 255) / 256 : 148L * 16);
         unshuffle8_u8_kernel<O><<<grid, 256, 0, stream>>>(F, reinterpret_cast<O *>(L), T, H, W);

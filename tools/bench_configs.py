@@ -2,6 +2,8 @@
 
     python tools/bench_configs.py [--quick]
 
+  C1  one OTSM ResBlock, T=8, 64 ch, 32x32, fp32: the fp64 CPU oracle's seconds on this host, the GPU fp32
+      validation mode's time and its rel-L2 against the oracle
   C2  encode front end (PixelUnshuffle + Latent Channel Expansion), 720p, 32 frames: frames/s and
       achieved HBM GB/s against MEASURED_PEAKS.json (algorithmic bytes: frames read + latent written)
   C3  ResBlock skeleton decode, 720p, 16-frame batch, fp16 and bf16: frames/s
@@ -68,7 +70,7 @@ def c2(steps):
     # 8-bit HWC frames (R14): fused converter-warp encode, and the u8 unshuffle alone
     fu8 = torch.from_numpy(synthgen.frames_u8_hwc(T, H, W)).cuda()
     ms8 = timed(lambda: dvc.dvc_encode_pixelunshuffle(fu8, w, b, out=out), steps)
-    ms8u = timed(lambda: dvc.dvc_encode_pixelunshuffle(fu8, out=lat192), steps)
+    ms8u = timed(lambda: dvc.dvc_encode_pixelunshuffle(fu8, out=lat192, latent_dtype=torch.bfloat16), steps)
     alg8, alg8u = fu8.numel() + out.numel() * 2, fu8.numel() + lat192.numel() * 2
     pk = peaks()
     return {"config": "C2 encode 720p x32 (bf16)", "ms": ms, "frames_per_s": T / (ms / 1e3),
@@ -78,6 +80,31 @@ def c2(steps):
             "u8_hwc_ms": ms8, "u8_hwc_gbs": alg8 / (ms8 / 1e3) / 1e9, "u8_hwc_frac": alg8 / (ms8 / 1e3) / 1e9 / pk,
             "u8_unshuffle_only_ms": ms8u, "u8_unshuffle_only_frac": alg8u / (ms8u / 1e3) / 1e9 / pk,
             "peak_gbs": pk}
+
+
+def c1(steps):
+    """C1: one OTSM ResBlock, 8 frames, 64 channels, 32x32, fp32 -- the fp64 CPU oracle timed on this host
+    (the config's purpose, "CPU oracle in seconds") next to the GPU fp32 validation mode, with parity."""
+    import time
+
+    import numpy as np
+
+    import oracle
+    from tests.gpu_helpers import rb_device, rel_l2
+    w = synthgen.resblock_weights(64, 64)
+    x = synthgen.normal((8, 32, 32, 64))
+    w64 = {k: (None if v is None else v.astype(np.float64)) for k, v in w.items()}
+    t0 = time.perf_counter()
+    ref, _ = oracle.resblock(x.astype(np.float64), None, w64, 32, 8)
+    cpu_s = time.perf_counter() - t0
+    wd, _ = rb_device(w, torch.float32)
+    xd = torch.from_numpy(x).cuda()
+    prm = dvc.ResBlockParams(wd, 64, 0, 32, 8)
+    ms = timed(lambda: dvc.dvc_resblock_tsm_forward(prm, xd), steps)
+    err = rel_l2(dvc.dvc_resblock_tsm_forward(prm, xd).double().cpu().numpy(), ref)
+    return {"config": "C1 single OTSM ResBlock, T=8, 64 ch, 32x32, fp32", "cpu_oracle_s": cpu_s,
+            "cpu_oracle_threads": oracle.num_threads(), "cpu_affinity_cores": len(os.sched_getaffinity(0)),
+            "gpu_fp32_ms": ms, "rel_l2_vs_oracle": err, "gflop": 1.208}
 
 
 def decode_fps(dtype, h, w, T, steps):
@@ -151,12 +178,16 @@ def main():
     ap.add_argument("--only", default=None, help="C2 | C3 | C4 | C5 | F4")
     args = ap.parse_args()
     steps = 3 if args.quick else 10
+    if args.only == "C1":
+        print(json.dumps(c1(steps)), flush=True)
+        return
     if args.only == "C2":
         print(json.dumps(c2(steps)), flush=True)
         return
     if args.only == "C5":
         print(json.dumps(c5([1, 2, 4, 8, 16, 32, 64], steps)), flush=True)
         return
+    print(json.dumps(c1(steps)), flush=True)
     print(json.dumps(c2(steps)), flush=True)
     for dt, name in ((torch.float16, "fp16"), (torch.bfloat16, "bf16")):
         ms, fps = decode_fps(dt, 90, 160, 16, steps)
