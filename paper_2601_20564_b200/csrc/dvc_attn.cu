@@ -283,8 +283,10 @@ struct AttnSmem {
     static constexpr int off_bar = off_v + STAGES * V;
     // barriers: q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_full[2], 6 spare
     static constexpr int nbar = 1 + 2 * STAGES + 3 * 4;   // + s_full[4], p_full[4], o_full[4] (NT <= 3)
-    static constexpr int off_red = off_bar + nbar * 8 + 16;     // [NT tiles][2 halves][128 rows] float exchange
-    static constexpr int bytes = off_red + NT * 2 * 128 * 4 + 1024;   // + alignment slack
+    // [NT tiles][2 key-tile parities][2 halves][128 rows] float exchange (parity double buffer: a thread's
+    // write for key tile j+1 never lands in the slot its partner may still be reading for tile j)
+    static constexpr int off_red = off_bar + nbar * 8 + 16;
+    static constexpr int bytes = off_red + NT * 4 * 128 * 4 + 1024;   // + alignment slack
     // TMEM columns (512 allocated)
     // S_t at t*KT, P_t (KT/2 packed columns) at tm_p + t*KT/2, O_t at tm_o + t*64
     static constexpr int tm_o = NT == 3 ? 320 : 256, tm_o_step = NT == 1 ? 0 : 64;
@@ -462,7 +464,7 @@ __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
         const int tt = (warp >> 2) % NT, q4 = warp & 3, half = warp / (4 * NT);
         const int row = q4 * 32 + lane;
         const uint32_t bar_id = 1 + tt * 4 + q4;
-        float *red = reinterpret_cast<float *>(smem + L::off_red) + tt * 256;
+        float *red = reinterpret_cast<float *>(smem + L::off_red) + tt * 512;
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
         const uint32_t tS = tmem + lane_off + tt * KT + half * (KT / 2);
         const uint32_t tO = tmem + lane_off + L::tm_o + tt * L::tm_o_step;
@@ -500,9 +502,10 @@ __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
                     mxp[k] = fmaxf(mxp[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
             float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
                              fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-            red[half * 128 + row] = mx;
+            float *rj = red + (j & 1) * 256;
+            rj[half * 128 + row] = mx;
             pair_sync();
-            mx = fmaxf(mx, red[(half ^ 1) * 128 + row]);
+            mx = fmaxf(mx, rj[(half ^ 1) * 128 + row]);
             const float mt = mx * scale_log2;
             if (j == 0) {
                 m = mt;

@@ -26,8 +26,9 @@ for r in data:
     d = k.setdefault(int(r[iID]), {"name": r[iN].split("(")[0].replace("void ", ""), "grid": r[iG]})
     d[r[iM]] = float(r[iV].replace(",", ""))
 items = list(k.values())
-steps = 2
-second = items[len(items) // 2:]
+# one encode launch per bench step (warm-up, timed and instrumented passes are all in the capture)
+steps = max(1, sum(1 for d in items if d["name"].startswith("encode_kernel")))
+second = items[-(len(items) // steps):]
 tot = collections.defaultdict(lambda: [0, 0.0, 0.0])
 for d in items:
     t = d["gpu__time_duration.sum"]
@@ -41,7 +42,8 @@ conv_ns = sum(v[1] for n, v in tot.items() if "conv_" in n) / steps
 with open(f"profiles/{rnd}_launches.txt", "w") as f:
     f.write(f"# ncu launch list ({tag}): ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
             f"--clock-control none -c 500 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline\n"
-            f"# 2 steps captured (warm-up + timed); times are serialized, cold-cache (ncu flushes caches): "
+            f"# {steps} steps captured (warm-up, timed and instrumented passes); times are serialized, "
+            f"cold-cache (ncu flushes caches): "
             f"compare SHARES with bench.py, not absolutes\n")
     f.write(f"# launches per step {len(items) / steps:.0f}; serialized ms per step {allt / 1e6 / steps:.3f}\n")
     f.write(f"{'kernel':60s} {'n/step':>7s} {'ms/step':>8s} {'share':>6s} {'DRAM GB/s':>10s}\n")
