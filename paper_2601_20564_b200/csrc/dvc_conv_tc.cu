@@ -21,6 +21,8 @@
 // MMA commits (tcgen05.commit) free a stage; a final commit signals the epilogue.
 #include <cuda.h>
 #include <mutex>
+#include <unordered_map>
+#include <cstring>
 #include "dvc_conv.cuh"
 #include "dvc_ptx.cuh"
 
@@ -300,17 +302,69 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 }
 
 // ----------------------------------------------------------------- host side
+// cuTensorMapEncodeTiled behind a small cache: a decode step encodes ~400 tensor maps (every conv
+// launch describes its activations, weights and output), almost always with the same arguments as the
+// previous step, so the host cost of a repeated call drops to a hash lookup (the key is every argument
+// of the encode; the cache is cleared when it grows past 8192 entries).
+static PFN_encodeTiled_t g_encode_raw = nullptr;
+namespace {
+struct MapKey {
+    uint64_t w[26];
+    bool operator==(const MapKey &o) const { return memcmp(w, o.w, sizeof(w)) == 0; }
+};
+struct MapKeyHash {
+    size_t operator()(const MapKey &k) const {
+        uint64_t h = 1469598103934665603ull;
+        for (uint64_t v : k.w) h = (h ^ v) * 1099511628211ull;
+        return (size_t)h;
+    }
+};
+}  // namespace
+static CUresult encode_cached(CUtensorMap *map, CUtensorMapDataType dt, cuuint32_t rank, void *addr,
+                              const cuuint64_t *gdim, const cuuint64_t *gstride, const cuuint32_t *box,
+                              const cuuint32_t *estr, CUtensorMapInterleave il, CUtensorMapSwizzle sw,
+                              CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob) {
+    if (rank < 1 || rank > 5) return g_encode_raw(map, dt, rank, addr, gdim, gstride, box, estr, il, sw, l2, oob);
+    MapKey k;
+    memset(&k, 0, sizeof(k));
+    k.w[0] = (uint64_t)dt | ((uint64_t)rank << 8) | ((uint64_t)il << 16) | ((uint64_t)sw << 24) |
+             ((uint64_t)l2 << 32) | ((uint64_t)oob << 40);
+    k.w[1] = (uint64_t)(uintptr_t)addr;
+    for (cuuint32_t i = 0; i < rank; ++i) {
+        k.w[2 + i] = gdim[i];
+        k.w[7 + i] = i + 1 < rank ? gstride[i] : 0;
+        k.w[12 + i] = box[i];
+        k.w[17 + i] = estr[i];
+    }
+    static std::mutex mu;
+    static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(k);
+        if (it != cache.end()) {
+            *map = it->second;
+            return CUDA_SUCCESS;
+        }
+    }
+    const CUresult r = g_encode_raw(map, dt, rank, addr, gdim, gstride, box, estr, il, sw, l2, oob);
+    if (r == CUDA_SUCCESS) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (cache.size() > 8192) cache.clear();
+        cache.emplace(k, *map);
+    }
+    return r;
+}
+
 PFN_encodeTiled_t get_encode_fn() {
-    static PFN_encodeTiled_t fn = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
         void *ptr = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_encodeTiled_t>(ptr);
+            g_encode_raw = reinterpret_cast<PFN_encodeTiled_t>(ptr);
     });
-    return fn;
+    return g_encode_raw ? encode_cached : nullptr;
 }
 
 // 2D [rows][cols] 16-bit matrix, box {64 cols, box_rows}, SWIZZLE_128B, OOB zero fill.
