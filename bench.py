@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: one GOP split over the ranks (halo per ResBlock); weak: one GOP per GPU")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"], help="halo transport (strong, N>1)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="test only: every rank on cuda:0 with a gloo process group (the N>1 code path on one GPU)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch/rendezvous check only: every rank joins a gloo group, rank 0 prints the ranks")
     ap.add_argument("--attention", action="store_true",
@@ -305,9 +307,14 @@ def run_ours(args):
 
     import synthgen
     rank, world, local = dist_env()
+    if args.share_device:   # test mode: all ranks share cuda:0; plumbing over gloo (NCCL refuses shared GPUs)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2601_20564_b200 as dvc
     dvc.device_check(local)
     dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float16
@@ -348,7 +355,7 @@ def run_ours(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if args.share_device else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

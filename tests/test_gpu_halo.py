@@ -161,3 +161,22 @@ def test_ipc_halo_two_processes_equals_single_rank(dvc):
         ref = dvc.dvc_unet_decode_gop(net, lat, ctx, carry_out=k).cpu()
         assert torch.equal(torch.cat([got[r][call][0] for r in range(world)]), ref), call
         assert torch.equal(got[world - 1][call][1], k.cpu()), call
+
+
+def test_bench_multi_rank_path_on_one_gpu(dvc):
+    """bench.py's N > 1 path end to end (torchrun re-launch, IPC handle exchange over the process group,
+    P2P halo per ResBlock, max-over-ranks timing, e2e) with both ranks sharing cuda:0 (--share-device:
+    gloo plumbing, since NCCL refuses two ranks on one GPU).  The throughput of time-sliced ranks means
+    nothing; the line's shape and rc do."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if not k.startswith("DVC_") and k not in ("WORLD_SIZE", "RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--share-device", "--steps", "2",
+                        "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, env=env,
+                       cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["config"]["frames_per_gpu"] == 16
+    assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
