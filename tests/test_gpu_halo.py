@@ -180,3 +180,19 @@ def test_bench_multi_rank_path_on_one_gpu(dvc):
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "strong" and line["config"]["frames_per_gpu"] == 16
     assert line["value"] > 0 and line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+
+
+@pytest.mark.parametrize("h,w,T,world", [(90, 160, 8, 4), (135, 240, 6, 2)])
+def test_loopback_halo_full_size(dvc, h, w, T, world):
+    """G11 at the configs' latent sizes (720p headline, 1080p C4) and widths: the P2P halo between
+    concurrent loopback ranks equals the single-rank decode bit for bit, carry_out included."""
+    dtype = torch.bfloat16
+    net = _net(dvc, dtype, (240, 480, 960, 960), 256, h, w, T, 24)
+    comms = dvc.Comm.local_group(world, net)
+    lat, ctx = _inputs(T, h, w, 256, dtype, 40)
+    ref_k = torch.empty(net.carry_elems, dtype=dtype, device="cuda")
+    ref = dvc.dvc_unet_decode_gop(net, lat, ctx, carry_out=ref_k)
+    for _ in range(3):
+        k = torch.zeros(net.carry_elems, dtype=dtype, device="cuda")
+        assert torch.equal(_loopback(dvc, net, comms, lat, ctx, k), ref)
+        assert torch.equal(k, ref_k)
