@@ -79,6 +79,10 @@ struct FzDesc {
     const void *bias0, *bias1, *residual;
     void *out, *stats_out;
     dvc_dtype dt;
+    // up2: out is the exact 2x nearest upsampling [T][2H][2W][cout] of the conv's output (the
+    // epilogue's TMA store writes every staged box four times with element stride 2; the low-res
+    // output is never written; no statistics)
+    int up2 = 0;
 };
 dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream);
 bool conv_fz_applicable(int H, int W, dvc_dtype dt);

@@ -85,6 +85,7 @@ struct FzParams {
     int sw_mode;                // 0: 8-channel no-swizzle boxes only; 1/2: SW128 whole-chunk box for unshifted chunks (2: base offset)
     int nsteps;                 // K loop of a work item: (segment, 64-channel chunk) steps in issue order,
     unsigned char ord[64];      //   ord[i] = seg << 6 | chunk (raw 1x1 chunks interleaved among the 3x3 ones)
+    int up2;                    // output = exact 2x nearest upsampling (four strided TMA stores per chunk)
     int epi_tma;                // 1: epilogue stages 32-column chunks in shared memory, TMA-stores them and reads
                                 //    the box statistics back column-wise; 0: per-thread row stores + butterflies
     CUtensorMap omap[2];        // output [T][H][W][cout]: box {32, 8, 16, 1} SW64 / {16, 8, 16, 1} SW32
@@ -698,7 +699,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                     }
                     epi_stage_chunk<T>(f, m >= 0, two, r, q4, lane, sStage + par * kEpiStage, &p.omap[0], &p.omap[1],
                                        issuer, bx.valid, n, bx.x0, bx.y0, bx.t,
-                                       want_stats ? stats_box + (size_t)n * 2 : nullptr, red + par * 256);
+                                       want_stats ? stats_box + (size_t)n * 2 : nullptr, red + par * 256, p.up2 != 0);
                 }
                 continue;
             }
@@ -803,14 +804,18 @@ static dvc_status make_halo_map(CUtensorMap *map, const void *ptr, dvc_dtype dt,
 
 // output box {c, 8, 16, 1} of a [T][H][W][cout] tensor for the staged epilogue's TMA store: 32 channels
 // (64-byte rows, SWIZZLE_64B) or 16 (32-byte rows, SWIZZLE_32B), matching the staging layout
-static dvc_status make_out_map(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, int H, int W, int C, int box_c) {
+// up = 2: the tensor is the 2x upsampled output [T][2H][2W][C], walked with element stride 2 in x and
+// y so that a staged 8 x 16 box lands on one phase of the upsampled grid
+static dvc_status make_out_map(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, int H, int W, int C, int box_c,
+                               int up = 1) {
     PFN_encodeTiled_t enc = get_encode_fn();
     DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && C % 8 == 0, DVC_ERR_ARG, "fused conv: output alignment");
-    cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
-    cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)FZ_BX, (cuuint32_t)FZ_BY, 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const cuuint64_t Ho = (cuuint64_t)H * up, Wo = (cuuint64_t)W * up;
+    cuuint64_t gdim[4] = {(cuuint64_t)C, Wo, Ho, (cuuint64_t)T};
+    cuuint64_t gstride[3] = {(cuuint64_t)C * 2, Wo * C * 2, Ho * Wo * C * 2};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)(FZ_BX * up), (cuuint32_t)(FZ_BY * up), 1};
+    cuuint32_t estr[4] = {1, (cuuint32_t)up, (cuuint32_t)up, 1};
     CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, ptr,
                      gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
@@ -950,9 +955,12 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         const char *e = dvc_knob("DVC_FZ_EPI");
         p.epi_tma = e ? atoi(e) : 1;
     }
+    p.up2 = d.up2;
+    DVC_CHECK_ARG(!d.up2 || (p.epi_tma && d.stats_out == nullptr), DVC_ERR_UNSUPPORTED,
+                  "fused conv: the 2x-upsampled output needs the staged epilogue and no statistics");
     if (p.epi_tma) {
-        st = make_out_map(&p.omap[0], d.out, d.dt, d.T, d.H, d.W, d.cout, 32);
-        if (st == DVC_OK) st = make_out_map(&p.omap[1], d.out, d.dt, d.T, d.H, d.W, d.cout, 16);
+        st = make_out_map(&p.omap[0], d.out, d.dt, d.T, d.H, d.W, d.cout, 32, d.up2 ? 2 : 1);
+        if (st == DVC_OK) st = make_out_map(&p.omap[1], d.out, d.dt, d.T, d.H, d.W, d.cout, 16, d.up2 ? 2 : 1);
         if (st != DVC_OK) return st;
     }
     const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (size_t)p.nraw * FZ_RAW_SLOT +

@@ -44,12 +44,14 @@ __device__ __forceinline__ int epi_off(bool two, int r, int j) {
 
 // f: this row's ncol (= two ? 32 : 16) final values; live: the row is a pixel of the tensor.
 // store: issue the TMA store (the box is valid); (c0, x0, y0, t): the box's output coordinates.
+// up2: the output maps describe the 2x upsampled tensor with element stride 2 in x and y; the box
+// is stored at the four phases (2 x0 + ox, 2 y0 + oy), i.e. exact nearest 2x upsampling.
 // stats_col: &stats_box[c0 * 2] (per column: sum, sum of squares) or null; red: 256 floats.
 template <typename T>
 __device__ __forceinline__ void epi_stage_chunk(const float (&f)[32], bool live, bool two, int r, int q4, int lane,
                                                 uint8_t *st, const CUtensorMap *omap32, const CUtensorMap *omap16,
                                                 bool issuer, bool store, int c0, int x0, int y0, int t,
-                                                float *stats_col, float *red) {
+                                                float *stats_col, float *red, bool up2 = false) {
     const int ncol = two ? 32 : 16;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -65,7 +67,13 @@ __device__ __forceinline__ void epi_stage_chunk(const float (&f)[32], bool live,
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (issuer) {
         if (store) {
-            tma_store_4d(two ? omap32 : omap16, smem_u32(st), c0, x0, y0, t);
+            if (up2) {   // exact 2x nearest upsampling: maps with element stride 2 in x and y, four phases
+#pragma unroll
+                for (int ph = 0; ph < 4; ++ph)
+                    tma_store_4d(two ? omap32 : omap16, smem_u32(st), c0, 2 * x0 + (ph & 1), 2 * y0 + (ph >> 1), t);
+            } else {
+                tma_store_4d(two ? omap32 : omap16, smem_u32(st), c0, x0, y0, t);
+            }
             bulk_commit_group();
         }
         bulk_wait_group_read<1>();   // the other staging buffer has been read: reusable for chunk i+1

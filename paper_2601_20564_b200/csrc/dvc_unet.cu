@@ -455,8 +455,10 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
 
     int bi = 0;
     // one ResBlock with its halo exchange; sa/sb/sy: box statistics of x_a, x_b, y
-    auto run_block = [&](const void *xa, const void *xb, void *y, const void *sa, const void *sb,
-                         void *sy) -> dvc_status {
+    // up2: y receives the exact 2x nearest upsampling of the block output (no statistics, no
+    // Transformer2D after the block)
+    auto run_block = [&](const void *xa, const void *xb, void *y, const void *sa, const void *sb, void *sy,
+                         int up2 = 0) -> dvc_status {
         const RB &r = n->blk[bi];
         const int l = n->blevel[bi];
         const int H = n->lh[l], Wd = n->lw[l];
@@ -471,7 +473,12 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         }
         void *cout_ptr = nullptr;
         if (carry_out && rank == world - 1) cout_ptr = reinterpret_cast<uint8_t *>(carry_out) + off;
-        dvc_status e = resblock_launch(r, xa, xb, T, H, Wd, cin_ptr, cout_ptr, y, rbws, s, sa, sb, sy);
+        if (up2 && n->tf_of[bi] >= 0) {
+            set_error("internal: upsampled block output before a Transformer2D block");
+            return DVC_ERR_UNSUPPORTED;
+        }
+        dvc_status e = resblock_launch(r, xa, xb, T, H, Wd, cin_ptr, cout_ptr, y, rbws, s, sa, sb, up2 ? nullptr : sy,
+                                       up2);
         // f1: the Transformer2D block after this ResBlock, in place on y (its statistics refreshed)
         if (e == DVC_OK && n->tf_of[bi] >= 0)
             e = transformer_launch(n->tf[n->tf_of[bi]], y, T, H, Wd, y, rbws, s, sy, sy);
@@ -547,16 +554,24 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     }
     for (int u = 0; u < 4; ++u) {
         const int l = 3 - u;
+        // an exact 2x upsampler (45x80 -> 90x160 at 720p) with no Transformer2D after the level's last
+        // ResBlock: that block's conv2 epilogue writes the upsampled tensor itself (no nearest kernel, no
+        // low-res copy); the hb buffers are sized for the upsampled tensors
+        const bool fold = u < 3 && g_ws_cg != 0 && c.head_dim == 0 && n->lh[l - 1] == 2 * n->lh[l] &&
+                          n->lw[l - 1] == 2 * n->lw[l];
         for (int r = 0; r < 3; ++r) {
             --k;
-            if ((st = run_block(h, skip[k], hb[pp], hs, skst[k], hbst[pp])) != DVC_OK) return st;
+            if ((st = run_block(h, skip[k], hb[pp], hs, skst[k], hbst[pp], fold && r == 2)) != DVC_OK) return st;
             h = hb[pp];
             hs = hbst[pp];
             pp ^= 1;
         }
         if (u < 3) {
             void *nst = (u < 3) ? hbst[pp] : nullptr;
-            if (g_ws_cg != 0) {
+            if (fold) {   // h already holds nearest_to(block output, next skip size)
+                st = conv3(h, W[l], SEG_SAME, n->lh[l - 1], n->lw[l - 1], n->us[u], W[l], n->lh[l - 1], n->lw[l - 1],
+                           hb[pp], nst);
+            } else if (g_ws_cg != 0) {
                 // materialise nearest_to(h, next skip size) (exact copy) so the 3x3 conv runs on the TMA engine
                 if ((st = nearest_run(h, rbws, T, n->lh[l], n->lw[l], n->lh[l - 1], n->lw[l - 1], W[l], dt, s)) !=
                     DVC_OK)

@@ -353,6 +353,14 @@ dvc_status dvc_vae_decode(dvc_vae *v, const void *lat, int T, void *frames, void
         cur ^= 1;
         return e;
     };
+    // the last ResBlock of an up level writes the exact 2x nearest upsampling of its output straight into
+    // the scratch the upsampler conv reads (no nearest kernel, no low-res copy)
+    auto block_up2 = [&]() -> dvc_status {
+        const RB &r = v->blk[bi];
+        const int l = v->blevel[bi++];
+        return resblock_launch(r, buf[cur], nullptr, T, v->lh[l], v->lw[l], nullptr, nullptr, scr, rbws, s, bst[cur],
+                               nullptr, nullptr, 1);
+    };
     if ((st = block()) != DVC_OK) return st;
     if (c.mid_attn) {
         // x += out(softmax(q k^T / sqrt C) v), q|k|v = GN(x) W_qkv^T + b (single head, head_dim = C)
@@ -385,13 +393,15 @@ dvc_status dvc_vae_decode(dvc_vae *v, const void *lat, int T, void *frames, void
     if ((st = block()) != DVC_OK) return st;
     int ch = top;
     for (int i = 0; i < 4; ++i) {
+        const bool fold = i < 3 && v->lh[i + 1] == 2 * v->lh[i] && v->lw[i + 1] == 2 * v->lw[i];
         for (int r = 0; r < 3; ++r)
-            if ((st = block()) != DVC_OK) return st;
+            if ((st = (fold && r == 2) ? block_up2() : block()) != DVC_OK) return st;
         ch = c.width[3 - i];
         if (i < 3) {
-            // nearest 2x (exact copy) then 3x3 at the next level
-            if ((st = nearest_run(buf[cur], scr, T, v->lh[i], v->lw[i], v->lh[i + 1], v->lw[i + 1], ch, dt, s)) !=
-                DVC_OK)
+            // nearest 2x (exact copy; folded into the block above when the sizes double) then 3x3
+            if (!fold &&
+                (st = nearest_run(buf[cur], scr, T, v->lh[i], v->lw[i], v->lh[i + 1], v->lw[i + 1], ch, dt, s)) !=
+                    DVC_OK)
                 return st;
             if ((st = conv3(scr, ch, v->lh[i + 1], v->lw[i + 1], v->us[i], ch, buf[cur ^ 1], bst[cur ^ 1])) != DVC_OK)
                 return st;

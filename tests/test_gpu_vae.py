@@ -54,7 +54,10 @@ def _vae(dvc, dtype, h, w, T, mid_attn=True, attn_scale=2.0):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32])
-@pytest.mark.parametrize("h,w,T,mid", [(3, 4, 2, True), (6, 8, 2, True), (5, 7, 1, False)])
+@pytest.mark.parametrize("h,w,T,mid", [(3, 4, 2, True), (6, 8, 2, True), (5, 7, 1, False),
+                                        # H >= 32: the fused engine, whose conv2 epilogue writes the 2x
+                                        # upsampled block output directly (folded nearest)
+                                        (32, 8, 1, True)])
 def test_vae_decoder_parity(dvc, orc, dtype, h, w, T, mid):
     v, wts = _vae(dvc, dtype, h, w, T, mid)
     lat, lat64 = dev(synthgen.normal((T, h, w, 32), 1), dtype)
