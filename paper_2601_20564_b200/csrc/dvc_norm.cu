@@ -553,124 +553,34 @@ __global__ void __launch_bounds__(256) gn_finalize_box_kernel(const float2 *__re
 
 size_t box_stats_bytes(int T, int H, int W, int C) { return align256((size_t)T * boxes_per_frame(H, W) * C * 8); }
 
-// GroupNorm + SiLU of the (shifted) operand in ONE launch (the TMA engine's operand at levels with
-// H < 32): block (64-channel chunk, frame t) first reduces the box statistics of the groups its
-// channels belong to -- exactly gn_finalize_box_kernel's arithmetic and order (256 threads striding over
-// the (box, channel) items in fp64, warp xor tree, the 8 warps summed in order), so the coefficients are
-// bit-identical to the two-launch form -- then writes SiLU(GN(x)) for its 64 channels of every pixel of
-// the frame (warp = 4 pixels x 8 channel vectors: 128-byte row segments, four pixels in flight).
-template <typename T>
-__global__ void __launch_bounds__(256) gn_silu_fused_kernel(const ShiftSrc<T> X, const float2 *__restrict__ pa,
-                                                            const float2 *__restrict__ pb,
-                                                            const float2 *__restrict__ pk, int nbox, int G, double n,
-                                                            double eps, const T *__restrict__ gamma,
-                                                            const T *__restrict__ beta, T *__restrict__ out) {
-    griddep_wait();
-    __shared__ double s_S[8], s_Q[8];
-    __shared__ float s_mu[64], s_sc[64];
-    const int t = blockIdx.y, c0 = blockIdx.x * 64, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ca = X.ca, cb = X.cb, cs = X.cs, C = ca + cb, cg = C / G;
-    const int cend = min(C, c0 + 64);
-    for (int g = c0 / cg; g <= (cend - 1) / cg; ++g) {
-        const bool shifted = (g + 1) * cg <= cs;
-        const int tf = shifted ? t - 1 : t;
-        double S = 0.0, Q = 0.0;
-        if (tf >= 0 || pk != nullptr) {
-            const int n_items = nbox * cg;
-            for (int i = threadIdx.x; i < n_items; i += blockDim.x) {
-                const int b = i / cg, c = g * cg + (i - b * cg);
-                float2 v;
-                if (tf < 0) v = pk[(size_t)b * cs + c];
-                else if (c < ca) v = pa[((size_t)tf * nbox + b) * ca + c];
-                else v = pb[((size_t)tf * nbox + b) * cb + (c - ca)];
-                S += (double)v.x;
-                Q += (double)v.y;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            S += __shfl_xor_sync(0xffffffffu, S, o);
-            Q += __shfl_xor_sync(0xffffffffu, Q, o);
-        }
-        if (lane == 0) {
-            s_S[warp] = S;
-            s_Q[warp] = Q;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double SS = 0.0, QQ = 0.0;
-            for (int w = 0; w < 8; ++w) {
-                SS += s_S[w];
-                QQ += s_Q[w];
-            }
-            const double mu = SS / n;
-            double var = QQ / n - mu * mu;   // biased variance (R4)
-            if (var < 0.0) var = 0.0;
-            const float fmu = (float)mu, frs = (float)(1.0 / sqrt(var + eps));
-            for (int c = max(c0, g * cg); c < min(cend, (g + 1) * cg); ++c) {
-                s_mu[c - c0] = fmu;
-                s_sc[c - c0] = frs * Elem<T>::to_f(gamma[c]);
-            }
-        }
-        __syncthreads();
-    }
-    const int v = threadIdx.x & 7, pl = threadIdx.x >> 3;   // channel vector, pixel lane (32 lanes)
-    if (c0 + 8 * v >= C) return;
-    const VecSrc<T> src = vec_src(X, t, c0 / 8 + v);
-    float mu[8], sc[8], be[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int c = c0 + 8 * v + i;
-        sc[i] = s_sc[8 * v + i];
-        mu[i] = s_mu[8 * v + i];
-        be[i] = Elem<T>::to_f(beta[c]);
-        if (sizeof(T) == 2) {   // 16-bit outputs: z = f*sc + (beta - mu*sc), one FMA per element
-            be[i] = be[i] - mu[i] * sc[i];
-            mu[i] = 0.f;
-        }
-    }
-    T *o = out + (size_t)t * X.HW * C + c0 + 8 * v;
-    int p = pl;
-    if (src.mode == 1) {
-        for (; p + 3 * 32 < X.HW; p += 4 * 32) {
-            float f[4][8];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) load8(src.cur + (size_t)(p + 32 * j) * src.ld, f[j]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    f[j][i] = silu_t<T>(sizeof(T) == 2 ? fmaf(f[j][i], sc[i], be[i]) : (f[j][i] - mu[i]) * sc[i] + be[i]);
-                store8(o + (size_t)(p + 32 * j) * C, f[j]);
-            }
-        }
-    }
-    for (; p < X.HW; p += 32) {
-        float f[8];
-        src.load(p, f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            f[i] = silu_t<T>(sizeof(T) == 2 ? fmaf(f[i], sc[i], be[i]) : (f[i] - mu[i]) * sc[i] + be[i]);
-        store8(o + (size_t)p * C, f);
-    }
-}
-
 template <typename T>
 static dvc_status gn_silu_box_t(const NormArgs &a, const BoxStatsIn &bs, int H, int W, cudaStream_t stream) {
     ShiftSrc<T> X{reinterpret_cast<const T *>(a.xa), reinterpret_cast<const T *>(a.xb),
                   reinterpret_cast<const T *>(a.carry), a.ca, a.cb, a.cs, a.HW};
     const int C = a.ca + a.cb;
+    // one pass of 8 pixels in flight per thread: many short CTAs, no dependent load chains
+    const int cp = (256 / (C / 8)) * 8;
+    const int nchunk = (a.HW + cp - 1) / cp;
+    float2 *coef = reinterpret_cast<float2 *>(a.ws);
     ProfSlot s0 = prof_begin(stream);
-    DVC_CUDA(launch_pdl(gn_silu_fused_kernel<T>, dim3((C + 63) / 64, a.T), dim3(256), 0, stream, 1, X,
-                        reinterpret_cast<const float2 *>(bs.a), reinterpret_cast<const float2 *>(bs.b),
-                        reinterpret_cast<const float2 *>(bs.carry), boxes_per_frame(H, W), a.G,
-                        (double)(C / a.G) * a.HW, (double)a.eps, reinterpret_cast<const T *>(a.gamma),
-                        reinterpret_cast<const T *>(a.beta), reinterpret_cast<T *>(a.out)));
+    DVC_CUDA(launch_pdl(gn_finalize_box_kernel<T>, dim3(dim3(a.G, a.T)), dim3(256), 0, stream, 1, 
+        reinterpret_cast<const float2 *>(bs.a), a.ca, reinterpret_cast<const float2 *>(bs.b), a.cb,
+        reinterpret_cast<const float2 *>(bs.carry), a.cs, boxes_per_frame(H, W), a.G, (double)(C / a.G) * a.HW,
+        (double)a.eps, reinterpret_cast<const T *>(a.gamma), nullptr, coef));
     ++g_launches;
     if (s0.idx >= 0) {
         char lab[96];
-        snprintf(lab, sizeof(lab), "gn_silu T=%d HW=%d C=%d cs=%d", a.T, a.HW, C, a.cs);
+        snprintf(lab, sizeof(lab), "gn_finalize T=%d G=%d C=%d nbox=%d", a.T, a.G, C, boxes_per_frame(H, W));
         prof_end_aux(s0, stream, lab);
+    }
+    ProfSlot s1 = prof_begin(stream);
+    DVC_CUDA(launch_pdl(gn_silu_kernel<T>, dim3(dim3(nchunk, a.T)), dim3(256), 0, stream, 1, X, coef, reinterpret_cast<const T *>(a.beta),
+                                                             reinterpret_cast<T *>(a.out), cp));
+    ++g_launches;
+    if (s1.idx >= 0) {
+        char lab[96];
+        snprintf(lab, sizeof(lab), "gn_silu T=%d HW=%d C=%d cs=%d", a.T, a.HW, C, a.cs);
+        prof_end_aux(s1, stream, lab);
     }
     return check_launch("gn_silu_box");
 }
