@@ -86,6 +86,11 @@ struct FzDesc {
 };
 dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream);
 bool conv_fz_applicable(int H, int W, dvc_dtype dt);
+// the VAE output head (dvc_conv_out.cu): out[T][H][W][oc] = conv3x3(SiLU(x * scale + shift)) + b over a
+// 16-bit x [T][H][W][C] with coef float2 [T][C]; 16-bit, C in {16, 32, 48, 64}, oc <= 3
+bool conv_out_applicable(int C, int oc, dvc_dtype dt);
+dvc_status conv_out_run(const void *x, const void *coef, int T, int H, int W, int C, const void *w, const void *b,
+                        int oc, void *out, dvc_dtype dt, cudaStream_t stream);
 
 // spatial box of the TMA engine / box statistics for an H x W frame
 void choose_box(int H, int W, int *BX, int *BY);

@@ -9,9 +9,10 @@
 //   out = conv_out(SiLU(GN_out(x)))           3x3, 64 -> out_ch at full resolution
 // Frames are independent (no temporal shift): the ResBlocks run through the same engines as
 // the U-Net's with shift_p = 0 (fused GN-apply + SiLU producer, epilogue box statistics), the
-// mid attention through the tcgen05 attention kernel with head_dim = C (256).  conv_out's
-// 3 output channels are computed as a 16-channel tensor-core tile (zero weight rows) and
-// sliced by a copy kernel.
+// mid attention through the tcgen05 attention kernel with head_dim = C (256).  conv_out (16-bit)
+// is the streaming output head of dvc_conv_out.cu, writing the out_ch channels straight into the
+// frames; fp32 (and shapes it does not take) compute a 16-channel tile (zero weight rows) that a
+// copy kernel slices.
 #include <cstring>
 #include <vector>
 #include "dvc_attn.cuh"
@@ -157,7 +158,8 @@ size_t vplan(const dvc_vae &v, int T, size_t *offs) {
     sz[3] = std::max(rbws, align256((size_t)T * c.width[0] * 8) + gn_workspace_bytes(T, (int)hw(3), c.groups,
                                                                                       c.width[0]));
     sz[4] = sz[5] = st;
-    sz[6] = T * hw(3) * 16 * es;
+    // padded conv_out tile: only the paths that slice (fp32, shapes the output head does not take)
+    sz[6] = conv_out_applicable(c.width[0], c.out_ch, c.dt) ? 0 : T * hw(3) * 16 * es;
     size_t total = 0;
     for (int i = 0; i < kVRegions; ++i) {
         offs[i] = total;
@@ -411,6 +413,18 @@ dvc_status dvc_vae_decode(dvc_vae *v, const void *lat, int T, void *frames, void
     // out = conv_out(SiLU(GN_out(x))): GN-apply + SiLU fused into conv_out's operand producer when
     // the fused engine applies, else materialised; 16-channel tile, then the out_ch slice
     const int H = v->lh[3], W = v->lw[3];
+    if (conv_out_applicable(ch, c.out_ch, dt)) {   // streaming output head, straight into the frames
+        float2 *coef = reinterpret_cast<float2 *>(rbws);
+        NormArgs na{buf[cur], nullptr, nullptr, ch, 0, 0, T, H * W, c.groups, c.eps, v->gno_w, v->gno_b, coef, nullptr};
+        if ((st = gn_coef_box_run(na, BoxStatsIn{bst[cur], nullptr, nullptr}, H, W, dt, s)) != DVC_OK) return st;
+        ConvDesc prof{};
+        prof.seg[0] = ConvSeg{buf[cur], ch, SEG_SAME, H, W, 9, v->conv_out16.w, 9 * ch, 0, ch};
+        prof.nseg = 1, prof.T = T, prof.ho = H, prof.wo = W, prof.cout = c.out_ch;
+        ProfSlot slot = prof_begin(s);
+        st = conv_out_run(buf[cur], coef, T, H, W, ch, v->conv_out16.w, v->conv_out16.b, c.out_ch, frames, dt, s);
+        prof_end(slot, s, conv_flops(prof), "conv_out", prof);
+        return st;
+    }
     if (conv_fz_applicable(H, W, dt)) {
         float2 *coef = reinterpret_cast<float2 *>(rbws);
         NormArgs na{buf[cur], nullptr, nullptr, ch, 0, 0, T, H * W, c.groups, c.eps, v->gno_w, v->gno_b, coef, nullptr};

@@ -76,6 +76,26 @@ def test_vae_decoder_parity(dvc, orc, dtype, h, w, T, mid):
     assert torch.equal(out, dvc.dvc_vae_decode(v, lat))              # deterministic
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("h,w,T", [(4, 9, 2), (5, 4, 1)])
+def test_vae_decoder_parity_real_widths(dvc, orc, dtype, h, w, T):
+    # the paper's decoder widths (64, 128, 256, 256; 32 groups) at small latents: the 64-channel output
+    # head (dvc_conv_out.cu, KS = 4) with ragged 32-pixel tiles (72 = 2 x 32 + 8) and a frame narrower
+    # than one tile (32 pixels, 40 rows = 5 tiles), against the oracle end to end
+    named = synthgen.vae_weights(seed=11)
+    v = dvc.VAE(dvc.pack_weights(named, dtype), dtype=dtype, h=h, w=w, max_T=T)
+    exact = [(n, torch.from_numpy(a).to(dtype).double().numpy()) for n, a in named]
+    lat, lat64 = dev(synthgen.normal((T, h, w, 256), 4), dtype)
+    out = dvc.dvc_vae_decode(v, lat)
+    assert out.shape == (T, 8 * h, 8 * w, 3)
+    ref = orc.vae_decode(lat64, exact, mode=MODE[dtype])
+    err = rel_l2(host64(out), ref)
+    tol = TOL[dtype]
+    if dtype == torch.bfloat16:   # R31, as in test_vae_decoder_parity
+        tol = max(tol, 2 * rel_l2(ref, orc.vae_decode(lat64, exact, mode=None)))
+    assert err <= tol, (err, tol)
+
+
 def test_vae_frames_independent(dvc):
     h, w = 6, 8
     v, _ = _vae(dvc, torch.bfloat16, h, w, 3)
