@@ -673,10 +673,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) {
-                            if constexpr (CG == 1)
-                                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf]))
-                                             : "memory");
-                            else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                            tmem_drained_arrive(CG == 2 ? tempty_leader + (uint32_t)(buf * 8) : smem_u32(&tempty[buf]), CG == 2);
                         }
                     }
                     float f[32];
@@ -685,18 +682,8 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                         f[i] = __uint_as_float(va[i]);
                         f[16 + i] = __uint_as_float(vb[i]);
                     }
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        if (i >= 16 && !two) break;
-                        if (sb0) {
-                            const float4 e = *reinterpret_cast<const float4 *>(sb0 + n + i);
-                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
-                        }
-                        if (sb1) {
-                            const float4 e = *reinterpret_cast<const float4 *>(sb1 + n + i);
-                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
-                        }
-                    }
+                    if (sb0) epi_add_bias(f, sb0 + n, two);   // bias0 then bias1, as the other paths
+                    if (sb1) epi_add_bias(f, sb1 + n, two);
                     epi_stage_chunk<T>(f, m >= 0, two, r, q4, lane, sStage + par * kEpiStage, &p.omap[0], &p.omap[1],
                                        issuer, bx.valid, n, bx.x0, bx.y0, bx.t,
                                        want_stats ? stats_box + (size_t)n * 2 : nullptr, red + par * 256, p.up2 != 0);
@@ -733,10 +720,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if constexpr (CG == 1) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                                                        smem_u32(&tempty[buf]))
-                                                    : "memory");
-                else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                tmem_drained_arrive(CG == 2 ? tempty_leader + (uint32_t)(buf * 8) : smem_u32(&tempty[buf]), CG == 2);
             }
         }
     }

@@ -296,10 +296,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    if constexpr (CG == 1) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                                                            smem_u32(&tempty[buf]))
-                                                        : "memory");
-                    else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                    tmem_drained_arrive(CG == 2 ? tempty_leader + (uint32_t)(buf * 8) : smem_u32(&tempty[buf]), CG == 2);
                 }
                 continue;
             }
@@ -334,10 +331,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) {
-                            if constexpr (CG == 1)
-                                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf]))
-                                             : "memory");
-                            else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                            tmem_drained_arrive(CG == 2 ? tempty_leader + (uint32_t)(buf * 8) : smem_u32(&tempty[buf]), CG == 2);
                         }
                     }
                     float f[32];
@@ -346,18 +340,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                         f[i] = __uint_as_float(va[i]) * p.out_scale;
                         f[16 + i] = __uint_as_float(vb[i]) * p.out_scale;
                     }
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        if (i >= 16 && !two) break;
-                        if (sb0) {
-                            const float4 e = *reinterpret_cast<const float4 *>(sb0 + n + i);
-                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
-                        }
-                        if (sb1) {
-                            const float4 e = *reinterpret_cast<const float4 *>(sb1 + n + i);
-                            f[i] += e.x, f[i + 1] += e.y, f[i + 2] += e.z, f[i + 3] += e.w;
-                        }
-                    }
+                    if (sb0) epi_add_bias(f, sb0 + n, two);   // bias0 then bias1, as the other paths
+                    if (sb1) epi_add_bias(f, sb1 + n, two);
                     if (res && m >= 0) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) f[i] += rv[i];
@@ -395,10 +379,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if constexpr (CG == 1) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                                                        smem_u32(&tempty[buf]))
-                                                    : "memory");
-                else mbar_arrive_cluster(tempty_leader + (uint32_t)(buf * 8));
+                tmem_drained_arrive(CG == 2 ? tempty_leader + (uint32_t)(buf * 8) : smem_u32(&tempty[buf]), CG == 2);
             }
         }
     }

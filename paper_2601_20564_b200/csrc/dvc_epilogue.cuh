@@ -4,11 +4,11 @@
 //   registers (thread = box row r, final fp32 values) -> 16-bit rounding -> a swizzled [128][32]
 //   tile in shared memory (zeros for rows outside the frame) -> ONE TMA store of the output box
 //   {32, BX, BY, 1} (the hardware clips rows outside the tensor) -> the box statistics of the next
-//   GroupNorm read back column-wise (lane = column, warp q4 = rows 32 q4 .. 32 q4 + 31) and reduced
-//   with the canonical tree of dvc_boxstats.cuh: rows paired by bit 4, then 3, 2, 1, 0 (the xor
-//   butterfly's tree, with commutative fp32 adds), warps combined ((w0 + w1) + w2) + w3 -- bit for bit
-//   the partials every other producer writes (H4), without 62 shuffles per 16 columns and without
-//   32 uncoalesced 16-byte stores per warp instruction.
+//   GroupNorm read back column-wise (a lane pair per two columns, warp q4 = rows 32 q4 .. 32 q4 + 31,
+//   packed fp32 pairs) and reduced with the canonical tree of dvc_boxstats.cuh: rows paired by bit 4,
+//   then 3, 2, 1, 0 (the xor butterfly's tree, with commutative fp32 adds), warps combined
+//   ((w0 + w1) + w2) + w3 -- bit for bit the partials every other producer writes (H4), without 62
+//   shuffles per 16 columns and without 32 uncoalesced 16-byte stores per warp instruction.
 // Staging layouts match the TMA swizzle of the output maps: 64-byte rows with SWIZZLE_64B (16-byte
 // unit j of row r at j ^ ((r >> 1) & 3)), 32-byte rows with SWIZZLE_32B (j ^ ((r >> 2) & 1)).
 // All 128 epilogue threads (named barrier 1) call it for every chunk in the same order; two staging
@@ -29,6 +29,9 @@ template <> struct EpiPk<__nv_bfloat16> {
         return *reinterpret_cast<uint32_t *>(&h);
     }
     static __device__ __forceinline__ float unpack16(uint16_t u) { return __uint_as_float((uint32_t)u << 16); }
+    static __device__ __forceinline__ float2 unpack2(uint32_t u) {
+        return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
+    }
 };
 template <> struct EpiPk<__half> {
     static __device__ __forceinline__ uint32_t pack(float a, float b) {
@@ -36,7 +39,22 @@ template <> struct EpiPk<__half> {
         return *reinterpret_cast<uint32_t *>(&h);
     }
     static __device__ __forceinline__ float unpack16(uint16_t u) { return __half2float(__ushort_as_half(u)); }
+    static __device__ __forceinline__ float2 unpack2(uint32_t u) {
+        return __half22float2(*reinterpret_cast<const __half2 *>(&u));
+    }
 };
+
+// f[0 .. ncol) += b[0 .. ncol) (ncol = two ? 32 : 16), packed fp32 pairs (FADD2; per-element IEEE rn)
+__device__ __forceinline__ void epi_add_bias(float (&f)[32], const float *b, bool two) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+        if (i >= 16 && !two) break;
+        const float4 e = *reinterpret_cast<const float4 *>(b + i);
+        const float2 lo = __fadd2_rn(make_float2(f[i], f[i + 1]), make_float2(e.x, e.y));
+        const float2 hi = __fadd2_rn(make_float2(f[i + 2], f[i + 3]), make_float2(e.z, e.w));
+        f[i] = lo.x, f[i + 1] = lo.y, f[i + 2] = hi.x, f[i + 3] = hi.y;
+    }
+}
 
 __device__ __forceinline__ int epi_off(bool two, int r, int j) {
     return two ? r * 64 + ((j ^ ((r >> 1) & 3)) << 4) : r * 32 + ((j ^ ((r >> 2) & 1)) << 4);
@@ -79,25 +97,42 @@ __device__ __forceinline__ void epi_stage_chunk(const float (&f)[32], bool live,
         bulk_wait_group_read<1>();   // the other staging buffer has been read: reusable for chunk i+1
     }
     if (stats_col) {
-        const int c = lane;
-        if (c < ncol) {
-            float v[32], q[32];
+        // lane = (column pair cp = lane / 2, row parity b0 = lane % 2): the 16 rows 32 q4 + 2i + b0 of
+        // columns 2cp, 2cp + 1 in packed fp32 pairs (FMUL2 / FADD2, IEEE round-to-nearest per element).
+        // The tree over i (i, i + 8), (i, i + 4), (i, i + 2), (i, i + 1) is the canonical one's levels
+        // over rows differing in bit 4, 3, 2, 1; its last level (bit 0) is the lane pair (shuffle).
+        const int cp = lane >> 1, b0 = lane & 1, c = 2 * cp;
+        const bool lv = c < ncol;
+        float2 v[16], q[16];
+        if (lv) {
             const int j = c >> 3, e = (c & 7) * 2;
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int rr = q4 * 32 + k;
-                v[k] = EpiPk<T>::unpack16(*reinterpret_cast<const uint16_t *>(st + epi_off(two, rr, j) + e));
-                q[k] = __fmul_rn(v[k], v[k]);
+            for (int i = 0; i < 16; ++i) {
+                const int rr = q4 * 32 + 2 * i + b0;
+                v[i] = EpiPk<T>::unpack2(*reinterpret_cast<const uint32_t *>(st + epi_off(two, rr, j) + e));
+                q[i] = __fmul2_rn(v[i], v[i]);
             }
 #pragma unroll
-            for (int mm = 16; mm >= 1; mm >>= 1)
+            for (int mm = 8; mm >= 1; mm >>= 1)
 #pragma unroll
                 for (int k = 0; k < mm; ++k) {
-                    v[k] = __fadd_rn(v[k], v[k + mm]);
-                    q[k] = __fadd_rn(q[k], q[k + mm]);
+                    v[k] = __fadd2_rn(v[k], v[k + mm]);
+                    q[k] = __fadd2_rn(q[k], q[k + mm]);
                 }
-            red[q4 * 32 + c] = v[0];
-            red[128 + q4 * 32 + c] = q[0];
+        } else {
+            v[0] = q[0] = make_float2(0.f, 0.f);
+        }
+        float2 ov, oq;
+        ov.x = __shfl_xor_sync(0xffffffffu, v[0].x, 1);
+        ov.y = __shfl_xor_sync(0xffffffffu, v[0].y, 1);
+        oq.x = __shfl_xor_sync(0xffffffffu, q[0].x, 1);
+        oq.y = __shfl_xor_sync(0xffffffffu, q[0].y, 1);
+        if (lv && b0 == 0) {   // (row 2i) + (row 2i + 1); fp32 addition is commutative
+            const float2 sv = __fadd2_rn(v[0], ov), sq = __fadd2_rn(q[0], oq);
+            red[q4 * 32 + c] = sv.x;
+            red[q4 * 32 + c + 1] = sv.y;
+            red[128 + q4 * 32 + c] = sq.x;
+            red[128 + q4 * 32 + c + 1] = sq.y;
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (q4 < 2 && lane < ncol) {   // warp 0: sums, warp 1: sums of squares

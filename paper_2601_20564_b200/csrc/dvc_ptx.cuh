@@ -214,6 +214,16 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// TMEM accumulator drained (epilogue -> MMA issuer): a resource signal that publishes no memory.
+// The tcgen05.ld's are complete (tcgen05.wait::ld) and ordered by tcgen05.fence::before_thread_sync,
+// so the arrive is relaxed: a release would first wait for the epilogue's outstanding global stores
+// (box statistics) to become visible cluster-wide -- an L2 round trip per accumulator.
+__device__ __forceinline__ void tmem_drained_arrive(uint32_t addr, bool cluster) {
+    if (cluster)
+        asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+    else
+        asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
 // arrive + expect_tx on a barrier of any CTA of the cluster (shared::cluster address)
 __device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),

@@ -12,6 +12,6 @@ done
 if [ -n "$BREAKDOWN" ]; then
   for c in "${CFG[@]}"; do
     echo "== breakdown $c"
-    env DVC_LIB=ab/libdvc_exp.so $c timeout 300 python tools/conv_breakdown.py 2>&1 | grep -E "total|fz" | head -24
+    env DVC_LIB=ab/libdvc_exp.so $c timeout 300 python tools/conv_breakdown.py ${BARGS} 2>&1 | grep -E "total|fz" | head -24
   done
 fi

@@ -1,6 +1,7 @@
 """Device time of the headline step (encode + ResBlock-skeleton decode, 720p, 32 frames, bf16) for
 same-box A/B comparisons of library builds (DVC_LIB) and experiment knobs; not a bench number.
-    python tools/step_time.py [--steps 20] [--frames 32] [--attention]"""
+    python tools/step_time.py [--steps 20] [--frames 32] [--attention] [--vae]
+--vae: one 720p pruned-VAE decode (f2) of --frames frames instead."""
 import argparse
 import os
 import sys
@@ -16,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--frames", type=int, default=32)
 ap.add_argument("--attention", action="store_true")
+ap.add_argument("--vae", action="store_true")
 a = ap.parse_args()
 T, H, W = a.frames, 720, 1280
 h, w = H // 8, W // 8
@@ -36,6 +38,17 @@ ws = torch.empty(net.workspace_size(T), dtype=torch.uint8, device="cuda")
 def step():
     dvc.dvc_encode_pixelunshuffle(frames, we, be, out=lat)
     dvc.dvc_unet_decode_gop(net, lat, ctx, out=out, workspace=ws)
+
+
+if a.vae:   # the decoder alone, on the latent of one encode
+    step()
+    vae = dvc.VAE(dvc.pack_weights(synthgen.vae_weights(), dt), dtype=dt, h=h, w=w, max_T=T)
+    out = torch.empty((T, H, W, 3), dtype=dt, device="cuda")
+    vws = torch.empty(vae.workspace_size(T), dtype=torch.uint8, device="cuda")
+    del net, ws
+
+    def step():   # noqa: F811
+        dvc.dvc_vae_decode(vae, lat, out=out, workspace=vws)
 
 
 for _ in range(3):
