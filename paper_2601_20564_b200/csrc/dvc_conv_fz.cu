@@ -45,7 +45,7 @@ constexpr int FZ_COEF = FZ_SIDE + FZ_LBO;     // 26496
 constexpr int FZ_SLOT = 27648;                // 1024-aligned
 constexpr int FZ_RAW_SLOT = 128 * 128;        // one raw SW128 box {64, 8, 16}
 constexpr int FZ_SBO = FZ_HX * 16;            // between 8-row groups (image rows)
-constexpr int FZ_MAX_BSTAGES = 16;
+constexpr int FZ_MAX_BSTAGES = 24;
 constexpr int FZ_MAX_NTF = 6;   // even: keeps the barrier block a multiple of 16 B
 constexpr int FZ_MAX_RAW = 4;   // raw (1x1) ring slots
 #ifndef FZ_TFW
@@ -89,6 +89,8 @@ struct FzParams {
     int epi_tma;                // 1: epilogue stages 32-column chunks in shared memory, TMA-stores them and reads
                                 //    the box statistics back column-wise; 0: per-thread row stores + butterflies
     CUtensorMap omap[2];        // output [T][H][W][cout]: box {32, 8, 16, 1} SW64 / {16, 8, 16, 1} SW32
+    int wres;                   // 1: one N tile and nb == the weight stages of a work item: the weights are
+                                //    loaded once and stay resident (no per-item weight stream)
 };
 
 // UMMA descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B
@@ -261,6 +263,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         const uint32_t bfull0 = smem_u32(b_full), bempty0 = smem_u32(b_empty), sB0 = smem_u32(sB);
         const uint32_t lead_bfull0 = CG == 2 ? mapa_shared(bfull0, 0) : bfull0;
         for (int w = cluster_id; w < p.nwork; w += nclusters) {
+            if (p.wres && w != cluster_id) break;   // resident weights: one pass
             const int nt = w % p.ntile_n;
             const int n0 = nt * BN + (int)rank * BNH;
             for (int st_i = 0; st_i < p.nsteps; ++st_i) {
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                     if (!tf) {   // raw 1x1 chunk from the raw ring (SW128 box): one tap
                         FZ_TIMED(1, mbar_wait_spin_addr(rwfull0 + 8 * rb, rph));
                         tc_fence_after();
-                        FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
+                        if (!p.wres || it == 0) FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
                         tc_fence_after();
                         mma_stage<CG>(d, desc_lo(sR0 + (uint32_t)(rb * FZ_RAW_SLOT), 16), kDescHiSw128, 2u, b_lo,
                                       kDescHiSw128, p.idesc, ks, acc, bempty0 + 8 * bs);
@@ -568,7 +571,7 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                     const uint32_t a_row = sw ? 8u : 1u;   // one halo row in 16-byte units
 #pragma unroll
                     for (int tap = 0; tap < 9; ++tap) {
-                        FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
+                        if (!p.wres || it == 0) FZ_TIMED(2, mbar_wait_spin_addr(bfull0 + 8 * bs, bph));
                         tc_fence_after();
                         const uint32_t roff16 = (uint32_t)((tap / 3) * FZ_HX + tap % 3) * a_row;
                         // optional matrix base offset (bits 49-51): the 1024-B pattern phase of the start
@@ -959,6 +962,14 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     }
     if (nbst > FZ_MAX_BSTAGES) nbst = FZ_MAX_BSTAGES;
     DVC_CHECK_ARG(nbst >= 2, DVC_ERR_UNSUPPORTED, "fused conv: shared memory too small");
+    {   // resident weights when one N tile's stages for a whole work item fit (the VAE's 64-channel
+        // full-resolution convs: 9-18 stages of 4 KB); DVC_FZ_WRES=0 in experiment builds disables
+        int per_item = 0;
+        for (int i = 0; i < p.nsteps; ++i) per_item += d.seg[p.ord[i] >> 6].transform ? 9 : 1;
+        const char *e = dvc_knob("DVC_FZ_WRES");
+        p.wres = (e ? atoi(e) != 0 : true) && p.ntile_n == 1 && per_item <= nbst ? 1 : 0;
+        if (p.wres) nbst = per_item;
+    }
     p.nb = nbst;
     const size_t smem = fixed - 1024 + (size_t)nbst * bstage;
     static const bool prof = dvc_knob("DVC_FZ_PROF") != nullptr && atoi(dvc_knob("DVC_FZ_PROF")) != 0;
