@@ -24,6 +24,9 @@ timeout 900 python tools/bench_configs.py > gpurun_out/configs_$TAG.jsonl 2>&1
 timeout 600 python bench.py --attention --steps 5 --warmup 3 > gpurun_out/bench_attn_$TAG.json 2>&1
 timeout 600 python tools/bench_f1.py > gpurun_out/f1_$TAG.jsonl 2>&1
 timeout 300 python tools/bench_f2.py > gpurun_out/f2_$TAG.jsonl 2>&1
+timeout 300 python tools/conv_breakdown.py --vae --frames 8 > gpurun_out/vae_breakdown_$TAG.txt 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+  -k regex:conv_out --csv --log-file gpurun_out/convout_$TAG.csv python tools/vae_once.py 8 > /dev/null 2>&1
 timeout 600 python tools/bench_f3.py > gpurun_out/f3_$TAG.jsonl 2>&1
 timeout 300 python tools/bench_fp8.py > gpurun_out/fp8_$TAG.jsonl 2>&1
 echo done
