@@ -523,7 +523,7 @@ dvc_status make_out_map_box(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, in
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, ptr,
                      gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                     box_c == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed (%d)", (int)r);
     return DVC_OK;

@@ -16,7 +16,11 @@
 // GEMM per tile: M = 128 latent pixels, N = c_lat (<= 256), K = 192 (12 MMAs of K = 16); the
 // expansion weights [c_lat][192] stay resident in shared memory (3 SW128 boxes).  Two TMEM
 // accumulators (2 x N fp32 columns) let the epilogue (bias, 16-bit store) of tile i overlap the
-// MMAs of tile i+1; two A stages overlap the next tile's TMA with the current tile's MMAs.
+// MMAs of tile i+1.  The A operand streams through a ring of 16 KB colour planes (one
+// {64, 8, 16, 1} box = one K block of 64 each, three per tile), each refilled as soon as its four
+// MMAs retire.  The epilogue stages 64 columns at a time (SWIZZLE_128B, 128-byte output rows = whole
+// L2 lines) and keeps up to four TMA stores in flight; the stores are the bound (measured on the
+// B200, 720p x 32: 94 us with 32-column chunks and 2 stores in flight -> 82 us; loads alone 49 us).
 // Warps (256 threads): 0 TMA producer, 1 TMEM allocator + MMA issuer, 4-7 epilogue.
 // HBM-bound by design: per tile 48 KB of frames in, 128 x c_lat x 2 B of latent out.
 #include <cuda.h>
@@ -29,6 +33,8 @@ namespace dvc {
 
 constexpr int ENC_BX = 8, ENC_BY = 16;         // latent pixels per tile (128 MMA rows)
 constexpr int ENC_A_BYTES = 3 * 64 * 128 * 2;  // 49152: {64, 8, 16, 3} 16-bit box
+constexpr int ENC_PLANE = 64 * 128 * 2;         // 16384: one colour plane {64, 8, 16, 1}
+constexpr int ENC_NPLANE = 2 * ENC_A_BYTES / ENC_PLANE;   // 6: A-region capacity in colour planes
 constexpr int ENC_THREADS = 256;
 constexpr int ENC_U8_THREADS = 384;             // + warps 8-11: the u8 -> 16-bit converters
 constexpr int ENC_U8_HALF = 64 * 192;           // u8 staging slot: 64 frame rows x 64 pixels x 3 bytes
@@ -54,7 +60,10 @@ struct EncParams {
     int tiles_x, tiles_y, ntiles;
     const void *bias;
     void *out;          // latent [T][h][w][c_lat]
-    CUtensorMap omap[2];   // latent, box {32 | 16, 8, 16, 1}, SW64 / SW32 (staged epilogue, 16-bit frames)
+    CUtensorMap omap[3];   // latent, box {32 | 16, 8, 16, 1} SW64 / SW32, [2]: {64, 8, 16, 1} SW128 (staged epilogue)
+    int wide;              // c_lat % 64 == 0: 64-column chunks, 128-byte output rows (omap[2], 16 KB staging)
+    int nplane;            // 16-bit path: A ring depth in colour planes (wide: 4, the last two planes'
+                           // 32 KB hold two more staging tiles -> 4 stores in flight; else 6)
     uint32_t idesc;
 };
 
@@ -70,9 +79,9 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
     const int B_CHUNK = N * 128;               // one 64-column SW128 box of the weights
     uint8_t *sA = smem;                        // [2][ENC_A_BYTES]
     uint8_t *sB = sA + 2 * ENC_A_BYTES;        // [3][B_CHUNK]
-    uint64_t *a_full = reinterpret_cast<uint64_t *>(sB + 3 * B_CHUNK);
-    uint64_t *a_empty = a_full + 2;
-    uint64_t *tfull = a_empty + 2;
+    uint64_t *a_full = reinterpret_cast<uint64_t *>(sB + 3 * B_CHUNK);   // [6] (u8: [2] whole tiles)
+    uint64_t *a_empty = a_full + ENC_NPLANE;
+    uint64_t *tfull = a_empty + ENC_NPLANE;
     uint64_t *tempty = tfull + 2;
     uint64_t *b_full = tempty + 2;
     uint64_t *u_full = b_full + 2;    // [2] u8 staging slot landed (U8)
@@ -85,9 +94,11 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t ncols = 2 * N <= 128 ? 128 : 2 * N <= 256 ? 256 : 512;
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < ENC_NPLANE; ++i) {
             mbar_init(&a_full[i], U8 ? 8 : 1);   // U8: 4 converter warps x 2 half tiles
             mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
             mbar_init(&u_full[i], 1);
@@ -139,16 +150,19 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
                 }
                 continue;
             }
-            mbar_wait_spin(&a_empty[stage], phase ^ 1);
-            if (issue) {
-                const uint32_t fb = smem_u32(&a_full[stage]);
-                mbar_arrive_expect_tx_addr(fb, ENC_A_BYTES);
-                tma_load_4d(smem_u32(sA + stage * ENC_A_BYTES), &p.amap, fb, bx * ENC_BX * 8, 0, by * ENC_BY, t * 3);
-            }
-            __syncwarp();
-            if (++stage == 2) {
-                stage = 0;
-                phase ^= 1;
+#pragma unroll 1
+            for (int c = 0; c < 3; ++c) {   // one colour plane per ring slot
+                mbar_wait_spin(&a_empty[stage], phase ^ 1);
+                if (issue) {
+                    const uint32_t fb = smem_u32(&a_full[stage]);
+                    mbar_arrive_expect_tx_addr(fb, ENC_PLANE);
+                    tma_load_4d(smem_u32(sA + stage * ENC_PLANE), &p.amap, fb, bx * ENC_BX * 8, 0, by * ENC_BY, t * 3 + c);
+                }
+                __syncwarp();
+                if (++stage == p.nplane) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
         }
     } else if (warp == 1) {
@@ -162,9 +176,29 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1;
             mbar_wait_spin(&tempty[buf], use ^ 1);
+            const uint32_t d = tmem + (uint32_t)(buf * N);
+            if constexpr (!U8) {
+                // colour c = K block of 64 in ring slot `stage` (K step of 16 = dy += 2 = +256 B); B = weight
+                // box c (K step = +32 B inside the swizzled 128-byte rows); each plane is released by the
+                // commit of its own four MMAs
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    mbar_wait_spin(&a_full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_lo = desc_lo(sA0 + (uint32_t)(stage * ENC_PLANE), 128);
+                    const uint32_t b_lo = desc_lo(sB0 + (uint32_t)(c * B_CHUNK), 16);
+                    mma_stage<1>(d, a_lo, desc_hi_noswz(1024), 16u, b_lo, kDescHiSw128, p.idesc, 4u, c ? 1u : 0u,
+                                 smem_u32(&a_empty[stage]));
+                    if (++stage == p.nplane) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                commit_elected<1>(smem_u32(&tfull[buf]));
+                continue;
+            }
             mbar_wait_spin(&a_full[stage], phase);
             tc_fence_after();
-            const uint32_t d = tmem + (uint32_t)(buf * N);
             const uint32_t a_base = sA0 + (uint32_t)(stage * ENC_A_BYTES);
             // colour c = K block of 64: A at +16 KB per colour (K step of 16 = dy += 2 = +256 B),
             // B = weight box c (K step = +32 B inside the swizzled 128-byte rows)
@@ -261,6 +295,48 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
                 const bool issuer = warp == 4 && lane == 0;
                 const int bx0 = (rem % p.tiles_x) * ENC_BX, by0 = (rem / p.tiles_x) * ENC_BY;
                 int par = 0;
+                if (p.wide) {
+                    // 64 columns per chunk: one SWIZZLE_128B [128 rows][128 B] staging tile (16-byte unit j of
+                    // row r at j ^ (r & 7)) and one TMA store of the {64, 8, 16, 1} box -- whole 128-byte
+                    // output rows (full L2 lines) and half the barrier round trips of the 32-column form
+#pragma unroll 1
+                    const bool four = p.nplane == 4;   // four staging tiles: two in the A region
+                    for (int cc = 0; cc < N; cc += 64, par = (par + 1) & (four ? 3 : 1)) {
+                        uint32_t v[4][16];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16 * k), v[k]);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) tmem_wait16(v[k]);
+                        if (cc + 64 >= N) {   // accumulator drained
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0)
+                                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+                        }
+                        uint8_t *st = par < 2 ? sStage + par * (2 * kEpiStage) : sA + (par + 2) * ENC_PLANE;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int c = cc + 8 * j;
+                            const uint32_t *w = &v[j >> 1][(j & 1) * 8];
+                            uint4 u;
+                            u.x = live ? Pk2<T>::pack(__uint_as_float(w[0]) + sbias[c], __uint_as_float(w[1]) + sbias[c + 1]) : 0u;
+                            u.y = live ? Pk2<T>::pack(__uint_as_float(w[2]) + sbias[c + 2], __uint_as_float(w[3]) + sbias[c + 3]) : 0u;
+                            u.z = live ? Pk2<T>::pack(__uint_as_float(w[4]) + sbias[c + 4], __uint_as_float(w[5]) + sbias[c + 5]) : 0u;
+                            u.w = live ? Pk2<T>::pack(__uint_as_float(w[6]) + sbias[c + 6], __uint_as_float(w[7]) + sbias[c + 7]) : 0u;
+                            *reinterpret_cast<uint4 *>(st + r * 128 + ((j ^ (r & 7)) << 4)) = u;
+                        }
+                        fence_proxy_async_smem();
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (issuer) {
+                            tma_store_4d(&p.omap[2], smem_u32(st), cc, bx0, by0, t);
+                            bulk_commit_group();
+                            if (four) bulk_wait_group_read<3>();   // the next staging tile is reusable
+                            else bulk_wait_group_read<1>();
+                        }
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                    }
+                    continue;
+                }
 #pragma unroll 1
                 for (int cc = 0; cc < N; cc += 32, par ^= 1) {
                     uint32_t va[16], vb[16];
@@ -362,7 +438,7 @@ dvc_status encode_tma_run(const void *frames, dvc_dtype frame_dt, int T, int H, 
     } else {    // frames [T][3][H][W] as (x, dy, hb, t*3 + c)
         cuuint64_t gdim[4] = {(cuuint64_t)W, 8, (cuuint64_t)(H / 8), (cuuint64_t)T * 3};
         cuuint64_t gstride[3] = {(cuuint64_t)W * 2, (cuuint64_t)W * 16, (cuuint64_t)H * W * 2};
-        cuuint32_t box[4] = {ENC_BX * 8, 8, ENC_BY, 3};
+        cuuint32_t box[4] = {ENC_BX * 8, 8, ENC_BY, 1};   // one colour plane per TMA
         cuuint32_t estr[4] = {1, 1, 1, 1};
         r = enc(&p.amap, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
                 const_cast<void *>(frames), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -382,10 +458,13 @@ dvc_status encode_tma_run(const void *frames, dvc_dtype frame_dt, int T, int H, 
     p.out = latent;
     p.idesc = make_idesc(dt == DVC_BF16, 128, c_lat);
     const size_t smem = u8 ? 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 2048 + 2 * ENC_U8_HALF
-                           : 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 2048 + 2 * kEpiStage;
+                           : 1024 + 2 * ENC_A_BYTES + 3 * (size_t)c_lat * 128 + 2048 + 4 * kEpiStage;
     if (!u8) {
         st = make_out_map_box(&p.omap[0], latent, dt, T, H / 8, W / 8, c_lat, 32, ENC_BX, ENC_BY);
         if (st == DVC_OK) st = make_out_map_box(&p.omap[1], latent, dt, T, H / 8, W / 8, c_lat, 16, ENC_BX, ENC_BY);
+        p.wide = c_lat % 64 == 0;
+        if (st == DVC_OK && p.wide) st = make_out_map_box(&p.omap[2], latent, dt, T, H / 8, W / 8, c_lat, 64, ENC_BX, ENC_BY);
+        p.nplane = p.wide ? 4 : ENC_NPLANE;
         if (st != DVC_OK) return st;
     }
     auto kern = dt == DVC_BF16 ? (u8 ? encode_kernel<__nv_bfloat16, true> : encode_kernel<__nv_bfloat16, false>)

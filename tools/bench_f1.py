@@ -54,7 +54,7 @@ def attn(steps):
         T = 32
         qkv = torch.from_numpy(synthgen.normal((T, N, 3 * C), 11)).to(torch.bfloat16).cuda()
         out = torch.empty((T, N, C), dtype=torch.bfloat16, device="cuda")
-        ws = torch.empty(3 * T * C * ((N + 127) // 128 * 128) * 2 + 256, dtype=torch.uint8, device="cuda")
+        ws = None   # the library sizes and allocates its packed-operand workspace
         dvc.profile_begin()
         ms = timed(lambda: dvc.dvc_attention_forward(qkv, 48, out=out, workspace=ws), steps)
         dvc.profile_end()
