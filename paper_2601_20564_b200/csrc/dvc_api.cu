@@ -188,8 +188,14 @@ dvc_status resblock_validate(const RB &b, int T, int H, int W) {
 // are computed here; stats_y: where to put the box statistics of y (or null).
 static dvc_status resblock_body(const RB &b, const void *xa, const void *xb, int T, int H, int W,
                                 const void *carry_in, void *y, void *ws, cudaStream_t stream, const void *stats_a,
-                                const void *stats_b, void *stats_y, int up2) {
+                                const void *stats_b, void *stats_y, int up2, int up_ho, int up_wo) {
     const int HW = H * W, cin = b.ca + b.cb, cs = b.P > 0 ? cin / b.P : 0;
+    if (up2) {
+        up_ho = up_ho ? up_ho : 2 * H;
+        up_wo = up_wo ? up_wo : 2 * W;
+        DVC_CHECK_ARG((up_ho == 2 * H || up_ho == 2 * H - 1) && (up_wo == 2 * W || up_wo == 2 * W - 1), DVC_ERR_UNSUPPORTED,
+                      "resblock: upsampled output must be 2H (- 1) x 2W (- 1)");
+    }
     if (cs == 0) carry_in = nullptr;   // no shift: no carry
     const size_t es = dt_size(b.dt);
     uint8_t *p = reinterpret_cast<uint8_t *>(ws);
@@ -306,6 +312,8 @@ static dvc_status resblock_body(const RB &b, const void *xa, const void *xb, int
         f2.out = y;
         f2.stats_out = up2 ? nullptr : stats_y;
         f2.up2 = up2;
+        f2.up_ho = up_ho;
+        f2.up_wo = up_wo;
         f2.dt = b.dt;
         ConvDesc prof{};
         prof.seg[0] = ConvSeg{y1, b.cout, SEG_SAME, H, W, 9, b.conv2_w, 9 * b.cout, 0, b.cout};
@@ -384,19 +392,25 @@ static dvc_status resblock_body(const RB &b, const void *xa, const void *xb, int
     c2.wo = W;
     c2.cout = b.cout;
     c2.bias0 = b.conv2_b;
-    c2.out = up2 ? y1 : y;   // up2: the low-res output in Y1's (consumed) region, then upsampled
     c2.stats_out = up2 ? nullptr : stats_y;
     c2.dt = b.dt;
+    if (up2 && conv_ws_applicable(c2)) {   // the TMA engine's staged epilogue stores the upsampled tensor
+        c2.up2 = 1, c2.up_ho = up_ho, c2.up_wo = up_wo;
+        c2.out = y;
+        return conv_run(c2, stream);
+    }
+    c2.out = up2 ? y1 : y;   // up2 (fp32 / gather engine): the low-res output in Y1's (consumed) region, then upsampled
     if ((st = conv_run(c2, stream)) != DVC_OK || !up2) return st;
-    return nearest_run(y1, y, T, H, W, 2 * H, 2 * W, b.cout, b.dt, stream);
+    return nearest_run(y1, y, T, H, W, up_ho, up_wo, b.cout, b.dt, stream);
 }
 
 dvc_status resblock_launch(const RB &b, const void *xa, const void *xb, int T, int H, int W, const void *carry_in,
                            void *carry_out, void *y, void *ws, cudaStream_t stream, const void *stats_a,
-                           const void *stats_b, void *stats_y, int up2) {
+                           const void *stats_b, void *stats_y, int up2, int up_ho, int up_wo) {
     const int cs = b.P > 0 ? (b.ca + b.cb) / b.P : 0;
     DVC_CHECK_ARG(!up2 || stats_y == nullptr, DVC_ERR_ARG, "an upsampled block output has no statistics");
-    dvc_status st = resblock_body(b, xa, xb, T, H, W, carry_in, y, ws, stream, stats_a, stats_b, stats_y, up2);
+    dvc_status st = resblock_body(b, xa, xb, T, H, W, carry_in, y, ws, stream, stats_a, stats_b, stats_y, up2, up_ho,
+                                  up_wo);
     if (st != DVC_OK || !carry_out || cs == 0) return st;
     // carry_out = X[T-1][..., 0:C_in/P] (the raw block input; y never aliases x), enqueued after every
     // reader of carry_in, so an in-place carry update (carry_out == carry_in) is well defined

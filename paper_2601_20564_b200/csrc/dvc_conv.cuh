@@ -56,6 +56,10 @@ struct ConvDesc {
     // before bias and the 16-bit (dt) store
     int fp8 = 0;
     float out_scale = 1.f;
+    // up2 (TMA engine, staged epilogue): out is nearest_to(conv output, up_ho, up_wo) with up_ho in
+    // {2 ho - 1, 2 ho} and up_wo in {2 wo - 1, 2 wo} -- exactly the 2x phase replication clipped at
+    // the far edge (R11: floor(Y * ho / up_ho) = floor(Y / 2) for those sizes); no statistics
+    int up2 = 0, up_ho = 0, up_wo = 0;
     long M() const { return (long)T * ho * wo; }
 };
 
@@ -79,10 +83,11 @@ struct FzDesc {
     const void *bias0, *bias1, *residual;
     void *out, *stats_out;
     dvc_dtype dt;
-    // up2: out is the exact 2x nearest upsampling [T][2H][2W][cout] of the conv's output (the
-    // epilogue's TMA store writes every staged box four times with element stride 2; the low-res
-    // output is never written; no statistics)
-    int up2 = 0;
+    // up2: out is the nearest upsampling [T][up_ho][up_wo][cout] of the conv's output, up_ho in
+    // {2H - 1, 2H}, up_wo in {2W - 1, 2W} (0: 2H / 2W) -- the epilogue's TMA store writes every staged
+    // box four times with element stride 2, the far edge clipped by the tensor bounds; the low-res
+    // output is never written; no statistics
+    int up2 = 0, up_ho = 0, up_wo = 0;
 };
 dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream);
 bool conv_fz_applicable(int H, int W, dvc_dtype dt);

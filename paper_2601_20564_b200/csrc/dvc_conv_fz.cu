@@ -794,11 +794,12 @@ static dvc_status make_halo_map(CUtensorMap *map, const void *ptr, dvc_dtype dt,
 // up = 2: the tensor is the 2x upsampled output [T][2H][2W][C], walked with element stride 2 in x and
 // y so that a staged 8 x 16 box lands on one phase of the upsampled grid
 static dvc_status make_out_map(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, int H, int W, int C, int box_c,
-                               int up = 1) {
+                               int up = 1, int up_ho = 0, int up_wo = 0) {
     PFN_encodeTiled_t enc = get_encode_fn();
     DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && C % 8 == 0, DVC_ERR_ARG, "fused conv: output alignment");
-    const cuuint64_t Ho = (cuuint64_t)H * up, Wo = (cuuint64_t)W * up;
+    // up = 2: the real upsampled extent (2H - 1 clips the last phase-1 row)
+    const cuuint64_t Ho = up == 2 && up_ho ? up_ho : (cuuint64_t)H * up, Wo = up == 2 && up_wo ? up_wo : (cuuint64_t)W * up;
     cuuint64_t gdim[4] = {(cuuint64_t)C, Wo, Ho, (cuuint64_t)T};
     cuuint64_t gstride[3] = {(cuuint64_t)C * 2, Wo * C * 2, Ho * Wo * C * 2};
     cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)(FZ_BX * up), (cuuint32_t)(FZ_BY * up), 1};
@@ -945,9 +946,12 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     p.up2 = d.up2;
     DVC_CHECK_ARG(!d.up2 || (p.epi_tma && d.stats_out == nullptr), DVC_ERR_UNSUPPORTED,
                   "fused conv: the 2x-upsampled output needs the staged epilogue and no statistics");
+    DVC_CHECK_ARG(!d.up2 || ((d.up_ho == 0 || d.up_ho == 2 * d.H || d.up_ho == 2 * d.H - 1) &&
+                             (d.up_wo == 0 || d.up_wo == 2 * d.W || d.up_wo == 2 * d.W - 1)),
+                  DVC_ERR_UNSUPPORTED, "fused conv: upsampled output must be 2H (- 1) x 2W (- 1)");
     if (p.epi_tma) {
-        st = make_out_map(&p.omap[0], d.out, d.dt, d.T, d.H, d.W, d.cout, 32, d.up2 ? 2 : 1);
-        if (st == DVC_OK) st = make_out_map(&p.omap[1], d.out, d.dt, d.T, d.H, d.W, d.cout, 16, d.up2 ? 2 : 1);
+        st = make_out_map(&p.omap[0], d.out, d.dt, d.T, d.H, d.W, d.cout, 32, d.up2 ? 2 : 1, d.up_ho, d.up_wo);
+        if (st == DVC_OK) st = make_out_map(&p.omap[1], d.out, d.dt, d.T, d.H, d.W, d.cout, 16, d.up2 ? 2 : 1, d.up_ho, d.up_wo);
         if (st != DVC_OK) return st;
     }
     const size_t fixed = 1024 + (size_t)p.ntf * FZ_SLOT + (size_t)p.nraw * FZ_RAW_SLOT +

@@ -46,6 +46,7 @@ struct WsParams {
     float out_scale;
     int epi_tma;           // staged epilogue (dvc_epilogue.cuh): TMA-stored 32-column chunks
     CUtensorMap omap[2];   // output [T][H][W][cout], box {32 | 16, BX, BY, 1}, SW64 / SW32
+    int up2;               // ConvDesc::up2: omap describes the upsampled output, element stride 2
 };
 
 constexpr int kWsThreads = 256;
@@ -348,7 +349,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                     }
                     epi_stage_chunk<T>(f, m >= 0, two, r, q4, lane, sStage + par * kEpiStage, &p.omap[0], &p.omap[1],
                                        issuer, box < p.nbox, n, bx0, by0, bt,
-                                       want_stats ? stats_box + (size_t)n * 2 : nullptr, red + par * 256);
+                                       want_stats ? stats_box + (size_t)n * 2 : nullptr, red + par * 256, p.up2 != 0);
                 }
                 continue;
             }
@@ -512,15 +513,17 @@ static dvc_status make_bmap8(CUtensorMap *map, const void *ptr, long rows, long 
 
 // output box {c, BX, BY, 1} of a [T][H][W][C] 16-bit tensor for the staged epilogue's TMA store: 32 channels
 // (64-byte rows, SWIZZLE_64B) or 16 (32-byte rows, SWIZZLE_32B), matching dvc_epilogue.cuh's staging
+// up = 2: (H, W) are the upsampled extents and the map walks x and y with element stride 2, so a
+// staged BX x BY box lands on one phase of the 2x grid (the far row / column clipped when H or W is odd)
 dvc_status make_out_map_box(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, int H, int W, int C, int box_c, int BX,
-                            int BY) {
+                            int BY, int up) {
     PFN_encodeTiled_t enc = get_encode_fn();
     DVC_CHECK_ARG(enc != nullptr, DVC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     DVC_CHECK_ARG(((uintptr_t)ptr & 15) == 0 && C % 8 == 0, DVC_ERR_ARG, "conv output alignment");
     cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
     cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)BX, (cuuint32_t)BY, 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)(BX * up), (cuuint32_t)(BY * up), 1};
+    cuuint32_t estr[4] = {1, (cuuint32_t)up, (cuuint32_t)up, 1};
     CUresult r = enc(map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, ptr,
                      gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      box_c == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : box_c == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
@@ -628,9 +631,14 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
         const char *e = dvc_knob("DVC_WS_EPI");
         p.epi_tma = !d.geglu && (e ? atoi(e) != 0 : true);
     }
+    p.up2 = d.up2;
+    DVC_CHECK_ARG(!d.up2 || (p.epi_tma && !d.fp8 && d.stats_out == nullptr && (d.up_ho == 2 * d.ho || d.up_ho == 2 * d.ho - 1) &&
+                             (d.up_wo == 2 * d.wo || d.up_wo == 2 * d.wo - 1)),
+                  DVC_ERR_UNSUPPORTED, "conv: upsampled output needs the staged epilogue, no statistics, 2H(-1) x 2W(-1)");
     if (p.epi_tma) {
-        st = make_out_map_box(&p.omap[0], d.out, d.dt, d.T, d.ho, d.wo, d.cout, 32, p.BX, p.BY);
-        if (st == DVC_OK) st = make_out_map_box(&p.omap[1], d.out, d.dt, d.T, d.ho, d.wo, d.cout, 16, p.BX, p.BY);
+        const int oh = d.up2 ? d.up_ho : d.ho, ow = d.up2 ? d.up_wo : d.wo, up = d.up2 ? 2 : 1;
+        st = make_out_map_box(&p.omap[0], d.out, d.dt, d.T, oh, ow, d.cout, 32, p.BX, p.BY, up);
+        if (st == DVC_OK) st = make_out_map_box(&p.omap[1], d.out, d.dt, d.T, oh, ow, d.cout, 16, p.BX, p.BY, up);
         if (st != DVC_OK) return st;
     }
     if (CG == 2) {

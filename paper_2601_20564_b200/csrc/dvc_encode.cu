@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
 PFN_encodeTiled_t get_encode_fn();
 dvc_status make_bmap_rows(CUtensorMap *map, const void *ptr, dvc_dtype dt, long rows, long cols, int box_rows);
 dvc_status make_out_map_box(CUtensorMap *map, void *ptr, dvc_dtype dt, int T, int H, int W, int C, int box_c, int BX,
-                            int BY);
+                            int BY, int up = 1);
 
 bool encode_tma_applicable(dvc_dtype dt, int H, int W, int s, int c_lat) {
     return (dt == DVC_BF16 || dt == DVC_F16) && s == 8 && H % 8 == 0 && W % 8 == 0 && c_lat >= 16 && c_lat <= 256 &&

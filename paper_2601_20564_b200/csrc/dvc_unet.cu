@@ -458,7 +458,7 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     // up2: y receives the exact 2x nearest upsampling of the block output (no statistics, no
     // Transformer2D after the block)
     auto run_block = [&](const void *xa, const void *xb, void *y, const void *sa, const void *sb, void *sy,
-                         int up2 = 0) -> dvc_status {
+                         int up2 = 0, int up_ho = 0, int up_wo = 0) -> dvc_status {
         const RB &r = n->blk[bi];
         const int l = n->blevel[bi];
         const int H = n->lh[l], Wd = n->lw[l];
@@ -478,7 +478,7 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
             return DVC_ERR_UNSUPPORTED;
         }
         dvc_status e = resblock_launch(r, xa, xb, T, H, Wd, cin_ptr, cout_ptr, y, rbws, s, sa, sb, up2 ? nullptr : sy,
-                                       up2);
+                                       up2, up_ho, up_wo);
         // f1: the Transformer2D block after this ResBlock, in place on y (its statistics refreshed)
         if (e == DVC_OK && n->tf_of[bi] >= 0)
             e = transformer_launch(n->tf[n->tf_of[bi]], y, T, H, Wd, y, rbws, s, sy, sy);
@@ -554,14 +554,19 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
     }
     for (int u = 0; u < 4; ++u) {
         const int l = 3 - u;
-        // an exact 2x upsampler (45x80 -> 90x160 at 720p) with no Transformer2D after the level's last
-        // ResBlock: that block's conv2 epilogue writes the upsampled tensor itself (no nearest kernel, no
-        // low-res copy); the hb buffers are sized for the upsampled tensors
-        const bool fold = u < 3 && g_ws_cg != 0 && c.head_dim == 0 && n->lh[l - 1] == 2 * n->lh[l] &&
-                          n->lw[l - 1] == 2 * n->lw[l];
+        // an upsampler to 2H (- 1) x 2W (- 1) -- every level of the U-Net (R11: nearest_to onto the skip's
+        // size = the 2x phase replication clipped at the far edge; 720p: 12x20 -> 23x40 -> 45x80 -> 90x160)
+        // with no Transformer2D after the level's last ResBlock: that block's conv2 epilogue writes the
+        // upsampled tensor itself (no nearest kernel, no low-res copy); the hb buffers are sized for the
+        // upsampled tensors
+        const bool fold = u < 3 && g_ws_cg != 0 && c.head_dim == 0 &&
+                          (n->lh[l - 1] == 2 * n->lh[l] || n->lh[l - 1] == 2 * n->lh[l] - 1) &&
+                          (n->lw[l - 1] == 2 * n->lw[l] || n->lw[l - 1] == 2 * n->lw[l] - 1);
         for (int r = 0; r < 3; ++r) {
             --k;
-            if ((st = run_block(h, skip[k], hb[pp], hs, skst[k], hbst[pp], fold && r == 2)) != DVC_OK) return st;
+            if ((st = run_block(h, skip[k], hb[pp], hs, skst[k], hbst[pp], fold && r == 2, fold ? n->lh[l - 1] : 0,
+                                fold ? n->lw[l - 1] : 0)) != DVC_OK)
+                return st;
             h = hb[pp];
             hs = hbst[pp];
             pp ^= 1;
