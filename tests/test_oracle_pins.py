@@ -162,6 +162,23 @@ def test_nearest_to_vs_torch(orc, hi, ho):
     assert np.array_equal(u, _nhwc(ref))
 
 
+@pytest.mark.parametrize("h,w", [(12, 20), (23, 40), (68, 120), (2, 3), (9, 14), (1, 1)])
+def test_nearest_to_2h_minus_1_is_clipped_phase_replication(orc, h, w):
+    # the identity the GPU upsampler folds rely on (DESIGN §2 / §10): R11's nearest_to onto
+    # 2H or 2H - 1 rows (2W or 2W - 1 columns) is the exact 2x replication cropped at the far edge
+    v = np.random.default_rng(h * 100 + w).standard_normal((2, h, w, 3))
+    rep = np.repeat(np.repeat(v, 2, axis=1), 2, axis=2)
+    for ho in (2 * h - 1, 2 * h):
+        for wo in (2 * w - 1, 2 * w):
+            if ho < 1 or wo < 1:
+                continue
+            assert np.array_equal(orc.nearest_to(v, ho, wo), rep[:, :ho, :wo])
+    # and only there: one more row or one less breaks it (the fold is gated on these two sizes)
+    if h >= 2:
+        u = orc.nearest_to(v, 2 * h - 2, 2 * w)
+        assert not np.array_equal(u, rep[:, :2 * h - 2, :2 * w])
+
+
 # ---------------------------------------------------------------- rounding (R15)
 def test_round_spec_examples(orc):
     assert orc.rnd1(65520.0, "fp16") == math.inf
