@@ -49,10 +49,15 @@ struct WsParams {
     int up2;               // ConvDesc::up2: omap describes the upsampled output, element stride 2
 };
 
-constexpr int kWsThreads = 256;
+// EG epilogue warpgroups (warps 4-7, and 8-11 when EG = 2): group g drains the 32-column chunks
+// g, g + EG, ... of each accumulator with its own staging tiles, named barrier (1 + g) and store issuer,
+// so convolutions whose K loop is short (the f1 transformer linears, K = 240 .. 960) are not bound by
+// one warpgroup's drain / stage / store round trips per chunk
+template <int EG> constexpr int ws_threads() { return 128 + 128 * EG; }
 
-template <typename T, int CG, int STAGES>
-__global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_constant__ WsParams p) {
+template <typename T, int CG, int STAGES, int EG>
+__global__ void __launch_bounds__(ws_threads<EG>(), 1) conv_ws_kernel(const __grid_constant__ WsParams p) {
+    constexpr int kWsThreads = ws_threads<EG>();
     extern __shared__ uint8_t smem_raw[];
     // 1024-aligned, derived from smem_raw by pointer arithmetic so the compiler keeps the
     // shared address space (an integer round trip would turn every access generic)
@@ -62,14 +67,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
     const int B_STAGE = BNH * 128;
     uint8_t *sA = smem;
     uint8_t *sB = sA + STAGES * A_STAGE;
-    uint8_t *sStage = sB + STAGES * B_STAGE;   // [2] epilogue staging (epi_tma)
-    uint64_t *full = reinterpret_cast<uint64_t *>(sStage + (p.epi_tma ? 2 * kEpiStage : 0));
+    uint8_t *sStage = sB + STAGES * B_STAGE;   // [EG][2] epilogue staging (epi_tma)
+    uint64_t *full = reinterpret_cast<uint64_t *>(sStage + (p.epi_tma ? 2 * EG * kEpiStage : 0));
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [2][2][4][32] box-statistics staging
-    float *sbias = red + 512;   // [1 or 2][cout] bias0 (, bias1) in fp32 (16-byte aligned: even barrier count)
+    float *red = reinterpret_cast<float *>(tmem_slot + 4);   // [EG][2][2][4][32] box-statistics staging
+    float *sbias = red + 512 * EG;   // [1 or 2][cout] bias0 (, bias1) in fp32 (16-byte aligned: even barrier count)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], CG * 4);
+            mbar_init(&tempty[b], CG * 4 * EG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
@@ -202,6 +207,9 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
     } else if (warp >= 4) {
         // ===================== epilogue (both CTAs) =====================
         const int q4 = warp & 3;                 // TMEM lane quadrant of this warp
+        const int g = (warp - 4) >> 2;           // epilogue warpgroup: chunks g, g + EG, ...
+        const uint32_t gbar = 1u + (uint32_t)g;  // its named barrier
+        float *const gred = red + 512 * g;
         const int r = q4 * 32 + lane;            // accumulator row = pixel of this CTA's box
         const int by = r / p.BX, bx = r - by * p.BX;
         const float *sb0 = p.bias0 ? sbias : nullptr;
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
             if (p.geglu) {   // f1 GEGLU epilogue: out[m][n/2 + i] = (v_i + b) * gelu(g_i + b')
                 const int half = p.cout / 2;
 #pragma unroll 1
-                for (int cc = 0; cc < BN; cc += 32) {
+                for (int cc = 32 * g; cc < BN; cc += 32 * EG) {
                     uint32_t va[16], vb[16];
                     tmem_ld16_nowait(taddr + (uint32_t)cc, va);
                     tmem_ld16_nowait(taddr + (uint32_t)(cc + 16), vb);
@@ -302,7 +310,14 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                 continue;
             }
             if (p.epi_tma) {   // staged epilogue (dvc_epilogue.cuh)
-                const bool issuer = warp == 4 && lane == 0;
+                const bool issuer = warp == 4 + 4 * g && lane == 0;
+                if (32 * g >= BN) {   // no chunk for this group: the accumulator is drained as far as it goes
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0)
+                        tmem_drained_arrive(CG == 2 ? tempty_leader + (uint32_t)(buf * 8) : smem_u32(&tempty[buf]), CG == 2);
+                    continue;
+                }
                 int bt = p.T, bx0 = 0, by0 = 0;
                 if (box < p.nbox) {
                     bt = box / per;
@@ -311,7 +326,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                     bx0 = (rem % p.tiles_x) * p.BX;
                 }
 #pragma unroll 1
-                for (int cc = 0; cc < BN; cc += 32, par ^= 1) {
+                for (int cc = 32 * g; cc < BN; cc += 32 * EG, par ^= 1) {
                     const bool two = cc + 16 < BN;   // warp-uniform: 32 or 16 columns
                     const int n = nt * BN + cc;
                     uint32_t va[16], vb[16];
@@ -328,7 +343,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
                     }
                     tmem_wait16(va);
                     if (two) tmem_wait16(vb);
-                    if (cc + 32 >= BN) {   // the accumulator is drained: the MMA may reuse it
+                    if (cc + 32 * EG >= BN) {   // this group's last chunk: its part of the accumulator is drained
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) {
@@ -347,9 +362,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
 #pragma unroll
                         for (int i = 0; i < 32; ++i) f[i] += rv[i];
                     }
-                    epi_stage_chunk<T>(f, m >= 0, two, r, q4, lane, sStage + par * kEpiStage, &p.omap[0], &p.omap[1],
-                                       issuer, box < p.nbox, n, bx0, by0, bt,
-                                       want_stats ? stats_box + (size_t)n * 2 : nullptr, red + par * 256, p.up2 != 0);
+                    epi_stage_chunk<T>(f, m >= 0, two, r, q4, lane, sStage + (2 * g + par) * kEpiStage, &p.omap[0],
+                                       &p.omap[1], issuer, box < p.nbox, n, bx0, by0, bt,
+                                       want_stats ? stats_box + (size_t)n * 2 : nullptr, gred + par * 256, p.up2 != 0,
+                                       gbar);
                 }
                 continue;
             }
@@ -384,7 +400,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) conv_ws_kernel(const __grid_con
             }
         }
     }
-    if (p.epi_tma && warp == 4 && lane == 0) bulk_wait_group<0>();   // every staged store has landed
+    if (p.epi_tma && (warp == 4 || warp == 8) && lane == 0) bulk_wait_group<0>();   // every staged store has landed
     tc_fence_before();
     __syncthreads();
     if constexpr (CG == 2) cluster_sync_all();
@@ -458,12 +474,16 @@ void choose_box(int H, int W, int *BX, int *BY) {
 
 static int g_num_sms = 0;
 
-template <typename T, int CG, int STAGES>
+template <int CG, int STAGES, int EG>
+static size_t ws_smem_bytes(const WsParams &p) {
+    return 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + (p.epi_tma ? 2 * EG * kEpiStage : 0) +
+           8 * (2 * STAGES + 4) + 16 + 2048 * EG + (size_t)(p.bias1 ? 2 : 1) * p.cout * 4;   // bias1 staged only when present
+}
+
+template <typename T, int CG, int STAGES, int EG>
 static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
-    const size_t smem = 1024 + (size_t)STAGES * (128 * 128 + (p.bn / CG) * 128) + (p.epi_tma ? 2 * kEpiStage : 0) +
-                        8 * (2 * STAGES + 4) + 16 + 2048 +
-                        (size_t)(p.bias1 ? 2 : 1) * p.cout * 4;   // bias1 staged only when present
-    auto kern = conv_ws_kernel<T, CG, STAGES>;
+    const size_t smem = ws_smem_bytes<CG, STAGES, EG>(p);
+    auto kern = conv_ws_kernel<T, CG, STAGES, EG>;
     {   // host cost: the attribute is set once per kernel / size
         dvc_status ss_ = ensure_smem((const void *)kern, (int)smem);
         if (ss_ != DVC_OK) return ss_;
@@ -475,7 +495,7 @@ static dvc_status launch_ws(const WsParams &p, cudaStream_t stream) {
     }
     int clusters = g_num_sms / CG;
     if (clusters > p.nwork) clusters = p.nwork;
-    DVC_CUDA(launch_pdl(kern, dim3(clusters * CG), dim3(kWsThreads), smem, stream, CG, p));
+    DVC_CUDA(launch_pdl(kern, dim3(clusters * CG), dim3(ws_threads<EG>()), smem, stream, CG, p));
     ++g_launches;
     return check_launch("conv_ws_kernel");
 }
@@ -642,11 +662,30 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
         if (st != DVC_OK) return st;
     }
     if (CG == 2) {
-        if (bf) return launch_ws<__nv_bfloat16, 2, 6>(p, stream);
-        return launch_ws<__half, 2, 6>(p, stream);
+        // two epilogue warpgroups for 1x1 convolutions with a short K loop (<= 16 stages of 64 channels:
+        // the f1 transformer linears), where one warpgroup's per-chunk drain / stage / store round trips
+        // outlast the MMAs (same box, 720p T = 32: 240 -> 720 423 -> 301 us, 240 -> 240 152 -> 113 us,
+        // full U-Net 270 -> 275 frames/s; 3x3 convolutions measured neutral to slightly slower and keep
+        // one); 5 operand stages when the second group's staging does not fit beside 6 (DVC_WS_EG in
+        // experiment builds forces 1 or 2)
+        int kst = 0;
+        bool pointwise = true;
+        for (int s = 0; s < d.nseg; ++s) {
+            kst += p.seg_taps[s] * p.seg_nch[s];
+            pointwise = pointwise && p.seg_taps[s] == 1;
+        }
+        const char *e = dvc_knob("DVC_WS_EG");
+        const int eg = (p.epi_tma || p.geglu) && (e ? atoi(e) == 2 : pointwise && kst <= 16) ? 2 : 1;
+        if (eg == 2) {
+            const bool six = ws_smem_bytes<2, 6, 2>(p) <= 227 * 1024;
+            if (bf) return six ? launch_ws<__nv_bfloat16, 2, 6, 2>(p, stream) : launch_ws<__nv_bfloat16, 2, 5, 2>(p, stream);
+            return six ? launch_ws<__half, 2, 6, 2>(p, stream) : launch_ws<__half, 2, 5, 2>(p, stream);
+        }
+        if (bf) return launch_ws<__nv_bfloat16, 2, 6, 1>(p, stream);
+        return launch_ws<__half, 2, 6, 1>(p, stream);
     }
-    if (bf) return launch_ws<__nv_bfloat16, 1, 4>(p, stream);
-    return launch_ws<__half, 1, 4>(p, stream);
+    if (bf) return launch_ws<__nv_bfloat16, 1, 4, 1>(p, stream);
+    return launch_ws<__half, 1, 4, 1>(p, stream);
 }
 
 }  // namespace dvc

@@ -69,7 +69,7 @@ template <typename T>
 __device__ __forceinline__ void epi_stage_chunk(const float (&f)[32], bool live, bool two, int r, int q4, int lane,
                                                 uint8_t *st, const CUtensorMap *omap32, const CUtensorMap *omap16,
                                                 bool issuer, bool store, int c0, int x0, int y0, int t,
-                                                float *stats_col, float *red, bool up2 = false) {
+                                                float *stats_col, float *red, bool up2 = false, uint32_t bar = 1) {
     const int ncol = two ? 32 : 16;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -82,7 +82,7 @@ __device__ __forceinline__ void epi_stage_chunk(const float (&f)[32], bool live,
         *reinterpret_cast<uint4 *>(st + epi_off(two, r, j)) = u;
     }
     fence_proxy_async_smem();
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");   // this epilogue warpgroup's named barrier
     if (issuer) {
         if (store) {
             if (up2) {   // exact 2x nearest upsampling: maps with element stride 2 in x and y, four phases
@@ -134,14 +134,14 @@ __device__ __forceinline__ void epi_stage_chunk(const float (&f)[32], bool live,
             red[128 + q4 * 32 + c] = sq.x;
             red[128 + q4 * 32 + c + 1] = sq.y;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
         if (q4 < 2 && lane < ncol) {   // warp 0: sums, warp 1: sums of squares
             const float *src = red + q4 * 128;
             stats_col[lane * 2 + q4] =
                 __fadd_rn(__fadd_rn(__fadd_rn(src[lane], src[32 + lane]), src[64 + lane]), src[96 + lane]);
         }
     } else {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
     }
 }
 

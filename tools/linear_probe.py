@@ -1,6 +1,6 @@
 """Device time of single 1x1 / 3x3 convolutions on the TMA engine (the f1 transformer linears' shapes at
 720p, T = 32, bf16): algorithmic TFLOP/s and HBM GB/s (read x + w, write y) per shape, for same-box A/Bs.
-    python tools/linear_probe.py"""
+    python tools/linear_probe.py [cin cout k]"""
 import os
 import sys
 
@@ -12,6 +12,8 @@ import paper_2601_20564_b200 as dvc  # noqa: E402
 
 T, H, W, dt = 32, 90, 160, torch.bfloat16
 shapes = [(240, 240, 1), (240, 720, 1), (240, 1920, 1), (960, 240, 1), (480, 480, 1), (240, 240, 3)]
+if len(sys.argv) > 1:   # one shape: cin cout k (e.g. as an ncu target)
+    shapes = [tuple(int(v) for v in sys.argv[1:4])]
 for cin, cout, k in shapes:
     g = torch.Generator(device="cuda").manual_seed(1)
     x = torch.randn((T, H, W, cin), device="cuda", generator=g).to(dt)
