@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
         const int r = q4 * 32 + lane;   // accumulator row = latent pixel (r / 8, r % 8) of the box
         T *out = reinterpret_cast<T *>(p.out);
         int it = 0;
+        int wpar = 0;   // wide staging tile, cycled across tiles (a tile may have fewer chunks than tiles)
         for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1;
@@ -299,9 +300,10 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
                     // 64 columns per chunk: one SWIZZLE_128B [128 rows][128 B] staging tile (16-byte unit j of
                     // row r at j ^ (r & 7)) and one TMA store of the {64, 8, 16, 1} box -- whole 128-byte
                     // output rows (full L2 lines) and half the barrier round trips of the 32-column form
-#pragma unroll 1
                     const bool four = p.nplane == 4;   // four staging tiles: two in the A region
-                    for (int cc = 0; cc < N; cc += 64, par = (par + 1) & (four ? 3 : 1)) {
+#pragma unroll 1
+                    for (int cc = 0; cc < N; cc += 64, wpar = (wpar + 1) & (four ? 3 : 1)) {
+                        const int par = wpar;
                         uint32_t v[4][16];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16 * k), v[k]);

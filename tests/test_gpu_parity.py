@@ -108,6 +108,21 @@ def test_expansion(dvc, orc, dtype, T, H, W):
     assert err <= TOL[dtype], err
 
 
+@pytest.mark.parametrize("c_lat", [64, 128, 192, 240, 256])
+def test_expansion_latent_widths(dvc, orc, c_lat):
+    # the encoder's staged epilogue: 64-column chunks (1..4 per tile, staging tiles cycled across tiles) when
+    # c_lat % 64 == 0, 32/16-column chunks otherwise (240); 320 tiles on 148 CTAs: 2-3 tiles per CTA
+    T = 16
+    f, f64 = dev(synthgen.frames(T, 128, 1280), torch.bfloat16)
+    w, b = synthgen.expansion_weights(c_lat=c_lat)
+    wd, w64 = dev(w, torch.bfloat16)
+    bd, b64 = dev(b, torch.bfloat16)
+    out = host64(dvc.dvc_encode_pixelunshuffle(f, wd, bd))
+    ref = orc.encode(f64, w64, b64, 8, "bf16")
+    for t in range(T):   # per frame: a misplaced staging tile shows up as a frame-local error
+        assert rel_l2(out[t], ref[t]) <= 1e-2
+
+
 def test_expansion_identity_weights_exact(dvc, orc):   # P3 on the GPU: first 192 channels = unshuffle
     f, f64 = dev(synthgen.frames(2, 16, 24), torch.bfloat16)
     w = np.concatenate([np.eye(192), np.zeros((64, 192))]).astype(np.float32)
