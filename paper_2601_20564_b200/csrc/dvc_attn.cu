@@ -265,9 +265,13 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const float *__restrict_
 //   Q/K [rows][D]:  core (r8, kc) at kc*2048 + r8*128   (LBO 2048, SBO 128)
 //   V^T [D][keys]:  core (d8, kc) at kc*D*16 + d8*128   (LBO D*16, SBO 128)
 
-// head_dim <= 64: two query tiles per CTA (TMEM S0 S1 | O0 O1 | P0 P1), 4-stage K/V ring;
-// head_dim 256 (the VAE decoder's single-head mid attention, f2): one tile (S | P | O = 256
-// columns), K/V single-buffered (192 KB of operand tiles).
+// head_dim <= 64: two query tiles per CTA (TMEM S0 S1 | O0 O1 | P0 P1), 4-stage K/V ring, Q double-
+// buffered; head_dim 256 (the VAE decoder's single-head mid attention, f2): one tile (S | P | O = 256
+// columns), K/V and Q single-buffered (256 KB would not fit twice).
+// The kernel is persistent: one CTA per SM walks work items (query-tile group, head, frame) with a
+// static stride, keeping its TMEM allocation, barriers and pipelines; the next item's Q load and first
+// S MMAs overlap the current item's last PV and output normalisation (a fixed cost that was a third of
+// every CTA's time at the 720p level-2 shape, N = 920).
 template <int D, int KT = 128>
 struct AttnSmem {
     // KT = keys per S tile: 128 (two query tiles per CTA); 64 gives three query tiles per CTA (six
@@ -275,18 +279,21 @@ struct AttnSmem {
     // the per-iteration handshakes double), so only KT = 128 is instantiated
     static constexpr int NT = D <= 64 ? (KT == 64 ? 3 : 2) : 1;   // query tiles per CTA
     static constexpr int STAGES = D <= 64 ? (KT == 64 ? 6 : 4) : 1;
+    static constexpr int QB = D <= 64 ? 2 : 1;                     // Q buffers (items in flight)
     static constexpr int THREADS = (8 * NT + 2) * 32;     // 8 softmax warps per tile + MMA + TMA
     static constexpr int Q = 128 * D * 2;        // one query tile
     static constexpr int K = KT * D * 2;         // one key tile
     static constexpr int V = D * KT * 2;         // one transposed value tile
-    static constexpr int off_q = 0, off_k = NT * Q, off_v = off_k + STAGES * K;
+    static constexpr int off_q = 0, off_k = QB * NT * Q, off_v = off_k + STAGES * K;
     static constexpr int off_bar = off_v + STAGES * V;
-    // barriers: q_full, kv_full[S], kv_empty[S], s_full[2], p_full[2], o_full[2], 6 spare
-    static constexpr int nbar = 1 + 2 * STAGES + 3 * 4;   // + s_full[4], p_full[4], o_full[4] (NT <= 3)
-    // [NT tiles][2 key-tile parities][2 halves][128 rows] float exchange (parity double buffer: a thread's
-    // write for key tile j+1 never lands in the slot its partner may still be reading for tile j)
+    // barriers: q_full[2], q_empty[2], kv_full[S], kv_empty[S], then s_full[4], p_full[4], o_full[4],
+    // o_free[4] (NT <= 3; one slot of four per query tile)
+    static constexpr int nbar = 4 + 2 * STAGES + 4 * 4;
+    // [NT tiles][2 key-tile parities][2 halves][128 rows] float exchange of the row maxima (parity double
+    // buffer: a thread's write for key tile j+1 never lands in the slot its partner may still be reading
+    // for tile j), then [NT][2 halves][128] for the row sums at the end of an item
     static constexpr int off_red = off_bar + nbar * 8 + 16;
-    static constexpr int bytes = off_red + NT * 4 * 128 * 4 + 1024;   // + alignment slack
+    static constexpr int bytes = off_red + NT * 6 * 128 * 4 + 1024;   // + alignment slack
     // TMEM columns (512 allocated)
     // S_t at t*KT, P_t (KT/2 packed columns) at tm_p + t*KT/2, O_t at tm_o + t*64
     static constexpr int tm_o = NT == 3 ? 320 : 256, tm_o_step = NT == 1 ? 0 : 64;
@@ -336,33 +343,42 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 template <typename T, int D, int NPOLY, int KT>
 __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
     attn_tc_kernel(const T *__restrict__ qp, const T *__restrict__ kp, const T *__restrict__ vp, T *__restrict__ out,
-                   int N, int C, float scale_log2, uint32_t idesc_s, uint32_t idesc_o, int dbg) {
+                   int N, int C, int T_, float scale_log2, uint32_t idesc_s, uint32_t idesc_o, int dbg) {
     using L = AttnSmem<D, KT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sb = smem_u32(smem);
     const uint32_t bar0 = sb + L::off_bar;
-    constexpr int kAttnStages = L::STAGES, NT = L::NT;
-    const uint32_t q_full = bar0, kv_full = bar0 + 8, kv_empty = kv_full + 8 * kAttnStages;
+    constexpr int kAttnStages = L::STAGES, NT = L::NT, QB = L::QB;
+    const uint32_t q_full = bar0, q_empty = bar0 + 16;   // [QB]
+    const uint32_t kv_full = bar0 + 32, kv_empty = kv_full + 8 * kAttnStages;
     const uint32_t s_full = kv_empty + 8 * kAttnStages, p_full = s_full + 32;   // p_full also releases S
     const uint32_t o_full = p_full + 32;   // [t] at o_full + 8 t: O_t final
+    const uint32_t o_free = o_full + 32;   // [t]: group t has read O_t (the next item's PV may overwrite it)
     uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + L::off_bar + L::nbar * 8);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int t = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * 128 * NT;
+    const int heads = C / D;
+    const int ntiles = (N + 127) / 128;                       // 128-token tiles of the packed operands
+    const int nqg = (N + 128 * NT - 1) / (128 * NT);           // query-tile groups (one per item)
+    const int nitems = nqg * heads * T_;
     const int w_mma = 8 * NT, w_tma = 8 * NT + 1;
     const int nkt = (N + KT - 1) / KT;
     if (tid == 0) {
         uint64_t *b = reinterpret_cast<uint64_t *>(smem + L::off_bar);
-        mbar_init(&b[0], 1);
-        for (int i = 0; i < kAttnStages; ++i) {
-            mbar_init(&b[1 + i], 1);
-            mbar_init(&b[1 + kAttnStages + i], 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&b[i], 1);       // q_full[qb] (expect-tx)
+            mbar_init(&b[2 + i], 1);   // q_empty[qb] (tcgen05.commit)
         }
-        const int sf = 1 + 2 * kAttnStages;
+        for (int i = 0; i < kAttnStages; ++i) {
+            mbar_init(&b[4 + i], 1);
+            mbar_init(&b[4 + kAttnStages + i], 1);
+        }
+        const int sf = 4 + 2 * kAttnStages;
         for (int i = 0; i < NT; ++i) {
-            mbar_init(&b[sf + i], 1);       // s_full[t] (tcgen05.commit)
-            mbar_init(&b[sf + 4 + i], 8);   // p_full[t] (8 softmax warps per tile)
-            mbar_init(&b[sf + 8 + i], 1);   // o_full[t]
+            mbar_init(&b[sf + i], 1);        // s_full[t] (tcgen05.commit)
+            mbar_init(&b[sf + 4 + i], 8);    // p_full[t] (8 softmax warps per tile)
+            mbar_init(&b[sf + 8 + i], 1);    // o_full[t]
+            mbar_init(&b[sf + 12 + i], 8);   // o_free[t] (8 softmax warps per tile)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -376,84 +392,103 @@ __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
     // The MMA warp and the softmax groups are one latency chain (S -> softmax -> P -> PV, S):
     // they poll without a suspend hint (a suspended try_wait wakes late, measured ~1.6 us per
     // iteration of pure barrier round trips); the TMA producer runs ahead and may sleep.
+    // Ring and barrier phases run on per-CTA counters across the work items.
     if (warp == w_tma) {
         // ===================== TMA producer =====================
         if (elect_one()) {
-            const int ntiles = (N + 127) / 128, heads = gridDim.y;
-            const size_t base = ((size_t)t * heads + h) * ntiles * (128 * D);   // this (frame, head)
-            const int qt = blockIdx.x * NT;
-            const uint32_t nq = (uint32_t)min(NT, ntiles - qt);
-            mbar_arrive_expect_tx_addr(q_full, nq * L::Q);
-            for (uint32_t i = 0; i < nq; ++i)
-                bulk_load(sb + L::off_q + i * L::Q, qp + base + (size_t)(qt + i) * 128 * D, L::Q, q_full);
-            for (int j = 0; j < nkt; ++j) {
-                const int st = j % kAttnStages;
-                if (j >= kAttnStages) mbar_wait_addr(kv_empty + 8 * st, ((j / kAttnStages) - 1) & 1);
-                mbar_arrive_expect_tx_addr(kv_full + 8 * st, L::K + L::V);
-                bulk_load(sb + L::off_k + st * L::K, kp + base + (size_t)j * KT * D, L::K, kv_full + 8 * st);
-                bulk_load(sb + L::off_v + st * L::V, vp + base + (size_t)j * KT * D, L::V, kv_full + 8 * st);
+            int jg = 0;
+            for (int item = blockIdx.x, it = 0; item < nitems; item += gridDim.x, ++it) {
+                const int qg = item % nqg, h = (item / nqg) % heads, t = item / (nqg * heads);
+                const size_t base = ((size_t)t * heads + h) * ntiles * (128 * D);   // this (frame, head)
+                const int qt = qg * NT, qb = it % QB, use = it / QB;
+                const uint32_t nq = (uint32_t)min(NT, ntiles - qt);
+                if (use > 0) mbar_wait_addr(q_empty + 8 * qb, (use - 1) & 1);   // the previous user's S MMAs retired
+                mbar_arrive_expect_tx_addr(q_full + 8 * qb, nq * L::Q);
+                for (uint32_t i = 0; i < nq; ++i)
+                    bulk_load(sb + L::off_q + (qb * NT + i) * L::Q, qp + base + (size_t)(qt + i) * 128 * D, L::Q,
+                              q_full + 8 * qb);
+                for (int j = 0; j < nkt; ++j, ++jg) {
+                    const int st = jg % kAttnStages;
+                    if (jg >= kAttnStages) mbar_wait_addr(kv_empty + 8 * st, ((jg / kAttnStages) - 1) & 1);
+                    mbar_arrive_expect_tx_addr(kv_full + 8 * st, L::K + L::V);
+                    bulk_load(sb + L::off_k + st * L::K, kp + base + (size_t)j * KT * D, L::K, kv_full + 8 * st);
+                    bulk_load(sb + L::off_v + st * L::V, vp + base + (size_t)j * KT * D, L::V, kv_full + 8 * st);
+                }
             }
         }
     } else if (warp == w_mma) {
         // ===================== MMA issuer =====================
         if (elect_one()) {
-            mbar_wait_spin_addr(q_full, 0);
-            tc_fence_after();
-            auto issue_s = [&](int tt, int j) {
-                const int st = j % kAttnStages;
-                const uint32_t qa = sb + L::off_q + tt * L::Q, ka = sb + L::off_k + st * L::K;
+            int jg = 0, cp = 0;   // K/V ring position; P_t(j) handshakes so far
+            for (int item = blockIdx.x, it = 0; item < nitems; item += gridDim.x, ++it) {
+                const int qb = it % QB;
+                mbar_wait_spin_addr(q_full + 8 * qb, (it / QB) & 1);
+                tc_fence_after();
+                auto issue_s = [&](int tt, int jj) {   // jj: ring position of the key tile
+                    const int st = jj % kAttnStages;
+                    const uint32_t qa = sb + L::off_q + (qb * NT + tt) * L::Q, ka = sb + L::off_k + st * L::K;
 #pragma unroll
-                for (int ks = 0; ks < D / 16; ++ks) {
-                    if (dbg & 2) break;   // DVC_ATTN_DEBUG bit 1: no MMAs (pipeline-only timing)
-                    const uint64_t ad = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(qa + ks * 4096, 2048);
-                    const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(ka + ks * 2 * KT * 16, KT * 16);
-                    tc_mma(tmem + tt * KT, ad, bd, idesc_s, ks > 0);
-                }
-                tc_commit_addr(s_full + 8 * tt);
-            };
-            auto issue_pv = [&](int tt, int j) {   // A = P_t from TMEM (8 columns per K step)
-                const int st = j % kAttnStages;
-                const uint32_t va = sb + L::off_v + st * L::V;
+                    for (int ks = 0; ks < D / 16; ++ks) {
+                        if (dbg & 2) break;   // DVC_ATTN_DEBUG bit 1: no MMAs (pipeline-only timing)
+                        const uint64_t ad = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(qa + ks * 4096, 2048);
+                        const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(ka + ks * 2 * KT * 16, KT * 16);
+                        tc_mma(tmem + tt * KT, ad, bd, idesc_s, ks > 0);
+                    }
+                    tc_commit_addr(s_full + 8 * tt);
+                };
+                auto issue_pv = [&](int tt, int jj, bool first) {   // A = P_t from TMEM (8 columns per K step)
+                    const int st = jj % kAttnStages;
+                    const uint32_t va = sb + L::off_v + st * L::V;
 #pragma unroll
-                for (int ks = 0; ks < KT / 16; ++ks) {
-                    if (dbg & 2) break;
-                    const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(va + ks * 2 * D * 16, D * 16);
-                    tc_mma_ts(tmem + L::tm_o + tt * L::tm_o_step, tmem + L::tm_p + tt * L::tm_p_step + ks * 8, bd, idesc_o,
-                              (j > 0 || ks > 0) ? 1u : 0u);
+                    for (int ks = 0; ks < KT / 16; ++ks) {
+                        if (dbg & 2) break;
+                        const uint64_t bd = ((uint64_t)desc_hi_noswz(128) << 32) | desc_lo(va + ks * 2 * D * 16, D * 16);
+                        tc_mma_ts(tmem + L::tm_o + tt * L::tm_o_step, tmem + L::tm_p + tt * L::tm_p_step + ks * 8, bd,
+                                  idesc_o, (!first || ks > 0) ? 1u : 0u);
+                    }
+                };
+                // the first S tiles: S_t columns are free (the previous item's last p_full was awaited)
+                mbar_wait_spin_addr(kv_full + 8 * (jg % kAttnStages), (jg / kAttnStages) & 1);
+                tc_fence_after();
+                for (int tt = 0; tt < NT; ++tt) issue_s(tt, jg);
+                for (int j = 0; j < nkt; ++j, ++jg, ++cp) {
+                    const bool more = j + 1 < nkt;
+                    if constexpr (kAttnStages == 1) {
+                        // single K/V buffer: PV(j) must retire before K/V(j+1) can land
+                        mbar_wait_spin_addr(p_full, cp & 1);
+                        tc_fence_after();
+                        if (j == 0 && it > 0) {   // O is overwritten by this item's first PV
+                            mbar_wait_spin_addr(o_free, (it - 1) & 1);
+                            tc_fence_after();
+                        }
+                        issue_pv(0, jg, j == 0);
+                        tc_commit_addr(kv_empty);
+                        if (more) {
+                            mbar_wait_spin_addr(kv_full, (jg + 1) & 1);
+                            tc_fence_after();
+                            issue_s(0, jg + 1);
+                        }
+                    } else {
+                        if (more) {
+                            mbar_wait_spin_addr(kv_full + 8 * ((jg + 1) % kAttnStages), ((jg + 1) / kAttnStages) & 1);
+                            tc_fence_after();
+                        }
+                        for (int tt = 0; tt < NT; ++tt) {
+                            mbar_wait_spin_addr(p_full + 8 * tt, cp & 1);   // P_t(j) written, S_t(j) released
+                            tc_fence_after();
+                            if (j == 0 && it > 0) {   // O_t is overwritten by this item's first PV
+                                mbar_wait_spin_addr(o_free + 8 * tt, (it - 1) & 1);
+                                tc_fence_after();
+                            }
+                            issue_pv(tt, jg, j == 0);
+                            if (more) issue_s(tt, jg + 1);
+                        }
+                        tc_commit_addr(kv_empty + 8 * (jg % kAttnStages));
+                    }
                 }
-            };
-            mbar_wait_spin_addr(kv_full, 0);
-            tc_fence_after();
-            for (int tt = 0; tt < NT; ++tt) issue_s(tt, 0);
-            for (int j = 0; j < nkt; ++j) {
-                const int stn = (j + 1) % kAttnStages;
-                const bool more = j + 1 < nkt;
-                if constexpr (kAttnStages == 1) {
-                    // single K/V buffer: PV(j) must retire before K/V(j+1) can land
-                    mbar_wait_spin_addr(p_full, j & 1);
-                    tc_fence_after();
-                    issue_pv(0, j);
-                    tc_commit_addr(kv_empty);
-                    if (more) {
-                        mbar_wait_spin_addr(kv_full, (j + 1) & 1);
-                        tc_fence_after();
-                        issue_s(0, j + 1);
-                    }
-                } else {
-                    if (more) {
-                        mbar_wait_spin_addr(kv_full + 8 * stn, ((j + 1) / kAttnStages) & 1);
-                        tc_fence_after();
-                    }
-                    for (int tt = 0; tt < NT; ++tt) {
-                        mbar_wait_spin_addr(p_full + 8 * tt, j & 1);   // P_t(j) written, S_t(j) released
-                        tc_fence_after();
-                        issue_pv(tt, j);
-                        if (more) issue_s(tt, j + 1);
-                    }
-                    tc_commit_addr(kv_empty + 8 * (j % kAttnStages));
-                }
+                for (int tt = 0; tt < NT; ++tt) tc_commit_addr(o_full + 8 * tt);   // O_t final
+                tc_commit_addr(q_empty + 8 * qb);   // this item's S MMAs (Q readers) have all retired
             }
-            for (int tt = 0; tt < NT; ++tt) tc_commit_addr(o_full + 8 * tt);   // O_t final
         }
     } else {
         // ===================== softmax groups =====================
@@ -464,119 +499,127 @@ __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
         const int tt = (warp >> 2) % NT, q4 = warp & 3, half = warp / (4 * NT);
         const int row = q4 * 32 + lane;
         const uint32_t bar_id = 1 + tt * 4 + q4;
-        float *red = reinterpret_cast<float *>(smem + L::off_red) + tt * 512;
+        float *red = reinterpret_cast<float *>(smem + L::off_red) + tt * 768;   // [2 parities][2][128] + [2][128]
         const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
         const uint32_t tS = tmem + lane_off + tt * KT + half * (KT / 2);
         const uint32_t tO = tmem + lane_off + L::tm_o + tt * L::tm_o_step;
         const uint32_t tP = tmem + lane_off + L::tm_p + tt * L::tm_p_step + half * (KT / 4);
         auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
-        float m = -INFINITY, l = 0.f;
-        for (int j = 0; j < nkt; ++j) {
-            mbar_wait_spin_addr(s_full + 8 * tt, j & 1);
-            tc_fence_after();
-            if (dbg & 1) {   // DVC_ATTN_DEBUG bit 0: no softmax (MMA/TMA pipeline timing)
+        int cs = 0;   // S_t handshakes so far (ring parity of s_full and of the max exchange)
+        for (int item = blockIdx.x, it = 0; item < nitems; item += gridDim.x, ++it) {
+            float m = -INFINITY, l = 0.f;
+            for (int j = 0; j < nkt; ++j, ++cs) {
+                mbar_wait_spin_addr(s_full + 8 * tt, cs & 1);
+                tc_fence_after();
+                if (dbg & 1) {   // DVC_ATTN_DEBUG bit 0: no softmax (MMA/TMA pipeline timing)
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(p_full + 8 * tt);
+                    continue;
+                }
+                constexpr int HK = KT / 2;   // keys of this thread's half row
+                const int kvalid = N - j * KT - half * HK;   // keys >= kvalid of this half are padding
+                uint32_t sr[HK];
+#pragma unroll
+                for (int c = 0; c < HK / 32; ++c)
+                    tmem_ld32_nowait(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+#pragma unroll
+                for (int c = 0; c < HK / 32; ++c) tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+                if (kvalid < HK) {
+#pragma unroll
+                    for (int i = 0; i < HK; ++i)
+                        if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
+                }
+                float mxp[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mxp[i] = fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[8 + i]));
+#pragma unroll
+                for (int i = 16; i < HK; i += 16)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        mxp[k] = fmaxf(mxp[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
+                float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                                 fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+                float *rj = red + (cs & 1) * 256;
+                rj[half * 128 + row] = mx;
+                pair_sync();
+                mx = fmaxf(mx, rj[(half ^ 1) * 128 + row]);
+                const float mt = mx * scale_log2;
+                if (j == 0) {
+                    m = mt;
+                } else {
+                    const bool move = mt > m + 8.f;   // lazy maximum: P stays <= 2^8 (same decision in both halves)
+                    if (__any_sync(0xffffffffu, move)) {
+                        const float alpha = move ? ex2f(m - mt) : 1.f;
+#pragma unroll
+                        for (int c = 0; c < D / 16; ++c) {
+                            if ((c & 1) != half) continue;   // O column chunks split between the halves
+                            uint32_t r[16];
+                            tmem_ld16(tO + c * 16, r);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+                            tmem_st16(tO + c * 16, r);
+                        }
+                        tmem_wait_st();
+                        l *= alpha;
+                        if (move) m = mt;
+                    }
+                }
+                // packed fp32x2 arithmetic (FFMA2 / FADD2): two scores per instruction
+                float2 rsp[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+                const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
+#pragma unroll
+                for (int c = 0; c < HK / 32; ++c) {   // 32 keys -> 16 packed columns of P_t in TMEM
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int e = c * 32 + q * 8 + 2 * i;
+                            const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])),
+                                                        sc2, nm2);
+                            const float2 p = 2 * i < NPOLY ? ex2_poly2(x) : make_float2(ex2f(x.x), ex2f(x.y));
+                            rsp[i] = __fadd2_rn(rsp[i], p);   // padding: x = -inf -> ~0
+                            pk[q * 4 + i] = pack2<T>(p.x, p.y);
+                        }
+                    }
+                    tmem_st16(tP + c * 16, pk);
+                }
+                tmem_wait_st();
+                l += ((rsp[0].x + rsp[1].x) + (rsp[2].x + rsp[3].x)) + ((rsp[0].y + rsp[1].y) + (rsp[2].y + rsp[3].y));
+                tc_fence_before();     // S reads, P stores, O rescale ordered before the release
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full + 8 * tt);
-                continue;
             }
-            constexpr int HK = KT / 2;   // keys of this thread's half row
-            const int kvalid = N - j * KT - half * HK;   // keys >= kvalid of this half are padding
-            uint32_t sr[HK];
-#pragma unroll
-            for (int c = 0; c < HK / 32; ++c)
-                tmem_ld32_nowait(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-#pragma unroll
-            for (int c = 0; c < HK / 32; ++c) tmem_wait32(*reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
-            if (kvalid < HK) {
-#pragma unroll
-                for (int i = 0; i < HK; ++i)
-                    if (i >= kvalid) sr[i] = __float_as_uint(-INFINITY);
-            }
-            float mxp[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) mxp[i] = fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[8 + i]));
-#pragma unroll
-            for (int i = 16; i < HK; i += 16)
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    mxp[k] = fmaxf(mxp[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
-            float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-            float *rj = red + (j & 1) * 256;
-            rj[half * 128 + row] = mx;
+            // row sum = both halves' partial sums (same reference max m), through the item's own slots
+            float *rl = red + 512;
+            rl[half * 128 + row] = l;
             pair_sync();
-            mx = fmaxf(mx, rj[(half ^ 1) * 128 + row]);
-            const float mt = mx * scale_log2;
-            if (j == 0) {
-                m = mt;
-            } else {
-                const bool move = mt > m + 8.f;   // lazy maximum: P stays <= 2^8 (same decision in both halves)
-                if (__any_sync(0xffffffffu, move)) {
-                    const float alpha = move ? ex2f(m - mt) : 1.f;
+            l += rl[(half ^ 1) * 128 + row];
+            mbar_wait_spin_addr(o_full + 8 * tt, it & 1);
+            tc_fence_after();
+            const int qg = item % nqg, h = (item / nqg) % heads, t = item / (nqg * heads);
+            const int n = qg * 128 * NT + tt * 128 + row;
+            const float inv = 1.f / l;
 #pragma unroll
-                    for (int c = 0; c < D / 16; ++c) {
-                        if ((c & 1) != half) continue;   // O column chunks split between the halves
-                        uint32_t r[16];
-                        tmem_ld16(tO + c * 16, r);
+            for (int c = 0; c < D / 16; ++c) {
+                if ((c & 1) != half) continue;
+                uint32_t r[16];
+                tmem_ld16(tO + c * 16, r);
+                if (n < N) {
+                    T *y = out + ((size_t)t * N + n) * C + h * D + c * 16;
+                    float f[8];
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                        tmem_st16(tO + c * 16, r);
-                    }
-                    tmem_wait_st();
-                    l *= alpha;
-                    if (move) m = mt;
+                    for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]) * inv;
+                    store8(y, f);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[8 + i]) * inv;
+                    store8(y + 8, f);
                 }
             }
-            // packed fp32x2 arithmetic (FFMA2 / FADD2): two scores per instruction
-            float2 rsp[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-            const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m, -m);
-#pragma unroll
-            for (int c = 0; c < HK / 32; ++c) {   // 32 keys -> 16 packed columns of P_t in TMEM
-                uint32_t pk[16];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int e = c * 32 + q * 8 + 2 * i;
-                        const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])),
-                                                    sc2, nm2);
-                        const float2 p = 2 * i < NPOLY ? ex2_poly2(x) : make_float2(ex2f(x.x), ex2f(x.y));
-                        rsp[i] = __fadd2_rn(rsp[i], p);   // padding: x = -inf -> ~0
-                        pk[q * 4 + i] = pack2<T>(p.x, p.y);
-                    }
-                }
-                tmem_st16(tP + c * 16, pk);
-            }
-            tmem_wait_st();
-            l += ((rsp[0].x + rsp[1].x) + (rsp[2].x + rsp[3].x)) + ((rsp[0].y + rsp[1].y) + (rsp[2].y + rsp[3].y));
-            tc_fence_before();     // S reads, P stores, O rescale ordered before the release
+            tc_fence_before();   // O_t read: the next item's first PV may overwrite it
+            pair_sync();         // the partner has read rl[] (the next item's exchange may reuse it)
             __syncwarp();
-            if (lane == 0) mbar_arrive(p_full + 8 * tt);
-        }
-        // row sum = both halves' partial sums (same reference max m)
-        pair_sync();   // the partner has finished reading red[] of the last iteration
-        red[half * 128 + row] = l;
-        pair_sync();
-        l += red[(half ^ 1) * 128 + row];
-        mbar_wait_spin_addr(o_full + 8 * tt, 0);
-        tc_fence_after();
-        const int n = q0 + tt * 128 + row;
-        const float inv = 1.f / l;
-#pragma unroll
-        for (int c = 0; c < D / 16; ++c) {
-            if ((c & 1) != half) continue;
-            uint32_t r[16];
-            tmem_ld16(tO + c * 16, r);
-            if (n < N) {
-                T *y = out + ((size_t)t * N + n) * C + h * D + c * 16;
-                float f[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]) * inv;
-                store8(y, f);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[8 + i]) * inv;
-                store8(y + 8, f);
-            }
+            if (lane == 0) mbar_arrive(o_free + 8 * tt);
         }
     }
     griddep_launch();
@@ -626,9 +669,16 @@ static dvc_status attn_tc_launch(const void *qkv, void *ws, void *out, int T_, i
     }
     const int bf = std::is_same<T, __nv_bfloat16>::value ? 1 : 0;
     const float scale_log2 = 1.4426950408889634f / sqrtf((float)D);
-    DVC_CUDA(launch_pdl(kfn, dim3((N + 128 * L::NT - 1) / (128 * L::NT), C / D, T_), dim3(L::THREADS), (size_t)L::bytes,
-                        stream, 1, (const T *)qp, (const T *)kp, (const T *)vp, reinterpret_cast<T *>(out), N, C,
-                        scale_log2, make_idesc(bf, 128, KT), make_idesc(bf, 128, D), attn_debug()));
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long items = (long)((N + 128 * L::NT - 1) / (128 * L::NT)) * (C / D) * T_;   // persistent: one CTA per SM
+    DVC_CUDA(launch_pdl(kfn, dim3((unsigned)(items < nsm ? items : nsm)), dim3(L::THREADS), (size_t)L::bytes, stream, 1,
+                        (const T *)qp, (const T *)kp, (const T *)vp, reinterpret_cast<T *>(out), N, C, T_, scale_log2,
+                        make_idesc(bf, 128, KT), make_idesc(bf, 128, D), attn_debug()));
     ++g_launches;
     char lab[96];
     snprintf(lab, sizeof(lab), "attn_tc T=%d N=%d C=%d d=%d", T_, N, C, D);
