@@ -137,11 +137,10 @@ __device__ __forceinline__ float silu_f(float z) { return z / (1.0f + __expf(-z)
 
 // SiLU(z) = z / (1 + e^-z) for 16-bit outputs: two MUFU ops (ex2.approx, rcp.approx,
 // each <= 2 ulp in fp32), far below the 16-bit rounding of the result.
-__device__ __forceinline__ float silu_fast(float z) {
-    float e, r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * -1.4426950408889634f));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
-    return z * r;
+__device__ __forceinline__ float tanh_fast(float x) {   // tanh.approx.f32: max rel. error 2^-11
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }

@@ -253,8 +253,8 @@ template <typename T>
 __device__ __forceinline__ float silu_t(float z) {
     if constexpr (sizeof(T) == 4) {
         return z / (1.0f + expf(-z));   // validation mode: accurate
-    } else {
-        return silu_fast(z);
+    } else {   // z holds hz = z / 2 (the affine is pre-scaled): SiLU = hz + hz tanh(hz), ONE MUFU op (R23)
+        return fmaf(z, tanh_fast(z), z);
     }
 }
 
@@ -276,8 +276,9 @@ __global__ void __launch_bounds__(256) gn_silu_kernel(const ShiftSrc<T> X, const
         sc[i] = cf.y;
         mu[i] = cf.x;
         be[i] = Elem<T>::to_f(beta[8 * v + i]);
-        if (sizeof(T) == 2) {   // 16-bit outputs: z = f*sc + (beta - mu*sc), one FMA per element
-            be[i] = be[i] - mu[i] * sc[i];
+        if (sizeof(T) == 2) {   // 16-bit outputs: hz = f*sc/2 + (beta - mu*sc)/2, one FMA per element
+            be[i] = 0.5f * (be[i] - mu[i] * sc[i]);
+            sc[i] *= 0.5f;
             mu[i] = 0.f;
         }
     }
