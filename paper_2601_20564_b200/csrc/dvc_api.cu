@@ -10,6 +10,7 @@
 #include <mutex>
 #include <map>
 #include <tuple>
+#include <nvtx3/nvToolsExt.h>
 #include "dvc_conv.cuh"
 #include "dvc_norm.cuh"
 #include "dvc_resblock.cuh"
@@ -28,6 +29,16 @@ void set_error(const char *fmt, ...) {
 
 // Raise a kernel's dynamic shared memory limit once per (kernel, device, size): the cache records a
 // size only after cudaFuncSetAttribute succeeded, so a failed call is retried (and reported) next time.
+NvtxRange::NvtxRange(const char *fmt, ...) {
+    char name[96];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(name, sizeof(name), fmt, ap);
+    va_end(ap);
+    nvtxRangePushA(name);
+}
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
+
 dvc_status ensure_smem(const void *kern, int smem) {
     static std::mutex mu;
     std::lock_guard<std::mutex> lock(mu);
@@ -535,6 +546,7 @@ dvc_status dvc_device_check(int device) {
 dvc_status dvc_encode_pixelunshuffle(const void *frames, dvc_dtype frame_dt, int T, int H, int W, int s,
                                      const void *w_exp, const void *b_exp, int c_lat, void *latent, dvc_dtype dt,
                                      void *stream) {
+    NvtxRange nv("dvc_encode_pixelunshuffle T=%d %dx%d", T, H, W);
     DVC_CHECK_ARG(frames && latent, DVC_ERR_ARG, "null frames/latent");
     DVC_CHECK_ARG(dt_valid(dt) && (dt_valid(frame_dt) || frame_dt == DVC_U8), DVC_ERR_ARG, "bad dtype");
     DVC_CHECK_ARG(frame_dt == dt || frame_dt == DVC_U8, DVC_ERR_UNSUPPORTED,
@@ -585,6 +597,7 @@ dvc_status dvc_resblock_workspace_size(const dvc_resblock *b, int T, int H, int 
 dvc_status dvc_resblock_tsm_forward(const dvc_resblock *b, const void *x_a, const void *x_b, int T, int H, int W,
                                     const void *carry_in, void *carry_out, void *y, void *workspace,
                                     size_t ws_bytes, void *stream) {
+    NvtxRange nv("dvc_resblock_tsm_forward T=%d %dx%d", T, H, W);
     DVC_CHECK_ARG(b && x_a && y && workspace, DVC_ERR_ARG, "null argument");
     RB r = rb_from_abi(b);
     dvc_status st = resblock_validate(r, T, H, W);

@@ -904,6 +904,7 @@ dvc_status dvc_transformer_workspace_size(const dvc_transformer *b, int T, int H
 
 dvc_status dvc_transformer_forward(const dvc_transformer *b, const void *x, int T, int H, int W, void *y,
                                    void *workspace, size_t ws_bytes, void *stream) {
+    NvtxRange nv("dvc_transformer_forward T=%d %dx%d", T, H, W);
     DVC_CHECK_ARG(b && x && y && workspace, DVC_ERR_ARG, "null argument");
     const TF t = tf_from_abi(b);
     dvc_status st = transformer_validate(t, T, H, W);

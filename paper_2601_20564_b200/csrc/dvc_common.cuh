@@ -145,6 +145,16 @@ __device__ __forceinline__ float tanh_fast(float x) {   // tanh.approx.f32: max 
 
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 
+// NVTX ranges (header-only NVTX v3: a no-op branch unless a tool such as ncu / nsys injects itself):
+// one per C-ABI call and one per U-Net block, so profiles can be filtered by block
+// (ncu --nvtx --nvtx-include "dvc_unet_decode_gop/block 05/").
+struct NvtxRange {
+    explicit NvtxRange(const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+    ~NvtxRange();
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 // true if `kern` already allows >= smem bytes of dynamic shared memory (records the new size otherwise)
 dvc_status ensure_smem(const void *kern, int smem);   // cudaFuncSetAttribute, cached
 

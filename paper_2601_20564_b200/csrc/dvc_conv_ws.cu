@@ -292,9 +292,9 @@ __global__ void __launch_bounds__(ws_threads<EG>(), 1) conv_ws_kernel(const __gr
                         float f[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            float a = __uint_as_float(va[i]), g = __uint_as_float(vb[i]);
-                            if (sb0) a += sb0[n + i], g += sb0[n + 16 + i];
-                            f[i] = a * (0.5f * g * (1.f + erff(g * 0.70710678118654752f)));
+                            float a = __uint_as_float(va[i]), gt = __uint_as_float(vb[i]);   // value, gate
+                            if (sb0) a += sb0[n + i], gt += sb0[n + 16 + i];
+                            f[i] = a * (0.5f * gt * (1.f + erff(gt * 0.70710678118654752f)));
                         }
                         Vec8<T> lo, hi;
                         round_store16<T>(f, lo, hi);

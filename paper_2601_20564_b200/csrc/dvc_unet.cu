@@ -426,6 +426,7 @@ dvc_status dvc_unet_workspace_size(const dvc_unet *n, int T, size_t *bytes) {
 dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, const void *ctx, int T,
                                const void *carry_in, void *carry_out, void *out, void *workspace, size_t ws_bytes,
                                void *stream) {
+    NvtxRange nv("dvc_unet_decode_gop T=%d", T);
     DVC_CHECK_ARG(n && lat && ctx && out && workspace, DVC_ERR_ARG, "null argument");
     DVC_CHECK_ARG(T >= 1 && T <= n->cfg.max_T, DVC_ERR_ARG, "T_local=%d outside [1, max_T=%d]", T, n->cfg.max_T);
     DVC_CHECK_ARG(((uintptr_t)workspace & 255) == 0, DVC_ERR_ARG, "workspace must be 256-byte aligned");
@@ -462,6 +463,7 @@ dvc_status dvc_unet_decode_gop(dvc_unet *n, dvc_comm *comm, const void *lat, con
         const RB &r = n->blk[bi];
         const int l = n->blevel[bi];
         const int H = n->lh[l], Wd = n->lw[l];
+        NvtxRange nvb("block %02d level %d", bi, l);
         const int cs = (r.ca + r.cb) / r.P;
         const size_t off = n->carry_off[bi] * es;
         const void *cin_ptr = carry_in ? reinterpret_cast<const uint8_t *>(carry_in) + off : nullptr;

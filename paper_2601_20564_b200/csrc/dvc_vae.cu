@@ -313,6 +313,7 @@ dvc_status dvc_vae_workspace_size(const dvc_vae *v, int T, size_t *bytes) {
 
 dvc_status dvc_vae_decode(dvc_vae *v, const void *lat, int T, void *frames, void *workspace, size_t ws_bytes,
                           void *stream) {
+    NvtxRange nv("dvc_vae_decode T=%d", T);
     DVC_CHECK_ARG(v && lat && frames && workspace, DVC_ERR_ARG, "null argument");
     DVC_CHECK_ARG(T >= 1 && T <= v->cfg.max_T, DVC_ERR_ARG, "T=%d outside [1, max_T=%d]", T, v->cfg.max_T);
     DVC_CHECK_ARG(((uintptr_t)workspace & 255) == 0, DVC_ERR_ARG, "workspace must be 256-byte aligned");
