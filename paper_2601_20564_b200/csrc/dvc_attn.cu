@@ -287,8 +287,9 @@ struct AttnSmem {
     static constexpr int off_q = 0, off_k = QB * NT * Q, off_v = off_k + STAGES * K;
     static constexpr int off_bar = off_v + STAGES * V;
     // barriers: q_full[2], q_empty[2], kv_full[S], kv_empty[S], then s_full[4], p_full[4], o_full[4],
-    // o_free[4] (NT <= 3; one slot of four per query tile)
-    static constexpr int nbar = 4 + 2 * STAGES + 4 * 4;
+    // o_free[4] (NT <= 3; one slot of four per query tile), v_full, v_empty (STAGES == 1: K and V move
+    // separately -- kv_full / kv_empty then track K alone)
+    static constexpr int nbar = 4 + 2 * STAGES + 4 * 4 + 2;
     // [NT tiles][2 key-tile parities][2 halves][128 rows] float exchange of the row maxima (parity double
     // buffer: a thread's write for key tile j+1 never lands in the slot its partner may still be reading
     // for tile j), then [NT][2 halves][128] for the row sums at the end of an item
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
     const uint32_t s_full = kv_empty + 8 * kAttnStages, p_full = s_full + 32;   // p_full also releases S
     const uint32_t o_full = p_full + 32;   // [t] at o_full + 8 t: O_t final
     const uint32_t o_free = o_full + 32;   // [t]: group t has read O_t (the next item's PV may overwrite it)
+    const uint32_t v_full = o_free + 32, v_empty = v_full + 8;   // STAGES == 1 only
     uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + L::off_bar + L::nbar * 8);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int heads = C / D;
@@ -380,6 +382,8 @@ __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
             mbar_init(&b[sf + 8 + i], 1);    // o_full[t]
             mbar_init(&b[sf + 12 + i], 8);   // o_free[t] (8 softmax warps per tile)
         }
+        mbar_init(&b[sf + 16], 1);   // v_full (expect-tx)
+        mbar_init(&b[sf + 17], 1);   // v_empty (tcgen05.commit)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == w_mma) tmem_alloc<1>(smem_u32(tslot), 512);
@@ -409,6 +413,17 @@ __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
                               q_full + 8 * qb);
                 for (int j = 0; j < nkt; ++j, ++jg) {
                     const int st = jg % kAttnStages;
+                    if constexpr (kAttnStages == 1) {
+                        // one buffer each: K(j) lands once S(j-1) has retired (overlapping softmax(j-1) and
+                        // PV(j-1)), V(j) once PV(j-1) has (overlapping S(j) and softmax(j))
+                        if (jg >= 1) mbar_wait_addr(kv_empty, (jg - 1) & 1);
+                        mbar_arrive_expect_tx_addr(kv_full, L::K);
+                        bulk_load(sb + L::off_k, kp + base + (size_t)j * KT * D, L::K, kv_full);
+                        if (jg >= 1) mbar_wait_addr(v_empty, (jg - 1) & 1);
+                        mbar_arrive_expect_tx_addr(v_full, L::V);
+                        bulk_load(sb + L::off_v, vp + base + (size_t)j * KT * D, L::V, v_full);
+                        continue;
+                    }
                     if (jg >= kAttnStages) mbar_wait_addr(kv_empty + 8 * st, ((jg / kAttnStages) - 1) & 1);
                     mbar_arrive_expect_tx_addr(kv_full + 8 * st, L::K + L::V);
                     bulk_load(sb + L::off_k + st * L::K, kp + base + (size_t)j * KT * D, L::K, kv_full + 8 * st);
@@ -451,22 +466,26 @@ __global__ void __launch_bounds__(AttnSmem<D, KT>::THREADS, 1)
                 mbar_wait_spin_addr(kv_full + 8 * (jg % kAttnStages), (jg / kAttnStages) & 1);
                 tc_fence_after();
                 for (int tt = 0; tt < NT; ++tt) issue_s(tt, jg);
+                if constexpr (kAttnStages == 1) tc_commit_addr(kv_empty);   // K(jg) free once S retires
                 for (int j = 0; j < nkt; ++j, ++jg, ++cp) {
                     const bool more = j + 1 < nkt;
                     if constexpr (kAttnStages == 1) {
-                        // single K/V buffer: PV(j) must retire before K/V(j+1) can land
+                        // single K and V buffers, released separately (K after S, V after PV)
                         mbar_wait_spin_addr(p_full, cp & 1);
                         tc_fence_after();
                         if (j == 0 && it > 0) {   // O is overwritten by this item's first PV
                             mbar_wait_spin_addr(o_free, (it - 1) & 1);
                             tc_fence_after();
                         }
+                        mbar_wait_spin_addr(v_full, jg & 1);
+                        tc_fence_after();
                         issue_pv(0, jg, j == 0);
-                        tc_commit_addr(kv_empty);
+                        tc_commit_addr(v_empty);
                         if (more) {
                             mbar_wait_spin_addr(kv_full, (jg + 1) & 1);
                             tc_fence_after();
                             issue_s(0, jg + 1);
+                            tc_commit_addr(kv_empty);
                         }
                     } else {
                         if (more) {
