@@ -147,7 +147,7 @@ inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 
 // NVTX ranges (header-only NVTX v3: a no-op branch unless a tool such as ncu / nsys injects itself):
 // one per C-ABI call and one per U-Net block, so profiles can be filtered by block
-// (ncu --nvtx --nvtx-include "dvc_unet_decode_gop/block 05/").
+// (ncu --nvtx --nvtx-include "regex:block 05 .*/").
 struct NvtxRange {
     explicit NvtxRange(const char *fmt, ...) __attribute__((format(printf, 2, 3)));
     ~NvtxRange();
