@@ -38,6 +38,20 @@ def test_attention_parity(dvc, orc, dtype, T, N, C, d):
     assert torch.equal(out, dvc.dvc_attention_forward(qkv, d))       # deterministic
 
 
+@pytest.mark.parametrize("d,C,T,N", [(48, 96, 40, 1000), (256, 256, 60, 700)])
+def test_attention_persistent_many_items_per_cta(dvc, orc, d, C, T, N):
+    # the persistent kernel: one CTA per SM walks (query-tile group, head, frame) items -- here 2-3
+    # items per CTA for head_dim 48 (40 frames x 2 heads x 4 groups = 320 items; Q double buffer,
+    # o_free / q_empty phases over items) and several for head_dim 256 (single K and V buffers released
+    # separately), ragged N (last key tile 104 / 60 keys), per frame against the oracle
+    qkv, q64 = dev(synthgen.normal((T, N, 3 * C), 21, scale=1.5), torch.bfloat16)
+    out = host64(dvc.dvc_attention_forward(qkv, d))
+    ref = orc.attention(q64[..., :C], q64[..., C:2 * C], q64[..., 2 * C:], d)
+    for t in range(T):
+        assert rel_l2(out[t], ref[t]) <= 1e-2, t
+    assert np.array_equal(out, host64(dvc.dvc_attention_forward(qkv, d)))   # deterministic
+
+
 def test_attention_sharp_softmax(dvc, orc):
     # large scores: the online max / rescale path must not overflow (p in [0, 1])
     T, N, C, d = 1, 520, 96, 48
