@@ -35,7 +35,7 @@ constexpr int ENC_BX = 8, ENC_BY = 16;         // latent pixels per tile (128 MM
 constexpr int ENC_A_BYTES = 3 * 64 * 128 * 2;  // 49152: {64, 8, 16, 3} 16-bit box
 constexpr int ENC_PLANE = 64 * 128 * 2;         // 16384: one colour plane {64, 8, 16, 1}
 constexpr int ENC_NPLANE = 2 * ENC_A_BYTES / ENC_PLANE;   // 6: A-region capacity in colour planes
-constexpr int ENC_THREADS = 256;
+constexpr int ENC_THREADS = 384;                // 16-bit frames: warps 4-7 and 8-11 = two epilogue groups
 constexpr int ENC_U8_THREADS = 384;             // + warps 8-11: the u8 -> 16-bit converters
 constexpr int ENC_U8_HALF = 64 * 192;           // u8 staging slot: 64 frame rows x 64 pixels x 3 bytes
 
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], U8 ? 4 : 8);   // epilogue warps (16-bit frames: two groups of 4)
             mbar_init(&u_full[i], 1);
             mbar_init(&u_empty[i], 4);
         }
@@ -274,9 +274,12 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
                 aphase ^= 1;
             }
         }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp >= 4 && (warp < 8 || !U8)) {
         // ===================== epilogue: + bias, 16-bit store =====================
+        // 16-bit frames: two warpgroups (warps 4-7, 8-11) take alternate 64-column chunks, each with its
+        // own two staging tiles, named barrier and store issuer (the stores are the bound)
         const int q4 = warp & 3;
+        const int g = (warp - 4) >> 2;
         const int r = q4 * 32 + lane;   // accumulator row = latent pixel (r / 8, r % 8) of the box
         T *out = reinterpret_cast<T *>(p.out);
         int it = 0;
@@ -293,23 +296,30 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
             tc_fence_after();
             const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * N);
             if constexpr (!U8) {   // staged epilogue (dvc_epilogue.cuh): one TMA store per 32 columns
-                const bool issuer = warp == 4 && lane == 0;
+                const bool issuer = warp == 4 + 4 * g && lane == 0;
                 const int bx0 = (rem % p.tiles_x) * ENC_BX, by0 = (rem / p.tiles_x) * ENC_BY;
                 int par = 0;
+                if (g == 1 && (!p.wide || N <= 64)) {   // the second group has no chunk of this tile
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+                    continue;
+                }
                 if (p.wide) {
                     // 64 columns per chunk: one SWIZZLE_128B [128 rows][128 B] staging tile (16-byte unit j of
                     // row r at j ^ (r & 7)) and one TMA store of the {64, 8, 16, 1} box -- whole 128-byte
                     // output rows (full L2 lines) and half the barrier round trips of the 32-column form
-                    const bool four = p.nplane == 4;   // four staging tiles: two in the A region
+                    // four staging tiles (two in the A region, nplane == 4): group g cycles tiles 2g, 2g + 1
 #pragma unroll 1
-                    for (int cc = 0; cc < N; cc += 64, wpar = (wpar + 1) & (four ? 3 : 1)) {
-                        const int par = wpar;
+                    for (int cc = 64 * g; cc < N; cc += 128, wpar ^= 1) {
+                        const int par = 2 * g + wpar;
                         uint32_t v[4][16];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) tmem_ld16_nowait(taddr + (uint32_t)(cc + 16 * k), v[k]);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) tmem_wait16(v[k]);
-                        if (cc + 64 >= N) {   // accumulator drained
+                        if (cc + 128 >= N) {   // this group's part of the accumulator is drained
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0)
@@ -328,14 +338,13 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
                             *reinterpret_cast<uint4 *>(st + r * 128 + ((j ^ (r & 7)) << 4)) = u;
                         }
                         fence_proxy_async_smem();
-                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");   // this group's barrier
                         if (issuer) {
                             tma_store_4d(&p.omap[2], smem_u32(st), cc, bx0, by0, t);
                             bulk_commit_group();
-                            if (four) bulk_wait_group_read<3>();   // the next staging tile is reusable
-                            else bulk_wait_group_read<1>();
+                            bulk_wait_group_read<1>();   // the group's other staging tile is reusable
                         }
-                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
                     }
                     continue;
                 }
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(U8 ? ENC_U8_THREADS : ENC_THREADS, 1) encode_k
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
         }
     }
-    if (!U8 && warp == 4 && lane == 0) bulk_wait_group<0>();   // every staged store has landed
+    if (!U8 && (warp == 4 || warp == 8) && lane == 0) bulk_wait_group<0>();   // every staged store has landed
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
