@@ -156,10 +156,10 @@ __device__ __forceinline__ long seg_src_pixel(const ConvSeg &s, int ho, int wo, 
 
 
 // N tile of a conv engine: the whole C_out if it fits one MMA (<= 256), else the largest divisor
-// (multiple of `quantum`, half-tile a multiple of 8 rows for CTA pairs).  Narrower tiles for calls
-// that do not fill a wave (few frames per call) were measured SLOWER on B200 (C5 at T = 4: 1032 ->
-// 906 frames/s with 96-column tiles at the 12x20 level): each narrower tile re-streams the whole A
-// operand through L2 and shared memory for fewer FLOPs.
+// (multiple of `quantum`, half-tile a multiple of 8 rows for CTA pairs).  The TMA engine narrows it
+// further only while a call fills less than half a wave (conv_ws_run): each narrower tile re-streams
+// the whole A operand, which a blanket rule paid for (C5 at T = 4: 1032 -> 906 frames/s), but calls
+// with a few dozen work items gain (T = 1 / 2 / 4: 375 -> 449 / 671 -> 767 / 1030 -> 1102 frames/s).
 inline int choose_bn(int cout, int cg, int quantum) {
     for (int c = cout < 256 ? cout : 256; c >= 16; c -= 16)
         if (cout % c == 0 && c % quantum == 0 && (c / cg) % 8 == 0) return c;

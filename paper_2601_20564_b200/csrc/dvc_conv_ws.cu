@@ -597,6 +597,27 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
     p.nbox = d.T * p.tiles_x * p.tiles_y;
     p.ntile_n = d.cout / bn;
     p.nwork = ((p.nbox + CG - 1) / CG) * p.ntile_n;
+    {   // few frames per call (streaming / strong scaling: e.g. the 12x20 level at T = 4 has 16 work items
+        // for 74 CTA pairs): narrower N tiles while the call fills less than half a wave.  Splitting N
+        // leaves every output's K accumulation order unchanged, so results stay bit-identical for any T.
+        if (g_num_sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const char *e = dvc_knob("DVC_WS_NARROW");
+        const bool narrow = (e ? atoi(e) != 0 : true) && !d.geglu && !d.fp8;
+        const int half_wave = g_num_sms / CG / 2, mboxes = (p.nbox + CG - 1) / CG;
+        while (narrow && mboxes * p.ntile_n < half_wave) {
+            int nb = 0;
+            for (int c = p.bn - 16; c >= 64 && !nb; c -= 16)
+                if (d.cout % c == 0 && (c / CG) % 8 == 0) nb = c;
+            if (!nb) break;
+            p.bn = nb;
+            p.ntile_n = d.cout / nb;
+            p.nwork = mboxes * p.ntile_n;
+        }
+    }
     p.bias0 = d.bias0;
     p.bias1 = d.bias1;
     p.residual = d.residual;
@@ -623,11 +644,11 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
                         const long r = d.seg[s2].w_col0 + (long)d.seg[s2].taps * ((d.seg[s2].c_src + 63) / 64) * d.cout;
                         if (r > rows) rows = r;
                     }
-                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, rows, 64, bn / CG);
+                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, rows, 64, p.bn / CG);
             } else if (d.fp8)
-                st = make_bmap8(&p.bmap[idx], g.w, d.cout, g.w_ld, bn / CG);
+                st = make_bmap8(&p.bmap[idx], g.w, d.cout, g.w_ld, p.bn / CG);
             else
-                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
+                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, p.bn / CG);
             if (st != DVC_OK) return st;
         }
         p.bidx[s] = idx;
@@ -641,7 +662,7 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
     }
     const int bf = d.dt == DVC_BF16;
     // kind::f8f6f4 with A/B format 0 = E4M3 (the same descriptor fields as kind::f16)
-    p.idesc = make_idesc(d.fp8 ? 0 : bf, 128 * CG, bn);
+    p.idesc = make_idesc(d.fp8 ? 0 : bf, 128 * CG, p.bn);
     if (d.fp8)
         for (int s = 0; s < d.nseg; ++s)
             DVC_CHECK_ARG(d.seg[s].c_src % 32 == 0 && !d.seg[s].packed && d.seg[s].w_ld % 16 == 0, DVC_ERR_UNSUPPORTED,
