@@ -832,6 +832,26 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
     p.nbox = d.T * p.tiles_x * p.tiles_y;
     p.ntile_n = d.cout / bn;
     p.nwork = ((p.nbox + CG - 1) / CG) * p.ntile_n;
+    {   // few frames per call: narrower N tiles while the call fills less than half a wave (as the TMA
+        // engine; N-splitting keeps each output's K order, results stay bit-identical for any T)
+        if (g_fz_sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&g_fz_sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const char *e = dvc_knob("DVC_FZ_NARROW");
+        const bool narrow = e ? atoi(e) != 0 : true;
+        const int half_wave = g_fz_sms / CG / 2, mboxes = (p.nbox + CG - 1) / CG;
+        while (narrow && mboxes * p.ntile_n < half_wave) {
+            int nb = 0;
+            for (int c = p.bn - 16; c >= 64 && !nb; c -= 16)
+                if (d.cout % c == 0 && (c / CG) % 8 == 0) nb = c;
+            if (!nb) break;
+            p.bn = nb;
+            p.ntile_n = d.cout / nb;
+            p.nwork = mboxes * p.ntile_n;
+        }
+    }
     p.bias0 = d.bias0;
     p.bias1 = d.bias1;
     p.out = d.out;
@@ -868,9 +888,9 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
                         const long r = d.seg[s2].col0 + (long)d.seg[s2].taps * ((d.seg[s2].c + 63) / 64) * d.cout;
                         if (r > rows) rows = r;
                     }
-                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, rows, 64, bn / CG);
+                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, rows, 64, p.bn / CG);
             } else
-                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, bn / CG);
+                st = make_bmap_rows(&p.bmap[idx], g.w, d.dt, d.cout, g.w_ld, p.bn / CG);
             if (st != DVC_OK) return st;
         }
         p.seg[s] = FzSeg{g.src, g.c, g.cglob0, g.taps, g.transform, g.shift, idx, g.col0, g.tapstride, g.packed};
@@ -888,7 +908,7 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
         st = make_halo_map(&p.cmap, d.carry_pad, d.dt, 1, d.H, d.W, d.cs_pad);
         if (st != DVC_OK) return st;
     }
-    p.idesc = make_idesc(d.dt == DVC_BF16, 128 * CG, bn);
+    p.idesc = make_idesc(d.dt == DVC_BF16, 128 * CG, p.bn);
     {
         static const int sw_env = dvc_knob("DVC_FZ_SW") ? atoi(dvc_knob("DVC_FZ_SW")) : 1;
         p.sw_mode = sw_env;
@@ -958,7 +978,7 @@ dvc_status conv_fz_run(const FzDesc &d, cudaStream_t stream) {
                          (p.epi_tma ? 2 * kEpiStage : 0) + 8 * (4 + 2 * FZ_MAX_RAW + 3 * FZ_MAX_NTF + 2 * FZ_MAX_BSTAGES) +
                          16 + 2048 /* red */ +
                          1024 /* static */ + 16 + (size_t)2 * d.cout * 4 /* bias */;
-    const size_t bstage = (size_t)(bn / CG) * 128;
+    const size_t bstage = (size_t)(p.bn / CG) * 128;
     int nbst = (int)((227 * 1024 - fixed) / bstage);
     {
         const char *e = dvc_knob("DVC_FZ_NB");
