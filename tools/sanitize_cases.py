@@ -1,6 +1,8 @@
 """Small launches of every kernel family on the decode path for compute-sanitizer (memcheck, racecheck,
 synccheck): the C1-sized ResBlock on both conv engines (fused H >= 32, TMA engine H < 32, with a carry),
-the encoder (16-bit and u8 frames), a small skeleton decode and one attention block.
+the encoder (16-bit and u8 frames), a small full-U-Net decode (attention, EG = 2 linears), a small skeleton
+decode (upsampler folds onto odd sizes, narrow N tiles) and the persistent attention with several items per
+CTA (head_dim 48 and 256).
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py"""
 import os
 import sys
@@ -32,5 +34,12 @@ SMALL = (32, 64, 96, 96)
 named = synthgen.unet_weights(SMALL, 32, 32, attention=True)
 net = dvc.UNet(dvc.unet_config(SMALL, 32, 32, 8, 8, 1e-5, dt, 12, 20, 2, head_dim=16), dvc.pack_weights(named, dt))
 out = dvc.dvc_unet_decode_gop(net, dev(synthgen.normal((2, 12, 20, 32), 1)), dev(synthgen.normal((2, 12, 20, 32), 5)))
+# skeleton (no Transformer2D): the upsampler folds onto 2H - 1 / 2W - 1 (12x20 -> 6x10 -> 3x5 -> 2x3 and
+# back) on the TMA engine's phase stores, T-adaptive N tiles at T = 2
+net0 = dvc.UNet(dvc.unet_config(SMALL, 32, 32, 8, 8, 1e-5, dt, 12, 20, 2), dvc.pack_weights(synthgen.unet_weights(SMALL, 32, 32), dt))
+out0 = dvc.dvc_unet_decode_gop(net0, dev(synthgen.normal((2, 12, 20, 32), 1)), dev(synthgen.normal((2, 12, 20, 32), 5)))
+# persistent attention with several items per CTA: head_dim 48 (160 items) and 256 (180 items)
+att = dvc.dvc_attention_forward(dev(synthgen.normal((40, 300, 3 * 96), 11)), 48)
+att2 = dvc.dvc_attention_forward(dev(synthgen.normal((60, 300, 3 * 256), 12)), 256)
 torch.cuda.synchronize()
 print("sanitize cases done", float(y.float().abs().mean()), float(out.float().abs().mean()), dvc.launch_count())
