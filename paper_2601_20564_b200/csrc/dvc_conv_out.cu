@@ -117,10 +117,12 @@ __device__ __forceinline__ float co_silu_h(float hz) {
     return fmaf(hz, y, hz);
 }
 
-// shared memory: 2 stages of max([C/8][CO_GP] operand, [9 oc][CO_PXS] fp32 P) | 2 mbarriers
+// shared memory: 2 stages of max([C/8][CO_GP] operand, [9 oc][CO_PXS] fp32 P) | 2 mbarriers.  C = 64: the
+// operand is ONE SWIZZLE_128B halo box {64, 34, 10} (128-byte rows, 8x fewer TMA row requests than eight
+// 16-byte-row boxes), [CO_ROWS][128 B] with 16-byte unit u of row r at u ^ (r & 7); the same bytes.
 __host__ __device__ inline int co_stage_bytes(int C) {
     const int op = (C / 8) * CO_GP, pb = 9 * CO_MAX_OC * CO_PXS * 4;
-    return ((op > pb ? op : pb) + 127) / 128 * 128;
+    return ((op > pb ? op : pb) + 1023) / 1024 * 1024;   // 1024-aligned stages (SW128 pattern)
 }
 __host__ __device__ inline int co_smem_bytes(int C) { return 2 * co_stage_bytes(C) + 16; }
 
@@ -172,9 +174,13 @@ __global__ void __launch_bounds__(CO_THREADS, 2) conv_out_kernel(const __grid_co
         const uint32_t bar = smem_u32(&full[s]);
         mbar_arrive_expect_tx_addr(bar, (uint32_t)(C / 8) * CO_HP * 16u);
         const uint32_t dst = smem_u32(smem + s * sbytes);
+        if constexpr (KS == 4) {
+            tma_load_4d(dst, &xmap, bar, 0, tx * CO_TW - 1, ty * CO_TH - 1, t);
+        } else {
 #pragma unroll
-        for (int cg = 0; cg < C / 8; ++cg)
-            tma_load_4d(dst + cg * CO_GP, &xmap, bar, cg * 8, tx * CO_TW - 1, ty * CO_TH - 1, t);
+            for (int cg = 0; cg < C / 8; ++cg)
+                tma_load_4d(dst + cg * CO_GP, &xmap, bar, cg * 8, tx * CO_TW - 1, ty * CO_TH - 1, t);
+        }
     };
     int tile = blockIdx.x;
     if (tid == 0) {
@@ -214,7 +220,14 @@ __global__ void __launch_bounds__(CO_THREADS, 2) conv_out_kernel(const __grid_co
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
                 uint32_t a[4];
-                ldsm_x4(sbase + (uint32_t)(grp * 16 * 16 + 2 * ks * CO_GP), a[0], a[1], a[2], a[3]);
+                if constexpr (KS == 4) {   // SW128 rows: this lane's row rr, 8-channel unit 2 ks + (lane >> 4)
+                    const uint32_t rr = (uint32_t)(grp * 16 + (lane & 7) + 8 * ((lane >> 3) & 1));
+                    const uint32_t u = (uint32_t)(2 * ks + ((lane >> 4) & 1));
+                    const uint32_t row_addr = smem_u32(st) + rr * 128u;   // TMA swizzles on absolute address bits
+                    ldsm_x4(row_addr + ((u ^ ((row_addr >> 7) & 7u)) << 4), a[0], a[1], a[2], a[3]);
+                } else {
+                    ldsm_x4(sbase + (uint32_t)(grp * 16 * 16 + 2 * ks * CO_GP), a[0], a[1], a[2], a[3]);
+                }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {   // a[j]: row g + 8 (j & 1), channels 16 ks + 8 (j >> 1) + 2q, +1
                     const float4 c = __ldg(cf + ks * 8 + (j >> 1) * 4);
@@ -291,11 +304,14 @@ dvc_status conv_out_run(const void *x, const void *coef, int T, int H, int W, in
     CUtensorMap map;
     cuuint64_t gdim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)T};
     cuuint64_t gstride[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
-    cuuint32_t box[4] = {8, (cuuint32_t)CO_HX, (cuuint32_t)CO_HY, 1};
+    const bool wide = C == 64;   // one SWIZZLE_128B box of all 64 channels (else one 8-channel box per group)
+    cuuint32_t box[4] = {wide ? 64u : 8u, (cuuint32_t)CO_HX, (cuuint32_t)CO_HY, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(&map, dt == DVC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
                      const_cast<void *>(x), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     wide ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                     wide ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     DVC_CHECK_ARG(r == CUDA_SUCCESS, DVC_ERR_CUDA, "cuTensorMapEncodeTiled (conv_out) failed (%d)", (int)r);
 
     CoParams p;
