@@ -58,3 +58,18 @@ def test_dvc_conv_parity(dvc, orc, dtype):
     y = dvc.dvc_conv(x.cuda(), w.cuda(), b.cuda())
     ref = orc.conv2d(x.double().numpy(), w.double().numpy(), b.double().numpy())
     assert rel_l2(host64(y), ref) <= (1e-2 if dtype != torch.float32 else 1e-5)
+
+
+@pytest.mark.parametrize("H,W,cin,cout", [(12, 20, 960, 960), (23, 40, 480, 960)])
+def test_narrow_n_tiles_are_bit_exact(dvc, H, W, cin, cout):
+    # T-adaptive N tiles (the TMA engine narrows its N tile while a call fills less than half a wave):
+    # T = 1 runs narrow tiles, T = 48 the full-width ones; N-splitting keeps every output's K order, so
+    # the frames must agree bit for bit
+    T = 48
+    x = torch.from_numpy(synthgen.normal((T, H, W, cin), 41)).to(torch.bfloat16).cuda()
+    w = torch.from_numpy(synthgen.normal((cout, 3, 3, cin), 42, scale=1 / 90)).to(torch.bfloat16).cuda()
+    b = torch.from_numpy(synthgen.normal((cout,), 43, scale=0.1)).to(torch.bfloat16).cuda()
+    full = dvc.dvc_conv(x, w, b)
+    for t in (0, 17, T - 1):
+        one = dvc.dvc_conv(x[t:t + 1].contiguous(), w, b)
+        assert torch.equal(one[0], full[t]), t
