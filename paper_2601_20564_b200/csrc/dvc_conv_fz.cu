@@ -605,6 +605,9 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
         T *out = reinterpret_cast<T *>(p.out);
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
         int it = 0;
+        // staging-buffer / reduction parity, kept across work items: an odd chunk count per item (narrow
+        // N tiles) must not restart on the buffer whose TMA store may still be reading it
+        int par = 0;
         for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1;
@@ -653,7 +656,6 @@ __global__ void __launch_bounds__(kFzThreads, 1) conv_fz_kernel(const __grid_con
                 if (want_stats) box_row_values(f, true, x);
             };
             const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
-            int par = 0;
             if (p.epi_tma) {
                 // Staged epilogue, per 32-column chunk: TMEM -> registers (thread = box row) -> + bias,
                 // 16-bit rounding -> a swizzled [128 rows][32 cols] tile in shared memory (zeros for rows

@@ -218,6 +218,9 @@ __global__ void __launch_bounds__(ws_threads<EG>(), 1) conv_ws_kernel(const __gr
         T *out = reinterpret_cast<T *>(p.out);
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
         int it = 0;
+        // staging-buffer / reduction parity, kept across work items: an odd chunk count per item (narrow
+        // N tiles) must not restart on the buffer whose TMA store may still be reading it
+        int par = 0;
         for (int w = cluster_id; w < p.nwork; w += nclusters, ++it) {
             const int buf = it & 1;
             const uint32_t use = (uint32_t)(it >> 1) & 1;
@@ -277,7 +280,6 @@ __global__ void __launch_bounds__(ws_threads<EG>(), 1) conv_ws_kernel(const __gr
             // 32 columns per step: two tcgen05.ld in flight, two butterflies, one barrier, and the
             // combine split over warps 0 / 1 (canonical order, dvc_boxstats.cuh)
             const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * BN);
-            int par = 0;
             if (p.geglu) {   // f1 GEGLU epilogue: out[m][n/2 + i] = (v_i + b) * gelu(g_i + b')
                 const int half = p.cout / 2;
 #pragma unroll 1
@@ -615,6 +617,12 @@ dvc_status conv_ws_run(const ConvDesc &d, cudaStream_t stream) {
             if (!nb) break;
             p.bn = nb;
             p.ntile_n = d.cout / nb;
+            p.nwork = mboxes * p.ntile_n;
+        }
+        const char *eb = dvc_knob("DVC_WS_BN");   // experiment builds: force the N tile
+        if (eb && !d.geglu && atoi(eb) >= 16 && d.cout % atoi(eb) == 0 && (atoi(eb) / CG) % 8 == 0) {
+            p.bn = atoi(eb);
+            p.ntile_n = d.cout / p.bn;
             p.nwork = mboxes * p.ntile_n;
         }
     }
