@@ -73,3 +73,23 @@ def test_narrow_n_tiles_are_bit_exact(dvc, H, W, cin, cout):
     for t in (0, 17, T - 1):
         one = dvc.dvc_conv(x[t:t + 1].contiguous(), w, b)
         assert torch.equal(one[0], full[t]), t
+
+
+def test_odd_epilogue_chunk_count_is_repeatable(dvc, orc):
+    # 1x1 conv 128 -> 64 on the TMA engine: two epilogue warpgroups, ONE 32-column staged chunk each per
+    # work item (an odd count), ~20 items per CTA pair. The staging-buffer parity runs across items, so
+    # no item writes the buffer whose TMA store from the previous item may still be reading it: every
+    # run, and every frame run alone, must give the same bits
+    T, H, W, cin, cout = 16, 90, 160, 128, 64
+    x = torch.from_numpy(synthgen.normal((T, H, W, cin), 51)).to(torch.bfloat16).cuda()
+    w = torch.from_numpy(synthgen.normal((cout, 1, 1, cin), 52, scale=1 / 12)).to(torch.bfloat16).cuda()
+    b = torch.from_numpy(synthgen.normal((cout,), 53, scale=0.1)).to(torch.bfloat16).cuda()
+    ref = dvc.dvc_conv(x, w, b)
+    for _ in range(20):
+        assert torch.equal(dvc.dvc_conv(x, w, b), ref)
+    one = dvc.dvc_conv(x[5:6].contiguous(), w, b)
+    assert torch.equal(one[0], ref[5])
+    # values: a corner crop against the fp64 oracle (a 1x1 conv is per pixel)
+    xc = x[:1, :8, :16].cpu().double().numpy()
+    exact = orc.conv2d(xc, w.cpu().double().numpy(), b.cpu().double().numpy())
+    assert rel_l2(host64(ref[:1, :8, :16]), exact) <= 1e-2
